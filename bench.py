@@ -1,0 +1,331 @@
+"""bench.py — wsort throughput on B200 (BASELINE.json metric: "words sorted/sec and input GB/s vs
+HBM roofline at 1/2/4/8 B200").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--algo auto] [--impl wsort|reference]
+
+A step is one pass of the whole hot path (wsort_tokenize + wsort_sort: K1 tokenize, K2 offsets,
+K3 pack+scatter, K4 sort, K5 emit) over the config's synthetic text, device-resident when the timed
+region starts. One JSON line on rank 0. Default workload: config 4 (1 GiB, seed 4; the config the
+metric is quoted at 1/2/4/8 GPUs, and the largest single-GPU config). Inputs (1 GiB text, ~1 GB of
+keys) are larger than the 126 MB L2, so no extra L2 flush is done between steps.
+
+--impl reference times the CPU oracle (oracle/, the paper's sequential merge sort per length bucket)
+as it stands on this host, on a bounded prefix of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "words sorted/sec (input GB/s and HBM roofline alongside)"
+UNIT = "words/s"
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--algo", default="auto")
+    ap.add_argument("--impl", default="wsort", choices=["wsort", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample-mb", type=int, default=96)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, device: int):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = d.get(kernel)
+    return None if v is None else float(v.get("dram_bytes_per_launch"))
+
+
+def cpu_baseline(text, sample_mb: int):
+    """The oracle as it stands (single thread, merge sort per bucket) on a bounded prefix."""
+    import numpy as np
+
+    import oracle
+
+    n = min(len(text), sample_mb << 20)
+    # cut at a separator so that the sample holds whole words of the workload
+    while 0 < n < len(text) and (int(text[n - 1]) | 0x20) - 97 in range(26) and (int(text[n]) | 0x20) - 97 in range(26):
+        n -= 1
+    sample = np.ascontiguousarray(text[:n])
+    t0 = time.perf_counter()
+    out = oracle.sort(sample, oracle.MERGE)
+    dt = time.perf_counter() - t0
+    return {"value": out.n_words / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {n} bytes ({n / 2**20:.0f} MiB, {out.n_words} words) of the workload; "
+                      f"oracle_sort(MERGE): tokenize+bucket+merge sort+emit, {dt:.2f} s",
+            "seconds": dt, "input_gbs": n / dt / 1e9}
+
+
+def run_reference(args, rank, world):
+    import numpy as np
+
+    import build_native
+    import gen
+
+    if rank != 0:
+        return
+    build_native.build_gen()
+    build_native.build_oracle()
+    import oracle
+
+    cfg = gen.CONFIGS[args.config]
+    sample_mb = max(1, min(args.cpu_sample_mb, 32))
+    n = min(cfg.n, sample_mb << 20)
+    text, _ = gen.generate(args.config, n=n)
+    for _ in range(args.warmup):
+        oracle.sort(text, oracle.MERGE)
+    times = []
+    words = 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        out = oracle.sort(text, oracle.MERGE)
+        times.append(time.perf_counter() - t0)
+        words = out.n_words
+    ms = 1000 * sum(times) / len(times)
+    value = words / (ms / 1000)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": cfg.name, "n_bytes": cfg.n, "seed": cfg.seed, "sample_bytes": n,
+                   "words_per_step": words},
+        "input_gbs": n / (ms / 1000) / 1e9,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {n} bytes of {cfg.name} per step (oracle merge sort, 1 thread)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_wsort(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import build_native
+    import gen
+
+    build_native.build_gen()
+    build_native.build_wsort()
+    from paper_1411_5283_b200 import WSort
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    stream = torch.cuda.current_stream(dev)
+    cfg = gen.CONFIGS[args.config]
+    if world > 1:
+        raise SystemExit("multi-GPU bench path: see paper_1411_5283_b200/dist.py (not wired in this build)")
+
+    # host text in pinned memory (the e2e leg copies it every step)
+    host = torch.empty(cfg.n, dtype=torch.uint8, pin_memory=True)
+    text, _ = gen.generate(args.config, out=host.numpy())
+    ws = WSort(dev, stream=stream.cuda_stream)
+    ws.load_text(host)
+    n_words = ws.tokenize()
+    ws.sort(args.algo)
+    sizes = ws.sizes()
+    words_len = int(sizes.words_len)
+
+    for _ in range(args.warmup):
+        ws.tokenize()
+        ws.sort(args.algo)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+
+    ws.reset_kernel_stats()
+    ws.set_profiling(True)
+    l0 = ws.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ws.tokenize()
+            ws.sort(args.algo)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = ws.launch_count() - l0
+    stats = ws.kernel_stats()
+    ws.set_profiling(False)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+
+    total_words = n_words * world
+    value = total_words / (ms / 1000)
+    input_gbs = cfg.n * world / (ms / 1000) / 1e9
+    peak, peak_src = measured_peaks()
+
+    # dominant kernel and its roofline
+    dom = max(stats.items(), key=lambda kv: kv[1]["ms"])
+    dname, d = dom
+    avg_ms = d["ms"] / d["launches"]
+    bytes_per_launch = d["bytes"] / d["launches"]
+    achieved = bytes_per_launch / (avg_ms / 1000) / 1e9
+    kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
+                   "share": v["ms"] / sum(x["ms"] for x in stats.values()),
+                   "gbs": (v["bytes"] / (v["ms"] / 1000) / 1e9) if v["ms"] > 0 else None}
+               for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
+    pipeline_bytes = sum(v["bytes"] for v in stats.values()) / args.steps
+    alg_min = cfg.n + words_len   # read the text once + write the output once
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": cfg.name, "n_bytes": cfg.n, "seed": cfg.seed, "words": n_words,
+                   "output_bytes": words_len, "algo": args.algo,
+                   "l2": "inputs larger than L2 (1 GiB text + ~1 GB keys per step); no extra flush"},
+        "input_gbs": input_gbs,
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(dname), "peak_source": peak_src,
+                     "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms},
+        "pipeline": {"modelled_bytes_per_step": pipeline_bytes,
+                     "modelled_gbs": pipeline_bytes / (ms / 1000) / 1e9,
+                     "modelled_frac": pipeline_bytes / (ms / 1000) / 1e9 / peak,
+                     "alg_min_bytes_per_step": alg_min,
+                     "alg_min_frac": alg_min / (ms / 1000) / 1e9 / peak},
+        "kernels": kernels,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    if not args.no_e2e and rank == 0:
+        out = torch.empty(words_len + 64, dtype=torch.uint8, pin_memory=True).numpy()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            ws.load_text(host)
+            ws.tokenize()
+            ws.sort(args.algo)
+            ws.fetch(out=out)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = e0.elapsed_time(e1) / args.e2e_steps
+        line["e2e"] = {"value": n_words / (ems / 1000), "unit": UNIT, "h2d_bytes_per_step": cfg.n,
+                       "d2h_bytes_per_step": words_len + 8 * (sizes.max_len + 2), "ms_per_step": ems,
+                       "path": "wsort_load_text(pinned host) + tokenize + sort + wsort_fetch(pinned host)"}
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline(text, args.cpu_sample_mb)
+    ws.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    try:
+        run_wsort(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,170 @@
+/*
+ * wsort.h — C ABI of libwsort, a B200-native (sm_100a) implementation of the hot path of
+ * arXiv 1411.5283, "Parallelize Bubble and Merge Sort Algorithms Using MPI".
+ *
+ * The method (§3 Methodology, Pre-processing) sorts every word of a text in three
+ * phases:
+ *   1. remove the special characters                       -> wsort_tokenize  (kernel K1)
+ *   2. split the words into per-length sub-arrays, sized by
+ *      the number of words of each length,
+ *      "all shorter words come before longer words"         -> wsort_tokenize  (K2: histogram,
+ *                                                              offsets) and wsort_sort (K3: pack+scatter)
+ *   3. sort each sub-array "in the alphabetic order"        -> wsort_sort      (K4: radix or
+ *                                                              odd-even transposition + merge path; K5 emit)
+ * and returns the sorted word list plus the per-length bucket offsets (wsort_fetch).
+ *
+ * Readings of the paper fixed by this ABI (A1-A15):
+ *   A1/A8  a word is a maximal run of bytes in [A-Za-z]; every other byte value separates words;
+ *   A2     letters are folded to lower case; output words are lower case;
+ *   A3     duplicates are kept;
+ *   A4/A5  order = (length ascending, then unsigned byte order of the folded word);
+ *   A6     equal words keep source order (observable only through src_off);
+ *   A7     a word longer than WSORT_MAX_WORD_LEN letters is an error (WSORT_E_WORD_TOO_LONG);
+ *   A12    output = "word\n" per word, plus off[0..Lmax+1] with off[0]=0 and
+ *          off[L+1] = off[L] + (#words of length L); empty input -> no words, off = {0,0};
+ *   A13    (P>1) a word belongs to the shard that holds its first byte; the caller cuts shards
+ *          so that no word straddles a cut.
+ *
+ * Conventions.
+ *   - Every function returns an int32 status: WSORT_OK (0) or a negative WSORT_E_* code.
+ *     No C++ exception crosses the ABI. On failure the context keeps a message for
+ *     wsort_last_error().
+ *   - "host" pointers are ordinary CPU memory (pageable or pinned); "device" pointers are CUDA
+ *     device memory of the context's device (e.g. torch tensors' data_ptr()).
+ *   - The caller owns every buffer it passes; the library never keeps a caller pointer after a
+ *     call returns. The context owns all device scratch (text copy, keys, output).
+ *   - One context per host thread at a time; distinct contexts are independent.
+ *   - All GPU work is enqueued on the context's stream (wsort_create / wsort_set_stream).
+ */
+#ifndef WSORT_H
+#define WSORT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---- */
+#define WSORT_OK 0
+#define WSORT_E_INVALID_ARG (-1)       /* NULL where a pointer is required, bad enum, ... */
+#define WSORT_E_STATE (-2)             /* call out of order (see the state machine below) */
+#define WSORT_E_NOMEM (-3)             /* device or pinned-host allocation failed */
+#define WSORT_E_CUDA (-4)              /* a CUDA runtime error; message in wsort_last_error */
+#define WSORT_E_NCCL (-5)              /* reserved for the multi-GPU exchange */
+#define WSORT_E_TOO_LARGE (-6)         /* a shard of more than WSORT_MAX_SHARD_BYTES bytes */
+#define WSORT_E_WORD_TOO_LONG (-7)     /* some word has more than WSORT_MAX_WORD_LEN letters (A7) */
+#define WSORT_E_BUFFER_TOO_SMALL (-8)  /* wsort_fetch: a cap is short; sizes are still filled in */
+#define WSORT_E_NOFILE (-9)            /* wsort_load_file: path does not exist */
+#define WSORT_E_IO (-10)               /* wsort_load_file: exists but cannot be read */
+
+#define WSORT_MAX_WORD_LEN 255
+#define WSORT_MAX_SHARD_BYTES 0xFFFFFF00ull /* local byte offsets are 32-bit */
+
+/* where the caller's buffers live */
+enum wsort_mem { WSORT_MEM_HOST = 0, WSORT_MEM_DEVICE = 1 };
+
+/* in-bucket sort (phase 3) */
+enum wsort_algo {
+    WSORT_ALGO_AUTO = 0,       /* library picks (currently LSD radix: ncu evidence) */
+    WSORT_ALGO_OETS_MERGE = 1, /* odd-even transposition tiles (the data-parallel bubble sort,
+                                  PAPER.md:23) + merge-path merging (the paper's merge) */
+    WSORT_ALGO_LSD_RADIX = 2   /* segmented LSD radix over 2-letter (10-bit) digits */
+};
+
+/* wsort_sort flags */
+#define WSORT_FLAG_SRC_OFF 0x1u /* also produce src_off (needed before wsort_fetch asks for it) */
+
+typedef struct wsort_ctx wsort_ctx; /* opaque */
+
+/* Create a context on CUDA device `cuda_device`. `cuda_stream` is a cudaStream_t cast to an
+ * integer (e.g. torch.cuda.current_stream().cuda_stream); 0 = the context creates its own
+ * non-blocking stream. *out receives the context; on failure *out is NULL. */
+int wsort_create(wsort_ctx **out, int cuda_device, uintptr_t cuda_stream);
+
+/* Replace the stream used for subsequent calls (0 = the context's own stream). */
+int wsort_set_stream(wsort_ctx *c, uintptr_t cuda_stream);
+
+/* Load a text of n bytes (host or device memory, per `mem`) into context-owned device memory and
+ * reset the context to state LOADED. `global_base` is the byte offset of this text inside the
+ * whole corpus (0 for a single GPU); it is added to src_off. n may be 0.
+ * Errors: INVALID_ARG (bytes NULL with n>0, bad mem), TOO_LARGE (n > WSORT_MAX_SHARD_BYTES),
+ * NOMEM, CUDA. The copy is enqueued on the stream; the call returns after it has been enqueued
+ * (host source memory must stay valid until the next synchronising call, e.g. wsort_tokenize). */
+int wsort_load_text(wsort_ctx *c, const void *bytes, uint64_t n, int mem, uint64_t global_base);
+
+/* Helper: read a whole file and wsort_load_text it (global_base 0). NOFILE if it does not exist,
+ * IO if it cannot be read. */
+int wsort_load_file(wsort_ctx *c, const char *path);
+
+/* Phases 1-2: tokenize the loaded text on the GPU (kernel K1), build the length
+ * histogram and the bucket offsets (K2). Synchronises the stream once (the sizes are needed on
+ * the host to plan phase 3) and stores the number of words in *n_words (may be NULL).
+ * State: LOADED -> TOKENIZED. Errors: STATE, WORD_TOO_LONG (state stays LOADED), CUDA. */
+int wsort_tokenize(wsort_ctx *c, uint64_t *n_words);
+
+/* Phase 3: pack each word into a fixed-width key and scatter it into its length's
+ * sub-array (K3), sort every sub-array alphabetically (K4, algorithm `algo`), and decode the
+ * keys into the output text (K5). Asynchronous: returns once the work is enqueued.
+ * flags: WSORT_FLAG_SRC_OFF to also compute src_off. State: TOKENIZED|SORTED -> SORTED.
+ * Errors: STATE, INVALID_ARG (algo), NOMEM, CUDA. */
+int wsort_sort(wsort_ctx *c, int algo, unsigned flags);
+
+typedef struct {
+    int mem;               /* where the buffers below live: WSORT_MEM_HOST or WSORT_MEM_DEVICE */
+    uint8_t *words;        /* out: "w\n" per word, length-major then alphabetical; NULL = skip */
+    uint64_t words_cap;    /* in: capacity of words in bytes */
+    uint64_t words_len;    /* out: bytes of output = C + W (letters + newlines) */
+    uint64_t *bucket_off;  /* out: off[0..max_len+1] (u64); NULL = skip */
+    uint32_t bucket_cap;   /* in: capacity of bucket_off in entries (needs max_len + 2) */
+    uint32_t max_len;      /* out: longest word (0 if none) */
+    uint64_t *src_off;     /* out (optional, needs WSORT_FLAG_SRC_OFF): global byte offset of each
+                              word's first letter, in output order (ties in source order, A6) */
+    uint64_t src_cap;      /* in: capacity of src_off in entries */
+    uint64_t n_words;      /* out: number of words W */
+    uint64_t word_base;    /* out: global index of this context's first word (0 for one GPU) */
+    uint64_t byte_base;    /* out: global byte position of this context's output (0 for one GPU) */
+} wsort_result;
+
+/* Copy results into the caller's buffers (synchronises the stream). Sizes (words_len, max_len,
+ * n_words) are always filled in. After wsort_tokenize only bucket_off/max_len/n_words are
+ * available (words/src_off must be NULL, else STATE). A cap that is too small returns
+ * BUFFER_TOO_SMALL (sizes filled, nothing copied). src_off without WSORT_FLAG_SRC_OFF -> STATE. */
+int wsort_fetch(wsort_ctx *c, wsort_result *r);
+
+/* Device pointers of the context-owned results (valid until the next load/sort/destroy), for
+ * zero-copy consumers. Any out pointer may be NULL. State: SORTED (words, src_off) or
+ * TOKENIZED (bucket_off only). */
+int wsort_device_results(wsort_ctx *c, const uint8_t **words, const uint64_t **bucket_off,
+                         const uint64_t **src_off);
+
+/* Last error message of this context (NUL-terminated, truncated to cap). */
+int wsort_last_error(const wsort_ctx *c, char *msg, size_t cap);
+
+/* Static description of a status code. */
+const char *wsort_strerror(int status);
+
+/* Release all device and host resources of the context (NULL is a no-op). */
+void wsort_destroy(wsort_ctx *c);
+
+/* ---- measurement (bench.py roofline accounting) ---- */
+typedef struct {
+    char name[32];          /* kernel class, e.g. "k1_tokenize_count" */
+    uint64_t launches;      /* launches since the last reset */
+    double total_ms;        /* sum of CUDA-event durations of those launches */
+    double bytes;           /* sum of ALGORITHMIC bytes (DESIGN.md per-kernel model) */
+} wsort_kernel_stat;
+
+/* on != 0: bracket every kernel launch with CUDA events on the context's stream. */
+int wsort_set_profiling(wsort_ctx *c, int on);
+/* Synchronises; fills up to cap entries and *n with the number of kernel classes seen. */
+int wsort_kernel_stats(wsort_ctx *c, wsort_kernel_stat *out, int cap, int *n);
+int wsort_reset_kernel_stats(wsort_ctx *c);
+/* Number of kernel launches enqueued by this context since creation. */
+uint64_t wsort_launch_count(const wsort_ctx *c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WSORT_H */

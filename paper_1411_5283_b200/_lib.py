@@ -1,0 +1,104 @@
+"""ctypes declarations of libwsort's C ABI (include/wsort.h). Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwsort.so")
+
+OK = 0
+E_INVALID_ARG = -1
+E_STATE = -2
+E_NOMEM = -3
+E_CUDA = -4
+E_NCCL = -5
+E_TOO_LARGE = -6
+E_WORD_TOO_LONG = -7
+E_BUFFER_TOO_SMALL = -8
+E_NOFILE = -9
+E_IO = -10
+
+MEM_HOST = 0
+MEM_DEVICE = 1
+
+ALGO_AUTO = 0
+ALGO_OETS_MERGE = 1
+ALGO_LSD_RADIX = 2
+ALGOS = {"auto": ALGO_AUTO, "oets_merge": ALGO_OETS_MERGE, "lsd_radix": ALGO_LSD_RADIX}
+
+FLAG_SRC_OFF = 0x1
+MAX_WORD_LEN = 255
+
+# every symbol include/wsort.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "wsort_create", "wsort_set_stream", "wsort_load_text", "wsort_load_file", "wsort_tokenize",
+    "wsort_sort", "wsort_fetch", "wsort_device_results", "wsort_last_error", "wsort_strerror",
+    "wsort_destroy", "wsort_set_profiling", "wsort_kernel_stats", "wsort_reset_kernel_stats",
+    "wsort_launch_count",
+]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [
+        ("mem", ctypes.c_int),
+        ("words", ctypes.c_void_p),
+        ("words_cap", ctypes.c_uint64),
+        ("words_len", ctypes.c_uint64),
+        ("bucket_off", ctypes.c_void_p),
+        ("bucket_cap", ctypes.c_uint32),
+        ("max_len", ctypes.c_uint32),
+        ("src_off", ctypes.c_void_p),
+        ("src_cap", ctypes.c_uint64),
+        ("n_words", ctypes.c_uint64),
+        ("word_base", ctypes.c_uint64),
+        ("byte_base", ctypes.c_uint64),
+    ]
+
+
+class KernelStat(ctypes.Structure):
+    _fields_ = [
+        ("name", ctypes.c_char * 32),
+        ("launches", ctypes.c_uint64),
+        ("total_ms", ctypes.c_double),
+        ("bytes", ctypes.c_double),
+    ]
+
+
+_lib = None
+
+
+def load():
+    """Load libwsort.so. Raises if it is missing: there is no CPU fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`. "
+            "wsort has no CPU fallback.")
+    L = ctypes.CDLL(LIB_PATH)
+    P, U64, I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int
+    L.wsort_create.argtypes = [ctypes.POINTER(P), I, ctypes.c_size_t]
+    L.wsort_set_stream.argtypes = [P, ctypes.c_size_t]
+    L.wsort_load_text.argtypes = [P, P, U64, I, U64]
+    L.wsort_load_file.argtypes = [P, ctypes.c_char_p]
+    L.wsort_tokenize.argtypes = [P, ctypes.POINTER(U64)]
+    L.wsort_sort.argtypes = [P, I, ctypes.c_uint]
+    L.wsort_fetch.argtypes = [P, ctypes.POINTER(Result)]
+    L.wsort_device_results.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]
+    L.wsort_last_error.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
+    L.wsort_strerror.argtypes = [I]
+    L.wsort_strerror.restype = ctypes.c_char_p
+    L.wsort_destroy.argtypes = [P]
+    L.wsort_destroy.restype = None
+    L.wsort_set_profiling.argtypes = [P, I]
+    L.wsort_kernel_stats.argtypes = [P, ctypes.POINTER(KernelStat), I, ctypes.POINTER(I)]
+    L.wsort_reset_kernel_stats.argtypes = [P]
+    L.wsort_launch_count.argtypes = [P]
+    L.wsort_launch_count.restype = U64
+    for name in EXPORTS:
+        if name not in ("wsort_strerror", "wsort_destroy", "wsort_launch_count"):
+            getattr(L, name).restype = I
+    _lib = L
+    return L

@@ -1,0 +1,190 @@
+"""High-level Python API over libwsort (argument marshalling only).
+
+    ws = WSort(device=0)                    # one context = one GPU stream + owned device scratch
+    ws.load_text(text)                      # bytes / np.uint8 / torch.uint8 (host or cuda)
+    n = ws.tokenize()                       # phases 1-2: K1 + K2
+    ws.sort("auto", src_off=False)          # phase 3: K3 pack+scatter, K4 sort, K5 emit
+    words, off = ws.fetch()                 # b"w\\n"*, off[0..Lmax+1]
+
+or simply ``words, off = sort(text)``.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib as L
+
+
+class WSortError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"wsort error {status} ({L.load().wsort_strerror(status).decode()}): {msg}")
+        self.status = status
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class WSort:
+    """One libwsort context on one CUDA device."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self._lib = L.load()
+        h = ctypes.c_void_p()
+        if stream is None:
+            torch = _torch()
+            if not torch.cuda.is_available():
+                raise WSortError(L.E_CUDA, "no CUDA device (wsort has no CPU fallback)")
+            with torch.cuda.device(device):
+                stream = torch.cuda.current_stream(device).cuda_stream
+        rc = self._lib.wsort_create(ctypes.byref(h), int(device), int(stream))
+        if rc != L.OK:
+            raise WSortError(rc, f"wsort_create(device={device})")
+        self._h = h
+        self.device = device
+        self._src = False
+        self._keep = None
+
+    # ------------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.wsort_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, rc: int, what: str):
+        if rc != L.OK:
+            buf = ctypes.create_string_buffer(512)
+            self._lib.wsort_last_error(self._h, buf, 512)
+            raise WSortError(rc, f"{what}: {buf.value.decode(errors='replace')}")
+
+    def set_stream(self, stream: int):
+        self._check(self._lib.wsort_set_stream(self._h, int(stream)), "wsort_set_stream")
+
+    # ------------------------------------------------------------------ pipeline
+    def load_text(self, text, global_base: int = 0):
+        """Copy `text` into the context (bytes, bytearray, numpy uint8 or torch uint8, host or cuda)."""
+        mem, ptr, n, keep = _as_buffer(text)
+        self._keep = keep   # host source must live until the next synchronising call
+        self._check(self._lib.wsort_load_text(self._h, ptr, n, mem, int(global_base)), "wsort_load_text")
+
+    def load_file(self, path: str):
+        self._check(self._lib.wsort_load_file(self._h, path.encode()), "wsort_load_file")
+
+    def tokenize(self) -> int:
+        n = ctypes.c_uint64(0)
+        rc = self._lib.wsort_tokenize(self._h, ctypes.byref(n))
+        self._keep = None
+        self._check(rc, "wsort_tokenize")
+        return int(n.value)
+
+    def sort(self, algo: str | int = "auto", src_off: bool = False):
+        a = L.ALGOS[algo] if isinstance(algo, str) else int(algo)
+        self._check(self._lib.wsort_sort(self._h, a, L.FLAG_SRC_OFF if src_off else 0), "wsort_sort")
+        self._src = src_off
+
+    def sizes(self) -> L.Result:
+        r = L.Result()
+        r.mem = L.MEM_HOST
+        self._check(self._lib.wsort_fetch(self._h, ctypes.byref(r)), "wsort_fetch(sizes)")
+        return r
+
+    def offsets(self) -> list:
+        """off[0..Lmax+1] (available after tokenize)."""
+        r = self.sizes()
+        off = np.zeros(r.max_len + 2, np.uint64)
+        r.bucket_off = off.ctypes.data
+        r.bucket_cap = off.size
+        self._check(self._lib.wsort_fetch(self._h, ctypes.byref(r)), "wsort_fetch(off)")
+        return [int(x) for x in off]
+
+    def fetch(self, src_off: bool = False, out: np.ndarray | None = None):
+        """Host results: (words: bytes-like, off: list[int]) or (words, off, src_off: np.uint64[W])."""
+        r = self.sizes()
+        words = out if out is not None else np.empty(max(r.words_len, 1), np.uint8)
+        off = np.zeros(r.max_len + 2, np.uint64)
+        src = np.empty(max(r.n_words, 1), np.uint64) if src_off else None
+        r.words = words.ctypes.data
+        r.words_cap = words.size
+        r.bucket_off = off.ctypes.data
+        r.bucket_cap = off.size
+        if src_off:
+            r.src_off = src.ctypes.data
+            r.src_cap = src.size
+        self._check(self._lib.wsort_fetch(self._h, ctypes.byref(r)), "wsort_fetch")
+        w = words[: r.words_len]
+        offl = [int(x) for x in off]
+        if src_off:
+            return w, offl, src[: r.n_words]
+        return w, offl
+
+    def fetch_device(self):
+        """(words: torch.uint8 cuda tensor (a copy), off: list[int])."""
+        torch = _torch()
+        r = self.sizes()
+        words = torch.empty(max(r.words_len, 1), dtype=torch.uint8, device=f"cuda:{self.device}")
+        off = np.zeros(r.max_len + 2, np.uint64)
+        rr = L.Result()
+        rr.mem = L.MEM_DEVICE
+        rr.words = words.data_ptr()
+        rr.words_cap = words.numel()
+        self._check(self._lib.wsort_fetch(self._h, ctypes.byref(rr)), "wsort_fetch(device)")
+        return words[: r.words_len], self.offsets()
+
+    # ------------------------------------------------------------------ measurement
+    def set_profiling(self, on: bool):
+        self._check(self._lib.wsort_set_profiling(self._h, 1 if on else 0), "wsort_set_profiling")
+
+    def kernel_stats(self) -> dict:
+        arr = (L.KernelStat * 64)()
+        n = ctypes.c_int(0)
+        self._check(self._lib.wsort_kernel_stats(self._h, arr, 64, ctypes.byref(n)), "wsort_kernel_stats")
+        return {arr[i].name.decode(): {"launches": int(arr[i].launches), "ms": arr[i].total_ms,
+                                       "bytes": arr[i].bytes} for i in range(n.value)}
+
+    def reset_kernel_stats(self):
+        self._check(self._lib.wsort_reset_kernel_stats(self._h), "wsort_reset_kernel_stats")
+
+    def launch_count(self) -> int:
+        return int(self._lib.wsort_launch_count(self._h))
+
+
+def _as_buffer(text):
+    """(mem, pointer, nbytes, keepalive) for bytes / numpy / torch inputs."""
+    if isinstance(text, (bytes, bytearray, memoryview)):
+        a = np.frombuffer(bytes(text), dtype=np.uint8)
+        return L.MEM_HOST, (a.ctypes.data if a.size else None), a.size, a
+    if isinstance(text, np.ndarray):
+        a = np.ascontiguousarray(text).view(np.uint8).reshape(-1)
+        return L.MEM_HOST, (a.ctypes.data if a.size else None), a.size, a
+    torch = _torch()
+    if isinstance(text, torch.Tensor):
+        t = text.contiguous().view(torch.uint8).reshape(-1)
+        mem = L.MEM_DEVICE if t.is_cuda else L.MEM_HOST
+        return mem, (t.data_ptr() if t.numel() else None), t.numel(), t
+    raise TypeError(f"unsupported text type {type(text)}")
+
+
+def sort(text, algo: str = "auto", src_off: bool = False, device: int = 0):
+    """One-shot: (words: bytes, bucket_off: list[int]) [+ src_off] for `text` on cuda:`device`."""
+    with WSort(device) as ws:
+        ws.load_text(text)
+        ws.tokenize()
+        ws.sort(algo, src_off=src_off)
+        res = ws.fetch(src_off=src_off)
+        return (res[0].tobytes(),) + tuple(res[1:])

@@ -1,0 +1,70 @@
+// k_emit.cu — K5: decode the sorted keys of every length bucket into the output text
+// ("The final step merges all the chunks and prints the results"; reading A12:
+// one word per line). Word i of bucket L lands at byte byte_off[L] + (i - off[L]) * (L + 1), so no
+// scan is needed. A tile decodes its keys into a shared-memory stage placed at the same 16-byte
+// phase as its global destination and writes it out with aligned 16-byte stores.
+#include "wsort_internal.cuh"
+
+namespace wsort {
+namespace {
+
+constexpr int kEThreads = 256;
+
+__global__ void __launch_bounds__(kEThreads) k_emit(EmitArgs a) {
+    __shared__ __align__(16) uint8_t stage[kEmitStage + 32];
+    const int t = threadIdx.x;
+    const TileDesc td = a.tiles[blockIdx.x];
+    const uint32_t L = td.L;
+    const BucketInfo b = a.buckets[L];
+    const uint32_t te = kEmitStage / (L + 1);
+    const uint32_t k0 = td.tile * te;
+    const uint32_t nk = min(te, b.n - k0);
+    const uint32_t kw = b.kw;
+    const uint32_t *keys = (b.final_b ? a.keys_b : a.keys_a) + b.key_off;
+    const uint64_t ob = b.byte_off + (uint64_t)k0 * (L + 1);
+    const uint32_t head = (uint32_t)(ob & 15u);
+
+    for (uint32_t k = t; k < nk; k += kEThreads) {
+        uint8_t *o = stage + head + k * (L + 1);
+        const uint32_t *kp = keys + (uint64_t)(k0 + k) * kw;
+        for (uint32_t q = 0; q < kw; q++) {
+            const uint32_t word = __ldg(kp + q);
+#pragma unroll
+            for (int j = 0; j < 6; j++) {
+                const uint32_t li = q * 6 + j;
+                if (li < L) o[li] = (uint8_t)(((word >> (25 - 5 * j)) & 31u) | 0x60u);
+            }
+        }
+        o[L] = '\n';
+    }
+    if (a.src_off) {
+        const uint32_t *pay = (b.final_b ? a.pay_b : a.pay_a) + b.word_off + k0;
+        uint64_t *so = a.src_off + b.word_off + k0;
+        for (uint32_t k = t; k < nk; k += kEThreads) so[k] = a.global_base + __ldg(pay + k);
+    }
+    __syncthreads();
+
+    const uint64_t total = (uint64_t)nk * (L + 1);
+    const uint64_t end = ob + total;
+    const uint64_t a0 = (ob + 15) & ~15ull, a1 = end & ~15ull;
+    if (a0 >= a1) {  // no full aligned chunk
+        for (uint64_t x = ob + t; x < end; x += kEThreads) a.words[x] = stage[head + (x - ob)];
+        return;
+    }
+    for (uint64_t x = ob + t; x < a0; x += kEThreads) a.words[x] = stage[head + (x - ob)];
+    for (uint64_t x = a1 + t; x < end; x += kEThreads) a.words[x] = stage[head + (x - ob)];
+    const uint64_t base16 = ob & ~15ull;   // stage offset of global address x is x - base16
+    uint4 *dst = reinterpret_cast<uint4 *>(a.words);
+    for (uint64_t x = a0 + 16ull * t; x < a1; x += 16ull * kEThreads)
+        dst[x >> 4] = *reinterpret_cast<const uint4 *>(stage + (x - base16));
+}
+
+}  // namespace
+
+cudaError_t launch_emit(const EmitArgs &a, cudaStream_t s) {
+    if (a.ntiles == 0) return cudaSuccess;
+    k_emit<<<a.ntiles, kEThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace wsort

@@ -1,0 +1,655 @@
+// wsort_api.cu — the libwsort host runtime and C ABI (include/wsort.h).
+//
+// The context owns every device buffer of the pipeline and enqueues all work on one CUDA stream:
+//   wsort_load_text  H2D/D2D copy of the text into a zero-padded device buffer
+//   wsort_tokenize   K1 (per-CTA length histograms) + K2 (offsets), one stream sync for the sizes
+//   wsort_sort       host planning of buckets and tiles -> one H2D of the plan ->
+//                    K3 (pack + scatter) -> K4 (radix: histogram, scan, passes | OETS + merge) -> K5
+//   wsort_fetch      copies results into the caller's buffers
+// Grow-only allocations: repeated calls on inputs of the same size allocate nothing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cerrno>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "wsort.h"
+#include "wsort_internal.cuh"
+
+using namespace wsort;
+
+namespace {
+
+enum State { ST_CREATED = 0, ST_LOADED = 1, ST_TOKENIZED = 2, ST_SORTED = 3 };
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+struct KernelClass {
+    std::string name;
+    uint64_t launches = 0;
+    double ms = 0;
+    double bytes = 0;
+};
+
+struct PendingEv {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes;
+};
+
+}  // namespace
+
+struct wsort_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    int sms = 148;
+    State state = ST_CREATED;
+    char err[512] = {0};
+
+    // text
+    DevBuf text_alloc;
+    uint64_t n = 0;
+    uint64_t global_base = 0;
+    const uint8_t *d_text = nullptr;
+
+    // tokenizer
+    TkArgs tk{};
+    DevBuf cta_hist, cta_base, d_sum;
+    Summary *h_sum = nullptr;   // pinned
+
+    // sort
+    DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan;
+    size_t status_bytes_clean = 0;   // both status buffers are zero over this prefix
+    std::vector<uint8_t> hplan;
+    uint8_t *h_plan_pinned = nullptr;
+    size_t h_plan_cap = 0;
+    bool sorted_with_src = false;
+    int last_algo = 0;
+
+    // profiling
+    bool prof = false;
+    std::vector<KernelClass> classes;
+    std::vector<PendingEv> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    uint64_t launches = 0;
+};
+
+namespace {
+
+int set_err(wsort_ctx *c, int code, const char *fmt, ...) {
+    if (c) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(c->err, sizeof c->err, fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+int cuda_err(wsort_ctx *c, cudaError_t e, const char *what) {
+    return set_err(c, e == cudaErrorMemoryAllocation ? WSORT_E_NOMEM : WSORT_E_CUDA, "%s: %s (%s)", what,
+                   cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CK(call, what)                                  \
+    do {                                                \
+        cudaError_t _e = (call);                        \
+        if (_e != cudaSuccess) return cuda_err(c, _e, what); \
+    } while (0)
+
+int ensure(wsort_ctx *c, DevBuf &b, size_t bytes, const char *what, bool zero = false) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return WSORT_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    size_t want = bytes + bytes / 16;   // headroom for slightly larger inputs
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(c, WSORT_E_NOMEM, "cudaMalloc(%zu) for %s failed: %s", want, what, cudaGetErrorString(e));
+    }
+    b.cap = want;
+    if (zero) CK(cudaMemsetAsync(b.p, 0, want, c->stream), "memset");
+    return WSORT_OK;
+}
+
+int class_id(wsort_ctx *c, const char *name) {
+    for (size_t i = 0; i < c->classes.size(); i++)
+        if (c->classes[i].name == name) return (int)i;
+    c->classes.push_back(KernelClass{name});
+    return (int)c->classes.size() - 1;
+}
+
+cudaEvent_t get_event(wsort_ctx *c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+template <class F>
+int launch(wsort_ctx *c, const char *name, double bytes, F f) {
+    PendingEv pe{};
+    if (c->prof) {
+        pe.cls = class_id(c, name);
+        pe.a = get_event(c);
+        pe.b = get_event(c);
+        pe.bytes = bytes;
+        cudaEventRecord(pe.a, c->stream);
+    }
+    cudaError_t e = f();
+    if (e != cudaSuccess) return cuda_err(c, e, name);
+    c->launches++;
+    if (c->prof) {
+        cudaEventRecord(pe.b, c->stream);
+        c->pending.push_back(pe);
+    }
+    return WSORT_OK;
+}
+
+void drain_events(wsort_ctx *c) {
+    for (auto &pe : c->pending) {
+        float ms = 0;
+        cudaEventSynchronize(pe.b);
+        cudaEventElapsedTime(&ms, pe.a, pe.b);
+        KernelClass &k = c->classes[pe.cls];
+        k.launches++;
+        k.ms += ms;
+        k.bytes += pe.bytes;
+        c->ev_pool.push_back(pe.a);
+        c->ev_pool.push_back(pe.b);
+    }
+    c->pending.clear();
+}
+
+// Tokenizer geometry: the same CTA -> byte-range mapping for K1 and K3.
+void plan_tokenizer(wsort_ctx *c) {
+    TkArgs &a = c->tk;
+    a.text = c->d_text;
+    a.n = c->n;
+    a.nsteps = (uint32_t)((c->n + kTkStep - 1) / kTkStep);
+    uint32_t want = (uint32_t)c->sms * 4;
+    uint32_t g = std::min<uint32_t>(a.nsteps, want);
+    a.steps_per_cta = g ? (a.nsteps + g - 1) / g : 0;
+    a.grid = a.steps_per_cta ? (a.nsteps + a.steps_per_cta - 1) / a.steps_per_cta : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *wsort_strerror(int s) {
+    switch (s) {
+        case WSORT_OK: return "ok";
+        case WSORT_E_INVALID_ARG: return "invalid argument";
+        case WSORT_E_STATE: return "call out of order";
+        case WSORT_E_NOMEM: return "out of memory";
+        case WSORT_E_CUDA: return "CUDA error";
+        case WSORT_E_NCCL: return "NCCL error";
+        case WSORT_E_TOO_LARGE: return "shard too large";
+        case WSORT_E_WORD_TOO_LONG: return "word longer than 255 letters";
+        case WSORT_E_BUFFER_TOO_SMALL: return "buffer too small";
+        case WSORT_E_NOFILE: return "no such file";
+        case WSORT_E_IO: return "I/O error";
+        default: return "unknown status";
+    }
+}
+
+int wsort_create(wsort_ctx **out, int cuda_device, uintptr_t cuda_stream) {
+    if (!out) return WSORT_E_INVALID_ARG;
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return WSORT_E_CUDA;
+    }
+    if (cuda_device < 0 || cuda_device >= ndev) return WSORT_E_INVALID_ARG;
+    wsort_ctx *c = new (std::nothrow) wsort_ctx();
+    if (!c) return WSORT_E_NOMEM;
+    c->device = cuda_device;
+    if (cudaSetDevice(cuda_device) != cudaSuccess) {
+        delete c;
+        return WSORT_E_CUDA;
+    }
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    if (cuda_stream) {
+        c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete c;
+            return WSORT_E_CUDA;
+        }
+        c->stream = c->own_stream;
+    }
+    if (cudaMallocHost(&c->h_sum, sizeof(Summary)) != cudaSuccess) {
+        cudaGetLastError();
+        if (c->own_stream) cudaStreamDestroy(c->own_stream);
+        delete c;
+        return WSORT_E_NOMEM;
+    }
+    *out = c;
+    return WSORT_OK;
+}
+
+int wsort_set_stream(wsort_ctx *c, uintptr_t cuda_stream) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    if (!cuda_stream && !c->own_stream) {
+        if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) return WSORT_E_CUDA;
+    }
+    c->stream = cuda_stream ? reinterpret_cast<cudaStream_t>(cuda_stream) : c->own_stream;
+    return WSORT_OK;
+}
+
+void wsort_destroy(wsort_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    DevBuf *bufs[] = {&c->text_alloc, &c->cta_hist, &c->cta_base, &c->d_sum, &c->keys_a, &c->keys_b,
+                      &c->pay_a, &c->pay_b, &c->words, &c->src_off, &c->dh, &c->status0, &c->status1,
+                      &c->tickets, &c->plan};
+    for (DevBuf *b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (c->h_sum) cudaFreeHost(c->h_sum);
+    if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
+    for (auto &pe : c->pending) {
+        cudaEventDestroy(pe.a);
+        cudaEventDestroy(pe.b);
+    }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+int wsort_last_error(const wsort_ctx *c, char *msg, size_t cap) {
+    if (!c || !msg || cap == 0) return WSORT_E_INVALID_ARG;
+    snprintf(msg, cap, "%s", c->err);
+    return WSORT_OK;
+}
+
+int wsort_load_text(wsort_ctx *c, const void *bytes, uint64_t n, int mem, uint64_t global_base) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    if (n && !bytes) return set_err(c, WSORT_E_INVALID_ARG, "bytes is NULL with n=%llu", (unsigned long long)n);
+    if (mem != WSORT_MEM_HOST && mem != WSORT_MEM_DEVICE) return set_err(c, WSORT_E_INVALID_ARG, "bad mem %d", mem);
+    if (n > WSORT_MAX_SHARD_BYTES)
+        return set_err(c, WSORT_E_TOO_LARGE, "shard of %llu bytes exceeds %llu", (unsigned long long)n,
+                       (unsigned long long)WSORT_MAX_SHARD_BYTES);
+    cudaSetDevice(c->device);
+    c->state = ST_CREATED;
+    uint64_t nsteps = (n + kTkStep - 1) / kTkStep;
+    size_t need = kTextFrontPad + nsteps * kTkStep + kTkHalo + 64;
+    int rc = ensure(c, c->text_alloc, need, "text");
+    if (rc) return rc;
+    uint8_t *base = static_cast<uint8_t *>(c->text_alloc.p);
+    uint8_t *t = base + kTextFrontPad;
+    CK(cudaMemsetAsync(base, 0, kTextFrontPad, c->stream), "memset text head");
+    if (n) CK(cudaMemcpyAsync(t, bytes, n, mem == WSORT_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                              c->stream), "copy text");
+    CK(cudaMemsetAsync(t + n, 0, need - kTextFrontPad - n, c->stream), "memset text tail");
+    c->d_text = t;
+    c->n = n;
+    c->global_base = global_base;
+    plan_tokenizer(c);
+    c->state = ST_LOADED;
+    return WSORT_OK;
+}
+
+int wsort_load_file(wsort_ctx *c, const char *path) {
+    if (!c || !path) return WSORT_E_INVALID_ARG;
+    FILE *f = fopen(path, "rb");
+    if (!f) {
+        FILE *probe = fopen(path, "r");
+        if (probe) fclose(probe);
+        return set_err(c, errno == ENOENT ? WSORT_E_NOFILE : WSORT_E_IO, "cannot open %s", path);
+    }
+    std::vector<uint8_t> data;
+    uint8_t chunk[1 << 16];
+    size_t got;
+    while ((got = fread(chunk, 1, sizeof chunk, f)) > 0) data.insert(data.end(), chunk, chunk + got);
+    bool bad = ferror(f) != 0;
+    fclose(f);
+    if (bad) return set_err(c, WSORT_E_IO, "read error on %s", path);
+    int rc = wsort_load_text(c, data.data(), data.size(), WSORT_MEM_HOST, 0);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->stream), "sync after file load");   // data is a local buffer
+    return WSORT_OK;
+}
+
+int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    if (c->state < ST_LOADED) return set_err(c, WSORT_E_STATE, "wsort_tokenize before wsort_load_text");
+    cudaSetDevice(c->device);
+    TkArgs &a = c->tk;
+    int rc;
+    if ((rc = ensure(c, c->cta_hist, (size_t)std::max<uint32_t>(a.grid, 1) * kHistBins * 4, "cta_hist"))) return rc;
+    if ((rc = ensure(c, c->cta_base, (size_t)std::max<uint32_t>(a.grid, 1) * 256 * 4, "cta_base"))) return rc;
+    if ((rc = ensure(c, c->d_sum, sizeof(Summary), "summary"))) return rc;
+    a.cta_hist = static_cast<uint32_t *>(c->cta_hist.p);
+    a.cta_base = static_cast<uint32_t *>(c->cta_base.p);
+    rc = launch(c, "k1_tokenize_count", (double)c->n, [&] { return launch_tokenize_count(a, c->stream); });
+    if (rc) return rc;
+    rc = launch(c, "k2_bucket_offsets", (double)a.grid * kHistBins * 4 * 2,
+                [&] { return launch_bucket_offsets(a, static_cast<Summary *>(c->d_sum.p), c->stream); });
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->h_sum, c->d_sum.p, sizeof(Summary), cudaMemcpyDeviceToHost, c->stream), "copy summary");
+    CK(cudaStreamSynchronize(c->stream), "tokenize");
+    const Summary &s = *c->h_sum;
+    if (s.too_long) {
+        c->state = ST_LOADED;
+        return set_err(c, WSORT_E_WORD_TOO_LONG, "%u word(s) longer than %d letters", s.too_long, kMaxLen);
+    }
+    if (n_words) *n_words = s.n_words;
+    c->state = ST_TOKENIZED;
+    return WSORT_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Plan layout (one H2D copy): BucketInfo[256] | radix tiles of every pass | emit tiles.
+struct SortPlan {
+    std::vector<BucketInfo> bk;
+    std::vector<std::vector<TileDesc>> pass_tiles;
+    std::vector<uint32_t> pass_tile_keys, pass_tile_words;
+    std::vector<TileDesc> emit_tiles;
+    uint32_t dh_rows = 0;
+};
+
+int sort_radix(wsort_ctx *c, bool want_src) {
+    const Summary &s = *c->h_sum;
+    const uint32_t lmax = s.max_len;
+    SortPlan P;
+    P.bk.assign(256, BucketInfo{});
+    uint32_t npasses = 0;
+    for (uint32_t L = 1; L <= lmax; L++) {
+        BucketInfo &b = P.bk[L];
+        b.key_off = s.key_off[L];
+        b.word_off = s.off[L];
+        b.byte_off = s.byte_off[L];
+        b.n = (uint32_t)(s.off[L + 1] - s.off[L]);
+        b.kw = kw_of(L);
+        b.ndig = ndig_of(L);
+        b.tile_keys = radix_tile_keys(b.kw);
+        if (!b.n) continue;
+        b.dh_row = P.dh_rows;
+        P.dh_rows += b.ndig;
+        b.final_b = b.ndig & 1u;
+        npasses = std::max(npasses, b.ndig);
+    }
+    P.pass_tiles.resize(npasses);
+    P.pass_tile_keys.assign(npasses, 0);
+    P.pass_tile_words.assign(npasses, 0);
+    for (uint32_t p = 0; p < npasses; p++) {
+        for (uint32_t L = 1; L <= lmax; L++) {
+            const BucketInfo &b = P.bk[L];
+            if (!b.n || b.ndig <= p) continue;
+            uint32_t nt = (b.n + b.tile_keys - 1) / b.tile_keys;
+            for (uint32_t i = 0; i < nt; i++) P.pass_tiles[p].push_back(TileDesc{L, i});
+            P.pass_tile_keys[p] = std::max(P.pass_tile_keys[p], b.tile_keys);
+            P.pass_tile_words[p] = std::max(P.pass_tile_words[p], b.tile_keys * b.kw);
+        }
+    }
+    for (uint32_t L = 1; L <= lmax; L++) {
+        const BucketInfo &b = P.bk[L];
+        if (!b.n) continue;
+        uint32_t te = kEmitStage / (L + 1);
+        uint32_t nt = (b.n + te - 1) / te;
+        for (uint32_t i = 0; i < nt; i++) P.emit_tiles.push_back(TileDesc{L, i});
+    }
+
+    // ---- device buffers ----
+    int rc;
+    const uint64_t key_words = s.key_off[256];
+    const uint64_t W = s.n_words;
+    if ((rc = ensure(c, c->keys_a, key_words * 4 + 64, "keys_a"))) return rc;
+    if ((rc = ensure(c, c->keys_b, key_words * 4 + 64, "keys_b"))) return rc;
+    if (want_src) {
+        if ((rc = ensure(c, c->pay_a, W * 4 + 64, "pay_a"))) return rc;
+        if ((rc = ensure(c, c->pay_b, W * 4 + 64, "pay_b"))) return rc;
+        if ((rc = ensure(c, c->src_off, W * 8 + 64, "src_off"))) return rc;
+    }
+    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    if ((rc = ensure(c, c->dh, (size_t)std::max<uint32_t>(P.dh_rows, 1) * kRadixBins * 4, "dh"))) return rc;
+    size_t max_tiles = 0;
+    for (auto &v : P.pass_tiles) max_tiles = std::max(max_tiles, v.size());
+    const size_t status_bytes = std::max<size_t>(max_tiles, 1) * kRadixBins * 4;
+    if (c->status0.cap < status_bytes || c->status1.cap < status_bytes) {
+        if ((rc = ensure(c, c->status0, status_bytes, "status0", true))) return rc;
+        if ((rc = ensure(c, c->status1, status_bytes, "status1", true))) return rc;
+        CK(cudaMemsetAsync(c->status0.p, 0, c->status0.cap, c->stream), "memset status0");
+        CK(cudaMemsetAsync(c->status1.p, 0, c->status1.cap, c->stream), "memset status1");
+    }
+    if ((rc = ensure(c, c->tickets, std::max<uint32_t>(npasses, 1) * 4, "tickets"))) return rc;
+
+    // ---- plan upload ----
+    size_t off_tiles = 256 * sizeof(BucketInfo);
+    std::vector<size_t> pass_off(npasses);
+    size_t cur = off_tiles;
+    for (uint32_t p = 0; p < npasses; p++) {
+        pass_off[p] = cur;
+        cur += P.pass_tiles[p].size() * sizeof(TileDesc);
+    }
+    size_t emit_off = cur;
+    cur += P.emit_tiles.size() * sizeof(TileDesc);
+    const size_t plan_bytes = cur;
+    if (c->h_plan_cap < plan_bytes) {
+        if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
+        c->h_plan_pinned = nullptr;
+        c->h_plan_cap = 0;
+        if (cudaMallocHost(&c->h_plan_pinned, plan_bytes * 2) != cudaSuccess) {
+            cudaGetLastError();
+            return set_err(c, WSORT_E_NOMEM, "pinned plan buffer");
+        }
+        c->h_plan_cap = plan_bytes * 2;
+    }
+    uint8_t *hp = c->h_plan_pinned;
+    memcpy(hp, P.bk.data(), off_tiles);
+    for (uint32_t p = 0; p < npasses; p++)
+        memcpy(hp + pass_off[p], P.pass_tiles[p].data(), P.pass_tiles[p].size() * sizeof(TileDesc));
+    memcpy(hp + emit_off, P.emit_tiles.data(), P.emit_tiles.size() * sizeof(TileDesc));
+    if ((rc = ensure(c, c->plan, plan_bytes, "plan"))) return rc;
+    CK(cudaMemcpyAsync(c->plan.p, hp, plan_bytes, cudaMemcpyHostToDevice, c->stream), "plan upload");
+    uint8_t *dp = static_cast<uint8_t *>(c->plan.p);
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(dp);
+
+    // ---- K3 ----
+    uint32_t *ka = static_cast<uint32_t *>(c->keys_a.p), *kb = static_cast<uint32_t *>(c->keys_b.p);
+    uint32_t *pa = want_src ? static_cast<uint32_t *>(c->pay_a.p) : nullptr;
+    uint32_t *pb = want_src ? static_cast<uint32_t *>(c->pay_b.p) : nullptr;
+    TkArgs &tk = c->tk;
+    tk.buckets = d_bk;
+    tk.keys = ka;
+    tk.payload = pa;
+    const double key_bytes = (double)key_words * 4;
+    rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes + (want_src ? 4.0 * W : 0.0),
+                [&] { return launch_pack_scatter(tk, c->stream); });
+    if (rc) return rc;
+
+    if (npasses) {
+        CK(cudaMemsetAsync(c->dh.p, 0, (size_t)P.dh_rows * kRadixBins * 4, c->stream), "memset dh");
+        CK(cudaMemsetAsync(c->tickets.p, 0, npasses * 4, c->stream), "memset tickets");
+        uint32_t *dh = static_cast<uint32_t *>(c->dh.p);
+        RadixArgs ra{};
+        ra.buckets = d_bk;
+        ra.tiles = reinterpret_cast<const TileDesc *>(dp + pass_off[0]);
+        ra.ntiles = (uint32_t)P.pass_tiles[0].size();
+        ra.kin = ka;
+        ra.dh = dh;
+        rc = launch(c, "k4_digit_hist", key_bytes, [&] { return launch_digit_hist(ra, c->stream); });
+        if (rc) return rc;
+        rc = launch(c, "k4_digit_scan", (double)P.dh_rows * kRadixBins * 8,
+                    [&] { return launch_digit_scan(dh, P.dh_rows, c->stream); });
+        if (rc) return rc;
+        uint32_t *st[2] = {static_cast<uint32_t *>(c->status0.p), static_cast<uint32_t *>(c->status1.p)};
+        for (uint32_t p = 0; p < npasses; p++) {
+            RadixArgs r{};
+            r.buckets = d_bk;
+            r.tiles = reinterpret_cast<const TileDesc *>(dp + pass_off[p]);
+            r.ntiles = (uint32_t)P.pass_tiles[p].size();
+            r.nzero = p ? (uint32_t)P.pass_tiles[p - 1].size() : 0u;
+            r.pass = p;
+            r.max_tile_keys = P.pass_tile_keys[p];
+            r.max_tile_words = P.pass_tile_words[p];
+            const bool even = (p & 1u) == 0;
+            r.kin = even ? ka : kb;
+            r.kout = even ? kb : ka;
+            r.pin = want_src ? (even ? pa : pb) : nullptr;
+            r.pout = want_src ? (even ? pb : pa) : nullptr;
+            r.dh = dh;
+            r.status = st[p & 1u];
+            r.status_other = st[(p + 1) & 1u];
+            r.ticket = static_cast<uint32_t *>(c->tickets.p) + p;
+            double act_bytes = 0;
+            for (uint32_t L = 1; L <= lmax; L++)
+                if (P.bk[L].n && P.bk[L].ndig > p)
+                    act_bytes += 2.0 * (double)P.bk[L].n * (P.bk[L].kw * 4 + (want_src ? 4 : 0));
+            rc = launch(c, "k4_radix_pass", act_bytes, [&] { return launch_radix_pass(r, c->stream); });
+            if (rc) return rc;
+        }
+        // leave both status buffers clean for the next sort
+        CK(cudaMemsetAsync(st[(npasses - 1) & 1u], 0, P.pass_tiles[npasses - 1].size() * kRadixBins * 4, c->stream),
+           "memset status");
+    }
+
+    EmitArgs ea{};
+    ea.buckets = d_bk;
+    ea.tiles = reinterpret_cast<const TileDesc *>(dp + emit_off);
+    ea.ntiles = (uint32_t)P.emit_tiles.size();
+    ea.keys_a = ka;
+    ea.keys_b = kb;
+    ea.pay_a = pa;
+    ea.pay_b = pb;
+    ea.words = static_cast<uint8_t *>(c->words.p);
+    ea.src_off = want_src ? static_cast<uint64_t *>(c->src_off.p) : nullptr;
+    ea.global_base = c->global_base;
+    rc = launch(c, "k5_emit", key_bytes + (double)s.byte_off[256] + (want_src ? 12.0 * W : 0.0),
+                [&] { return launch_emit(ea, c->stream); });
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    if (c->state < ST_TOKENIZED) return set_err(c, WSORT_E_STATE, "wsort_sort before wsort_tokenize");
+    if (algo != WSORT_ALGO_AUTO && algo != WSORT_ALGO_LSD_RADIX && algo != WSORT_ALGO_OETS_MERGE)
+        return set_err(c, WSORT_E_INVALID_ARG, "bad algo %d", algo);
+    if (flags & ~WSORT_FLAG_SRC_OFF) return set_err(c, WSORT_E_INVALID_ARG, "bad flags 0x%x", flags);
+    cudaSetDevice(c->device);
+    const bool want_src = (flags & WSORT_FLAG_SRC_OFF) != 0;
+    int rc;
+    if (algo == WSORT_ALGO_OETS_MERGE) return set_err(c, WSORT_E_INVALID_ARG, "OETS_MERGE not built yet");
+    rc = sort_radix(c, want_src);
+    if (rc) {
+        c->state = ST_TOKENIZED;
+        return rc;
+    }
+    c->sorted_with_src = want_src;
+    c->last_algo = algo;
+    c->state = ST_SORTED;
+    return WSORT_OK;
+}
+
+int wsort_fetch(wsort_ctx *c, wsort_result *r) {
+    if (!c || !r) return WSORT_E_INVALID_ARG;
+    if (c->state < ST_TOKENIZED) return set_err(c, WSORT_E_STATE, "wsort_fetch before wsort_tokenize");
+    if (r->mem != WSORT_MEM_HOST && r->mem != WSORT_MEM_DEVICE) return set_err(c, WSORT_E_INVALID_ARG, "bad mem");
+    cudaSetDevice(c->device);
+    const Summary &s = *c->h_sum;
+    r->n_words = s.n_words;
+    r->words_len = s.byte_off[256];
+    r->max_len = s.max_len;
+    r->word_base = 0;
+    r->byte_base = 0;
+    const bool sorted = c->state == ST_SORTED;
+    if (!sorted && (r->words || r->src_off))
+        return set_err(c, WSORT_E_STATE, "words/src_off requested before wsort_sort");
+    if (r->src_off && !c->sorted_with_src) return set_err(c, WSORT_E_STATE, "src_off needs WSORT_FLAG_SRC_OFF");
+    const uint32_t noff = s.max_len + 2;
+    if ((r->bucket_off && r->bucket_cap < noff) || (r->words && r->words_cap < r->words_len) ||
+        (r->src_off && r->src_cap < r->n_words))
+        return set_err(c, WSORT_E_BUFFER_TOO_SMALL, "fetch: buffer too small");
+    const cudaMemcpyKind k = r->mem == WSORT_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (r->words && r->words_len)
+        CK(cudaMemcpyAsync(r->words, c->words.p, r->words_len, k, c->stream), "fetch words");
+    if (r->src_off && r->n_words)
+        CK(cudaMemcpyAsync(r->src_off, c->src_off.p, r->n_words * 8, k, c->stream), "fetch src_off");
+    CK(cudaStreamSynchronize(c->stream), "fetch");
+    if (r->bucket_off) {
+        if (r->mem == WSORT_MEM_HOST) {
+            memcpy(r->bucket_off, s.off, noff * sizeof(uint64_t));
+        } else {
+            CK(cudaMemcpy(r->bucket_off, s.off, noff * sizeof(uint64_t), cudaMemcpyHostToDevice), "fetch off");
+        }
+    }
+    return WSORT_OK;
+}
+
+int wsort_device_results(wsort_ctx *c, const uint8_t **words, const uint64_t **bucket_off, const uint64_t **src_off) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    if (c->state < ST_TOKENIZED) return set_err(c, WSORT_E_STATE, "no results yet");
+    if ((words || src_off) && c->state != ST_SORTED) return set_err(c, WSORT_E_STATE, "not sorted yet");
+    if (src_off && !c->sorted_with_src) return set_err(c, WSORT_E_STATE, "src_off needs WSORT_FLAG_SRC_OFF");
+    if (words) *words = static_cast<const uint8_t *>(c->words.p);
+    if (bucket_off) *bucket_off = reinterpret_cast<const uint64_t *>(
+                        static_cast<const uint8_t *>(c->d_sum.p) + offsetof(Summary, off));
+    if (src_off) *src_off = static_cast<const uint64_t *>(c->src_off.p);
+    return WSORT_OK;
+}
+
+int wsort_set_profiling(wsort_ctx *c, int on) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    c->prof = on != 0;
+    return WSORT_OK;
+}
+
+int wsort_kernel_stats(wsort_ctx *c, wsort_kernel_stat *out, int cap, int *n) {
+    if (!c || (!out && cap > 0)) return WSORT_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    CK(cudaStreamSynchronize(c->stream), "stats sync");
+    drain_events(c);
+    int k = (int)c->classes.size();
+    if (n) *n = k;
+    for (int i = 0; i < k && i < cap; i++) {
+        memset(&out[i], 0, sizeof out[i]);
+        snprintf(out[i].name, sizeof out[i].name, "%s", c->classes[i].name.c_str());
+        out[i].launches = c->classes[i].launches;
+        out[i].total_ms = c->classes[i].ms;
+        out[i].bytes = c->classes[i].bytes;
+    }
+    return WSORT_OK;
+}
+
+int wsort_reset_kernel_stats(wsort_ctx *c) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    CK(cudaStreamSynchronize(c->stream), "stats sync");
+    drain_events(c);
+    for (auto &k : c->classes) {
+        k.launches = 0;
+        k.ms = 0;
+        k.bytes = 0;
+    }
+    return WSORT_OK;
+}
+
+uint64_t wsort_launch_count(const wsort_ctx *c) { return c ? c->launches : 0; }
+
+}  // extern "C"

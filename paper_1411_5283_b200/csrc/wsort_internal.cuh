@@ -1,0 +1,119 @@
+// wsort_internal.cuh — shared definitions of the libwsort kernels and host runtime (sm_100a).
+// Product code only; nothing here is shared with oracle/ or gen/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace wsort {
+
+constexpr int kMaxLen = 255;          // WSORT_MAX_WORD_LEN (reading A7)
+constexpr int kHistBins = 257;        // lengths 0..255 + "too long" bin 256
+
+// ---------------- tokenizer (K1 count, K3 pack+scatter) ----------------
+constexpr int kTkThreads = 256;
+constexpr int kTkStep = 8192;         // bytes per step = 32 bytes per thread
+constexpr int kTkPre = 16;            // bytes kept before the step (previous-byte lookup)
+constexpr int kTkHalo = 256;          // bytes kept after the step (tail of a word crossing the step)
+constexpr int kTkBuf = kTkPre + kTkStep + kTkHalo;   // 8464 bytes = 529 uint4
+constexpr int kTkMaxWords = kTkStep / 2;             // at most one word start per two bytes
+constexpr int kTextFrontPad = 256;    // zero bytes before text[0] in the device copy (alignment)
+
+// ---------------- keys ----------------
+// A word of length L is packed into KW(L) = ceil(L/6) u32 "key words": letter j (0-based) of the
+// word goes to key word j/6, bits [29-5*(j%6) .. 25-5*(j%6)], as its 5-bit code c & 0x1F
+// ('a'/'A' -> 1 ... 'z'/'Z' -> 26); unused positions are 0, which orders below 'a'. Within one
+// length bucket, unsigned comparison of key words in order == alphabetical order (reading A4).
+__host__ __device__ constexpr int kw_of(int L) { return (L + 5) / 6; }
+// LSD digits are 2 letters (10 bits): digit q (q = 0 is the most significant) covers letters
+// 2q, 2q+1 = key word q/3, bits [29-10*(q%3) .. 20-10*(q%3)].
+__host__ __device__ constexpr int ndig_of(int L) { return (L + 1) / 2; }
+constexpr int kRadixBins = 1024;
+
+struct Summary {                   // written by K2, copied to pinned host memory
+    uint64_t n_words;
+    uint64_t letters;
+    uint32_t max_len;
+    uint32_t too_long;             // number of words longer than kMaxLen
+    uint64_t off[kHistBins];       // off[L] = #words shorter than L (L = 0..256); off[256] = W
+    uint64_t key_off[kHistBins];   // u32 key-word offset of bucket L
+    uint64_t byte_off[kHistBins];  // output byte offset of bucket L
+};
+
+struct BucketInfo {                // per-length bucket, built on the host after tokenize
+    uint64_t key_off;              // u32 words into the key buffers
+    uint64_t word_off;             // off[L]
+    uint64_t byte_off;             // output byte offset
+    uint32_t n;                    // words in the bucket
+    uint32_t kw;                   // key words per word
+    uint32_t ndig;                 // LSD digits
+    uint32_t tile_keys;            // keys per radix / merge tile
+    uint32_t dh_row;               // first row of this bucket's digit histograms (rows of 1024)
+    uint32_t final_b;              // sorted keys end in buffer B (1) or A (0)
+};
+
+struct TileDesc {
+    uint32_t L;
+    uint32_t tile;                 // tile index within the bucket
+};
+
+// ---------------- launchers (defined in the .cu files) ----------------
+struct TkArgs {
+    const uint8_t *text;           // device copy, text[-kTextFrontPad..-1] = 0, zero tail padding
+    uint64_t n;
+    uint32_t nsteps;
+    uint32_t steps_per_cta;
+    uint32_t grid;
+    uint32_t *cta_hist;            // [grid][257]
+    uint32_t *cta_base;            // [grid][256]
+    const BucketInfo *buckets;     // [256]
+    uint32_t *keys;                // key buffer A
+    uint32_t *payload;             // optional u32 local source offsets (bucket order)
+};
+
+cudaError_t launch_tokenize_count(const TkArgs &a, cudaStream_t s);
+cudaError_t launch_bucket_offsets(const TkArgs &a, Summary *d_sum, cudaStream_t s);
+cudaError_t launch_pack_scatter(const TkArgs &a, cudaStream_t s);
+
+struct RadixArgs {
+    const BucketInfo *buckets;
+    const TileDesc *tiles;         // tiles of this pass
+    uint32_t ntiles;
+    uint32_t nzero;                // status slots of the other buffer to clear
+    uint32_t pass;
+    uint32_t max_tile_keys;        // largest tile (keys) among this launch's buckets
+    uint32_t max_tile_words;       // largest tile_keys * kw among this launch's buckets
+    const uint32_t *kin;
+    uint32_t *kout;
+    const uint32_t *pin;           // payload in (nullable)
+    uint32_t *pout;
+    uint32_t *dh;                  // digit histograms / bases [rows][1024]
+    uint32_t *status;              // look-back status of this pass [ntiles][1024]
+    uint32_t *status_other;        // the other status buffer (cleared here)
+    uint32_t *ticket;              // dynamic tile counter of this pass
+};
+
+cudaError_t launch_digit_hist(const RadixArgs &a, cudaStream_t s);
+cudaError_t launch_digit_scan(uint32_t *dh, uint32_t rows, cudaStream_t s);
+cudaError_t launch_radix_pass(const RadixArgs &a, cudaStream_t s);
+size_t radix_pass_smem(uint32_t tile_keys, uint32_t tile_words, bool payload);
+constexpr uint32_t kRadixTileWords = 8192;
+__host__ __device__ constexpr uint32_t radix_tile_keys(uint32_t kw) {
+    return (kRadixTileWords / kw / 32) * 32 > 32 ? (kRadixTileWords / kw / 32) * 32 : 32;
+}
+
+struct EmitArgs {
+    const BucketInfo *buckets;
+    const TileDesc *tiles;
+    uint32_t ntiles;
+    const uint32_t *keys_a;
+    const uint32_t *keys_b;
+    const uint32_t *pay_a;         // nullable
+    const uint32_t *pay_b;
+    uint8_t *words;
+    uint64_t *src_off;             // nullable
+    uint64_t global_base;
+};
+constexpr int kEmitStage = 16384;  // smem bytes of output staged per emit tile
+cudaError_t launch_emit(const EmitArgs &a, cudaStream_t s);
+
+}  // namespace wsort
