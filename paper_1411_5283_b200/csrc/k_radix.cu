@@ -4,27 +4,30 @@
 // Digits are 2 letters (10 bits, 1024 bins); bucket L needs ndig(L) = ceil(L/2) passes, least
 // significant digit first. One launch per pass processes every bucket that still has a digit left;
 // tiles never cross a bucket. Each pass is a single sweep (Onesweep-style): digit totals for all
-// passes come from one up-front histogram kernel; each tile ranks its keys stably in shared memory
-// (warp match_any + per-warp counters), publishes its per-digit counts, resolves its global
-// per-digit offset with a decoupled look-back over the preceding tiles of the same bucket, reorders
-// its keys in shared memory and writes them out coalesced. Because every pass is stable, equal keys
-// (identical words) keep their source order (reading A6), so the optional payload (source offsets)
-// comes out in the stable order.
+// passes come from one up-front histogram kernel; each tile
+//   1. loads its keys (coalesced) into shared memory,
+//   2. counts its 10-bit digits with shared-memory atomics and publishes the counts at once,
+//   3. sorts itself stably by the digit in shared memory with two 5-bit counting sub-passes
+//      (one per letter of the digit; thread-private counters + a block scan: no warp-match
+//      instructions, which measured ~64 SM-cycles each on B200 against ~3 for an smem atomic),
+//   4. resolves its global per-digit offsets with a decoupled look-back over the preceding tiles of
+//      the same bucket, and
+//   5. writes its keys out coalesced (keys with the same digit are contiguous on both sides).
+// Every pass is stable, so equal keys (identical words) keep their source order (reading A6) and
+// the optional payload (source offsets) comes out in stable order.
 #include "wsort_internal.cuh"
 
 namespace wsort {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
-constexpr int kRThreads = 512;
-constexpr int kRWarps = kRThreads / 32;
-constexpr uint32_t kInc = 0x80000000u;   // status: inclusive prefix available (else count + 1)
+constexpr int kNT = kRadixThreads;        // 256
+constexpr int kNW = kNT / 32;
+constexpr uint32_t kInc = 0x80000000u;    // status: inclusive prefix available (else count + 1)
+constexpr uint32_t kSentinel = 0xffffffffu;  // every 5-bit field = 31 > any letter code (<= 26)
 
-__device__ __forceinline__ uint32_t lanemask_lt() {
-    uint32_t m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
+__host__ __device__ __forceinline__ uint32_t padw(uint32_t i) { return i + (i >> 5); }   // bank-conflict padding
+
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -36,38 +39,327 @@ __device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
 
 __device__ __forceinline__ uint32_t digit_of(uint32_t word, uint32_t sh) { return (word >> sh) & 1023u; }
 
-// Histogram of every digit of every key of one tile (all passes at once).
-__global__ void __launch_bounds__(kRThreads) k_digit_hist(RadixArgs a) {
-    extern __shared__ uint32_t h[];
+// Exclusive scan over the block; returns this thread's exclusive prefix, *total = block total.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *wsum, uint32_t *total) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < kNW ? wsum[lane] : 0u, wi = w;
+#pragma unroll
+        for (int o = 1; o < kNW; o <<= 1) {
+            uint32_t y = __shfl_up_sync(kFull, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < kNW) wsum[lane] = wi - w;
+        if (lane == kNW - 1) wsum[kNW] = wi;
+    }
+    __syncthreads();
+    uint32_t r = wsum[warp] + incl - v;
+    if (total) *total = wsum[kNW];
+    return r;
+}
+
+// In-place exclusive scan of the 32 x kNT thread-private counters in (bin, thread) order.
+// Thread t owns the 32 consecutive linear entries [32t, 32t+32).
+__device__ __forceinline__ void scan_counters(uint32_t *cnt, uint32_t *wsum) {
+    const int t = threadIdx.x;
+    uint32_t *c = cnt + padw(32 * t);   // the 32 entries are contiguous after padding (33t .. 33t+31)
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 32; i++) s += c[i];
+    uint32_t run = block_excl_scan(s, wsum, nullptr);
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+        const uint32_t v = c[i];
+        c[i] = run;
+        run += v;
+    }
+}
+
+struct RSmem {
+    uint32_t *A, *B;          // padded key buffers (tile words)
+    uint32_t *PA, *PB;        // padded payload buffers (tile keys)
+    uint32_t *cnt;            // padded [32][kNT] counters
+    uint32_t *hist;           // [1024] tile digit counts, then tile-local start of each digit
+    uint32_t *gofs;           // [1024] global destination - tile-local position
+    uint32_t *wsum;           // [kNW + 1]
+};
+
+// One tile of one bucket. KW > 0: compile-time key width with keys in registers; KW == 0: runtime.
+template <int KW, bool kPay>
+__device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo &b, uint32_t j, uint32_t tile,
+                                           const RSmem &s) {
+    const int t = threadIdx.x;
+    const uint32_t kw = KW ? (uint32_t)KW : b.kw;
+    const uint32_t KPT = KW ? 32u / KW : b.tile_keys / kNT;
+    const uint32_t T = kNT * KPT;
+    const uint32_t q = b.ndig - 1 - a.pass, wi = q / 3, sh = 20 - 10 * (q % 3);
+    const uint32_t k0 = tile * b.tile_keys;
+    const uint32_t nk = min(b.tile_keys, b.n - k0);
+    constexpr int RK = KW ? 32 / KW : 1;   // register keys per thread
+
+    for (uint32_t i = t; i < kRadixBins; i += kNT) s.hist[i] = 0;
+    {
+        const uint32_t *src = a.kin + b.key_off + (uint64_t)k0 * kw;
+        const uint32_t nw = nk * kw, tw = T * kw;
+        for (uint32_t i = t; i < tw; i += kNT) s.A[padw(i)] = i < nw ? __ldg(src + i) : kSentinel;
+        if constexpr (kPay) {
+            const uint32_t *ps = a.pin + b.word_off + k0;
+            for (uint32_t i = t; i < T; i += kNT) s.PA[padw(i)] = i < nk ? __ldg(ps + i) : 0u;
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < 32; f++) s.cnt[padw(f * kNT + t)] = 0;
+    __syncthreads();
+
+    uint32_t key[RK][KW ? KW : 1];
+    uint32_t rk[(RK + 3) / 4];
+    uint32_t c4[4];
+
+    // ---- sub-pass 1: low 5 bits (second letter of the pair); also the 10-bit tile histogram ----
+    {
+#pragma unroll
+        for (int i = 0; i < (RK + 3) / 4; i++) rk[i] = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < KPT; k++) {
+            const uint32_t idx = t * KPT + k;
+            uint32_t w;
+            if constexpr (KW > 0) {
+#pragma unroll
+                for (int u = 0; u < KW; u++) key[k % RK][u] = s.A[padw(idx * KW + u)];
+                w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
+            } else {
+                w = s.A[padw(idx * kw + wi)];
+            }
+            const uint32_t d = digit_of(w, sh);
+            const uint32_t f = d & 31u;
+            uint32_t *cp = s.cnt + padw(f * kNT + t);
+            const uint32_t c = *cp;
+            *cp = c + 1;
+            if constexpr (KW > 0) rk[k / 4] |= c << (8 * (k % 4));
+            atomicAdd(&s.hist[d], 1u);
+        }
+    }
+    __syncthreads();
+    // publish this tile's digit counts (aggregate) as early as possible
+    uint32_t *st = a.status + (size_t)j * kRadixBins;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const uint32_t d = 4 * t + e;
+        c4[e] = d == 1023u ? 0u : s.hist[d];   // digit 1023 only ever holds sentinels
+        st_relaxed(st + d, tile == 0 ? (kInc | c4[e]) : c4[e] + 1u);
+    }
+    scan_counters(s.cnt, s.wsum);
+    __syncthreads();
+    // scatter A -> B by the low field
+#pragma unroll
+    for (uint32_t k = 0; k < KPT; k++) {
+        const uint32_t idx = t * KPT + k;
+        uint32_t w, r = 0;
+        if constexpr (KW > 0) {
+            w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
+            r = (rk[k / 4] >> (8 * (k % 4))) & 255u;
+        } else {
+            w = s.A[padw(idx * kw + wi)];
+        }
+        const uint32_t f = digit_of(w, sh) & 31u;
+        uint32_t pos;
+        if constexpr (KW > 0) {
+            pos = s.cnt[padw(f * kNT + t)] + r;
+#pragma unroll
+            for (int u = 0; u < KW; u++) s.B[padw(pos * KW + u)] = key[k % RK][u];
+        } else {
+            uint32_t *cp = s.cnt + padw(f * kNT + t);   // runtime path: rank by re-counting
+            pos = *cp;
+            *cp = pos + 1;
+            for (uint32_t u = 0; u < kw; u++) s.B[padw(pos * kw + u)] = s.A[padw(idx * kw + u)];
+        }
+        if constexpr (kPay) s.PB[padw(pos)] = s.PA[padw(idx)];
+    }
+    __syncthreads();
+
+    // ---- sub-pass 2: high 5 bits (first letter of the pair) ----
+#pragma unroll
+    for (int f = 0; f < 32; f++) s.cnt[padw(f * kNT + t)] = 0;
+    {
+#pragma unroll
+        for (int i = 0; i < (RK + 3) / 4; i++) rk[i] = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < KPT; k++) {
+            const uint32_t idx = t * KPT + k;
+            uint32_t w;
+            if constexpr (KW > 0) {
+#pragma unroll
+                for (int u = 0; u < KW; u++) key[k % RK][u] = s.B[padw(idx * KW + u)];
+                w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
+            } else {
+                w = s.B[padw(idx * kw + wi)];
+            }
+            const uint32_t f = digit_of(w, sh) >> 5;
+            uint32_t *cp = s.cnt + padw(f * kNT + t);
+            const uint32_t c = *cp;
+            *cp = c + 1;
+            if constexpr (KW > 0) rk[k / 4] |= c << (8 * (k % 4));
+        }
+    }
+    __syncthreads();
+    scan_counters(s.cnt, s.wsum);
+    // tile-local start of every digit (exclusive scan of the counts over digits)
+    {
+        const uint32_t s4 = c4[0] + c4[1] + c4[2] + c4[3];
+        uint32_t ex = block_excl_scan(s4, s.wsum, nullptr);
+        // decoupled look-back over the preceding tiles of this bucket, 4 digits per thread
+        uint32_t pre[4] = {0, 0, 0, 0};
+        if (tile != 0) {
+            uint32_t done = 0;
+            uint32_t jj = j - 1;
+            while (done != 0xfu) {
+                const uint32_t *sp = a.status + (size_t)jj * kRadixBins + 4 * t;
+                uint32_t v[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) v[e] = (done >> e) & 1u ? 1u : ld_relaxed(sp + e);
+                bool ready = true;
+#pragma unroll
+                for (int e = 0; e < 4; e++) ready &= v[e] != 0u;
+                if (!ready) continue;
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    if ((done >> e) & 1u) continue;
+                    if (v[e] & kInc) {
+                        pre[e] += v[e] & ~kInc;
+                        done |= 1u << e;
+                    } else {
+                        pre[e] += v[e] - 1u;
+                    }
+                }
+                jj--;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; e++) st_relaxed(st + 4 * t + e, kInc | (pre[e] + c4[e]));
+        }
+        const uint32_t *dbase = a.dh + (size_t)(b.dh_row + q) * kRadixBins;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const uint32_t d = 4 * t + e;
+            s.gofs[d] = (d == 1023u ? 0u : __ldg(dbase + d)) + pre[e] - ex;
+            ex += c4[e];
+        }
+    }
+    __syncthreads();
+    // scatter B -> A by the high field
+#pragma unroll
+    for (uint32_t k = 0; k < KPT; k++) {
+        const uint32_t idx = t * KPT + k;
+        uint32_t pos;
+        if constexpr (KW > 0) {
+            const uint32_t w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
+            const uint32_t f = digit_of(w, sh) >> 5;
+            pos = s.cnt[padw(f * kNT + t)] + ((rk[k / 4] >> (8 * (k % 4))) & 255u);
+#pragma unroll
+            for (int u = 0; u < KW; u++) s.A[padw(pos * KW + u)] = key[k % RK][u];
+        } else {
+            const uint32_t f = digit_of(s.B[padw(idx * kw + wi)], sh) >> 5;
+            uint32_t *cp = s.cnt + padw(f * kNT + t);
+            pos = *cp;
+            *cp = pos + 1;
+            for (uint32_t u = 0; u < kw; u++) s.A[padw(pos * kw + u)] = s.B[padw(idx * kw + u)];
+        }
+        if constexpr (kPay) s.PA[padw(pos)] = s.PB[padw(idx)];
+    }
+    __syncthreads();
+
+    // ---- coalesced write-out (the sentinels sort to the end and are dropped) ----
+    uint32_t *dst = a.kout + b.key_off;
+    if constexpr (KW == 1) {
+        for (uint32_t i = t; i < nk; i += kNT) {
+            const uint32_t w = s.A[padw(i)];
+            dst[s.gofs[digit_of(w, sh)] + i] = w;
+        }
+    } else {
+        const uint32_t nw = nk * kw;
+        for (uint32_t i = t; i < nw; i += kNT) {
+            const uint32_t k = i / kw, u = i - k * kw;
+            const uint32_t d = digit_of(s.A[padw(k * kw + wi)], sh);
+            dst[(uint64_t)(s.gofs[d] + k) * kw + u] = s.A[padw(i)];
+        }
+    }
+    if constexpr (kPay) {
+        uint32_t *pd = a.pout + b.word_off;
+        for (uint32_t i = t; i < nk; i += kNT) {
+            const uint32_t d = digit_of(s.A[padw(i * kw + wi)], sh);
+            pd[s.gofs[d] + i] = s.PA[padw(i)];
+        }
+    }
+}
+
+template <bool kPay>
+__global__ void __launch_bounds__(kNT, 2) k_radix_pass(RadixArgs a) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ uint32_t s_ticket;
+    __shared__ uint32_t s_wsum[kNW + 1];
+    const int t = threadIdx.x;
+    if (t == 0) s_ticket = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    const uint32_t j = s_ticket;
+    if (j < a.nzero)
+        for (uint32_t i = t; i < kRadixBins; i += kNT) a.status_other[(size_t)j * kRadixBins + i] = 0;
+    if (j >= a.ntiles) return;
+    const TileDesc td = a.tiles[j];
+    const BucketInfo b = a.buckets[td.L];
+
+    RSmem s;
+    const uint32_t tw = padw(a.max_tile_words) + 1, tk = padw(a.max_tile_keys) + 1;
+    s.A = smem;
+    s.B = s.A + tw;
+    s.cnt = s.B + tw;
+    s.hist = s.cnt + padw(32 * kNT) + 1;
+    s.gofs = s.hist + kRadixBins;
+    s.PA = s.gofs + kRadixBins;
+    s.PB = s.PA + (kPay ? tk : 0);
+    s.wsum = s_wsum;
+    if (b.kw == 1) radix_tile<1, kPay>(a, b, j, td.tile, s);
+    else if (b.kw == 2) radix_tile<2, kPay>(a, b, j, td.tile, s);
+    else radix_tile<0, kPay>(a, b, j, td.tile, s);
+}
+
+// Histogram of every digit of every key of one tile (all passes at once), smem atomics.
+__global__ void __launch_bounds__(kNT) k_digit_hist(RadixArgs a) {
+    extern __shared__ uint32_t h[];
+    const int t = threadIdx.x;
     const TileDesc td = a.tiles[blockIdx.x];
     const BucketInfo b = a.buckets[td.L];
     const uint32_t k0 = td.tile * b.tile_keys, k1 = min(k0 + b.tile_keys, b.n);
     const uint32_t nd = b.ndig, ns = min(nd, 12u), kw = b.kw;
-    for (uint32_t i = t; i < ns * kRadixBins; i += kRThreads) h[i] = 0;
+    for (uint32_t i = t; i < ns * kRadixBins; i += kNT) h[i] = 0;
     __syncthreads();
     const uint32_t *kin = a.kin + b.key_off;
-    for (uint32_t base = k0 + warp * 32; base < k1; base += kRThreads) {
-        const uint32_t k = base + lane;
-        const bool v = k < k1;
-        uint32_t word = 0, cur = 0xffffffffu;
-        for (uint32_t q = 0; q < nd; q++) {
-            const uint32_t wi = q / 3;
-            if (wi != cur) {
-                word = v ? __ldg(kin + (uint64_t)k * kw + wi) : 0u;
-                cur = wi;
-            }
-            const uint32_t d = v ? digit_of(word, 20 - 10 * (q % 3)) : 0xffffffffu;
-            const uint32_t peers = __match_any_sync(kFull, d);
-            if (v && lane == __ffs(peers) - 1) {
-                if (q < 12) atomicAdd(&h[q * kRadixBins + d], __popc(peers));
-                else atomicAdd(&a.dh[(size_t)(b.dh_row + q) * kRadixBins + d], __popc(peers));
+    if (kw == 1) {
+        for (uint32_t k = k0 + t; k < k1; k += kNT) {
+            const uint32_t w = __ldg(kin + k);
+            for (uint32_t q = 0; q < nd; q++) atomicAdd(&h[q * kRadixBins + digit_of(w, 20 - 10 * q)], 1u);
+        }
+    } else {
+        for (uint32_t k = k0 + t; k < k1; k += kNT) {
+            for (uint32_t q = 0; q < nd; q++) {
+                const uint32_t w = __ldg(kin + (uint64_t)k * kw + q / 3);
+                const uint32_t d = digit_of(w, 20 - 10 * (q % 3));
+                if (q < 12) atomicAdd(&h[q * kRadixBins + d], 1u);
+                else atomicAdd(&a.dh[(size_t)(b.dh_row + q) * kRadixBins + d], 1u);
             }
         }
     }
     __syncthreads();
-    for (uint32_t i = t; i < ns * kRadixBins; i += kRThreads)
-        if (h[i]) atomicAdd(&a.dh[(size_t)b.dh_row * kRadixBins + i], h[i]);
+    for (uint32_t i = t; i < ns * kRadixBins; i += kNT) {
+        const uint32_t v = h[i];
+        if (v) atomicAdd(&a.dh[(size_t)b.dh_row * kRadixBins + i], v);
+    }
 }
 
 // Exclusive scan of one 1024-bin histogram row per CTA (in place): digit counts -> digit bases.
@@ -97,184 +389,17 @@ __global__ void __launch_bounds__(1024) k_digit_scan(uint32_t *dh) {
     row[t] = wsum[warp] + incl - x;
 }
 
-// One LSD pass over all active buckets. Shared memory layout (dynamic):
-//   wh   u16 [16][1024]  per-warp digit counters, then per-warp exclusive prefixes
-//   cnt  u32 [1024]      tile digit counts
-//   toff u32 [1024]      tile-local exclusive prefix over digits
-//   gofs u32 [1024]      global destination - tile-local position, per digit (mod 2^32)
-//   dr   u32 [T]         digit | rank-within-warp << 10, per key
-//   kin  u32 [T*KW], kout u32 [T*KW], (payload) pin u32 [T], pout u32 [T]   (T*KW <= max_tile_words)
-template <bool kPay>
-__global__ void __launch_bounds__(kRThreads) k_radix_pass(RadixArgs a) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ uint32_t s_ticket;
-    __shared__ uint32_t s_wsum[kRWarps];
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint32_t TK = a.max_tile_keys, TW = a.max_tile_words;
-    uint16_t *wh = reinterpret_cast<uint16_t *>(smem);
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(smem + kRWarps * kRadixBins * 2);
-    uint32_t *toff = cnt + kRadixBins;
-    uint32_t *gofs = toff + kRadixBins;
-    uint32_t *dr = gofs + kRadixBins;
-    uint32_t *kin_s = dr + TK;
-    uint32_t *kout_s = kin_s + TW;
-    uint32_t *pin_s = kout_s + TW;
-    uint32_t *pout_s = pin_s + TK;
-
-    if (t == 0) s_ticket = atomicAdd(a.ticket, 1u);
-    __syncthreads();
-    const uint32_t j = s_ticket;
-    if (j < a.nzero)
-        for (uint32_t i = t; i < kRadixBins; i += kRThreads) a.status_other[(size_t)j * kRadixBins + i] = 0;
-    if (j >= a.ntiles) return;
-
-    const TileDesc td = a.tiles[j];
-    const BucketInfo b = a.buckets[td.L];
-    const uint32_t q = b.ndig - 1 - a.pass;
-    const uint32_t wi = q / 3, sh = 20 - 10 * (q % 3);
-    const uint32_t T = b.tile_keys, kw = b.kw;
-    const uint32_t k0 = td.tile * T;
-    const uint32_t nk = min(T, b.n - k0);
-    const uint32_t kpw = ((T + kRWarps * 32 - 1) / (kRWarps * 32)) * 32;   // keys per warp
-
-    for (uint32_t i = t; i < kRWarps * kRadixBins / 2; i += kRThreads) reinterpret_cast<uint32_t *>(wh)[i] = 0;
-    {
-        const uint32_t *src = a.kin + b.key_off + (uint64_t)k0 * kw;
-        const uint32_t nw = nk * kw;
-        for (uint32_t i = t; i < nw; i += kRThreads) kin_s[i] = __ldg(src + i);
-        if constexpr (kPay) {
-            const uint32_t *ps = a.pin + b.word_off + k0;
-            for (uint32_t i = t; i < nk; i += kRThreads) pin_s[i] = __ldg(ps + i);
-        }
-    }
-    __syncthreads();
-
-    // stable rank within each warp's contiguous key range
-    {
-        const uint32_t kb = warp * kpw, ke = min(kb + kpw, nk);
-        uint16_t *myh = wh + warp * kRadixBins;
-        for (uint32_t i = kb; i < kb + kpw; i += 32) {
-            const uint32_t k = i + lane;
-            const bool v = k < ke;
-            const uint32_t d = v ? digit_of(kin_s[k * kw + wi], sh) : 0xffffffffu;
-            const uint32_t peers = __match_any_sync(kFull, d);
-            const uint32_t before = v ? myh[d] : 0u;
-            __syncwarp();
-            if (v && lane == __ffs(peers) - 1) myh[d] = (uint16_t)(before + __popc(peers));
-            __syncwarp();
-            if (v) dr[k] = d | ((before + __popc(peers & lanemask_lt())) << 10);
-        }
-    }
-    __syncthreads();
-
-    // per digit: exclusive prefix over warps; tile counts; block scan over digits
-    uint32_t c2[2];
-#pragma unroll
-    for (int e = 0; e < 2; e++) {
-        const uint32_t d = 2 * t + e;
-        uint32_t run = 0;
-#pragma unroll
-        for (int w = 0; w < kRWarps; w++) {
-            uint32_t x = wh[w * kRadixBins + d];
-            wh[w * kRadixBins + d] = (uint16_t)run;
-            run += x;
-        }
-        c2[e] = run;
-    }
-    {
-        const uint32_t s = c2[0] + c2[1];
-        uint32_t incl = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = lane < kRWarps ? s_wsum[lane] : 0u, wi2 = w;
-#pragma unroll
-            for (int o = 1; o < kRWarps; o <<= 1) {
-                uint32_t y = __shfl_up_sync(kFull, wi2, o);
-                if (lane >= o) wi2 += y;
-            }
-            if (lane < kRWarps) s_wsum[lane] = wi2 - w;
-        }
-        __syncthreads();
-        const uint32_t excl = s_wsum[warp] + incl - s;
-        toff[2 * t] = excl;
-        toff[2 * t + 1] = excl + c2[0];
-    }
-
-    // decoupled look-back over the preceding tiles of this bucket
-    const uint32_t *dbase = a.dh + (size_t)(b.dh_row + q) * kRadixBins;
-#pragma unroll
-    for (int e = 0; e < 2; e++) {
-        const uint32_t d = 2 * t + e;
-        uint32_t *stp = a.status + (size_t)j * kRadixBins + d;
-        uint32_t prefix = 0;
-        if (td.tile == 0) {
-            st_relaxed(stp, kInc | c2[e]);
-        } else {
-            st_relaxed(stp, c2[e] + 1u);
-            uint32_t jj = j - 1;
-            for (;;) {
-                const uint32_t sv = ld_relaxed(a.status + (size_t)jj * kRadixBins + d);
-                if (sv == 0) continue;
-                if (sv & kInc) {
-                    prefix += sv & ~kInc;
-                    break;
-                }
-                prefix += sv - 1u;
-                jj--;
-            }
-            st_relaxed(stp, kInc | (prefix + c2[e]));
-        }
-        gofs[d] = dbase[d] + prefix - toff[d];
-    }
-    __syncthreads();
-
-    // reorder in shared memory by (digit, warp, rank)
-    for (uint32_t k = t; k < nk; k += kRThreads) {
-        const uint32_t x = dr[k];
-        const uint32_t d = x & 1023u, r = x >> 10, w = k / kpw;
-        const uint32_t pos = toff[d] + wh[w * kRadixBins + d] + r;
-        for (uint32_t u = 0; u < kw; u++) kout_s[pos * kw + u] = kin_s[k * kw + u];
-        if constexpr (kPay) pout_s[pos] = pin_s[k];
-    }
-    __syncthreads();
-
-    // coalesced write-out: keys with the same digit are contiguous in both smem and global
-    {
-        uint32_t *dst = a.kout + b.key_off;
-        const uint32_t nw = nk * kw;
-        for (uint32_t i = t; i < nw; i += kRThreads) {
-            const uint32_t k = i / kw, u = i - k * kw;
-            const uint32_t d = digit_of(kout_s[k * kw + wi], sh);
-            dst[(uint64_t)(gofs[d] + k) * kw + u] = kout_s[i];
-        }
-        if constexpr (kPay) {
-            uint32_t *pd = a.pout + b.word_off;
-            for (uint32_t k = t; k < nk; k += kRThreads) {
-                const uint32_t d = digit_of(kout_s[k * kw + wi], sh);
-                pd[gofs[d] + k] = pout_s[k];
-            }
-        }
-    }
-}
-
 }  // namespace
 
 size_t radix_pass_smem(uint32_t tile_keys, uint32_t tile_words, bool payload) {
-    size_t s = (size_t)kRWarps * kRadixBins * 2 + 3 * kRadixBins * 4 + (size_t)tile_keys * 4 +
-               2 * (size_t)tile_words * 4;
-    if (payload) s += 2 * (size_t)tile_keys * 4;
-    return s;
+    size_t w = 2 * (size_t)(padw(tile_words) + 1) + padw(32 * kNT) + 1 + 2 * kRadixBins;
+    if (payload) w += 2 * (size_t)(padw(tile_keys) + 1);
+    return w * 4;
 }
 
 cudaError_t launch_digit_hist(const RadixArgs &a, cudaStream_t s) {
     if (a.ntiles == 0) return cudaSuccess;
-    k_digit_hist<<<a.ntiles, kRThreads, 12 * kRadixBins * 4, s>>>(a);
+    k_digit_hist<<<a.ntiles, kNT, 12 * kRadixBins * 4, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -293,11 +418,11 @@ cudaError_t launch_radix_pass(const RadixArgs &a, cudaStream_t s) {
     if (pay) {
         e = cudaFuncSetAttribute(k_radix_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        k_radix_pass<true><<<grid, kRThreads, smem, s>>>(a);
+        k_radix_pass<true><<<grid, kNT, smem, s>>>(a);
     } else {
         e = cudaFuncSetAttribute(k_radix_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        k_radix_pass<false><<<grid, kRThreads, smem, s>>>(a);
+        k_radix_pass<false><<<grid, kNT, smem, s>>>(a);
     }
     return cudaGetLastError();
 }

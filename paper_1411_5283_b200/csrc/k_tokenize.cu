@@ -1,10 +1,10 @@
 // k_tokenize.cu — phases 1 and 2 of the method (§3 Methodology, Pre-processing):
-//   K1 k_tokenize<false>  "removing / ignoring the special characters": find every maximal run of
+//   K1 k_tokenize<0>      "removing / ignoring the special characters": find every maximal run of
 //                         ASCII letters (reading A1) and count words per length, per CTA;
 //   K2 k_bucket_offsets   the per-length sub-array sizes "decided depending on a number of elements
 //                         with the same number of characters": length histogram,
 //                         exclusive prefix off[], per-(CTA, length) scatter bases;
-//   K3 k_tokenize<true>   re-tokenize, pack each word into its fixed-width key (the paper's
+//   K3 k_tokenize<1|2>    re-tokenize, pack each word into its fixed-width key (the paper's
 //                         "array char 3D") and scatter it, stably, into its length's
 //                         sub-array ("all shorter words come before longer words").
 //
@@ -42,8 +42,23 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
+// Pack letters [0, min(L,6)) of the word at sb[start] into one key word (letter j -> bits 29-5j..25-5j).
+__device__ __forceinline__ uint32_t pack6(const uint32_t *buf32, uint32_t boff, uint32_t L) {
+    const uint32_t a = boff >> 2, sh = 8u * (boff & 3u);
+    const uint32_t w0 = buf32[a], w1 = buf32[a + 1], w2 = buf32[a + 2];
+    const uint32_t lo = __funnelshift_r(w0, w1, sh) & 0x1f1f1f1fu;   // codes of letters 0..3
+    const uint32_t hi = __funnelshift_r(w1, w2, sh) & 0x00001f1fu;   // codes of letters 4..5
+    const uint32_t r = __byte_perm(lo, 0, 0x0123);                   // letter 0 in the top byte
+    const uint32_t t1 = (r & 0x001f001fu) | ((r & 0x1f001f00u) >> 3);
+    const uint32_t t2 = (t1 & 0x3ffu) | ((t1 >> 16) << 10);           // 4 letters, 20 bits
+    const uint32_t u = ((hi & 0x1fu) << 5) | (hi >> 8);                // letters 4, 5
+    uint32_t key = (t2 << 10) | u;
+    if (L < 6) key &= ~((1u << (5u * (6u - L))) - 1u);
+    return key;
+}
+
 struct TkCommon {
-    uint4 buf[kTkBuf / 16];
+    uint4 buf[kTkBuf / 16 + 1];   // +16 B slack: key packing reads whole 32-bit words
     uint16_t sstart[kTkMaxWords];
     uint16_t send[kTkMaxWords + 2];
     uint32_t warp_tot[kTkThreads / 32];
@@ -127,15 +142,19 @@ __device__ __forceinline__ uint32_t stage_step(TkCommon &sm, const uint8_t *__re
     return S;
 }
 
-template <bool kScatter>
-struct SmemOf { using type = TkCountSmem; };
+// kMode: 0 = K1 count; 1 = K3 scatter, any order within a (CTA, length) run (keys only: the sort
+// that follows fixes the order of distinct keys, and equal keys are identical words);
+// 2 = K3 scatter, stable (text order within each length; needed for the src_off payload).
+template <int kMode>
+struct SmemOf { using type = TkScatterSmem; };
 template <>
-struct SmemOf<true> { using type = TkScatterSmem; };
+struct SmemOf<0> { using type = TkCountSmem; };
 
-template <bool kScatter>
+template <int kMode>
 __global__ void __launch_bounds__(kTkThreads) k_tokenize(TkArgs a) {
+    constexpr bool kScatter = kMode != 0;
     extern __shared__ __align__(16) uint8_t tk_smem[];
-    auto &sm = *reinterpret_cast<typename SmemOf<kScatter>::type *>(tk_smem);
+    auto &sm = *reinterpret_cast<typename SmemOf<kMode>::type *>(tk_smem);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t c = blockIdx.x;
     const uint32_t st0 = c * a.steps_per_cta;
@@ -156,14 +175,20 @@ __global__ void __launch_bounds__(kTkThreads) k_tokenize(TkArgs a) {
         const uint32_t S = stage_step(sm.c, a.text, s0);
         const uint32_t skip = sm.c.skip;
         if constexpr (!kScatter) {
-            for (uint32_t base = 0; base < S; base += kTkThreads) {
-                uint32_t k = base + t;
-                uint32_t L = 0;
-                if (k < S) L = min((uint32_t)sm.c.send[k + skip] - sm.c.sstart[k] + 1u, 256u);
-                uint32_t peers = __match_any_sync(kFull, L);
-                if (k < S && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[L], __popc(peers));
-            }
+            for (uint32_t k = t; k < S; k += kTkThreads)
+                atomicAdd(&sm.hist[min((uint32_t)sm.c.send[k + skip] - sm.c.sstart[k] + 1u, 256u)], 1u);
             __syncthreads();   // lists are rewritten by the next step
+        } else if constexpr (kMode == 1) {
+            const uint32_t *buf32 = reinterpret_cast<const uint32_t *>(sm.c.buf);
+            for (uint32_t k = t; k < S; k += kTkThreads) {
+                const uint32_t start = sm.c.sstart[k];
+                const uint32_t L = (uint32_t)sm.c.send[k + skip] - start + 1u;
+                const uint32_t idx = atomicAdd(&sm.run[L], 1u);
+                const uint32_t kw = (L + 5) / 6;
+                uint32_t *dst = a.keys + sm.key_off[L] + (uint64_t)idx * kw;
+                for (uint32_t q = 0; q < kw; q++) dst[q] = pack6(buf32, kTkPre + start + 6 * q, L - 6 * q);
+            }
+            __syncthreads();
         } else {
             // Phase A: warp w ranks words [kb, ke) by length, in text order (stable).
             const uint32_t kb = (S * warp) / (kTkThreads / 32), ke = (S * (warp + 1)) / (kTkThreads / 32);
@@ -200,17 +225,8 @@ __global__ void __launch_bounds__(kTkThreads) k_tokenize(TkArgs a) {
                 uint32_t start = sm.c.sstart[k];
                 const uint32_t kw = (L + 5) / 6;
                 uint32_t *dst = a.keys + sm.key_off[L] + (uint64_t)idx * kw;
-                const uint8_t *wp = sb + start;
-                for (uint32_t q = 0; q < kw; q++) {
-                    uint32_t word = 0;
-#pragma unroll
-                    for (int j = 0; j < 6; j++) {
-                        uint32_t li = q * 6 + j;
-                        uint32_t code = li < L ? (wp[li] & 31u) : 0u;
-                        word |= code << (25 - 5 * j);
-                    }
-                    dst[q] = word;
-                }
+                const uint32_t *buf32 = reinterpret_cast<const uint32_t *>(sm.c.buf);
+                for (uint32_t q = 0; q < kw; q++) dst[q] = pack6(buf32, kTkPre + start + 6 * q, L - 6 * q);
                 if (a.payload) a.payload[sm.word_off[L] + idx] = (uint32_t)(s0 + start);
             }
             __syncthreads();
@@ -282,7 +298,7 @@ __global__ void __launch_bounds__(256) k_bucket_offsets(TkArgs a, Summary *sum) 
 
 cudaError_t launch_tokenize_count(const TkArgs &a, cudaStream_t s) {
     if (a.grid == 0) return cudaSuccess;
-    k_tokenize<false><<<a.grid, kTkThreads, sizeof(TkCountSmem), s>>>(a);
+    k_tokenize<0><<<a.grid, kTkThreads, sizeof(TkCountSmem), s>>>(a);
     return cudaGetLastError();
 }
 
@@ -293,10 +309,16 @@ cudaError_t launch_bucket_offsets(const TkArgs &a, Summary *d_sum, cudaStream_t 
 
 cudaError_t launch_pack_scatter(const TkArgs &a, cudaStream_t s) {
     if (a.grid == 0) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_tokenize<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(TkScatterSmem));
-    if (e != cudaSuccess) return e;
-    k_tokenize<true><<<a.grid, kTkThreads, sizeof(TkScatterSmem), s>>>(a);
+    cudaError_t e;
+    if (a.payload) {
+        e = cudaFuncSetAttribute(k_tokenize<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TkScatterSmem));
+        if (e != cudaSuccess) return e;
+        k_tokenize<2><<<a.grid, kTkThreads, sizeof(TkScatterSmem), s>>>(a);
+    } else {
+        e = cudaFuncSetAttribute(k_tokenize<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TkScatterSmem));
+        if (e != cudaSuccess) return e;
+        k_tokenize<1><<<a.grid, kTkThreads, sizeof(TkScatterSmem), s>>>(a);
+    }
     return cudaGetLastError();
 }
 
