@@ -66,33 +66,52 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *wsum, 
     return r;
 }
 
-// In-place exclusive scan of the 32 x kNT thread-private counters in (bin, thread) order.
-// Thread t owns the 32 consecutive linear entries [32t, 32t+32).
+// Thread-private 16-bit counters: 32 bins x kNT threads, linear index j = bin * kNT + thread, held
+// as u16 pairs with one pad word per 32 words (conflict-free for both access patterns below).
+__device__ __forceinline__ uint16_t *cnt_at(uint32_t *cnt, uint32_t f, uint32_t t) {
+    const uint32_t j = f * kNT + t;
+    return reinterpret_cast<uint16_t *>(cnt + (j >> 1) + (j >> 6)) + (j & 1u);
+}
+constexpr uint32_t kCntWords = 32 * kNT / 2 + 32 * kNT / 64;
+
+// In-place exclusive scan of the counters in (bin, thread) order. Thread t owns linear entries
+// [32t, 32t+32) = the 16 words starting at 16t + t/2.
 __device__ __forceinline__ void scan_counters(uint32_t *cnt, uint32_t *wsum) {
     const int t = threadIdx.x;
-    uint32_t *c = cnt + padw(32 * t);   // the 32 entries are contiguous after padding (33t .. 33t+31)
+    uint32_t *c = cnt + 16 * t + (t >> 1);
     uint32_t s = 0;
 #pragma unroll
-    for (int i = 0; i < 32; i++) s += c[i];
+    for (int i = 0; i < 16; i++) {
+        const uint32_t x = c[i];
+        s += (x & 0xffffu) + (x >> 16);
+    }
     uint32_t run = block_excl_scan(s, wsum, nullptr);
 #pragma unroll
-    for (int i = 0; i < 32; i++) {
-        const uint32_t v = c[i];
-        c[i] = run;
-        run += v;
+    for (int i = 0; i < 16; i++) {
+        const uint32_t x = c[i];
+        const uint32_t lo = run;
+        run += x & 0xffffu;
+        c[i] = lo | (run << 16);
+        run += x >> 16;
     }
 }
 
+__device__ __forceinline__ void zero_counters(uint32_t *cnt) {
+#pragma unroll
+    for (int f = 0; f < 32; f++) *cnt_at(cnt, f, threadIdx.x) = 0;
+}
+
 struct RSmem {
-    uint32_t *A, *B;          // padded key buffers (tile words)
+    uint32_t *A, *B;          // padded key buffers (tile words); B == A on the register path
     uint32_t *PA, *PB;        // padded payload buffers (tile keys)
-    uint32_t *cnt;            // padded [32][kNT] counters
-    uint32_t *hist;           // [1024] tile digit counts, then tile-local start of each digit
+    uint32_t *cnt;            // kCntWords: 32 x kNT u16 counters
+    uint32_t *hist;           // [1024] tile digit counts
     uint32_t *gofs;           // [1024] global destination - tile-local position
     uint32_t *wsum;           // [kNW + 1]
 };
 
-// One tile of one bucket. KW > 0: compile-time key width with keys in registers; KW == 0: runtime.
+// One tile of one bucket. KW in {1,2}: keys in registers, one smem key buffer;
+// KW == 0: runtime key width, two smem key buffers.
 template <int KW, bool kPay>
 __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo &b, uint32_t j, uint32_t tile,
                                            const RSmem &s) {
@@ -104,19 +123,20 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
     const uint32_t k0 = tile * b.tile_keys;
     const uint32_t nk = min(b.tile_keys, b.n - k0);
     constexpr int RK = KW ? 32 / KW : 1;   // register keys per thread
+    uint32_t *const A = s.A;
+    uint32_t *const B = KW ? s.A : s.B;
 
     for (uint32_t i = t; i < kRadixBins; i += kNT) s.hist[i] = 0;
     {
         const uint32_t *src = a.kin + b.key_off + (uint64_t)k0 * kw;
         const uint32_t nw = nk * kw, tw = T * kw;
-        for (uint32_t i = t; i < tw; i += kNT) s.A[padw(i)] = i < nw ? __ldg(src + i) : kSentinel;
+        for (uint32_t i = t; i < tw; i += kNT) A[padw(i)] = i < nw ? __ldg(src + i) : kSentinel;
         if constexpr (kPay) {
             const uint32_t *ps = a.pin + b.word_off + k0;
             for (uint32_t i = t; i < T; i += kNT) s.PA[padw(i)] = i < nk ? __ldg(ps + i) : 0u;
         }
     }
-#pragma unroll
-    for (int f = 0; f < 32; f++) s.cnt[padw(f * kNT + t)] = 0;
+    zero_counters(s.cnt);
     __syncthreads();
 
     uint32_t key[RK][KW ? KW : 1];
@@ -124,28 +144,25 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
     uint32_t c4[4];
 
     // ---- sub-pass 1: low 5 bits (second letter of the pair); also the 10-bit tile histogram ----
-    {
 #pragma unroll
-        for (int i = 0; i < (RK + 3) / 4; i++) rk[i] = 0;
+    for (int i = 0; i < (RK + 3) / 4; i++) rk[i] = 0;
 #pragma unroll
-        for (uint32_t k = 0; k < KPT; k++) {
-            const uint32_t idx = t * KPT + k;
-            uint32_t w;
-            if constexpr (KW > 0) {
+    for (uint32_t k = 0; k < KPT; k++) {
+        const uint32_t idx = t * KPT + k;
+        uint32_t w;
+        if constexpr (KW > 0) {
 #pragma unroll
-                for (int u = 0; u < KW; u++) key[k % RK][u] = s.A[padw(idx * KW + u)];
-                w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
-            } else {
-                w = s.A[padw(idx * kw + wi)];
-            }
-            const uint32_t d = digit_of(w, sh);
-            const uint32_t f = d & 31u;
-            uint32_t *cp = s.cnt + padw(f * kNT + t);
-            const uint32_t c = *cp;
-            *cp = c + 1;
-            if constexpr (KW > 0) rk[k / 4] |= c << (8 * (k % 4));
-            atomicAdd(&s.hist[d], 1u);
+            for (int u = 0; u < KW; u++) key[k % RK][u] = A[padw(idx * KW + u)];
+            w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
+        } else {
+            w = A[padw(idx * kw + wi)];
         }
+        const uint32_t d = digit_of(w, sh);
+        uint16_t *cp = cnt_at(s.cnt, d & 31u, t);
+        const uint32_t c = *cp;
+        *cp = (uint16_t)(c + 1);
+        if constexpr (KW > 0) rk[k / 4] |= c << (8 * (k % 4));
+        atomicAdd(&s.hist[d], 1u);
     }
     __syncthreads();
     // publish this tile's digit counts (aggregate) as early as possible
@@ -158,63 +175,51 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
     }
     scan_counters(s.cnt, s.wsum);
     __syncthreads();
-    // scatter A -> B by the low field
+    // scatter A -> B by the low field (register path: every key is in registers, B == A)
 #pragma unroll
     for (uint32_t k = 0; k < KPT; k++) {
         const uint32_t idx = t * KPT + k;
-        uint32_t w, r = 0;
-        if constexpr (KW > 0) {
-            w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
-            r = (rk[k / 4] >> (8 * (k % 4))) & 255u;
-        } else {
-            w = s.A[padw(idx * kw + wi)];
-        }
-        const uint32_t f = digit_of(w, sh) & 31u;
         uint32_t pos;
         if constexpr (KW > 0) {
-            pos = s.cnt[padw(f * kNT + t)] + r;
+            const uint32_t w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
+            pos = *cnt_at(s.cnt, digit_of(w, sh) & 31u, t) + ((rk[k / 4] >> (8 * (k % 4))) & 255u);
 #pragma unroll
-            for (int u = 0; u < KW; u++) s.B[padw(pos * KW + u)] = key[k % RK][u];
+            for (int u = 0; u < KW; u++) B[padw(pos * KW + u)] = key[k % RK][u];
         } else {
-            uint32_t *cp = s.cnt + padw(f * kNT + t);   // runtime path: rank by re-counting
+            uint16_t *cp = cnt_at(s.cnt, digit_of(A[padw(idx * kw + wi)], sh) & 31u, t);   // re-count
             pos = *cp;
-            *cp = pos + 1;
-            for (uint32_t u = 0; u < kw; u++) s.B[padw(pos * kw + u)] = s.A[padw(idx * kw + u)];
+            *cp = (uint16_t)(pos + 1);
+            for (uint32_t u = 0; u < kw; u++) B[padw(pos * kw + u)] = A[padw(idx * kw + u)];
         }
         if constexpr (kPay) s.PB[padw(pos)] = s.PA[padw(idx)];
     }
     __syncthreads();
 
     // ---- sub-pass 2: high 5 bits (first letter of the pair) ----
+    zero_counters(s.cnt);
 #pragma unroll
-    for (int f = 0; f < 32; f++) s.cnt[padw(f * kNT + t)] = 0;
-    {
+    for (int i = 0; i < (RK + 3) / 4; i++) rk[i] = 0;
 #pragma unroll
-        for (int i = 0; i < (RK + 3) / 4; i++) rk[i] = 0;
+    for (uint32_t k = 0; k < KPT; k++) {
+        const uint32_t idx = t * KPT + k;
+        uint32_t w;
+        if constexpr (KW > 0) {
 #pragma unroll
-        for (uint32_t k = 0; k < KPT; k++) {
-            const uint32_t idx = t * KPT + k;
-            uint32_t w;
-            if constexpr (KW > 0) {
-#pragma unroll
-                for (int u = 0; u < KW; u++) key[k % RK][u] = s.B[padw(idx * KW + u)];
-                w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
-            } else {
-                w = s.B[padw(idx * kw + wi)];
-            }
-            const uint32_t f = digit_of(w, sh) >> 5;
-            uint32_t *cp = s.cnt + padw(f * kNT + t);
-            const uint32_t c = *cp;
-            *cp = c + 1;
-            if constexpr (KW > 0) rk[k / 4] |= c << (8 * (k % 4));
+            for (int u = 0; u < KW; u++) key[k % RK][u] = B[padw(idx * KW + u)];
+            w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
+        } else {
+            w = B[padw(idx * kw + wi)];
         }
+        uint16_t *cp = cnt_at(s.cnt, digit_of(w, sh) >> 5, t);
+        const uint32_t c = *cp;
+        *cp = (uint16_t)(c + 1);
+        if constexpr (KW > 0) rk[k / 4] |= c << (8 * (k % 4));
     }
     __syncthreads();
     scan_counters(s.cnt, s.wsum);
-    // tile-local start of every digit (exclusive scan of the counts over digits)
     {
-        const uint32_t s4 = c4[0] + c4[1] + c4[2] + c4[3];
-        uint32_t ex = block_excl_scan(s4, s.wsum, nullptr);
+        // tile-local start of every digit (exclusive scan of the counts over digits)
+        uint32_t ex = block_excl_scan(c4[0] + c4[1] + c4[2] + c4[3], s.wsum, nullptr);
         // decoupled look-back over the preceding tiles of this bucket, 4 digits per thread
         uint32_t pre[4] = {0, 0, 0, 0};
         if (tile != 0) {
@@ -225,10 +230,7 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
                 uint32_t v[4];
 #pragma unroll
                 for (int e = 0; e < 4; e++) v[e] = (done >> e) & 1u ? 1u : ld_relaxed(sp + e);
-                bool ready = true;
-#pragma unroll
-                for (int e = 0; e < 4; e++) ready &= v[e] != 0u;
-                if (!ready) continue;
+                if (!(v[0] && v[1] && v[2] && v[3])) continue;
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
                     if ((done >> e) & 1u) continue;
@@ -260,16 +262,14 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
         uint32_t pos;
         if constexpr (KW > 0) {
             const uint32_t w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
-            const uint32_t f = digit_of(w, sh) >> 5;
-            pos = s.cnt[padw(f * kNT + t)] + ((rk[k / 4] >> (8 * (k % 4))) & 255u);
+            pos = *cnt_at(s.cnt, digit_of(w, sh) >> 5, t) + ((rk[k / 4] >> (8 * (k % 4))) & 255u);
 #pragma unroll
-            for (int u = 0; u < KW; u++) s.A[padw(pos * KW + u)] = key[k % RK][u];
+            for (int u = 0; u < KW; u++) A[padw(pos * KW + u)] = key[k % RK][u];
         } else {
-            const uint32_t f = digit_of(s.B[padw(idx * kw + wi)], sh) >> 5;
-            uint32_t *cp = s.cnt + padw(f * kNT + t);
+            uint16_t *cp = cnt_at(s.cnt, digit_of(B[padw(idx * kw + wi)], sh) >> 5, t);
             pos = *cp;
-            *cp = pos + 1;
-            for (uint32_t u = 0; u < kw; u++) s.A[padw(pos * kw + u)] = s.B[padw(idx * kw + u)];
+            *cp = (uint16_t)(pos + 1);
+            for (uint32_t u = 0; u < kw; u++) A[padw(pos * kw + u)] = B[padw(idx * kw + u)];
         }
         if constexpr (kPay) s.PA[padw(pos)] = s.PB[padw(idx)];
     }
@@ -279,28 +279,30 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
     uint32_t *dst = a.kout + b.key_off;
     if constexpr (KW == 1) {
         for (uint32_t i = t; i < nk; i += kNT) {
-            const uint32_t w = s.A[padw(i)];
+            const uint32_t w = A[padw(i)];
             dst[s.gofs[digit_of(w, sh)] + i] = w;
         }
     } else {
         const uint32_t nw = nk * kw;
         for (uint32_t i = t; i < nw; i += kNT) {
             const uint32_t k = i / kw, u = i - k * kw;
-            const uint32_t d = digit_of(s.A[padw(k * kw + wi)], sh);
-            dst[(uint64_t)(s.gofs[d] + k) * kw + u] = s.A[padw(i)];
+            const uint32_t d = digit_of(A[padw(k * kw + wi)], sh);
+            dst[(uint64_t)(s.gofs[d] + k) * kw + u] = A[padw(i)];
         }
     }
     if constexpr (kPay) {
         uint32_t *pd = a.pout + b.word_off;
         for (uint32_t i = t; i < nk; i += kNT) {
-            const uint32_t d = digit_of(s.A[padw(i * kw + wi)], sh);
+            const uint32_t d = digit_of(A[padw(i * kw + wi)], sh);
             pd[s.gofs[d] + i] = s.PA[padw(i)];
         }
     }
 }
 
-template <bool kPay>
-__global__ void __launch_bounds__(kNT, 2) k_radix_pass(RadixArgs a) {
+// kGeneric = false: tiles of buckets with kw in {1, 2} (register path, one key buffer);
+// kGeneric = true: tiles of buckets with kw >= 3.
+template <bool kGeneric, bool kPay>
+__global__ void __launch_bounds__(kNT, kGeneric ? 1 : (kPay ? 1 : 3)) k_radix_pass(RadixArgs a) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_ticket;
     __shared__ uint32_t s_wsum[kNW + 1];
@@ -317,16 +319,19 @@ __global__ void __launch_bounds__(kNT, 2) k_radix_pass(RadixArgs a) {
     RSmem s;
     const uint32_t tw = padw(a.max_tile_words) + 1, tk = padw(a.max_tile_keys) + 1;
     s.A = smem;
-    s.B = s.A + tw;
+    s.B = s.A + (kGeneric ? tw : 0);
     s.cnt = s.B + tw;
-    s.hist = s.cnt + padw(32 * kNT) + 1;
+    s.hist = s.cnt + kCntWords;
     s.gofs = s.hist + kRadixBins;
     s.PA = s.gofs + kRadixBins;
     s.PB = s.PA + (kPay ? tk : 0);
     s.wsum = s_wsum;
-    if (b.kw == 1) radix_tile<1, kPay>(a, b, j, td.tile, s);
-    else if (b.kw == 2) radix_tile<2, kPay>(a, b, j, td.tile, s);
-    else radix_tile<0, kPay>(a, b, j, td.tile, s);
+    if constexpr (kGeneric) {
+        radix_tile<0, kPay>(a, b, j, td.tile, s);
+    } else {
+        if (b.kw == 1) radix_tile<1, kPay>(a, b, j, td.tile, s);
+        else radix_tile<2, kPay>(a, b, j, td.tile, s);
+    }
 }
 
 // Histogram of every digit of every key of one tile (all passes at once), smem atomics.
@@ -391,8 +396,8 @@ __global__ void __launch_bounds__(1024) k_digit_scan(uint32_t *dh) {
 
 }  // namespace
 
-size_t radix_pass_smem(uint32_t tile_keys, uint32_t tile_words, bool payload) {
-    size_t w = 2 * (size_t)(padw(tile_words) + 1) + padw(32 * kNT) + 1 + 2 * kRadixBins;
+size_t radix_pass_smem(uint32_t tile_keys, uint32_t tile_words, bool payload, bool generic) {
+    size_t w = (generic ? 2 : 1) * (size_t)(padw(tile_words) + 1) + kCntWords + 2 * kRadixBins;
     if (payload) w += 2 * (size_t)(padw(tile_keys) + 1);
     return w * 4;
 }
@@ -409,22 +414,21 @@ cudaError_t launch_digit_scan(uint32_t *dh, uint32_t rows, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_radix_pass(const RadixArgs &a, cudaStream_t s) {
+template <bool G, bool P>
+static cudaError_t launch_pass_t(const RadixArgs &a, uint32_t grid, cudaStream_t s) {
+    const size_t smem = radix_pass_smem(a.max_tile_keys, a.max_tile_words, P, G);
+    cudaError_t e = cudaFuncSetAttribute(k_radix_pass<G, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_radix_pass<G, P><<<grid, kNT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_radix_pass(const RadixArgs &a, bool generic, cudaStream_t s) {
     const uint32_t grid = a.ntiles > a.nzero ? a.ntiles : a.nzero;
     if (grid == 0) return cudaSuccess;
     const bool pay = a.pin != nullptr;
-    const size_t smem = radix_pass_smem(a.max_tile_keys, a.max_tile_words, pay);
-    cudaError_t e;
-    if (pay) {
-        e = cudaFuncSetAttribute(k_radix_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k_radix_pass<true><<<grid, kNT, smem, s>>>(a);
-    } else {
-        e = cudaFuncSetAttribute(k_radix_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k_radix_pass<false><<<grid, kNT, smem, s>>>(a);
-    }
-    return cudaGetLastError();
+    if (generic) return pay ? launch_pass_t<true, true>(a, grid, s) : launch_pass_t<true, false>(a, grid, s);
+    return pay ? launch_pass_t<false, true>(a, grid, s) : launch_pass_t<false, false>(a, grid, s);
 }
 
 }  // namespace wsort

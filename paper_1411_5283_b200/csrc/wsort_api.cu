@@ -67,7 +67,6 @@ struct wsort_ctx {
 
     // sort
     DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan;
-    size_t status_bytes_clean = 0;   // both status buffers are zero over this prefix
     std::vector<uint8_t> hplan;
     uint8_t *h_plan_pinned = nullptr;
     size_t h_plan_cap = 0;
@@ -361,13 +360,16 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
 
 namespace {
 
-// Plan layout (one H2D copy): BucketInfo[256] | radix tiles of every pass | emit tiles.
+// Plan layout (one H2D copy): BucketInfo[256] | radix tiles of every pass (class 0 then class 1)
+// | emit tiles. Radix tile classes: 0 = buckets with kw <= 2 (register path), 1 = kw >= 3.
 struct SortPlan {
     std::vector<BucketInfo> bk;
-    std::vector<std::vector<TileDesc>> pass_tiles;
-    std::vector<uint32_t> pass_tile_keys, pass_tile_words;
+    std::vector<std::vector<TileDesc>> tiles[2];            // [class][pass]
+    std::vector<uint32_t> tile_keys[2], tile_words[2];      // [class][pass] maxima
+    std::vector<double> bytes[2];                           // [class][pass] algorithmic bytes
     std::vector<TileDesc> emit_tiles;
     uint32_t dh_rows = 0;
+    uint32_t npasses = 0;
 };
 
 int sort_radix(wsort_ctx *c, bool want_src) {
@@ -375,7 +377,6 @@ int sort_radix(wsort_ctx *c, bool want_src) {
     const uint32_t lmax = s.max_len;
     SortPlan P;
     P.bk.assign(256, BucketInfo{});
-    uint32_t npasses = 0;
     for (uint32_t L = 1; L <= lmax; L++) {
         BucketInfo &b = P.bk[L];
         b.key_off = s.key_off[L];
@@ -389,19 +390,25 @@ int sort_radix(wsort_ctx *c, bool want_src) {
         b.dh_row = P.dh_rows;
         P.dh_rows += b.ndig;
         b.final_b = b.ndig & 1u;
-        npasses = std::max(npasses, b.ndig);
+        P.npasses = std::max(P.npasses, b.ndig);
     }
-    P.pass_tiles.resize(npasses);
-    P.pass_tile_keys.assign(npasses, 0);
-    P.pass_tile_words.assign(npasses, 0);
+    const uint32_t npasses = P.npasses;
+    for (int cl = 0; cl < 2; cl++) {
+        P.tiles[cl].resize(npasses);
+        P.tile_keys[cl].assign(npasses, 0);
+        P.tile_words[cl].assign(npasses, 0);
+        P.bytes[cl].assign(npasses, 0.0);
+    }
     for (uint32_t p = 0; p < npasses; p++) {
         for (uint32_t L = 1; L <= lmax; L++) {
             const BucketInfo &b = P.bk[L];
             if (!b.n || b.ndig <= p) continue;
+            const int cl = b.kw <= 2 ? 0 : 1;
             uint32_t nt = (b.n + b.tile_keys - 1) / b.tile_keys;
-            for (uint32_t i = 0; i < nt; i++) P.pass_tiles[p].push_back(TileDesc{L, i});
-            P.pass_tile_keys[p] = std::max(P.pass_tile_keys[p], b.tile_keys);
-            P.pass_tile_words[p] = std::max(P.pass_tile_words[p], b.tile_keys * b.kw);
+            for (uint32_t i = 0; i < nt; i++) P.tiles[cl][p].push_back(TileDesc{L, i});
+            P.tile_keys[cl][p] = std::max(P.tile_keys[cl][p], b.tile_keys);
+            P.tile_words[cl][p] = std::max(P.tile_words[cl][p], b.tile_keys * b.kw);
+            P.bytes[cl][p] += 2.0 * (double)b.n * (b.kw * 4 + (want_src ? 4 : 0));
         }
     }
     for (uint32_t L = 1; L <= lmax; L++) {
@@ -425,26 +432,30 @@ int sort_radix(wsort_ctx *c, bool want_src) {
     }
     if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
     if ((rc = ensure(c, c->dh, (size_t)std::max<uint32_t>(P.dh_rows, 1) * kRadixBins * 4, "dh"))) return rc;
-    size_t max_tiles = 0;
-    for (auto &v : P.pass_tiles) max_tiles = std::max(max_tiles, v.size());
-    const size_t status_bytes = std::max<size_t>(max_tiles, 1) * kRadixBins * 4;
+    size_t rows[2] = {0, 0};   // status rows per class: max tiles over passes
+    for (int cl = 0; cl < 2; cl++)
+        for (auto &v : P.tiles[cl]) rows[cl] = std::max(rows[cl], v.size());
+    const size_t status_bytes = std::max<size_t>(rows[0] + rows[1], 1) * kRadixBins * 4;
     if (c->status0.cap < status_bytes || c->status1.cap < status_bytes) {
-        if ((rc = ensure(c, c->status0, status_bytes, "status0", true))) return rc;
-        if ((rc = ensure(c, c->status1, status_bytes, "status1", true))) return rc;
+        if ((rc = ensure(c, c->status0, status_bytes, "status0"))) return rc;
+        if ((rc = ensure(c, c->status1, status_bytes, "status1"))) return rc;
         CK(cudaMemsetAsync(c->status0.p, 0, c->status0.cap, c->stream), "memset status0");
         CK(cudaMemsetAsync(c->status1.p, 0, c->status1.cap, c->stream), "memset status1");
     }
-    if ((rc = ensure(c, c->tickets, std::max<uint32_t>(npasses, 1) * 4, "tickets"))) return rc;
+    if ((rc = ensure(c, c->tickets, std::max<uint32_t>(2 * npasses, 1) * 4, "tickets"))) return rc;
 
     // ---- plan upload ----
-    size_t off_tiles = 256 * sizeof(BucketInfo);
-    std::vector<size_t> pass_off(npasses);
+    const size_t off_tiles = 256 * sizeof(BucketInfo);
+    std::vector<size_t> toff[2];
+    toff[0].resize(npasses);
+    toff[1].resize(npasses);
     size_t cur = off_tiles;
-    for (uint32_t p = 0; p < npasses; p++) {
-        pass_off[p] = cur;
-        cur += P.pass_tiles[p].size() * sizeof(TileDesc);
-    }
-    size_t emit_off = cur;
+    for (uint32_t p = 0; p < npasses; p++)
+        for (int cl = 0; cl < 2; cl++) {
+            toff[cl][p] = cur;
+            cur += P.tiles[cl][p].size() * sizeof(TileDesc);
+        }
+    const size_t emit_off = cur;
     cur += P.emit_tiles.size() * sizeof(TileDesc);
     const size_t plan_bytes = cur;
     if (c->h_plan_cap < plan_bytes) {
@@ -460,7 +471,8 @@ int sort_radix(wsort_ctx *c, bool want_src) {
     uint8_t *hp = c->h_plan_pinned;
     memcpy(hp, P.bk.data(), off_tiles);
     for (uint32_t p = 0; p < npasses; p++)
-        memcpy(hp + pass_off[p], P.pass_tiles[p].data(), P.pass_tiles[p].size() * sizeof(TileDesc));
+        for (int cl = 0; cl < 2; cl++)
+            memcpy(hp + toff[cl][p], P.tiles[cl][p].data(), P.tiles[cl][p].size() * sizeof(TileDesc));
     memcpy(hp + emit_off, P.emit_tiles.data(), P.emit_tiles.size() * sizeof(TileDesc));
     if ((rc = ensure(c, c->plan, plan_bytes, "plan"))) return rc;
     CK(cudaMemcpyAsync(c->plan.p, hp, plan_bytes, cudaMemcpyHostToDevice, c->stream), "plan upload");
@@ -482,12 +494,12 @@ int sort_radix(wsort_ctx *c, bool want_src) {
 
     if (npasses) {
         CK(cudaMemsetAsync(c->dh.p, 0, (size_t)P.dh_rows * kRadixBins * 4, c->stream), "memset dh");
-        CK(cudaMemsetAsync(c->tickets.p, 0, npasses * 4, c->stream), "memset tickets");
+        CK(cudaMemsetAsync(c->tickets.p, 0, 2 * npasses * 4, c->stream), "memset tickets");
         uint32_t *dh = static_cast<uint32_t *>(c->dh.p);
         RadixArgs ra{};
         ra.buckets = d_bk;
-        ra.tiles = reinterpret_cast<const TileDesc *>(dp + pass_off[0]);
-        ra.ntiles = (uint32_t)P.pass_tiles[0].size();
+        ra.tiles = reinterpret_cast<const TileDesc *>(dp + toff[0][0]);   // pass 0, both classes
+        ra.ntiles = (uint32_t)(P.tiles[0][0].size() + P.tiles[1][0].size());
         ra.kin = ka;
         ra.dh = dh;
         rc = launch(c, "k4_digit_hist", key_bytes, [&] { return launch_digit_hist(ra, c->stream); });
@@ -496,34 +508,41 @@ int sort_radix(wsort_ctx *c, bool want_src) {
                     [&] { return launch_digit_scan(dh, P.dh_rows, c->stream); });
         if (rc) return rc;
         uint32_t *st[2] = {static_cast<uint32_t *>(c->status0.p), static_cast<uint32_t *>(c->status1.p)};
+        uint32_t last[2] = {0, 0};   // last pass with tiles, per class
         for (uint32_t p = 0; p < npasses; p++) {
-            RadixArgs r{};
-            r.buckets = d_bk;
-            r.tiles = reinterpret_cast<const TileDesc *>(dp + pass_off[p]);
-            r.ntiles = (uint32_t)P.pass_tiles[p].size();
-            r.nzero = p ? (uint32_t)P.pass_tiles[p - 1].size() : 0u;
-            r.pass = p;
-            r.max_tile_keys = P.pass_tile_keys[p];
-            r.max_tile_words = P.pass_tile_words[p];
-            const bool even = (p & 1u) == 0;
-            r.kin = even ? ka : kb;
-            r.kout = even ? kb : ka;
-            r.pin = want_src ? (even ? pa : pb) : nullptr;
-            r.pout = want_src ? (even ? pb : pa) : nullptr;
-            r.dh = dh;
-            r.status = st[p & 1u];
-            r.status_other = st[(p + 1) & 1u];
-            r.ticket = static_cast<uint32_t *>(c->tickets.p) + p;
-            double act_bytes = 0;
-            for (uint32_t L = 1; L <= lmax; L++)
-                if (P.bk[L].n && P.bk[L].ndig > p)
-                    act_bytes += 2.0 * (double)P.bk[L].n * (P.bk[L].kw * 4 + (want_src ? 4 : 0));
-            rc = launch(c, "k4_radix_pass", act_bytes, [&] { return launch_radix_pass(r, c->stream); });
-            if (rc) return rc;
+            for (int cl = 0; cl < 2; cl++) {
+                const size_t base = cl ? rows[0] * kRadixBins : 0;
+                RadixArgs r{};
+                r.buckets = d_bk;
+                r.tiles = reinterpret_cast<const TileDesc *>(dp + toff[cl][p]);
+                r.ntiles = (uint32_t)P.tiles[cl][p].size();
+                r.nzero = p ? (uint32_t)P.tiles[cl][p - 1].size() : 0u;
+                if (!r.ntiles && !r.nzero) continue;
+                if (r.ntiles) last[cl] = p;
+                r.pass = p;
+                r.max_tile_keys = std::max<uint32_t>(P.tile_keys[cl][p], 32);
+                r.max_tile_words = std::max<uint32_t>(P.tile_words[cl][p], 32);
+                const bool even = (p & 1u) == 0;
+                r.kin = even ? ka : kb;
+                r.kout = even ? kb : ka;
+                r.pin = want_src ? (even ? pa : pb) : nullptr;
+                r.pout = want_src ? (even ? pb : pa) : nullptr;
+                r.dh = dh;
+                r.status = st[p & 1u] + base;
+                r.status_other = st[(p + 1) & 1u] + base;
+                r.ticket = static_cast<uint32_t *>(c->tickets.p) + 2 * p + cl;
+                rc = launch(c, cl ? "k4_radix_pass_long" : "k4_radix_pass", P.bytes[cl][p],
+                            [&] { return launch_radix_pass(r, cl == 1, c->stream); });
+                if (rc) return rc;
+            }
         }
         // leave both status buffers clean for the next sort
-        CK(cudaMemsetAsync(st[(npasses - 1) & 1u], 0, P.pass_tiles[npasses - 1].size() * kRadixBins * 4, c->stream),
-           "memset status");
+        for (int cl = 0; cl < 2; cl++) {
+            const size_t n = P.tiles[cl][last[cl]].size();
+            if (n)
+                CK(cudaMemsetAsync(st[last[cl] & 1u] + (cl ? rows[0] * kRadixBins : 0), 0, n * kRadixBins * 4,
+                                   c->stream), "memset status");
+        }
     }
 
     EmitArgs ea{};
