@@ -68,11 +68,12 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *wsum, 
 
 // Thread-private 16-bit counters: 32 bins x kNT threads, linear index j = bin * kNT + thread, held
 // as u16 pairs with one pad word per 32 words (conflict-free for both access patterns below).
-__device__ __forceinline__ uint16_t *cnt_at(uint32_t *cnt, uint32_t f, uint32_t t) {
-    const uint32_t j = f * kNT + t;
-    return reinterpret_cast<uint16_t *>(cnt + (j >> 1) + (j >> 6)) + (j & 1u);
-}
+// Bin f of thread t lives at u16 index 264 f + 2 (t/2 + t/64) + (t & 1).
 constexpr uint32_t kCntWords = 32 * kNT / 2 + 32 * kNT / 64;
+__device__ __forceinline__ uint16_t *cnt_base(uint32_t *cnt, uint32_t t) {
+    return reinterpret_cast<uint16_t *>(cnt + (t >> 1) + (t >> 6)) + (t & 1u);
+}
+constexpr uint32_t kCntRow = 264;   // u16 stride between bins of one thread
 
 // In-place exclusive scan of the counters in (bin, thread) order. Thread t owns linear entries
 // [32t, 32t+32) = the 16 words starting at 16t + t/2.
@@ -96,11 +97,6 @@ __device__ __forceinline__ void scan_counters(uint32_t *cnt, uint32_t *wsum) {
     }
 }
 
-__device__ __forceinline__ void zero_counters(uint32_t *cnt) {
-#pragma unroll
-    for (int f = 0; f < 32; f++) *cnt_at(cnt, f, threadIdx.x) = 0;
-}
-
 struct RSmem {
     uint32_t *A, *B;          // padded key buffers (tile words); B == A on the register path
     uint32_t *PA, *PB;        // padded payload buffers (tile keys)
@@ -110,21 +106,30 @@ struct RSmem {
     uint32_t *wsum;           // [kNW + 1]
 };
 
-// One tile of one bucket. KW in {1,2}: keys in registers, one smem key buffer;
-// KW == 0: runtime key width, two smem key buffers.
+template <int KW>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&k)[KW], uint32_t wi) {
+    uint32_t w = k[0];
+#pragma unroll
+    for (int u = 1; u < KW; u++) w = wi == (uint32_t)u ? k[u] : w;
+    return w;
+}
+
+// One tile of one bucket. KW in 1..8: keys in registers, one smem key buffer;
+// KW == 0: runtime key width, keys stay in two smem buffers.
 template <int KW, bool kPay>
 __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo &b, uint32_t j, uint32_t tile,
                                            const RSmem &s) {
     const int t = threadIdx.x;
     const uint32_t kw = KW ? (uint32_t)KW : b.kw;
-    const uint32_t KPT = KW ? 32u / KW : b.tile_keys / kNT;
+    constexpr int RK = KW ? 32 / KW : 1;   // register keys per thread
+    const uint32_t KPT = KW ? (uint32_t)RK : b.tile_keys / kNT;
     const uint32_t T = kNT * KPT;
     const uint32_t q = b.ndig - 1 - a.pass, wi = q / 3, sh = 20 - 10 * (q % 3);
     const uint32_t k0 = tile * b.tile_keys;
     const uint32_t nk = min(b.tile_keys, b.n - k0);
-    constexpr int RK = KW ? 32 / KW : 1;   // register keys per thread
     uint32_t *const A = s.A;
     uint32_t *const B = KW ? s.A : s.B;
+    uint16_t *const cb = cnt_base(s.cnt, t);
 
     for (uint32_t i = t; i < kRadixBins; i += kNT) s.hist[i] = 0;
     {
@@ -136,7 +141,8 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
             for (uint32_t i = t; i < T; i += kNT) s.PA[padw(i)] = i < nk ? __ldg(ps + i) : 0u;
         }
     }
-    zero_counters(s.cnt);
+#pragma unroll
+    for (int f = 0; f < 32; f++) cb[kCntRow * f] = 0;
     __syncthreads();
 
     uint32_t key[RK][KW ? KW : 1];
@@ -152,13 +158,13 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
         uint32_t w;
         if constexpr (KW > 0) {
 #pragma unroll
-            for (int u = 0; u < KW; u++) key[k % RK][u] = A[padw(idx * KW + u)];
-            w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
+            for (int u = 0; u < KW; u++) key[k][u] = A[padw(idx * KW + u)];
+            w = pick<KW>(key[k], wi);
         } else {
             w = A[padw(idx * kw + wi)];
         }
         const uint32_t d = digit_of(w, sh);
-        uint16_t *cp = cnt_at(s.cnt, d & 31u, t);
+        uint16_t *cp = cb + kCntRow * (d & 31u);
         const uint32_t c = *cp;
         *cp = (uint16_t)(c + 1);
         if constexpr (KW > 0) rk[k / 4] |= c << (8 * (k % 4));
@@ -181,12 +187,11 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
         const uint32_t idx = t * KPT + k;
         uint32_t pos;
         if constexpr (KW > 0) {
-            const uint32_t w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
-            pos = *cnt_at(s.cnt, digit_of(w, sh) & 31u, t) + ((rk[k / 4] >> (8 * (k % 4))) & 255u);
+            pos = cb[kCntRow * (digit_of(pick<KW>(key[k], wi), sh) & 31u)] + ((rk[k / 4] >> (8 * (k % 4))) & 255u);
 #pragma unroll
-            for (int u = 0; u < KW; u++) B[padw(pos * KW + u)] = key[k % RK][u];
+            for (int u = 0; u < KW; u++) B[padw(pos * KW + u)] = key[k][u];
         } else {
-            uint16_t *cp = cnt_at(s.cnt, digit_of(A[padw(idx * kw + wi)], sh) & 31u, t);   // re-count
+            uint16_t *cp = cb + kCntRow * (digit_of(A[padw(idx * kw + wi)], sh) & 31u);   // re-count
             pos = *cp;
             *cp = (uint16_t)(pos + 1);
             for (uint32_t u = 0; u < kw; u++) B[padw(pos * kw + u)] = A[padw(idx * kw + u)];
@@ -196,7 +201,8 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
     __syncthreads();
 
     // ---- sub-pass 2: high 5 bits (first letter of the pair) ----
-    zero_counters(s.cnt);
+#pragma unroll
+    for (int f = 0; f < 32; f++) cb[kCntRow * f] = 0;
 #pragma unroll
     for (int i = 0; i < (RK + 3) / 4; i++) rk[i] = 0;
 #pragma unroll
@@ -205,22 +211,40 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
         uint32_t w;
         if constexpr (KW > 0) {
 #pragma unroll
-            for (int u = 0; u < KW; u++) key[k % RK][u] = B[padw(idx * KW + u)];
-            w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
+            for (int u = 0; u < KW; u++) key[k][u] = B[padw(idx * KW + u)];
+            w = pick<KW>(key[k], wi);
         } else {
             w = B[padw(idx * kw + wi)];
         }
-        uint16_t *cp = cnt_at(s.cnt, digit_of(w, sh) >> 5, t);
+        uint16_t *cp = cb + kCntRow * (digit_of(w, sh) >> 5);
         const uint32_t c = *cp;
         *cp = (uint16_t)(c + 1);
         if constexpr (KW > 0) rk[k / 4] |= c << (8 * (k % 4));
     }
     __syncthreads();
     scan_counters(s.cnt, s.wsum);
+    // tile-local start of every digit (exclusive scan of the counts over digits)
+    uint32_t ex = block_excl_scan(c4[0] + c4[1] + c4[2] + c4[3], s.wsum, nullptr);
+    // scatter B -> A by the high field
+#pragma unroll
+    for (uint32_t k = 0; k < KPT; k++) {
+        const uint32_t idx = t * KPT + k;
+        uint32_t pos;
+        if constexpr (KW > 0) {
+            pos = cb[kCntRow * (digit_of(pick<KW>(key[k], wi), sh) >> 5)] + ((rk[k / 4] >> (8 * (k % 4))) & 255u);
+#pragma unroll
+            for (int u = 0; u < KW; u++) A[padw(pos * KW + u)] = key[k][u];
+        } else {
+            uint16_t *cp = cb + kCntRow * (digit_of(B[padw(idx * kw + wi)], sh) >> 5);
+            pos = *cp;
+            *cp = (uint16_t)(pos + 1);
+            for (uint32_t u = 0; u < kw; u++) A[padw(pos * kw + u)] = B[padw(idx * kw + u)];
+        }
+        if constexpr (kPay) s.PA[padw(pos)] = s.PB[padw(idx)];
+    }
+    // decoupled look-back over the preceding tiles of this bucket (4 digits per thread), as late as
+    // possible so that the predecessors have published their inclusive prefixes
     {
-        // tile-local start of every digit (exclusive scan of the counts over digits)
-        uint32_t ex = block_excl_scan(c4[0] + c4[1] + c4[2] + c4[3], s.wsum, nullptr);
-        // decoupled look-back over the preceding tiles of this bucket, 4 digits per thread
         uint32_t pre[4] = {0, 0, 0, 0};
         if (tile != 0) {
             uint32_t done = 0;
@@ -255,25 +279,6 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
         }
     }
     __syncthreads();
-    // scatter B -> A by the high field
-#pragma unroll
-    for (uint32_t k = 0; k < KPT; k++) {
-        const uint32_t idx = t * KPT + k;
-        uint32_t pos;
-        if constexpr (KW > 0) {
-            const uint32_t w = (KW == 1 || wi == 0) ? key[k % RK][0] : key[k % RK][KW - 1];
-            pos = *cnt_at(s.cnt, digit_of(w, sh) >> 5, t) + ((rk[k / 4] >> (8 * (k % 4))) & 255u);
-#pragma unroll
-            for (int u = 0; u < KW; u++) A[padw(pos * KW + u)] = key[k % RK][u];
-        } else {
-            uint16_t *cp = cnt_at(s.cnt, digit_of(B[padw(idx * kw + wi)], sh) >> 5, t);
-            pos = *cp;
-            *cp = (uint16_t)(pos + 1);
-            for (uint32_t u = 0; u < kw; u++) A[padw(pos * kw + u)] = B[padw(idx * kw + u)];
-        }
-        if constexpr (kPay) s.PA[padw(pos)] = s.PB[padw(idx)];
-    }
-    __syncthreads();
 
     // ---- coalesced write-out (the sentinels sort to the end and are dropped) ----
     uint32_t *dst = a.kout + b.key_off;
@@ -299,8 +304,8 @@ __device__ __forceinline__ void radix_tile(const RadixArgs &a, const BucketInfo 
     }
 }
 
-// kGeneric = false: tiles of buckets with kw in {1, 2} (register path, one key buffer);
-// kGeneric = true: tiles of buckets with kw >= 3.
+// kGeneric = false: tiles of buckets with kw <= kRadixRegMaxKw (register path, one key buffer);
+// kGeneric = true: tiles of buckets with larger keys.
 template <bool kGeneric, bool kPay>
 __global__ void __launch_bounds__(kNT, kGeneric ? 1 : (kPay ? 1 : 3)) k_radix_pass(RadixArgs a) {
     extern __shared__ __align__(16) uint32_t smem[];
@@ -329,8 +334,16 @@ __global__ void __launch_bounds__(kNT, kGeneric ? 1 : (kPay ? 1 : 3)) k_radix_pa
     if constexpr (kGeneric) {
         radix_tile<0, kPay>(a, b, j, td.tile, s);
     } else {
-        if (b.kw == 1) radix_tile<1, kPay>(a, b, j, td.tile, s);
-        else radix_tile<2, kPay>(a, b, j, td.tile, s);
+        switch (b.kw) {
+            case 1: radix_tile<1, kPay>(a, b, j, td.tile, s); break;
+            case 2: radix_tile<2, kPay>(a, b, j, td.tile, s); break;
+            case 3: radix_tile<3, kPay>(a, b, j, td.tile, s); break;
+            case 4: radix_tile<4, kPay>(a, b, j, td.tile, s); break;
+            case 5: radix_tile<5, kPay>(a, b, j, td.tile, s); break;
+            case 6: radix_tile<6, kPay>(a, b, j, td.tile, s); break;
+            case 7: radix_tile<7, kPay>(a, b, j, td.tile, s); break;
+            default: radix_tile<8, kPay>(a, b, j, td.tile, s); break;
+        }
     }
 }
 

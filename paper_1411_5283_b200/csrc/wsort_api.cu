@@ -361,7 +361,7 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
 namespace {
 
 // Plan layout (one H2D copy): BucketInfo[256] | radix tiles of every pass (class 0 then class 1)
-// | emit tiles. Radix tile classes: 0 = buckets with kw <= 2 (register path), 1 = kw >= 3.
+// | emit tiles. Radix tile classes: 0 = buckets with kw <= kRadixRegMaxKw (register path), 1 = wider.
 struct SortPlan {
     std::vector<BucketInfo> bk;
     std::vector<std::vector<TileDesc>> tiles[2];            // [class][pass]
@@ -403,7 +403,7 @@ int sort_radix(wsort_ctx *c, bool want_src) {
         for (uint32_t L = 1; L <= lmax; L++) {
             const BucketInfo &b = P.bk[L];
             if (!b.n || b.ndig <= p) continue;
-            const int cl = b.kw <= 2 ? 0 : 1;
+            const int cl = b.kw <= kRadixRegMaxKw ? 0 : 1;
             uint32_t nt = (b.n + b.tile_keys - 1) / b.tile_keys;
             for (uint32_t i = 0; i < nt; i++) P.tiles[cl][p].push_back(TileDesc{L, i});
             P.tile_keys[cl][p] = std::max(P.tile_keys[cl][p], b.tile_keys);

@@ -97,6 +97,7 @@ cudaError_t launch_digit_scan(uint32_t *dh, uint32_t rows, cudaStream_t s);
 cudaError_t launch_radix_pass(const RadixArgs &a, bool generic, cudaStream_t s);
 size_t radix_pass_smem(uint32_t tile_keys, uint32_t tile_words, bool payload, bool generic);
 constexpr int kRadixThreads = 256;
+constexpr uint32_t kRadixRegMaxKw = 8;   // key widths sorted with keys held in registers
 // keys per radix tile: 32 key words per thread (kw = 1: 8192 keys, kw = 2: 4096, ...), >= 1 key/thread
 __host__ __device__ constexpr uint32_t radix_tile_keys(uint32_t kw) {
     return kRadixThreads * (kw >= 32 ? 1u : 32u / kw);
