@@ -19,14 +19,14 @@ __global__ void __launch_bounds__(kEThreads) k_emit(EmitArgs a) {
     const uint32_t te = kEmitStage / (L + 1);
     const uint32_t k0 = td.tile * te;
     const uint32_t nk = min(te, b.n - k0);
-    const uint32_t kw = b.kw;
-    const uint32_t *keys = (b.final_b ? a.keys_b : a.keys_a) + b.key_off;
+    const uint32_t kw = b.kw, es = b.estride;
+    const uint32_t *keys = (b.final_b ? a.keys_b : a.keys_a) + b.elem_off;
     const uint64_t ob = b.byte_off + (uint64_t)k0 * (L + 1);
     const uint32_t head = (uint32_t)(ob & 15u);
 
     for (uint32_t k = t; k < nk; k += kEThreads) {
         uint8_t *o = stage + head + k * (L + 1);
-        const uint32_t *kp = keys + (uint64_t)(k0 + k) * kw;
+        const uint32_t *kp = keys + (uint64_t)(k0 + k) * es;
         for (uint32_t q = 0; q < kw; q++) {
             const uint32_t word = __ldg(kp + q);
 #pragma unroll
@@ -38,9 +38,13 @@ __global__ void __launch_bounds__(kEThreads) k_emit(EmitArgs a) {
         o[L] = '\n';
     }
     if (a.src_off) {
-        const uint32_t *pay = (b.final_b ? a.pay_b : a.pay_a) + b.word_off + k0;
         uint64_t *so = a.src_off + b.word_off + k0;
-        for (uint32_t k = t; k < nk; k += kEThreads) so[k] = a.global_base + __ldg(pay + k);
+        if (es > kw) {   // payload stored inline as the element's last word (variant A)
+            for (uint32_t k = t; k < nk; k += kEThreads) so[k] = a.global_base + __ldg(keys + (uint64_t)(k0 + k) * es + kw);
+        } else {
+            const uint32_t *pay = (b.final_b ? a.pay_b : a.pay_a) + b.word_off + k0;
+            for (uint32_t k = t; k < nk; k += kEThreads) so[k] = a.global_base + __ldg(pay + k);
+        }
     }
     __syncthreads();
 

@@ -66,7 +66,7 @@ struct wsort_ctx {
     Summary *h_sum = nullptr;   // pinned
 
     // sort
-    DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan;
+    DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y;
     std::vector<uint8_t> hplan;
     uint8_t *h_plan_pinned = nullptr;
     size_t h_plan_cap = 0;
@@ -260,7 +260,7 @@ void wsort_destroy(wsort_ctx *c) {
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->text_alloc, &c->cta_hist, &c->cta_base, &c->d_sum, &c->keys_a, &c->keys_b,
                       &c->pay_a, &c->pay_b, &c->words, &c->src_off, &c->dh, &c->status0, &c->status1,
-                      &c->tickets, &c->plan};
+                      &c->tickets, &c->plan, &c->va_x, &c->va_y};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_sum) cudaFreeHost(c->h_sum);
@@ -386,6 +386,8 @@ int sort_radix(wsort_ctx *c, bool want_src) {
         b.kw = kw_of(L);
         b.ndig = ndig_of(L);
         b.tile_keys = radix_tile_keys(b.kw);
+        b.elem_off = b.key_off;
+        b.estride = b.kw;
         if (!b.n) continue;
         b.dh_row = P.dh_rows;
         P.dh_rows += b.ndig;
@@ -561,6 +563,150 @@ int sort_radix(wsort_ctx *c, bool want_src) {
     return rc;
 }
 
+
+// Upload `bytes` of host data through the pinned plan buffer (one H2D copy) into c->plan.
+int upload_plan(wsort_ctx *c, const std::vector<uint8_t> &buf) {
+    if (c->h_plan_cap < buf.size()) {
+        if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
+        c->h_plan_pinned = nullptr;
+        c->h_plan_cap = 0;
+        if (cudaMallocHost(&c->h_plan_pinned, buf.size() * 2) != cudaSuccess) {
+            cudaGetLastError();
+            return set_err(c, WSORT_E_NOMEM, "pinned plan buffer");
+        }
+        c->h_plan_cap = buf.size() * 2;
+    }
+    memcpy(c->h_plan_pinned, buf.data(), buf.size());
+    int rc = ensure(c, c->plan, buf.size(), "plan");
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->plan.p, c->h_plan_pinned, buf.size(), cudaMemcpyHostToDevice, c->stream), "plan upload");
+    return WSORT_OK;
+}
+
+template <class T>
+size_t append(std::vector<uint8_t> &buf, const std::vector<T> &v) {
+    size_t off = buf.size();
+    buf.resize(off + v.size() * sizeof(T));
+    if (!v.empty()) memcpy(buf.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+}
+
+// Variant A: OETS tile sort + merge-path passes (PAPER.md:23 bubble sort in chunks, :76 merge).
+int sort_oets(wsort_ctx *c, bool want_src) {
+    const Summary &s = *c->h_sum;
+    const uint32_t lmax = s.max_len;
+    std::vector<BucketInfo> bk(256, BucketInfo{});
+    uint64_t eoff = 0;
+    uint32_t max_passes = 0, max_tw = 32;
+    std::vector<uint32_t> npass(256, 0);
+    for (uint32_t L = 1; L <= lmax; L++) {
+        BucketInfo &b = bk[L];
+        b.key_off = s.key_off[L];
+        b.word_off = s.off[L];
+        b.byte_off = s.byte_off[L];
+        b.n = (uint32_t)(s.off[L + 1] - s.off[L]);
+        b.kw = kw_of(L);
+        b.estride = b.kw + (want_src ? 1 : 0);
+        b.tile_keys = kMergeThreads * oets_elems_per_thread(b.estride);
+        b.elem_off = want_src ? eoff : b.key_off;
+        eoff += (uint64_t)b.n * b.estride;
+        if (!b.n) continue;
+        uint32_t nt = (b.n + b.tile_keys - 1) / b.tile_keys, m = 0;
+        while ((1u << m) < nt) m++;
+        npass[L] = m;
+        b.final_b = (m & 1u) ? 0u : 1u;   // tile sort writes X (= "b"), each merge pass swaps
+        max_passes = std::max(max_passes, m);
+        max_tw = std::max(max_tw, b.tile_keys * b.estride);
+    }
+    std::vector<TileDesc> sort_tiles, emit_tiles;
+    std::vector<std::vector<TileDesc>> merge_tiles(max_passes);
+    for (uint32_t L = 1; L <= lmax; L++) {
+        const BucketInfo &b = bk[L];
+        if (!b.n) continue;
+        const uint32_t nt = (b.n + b.tile_keys - 1) / b.tile_keys;
+        for (uint32_t i = 0; i < nt; i++) sort_tiles.push_back(TileDesc{L, i});
+        for (uint32_t m = 0; m < npass[L]; m++)
+            for (uint32_t i = 0; i < nt; i++) merge_tiles[m].push_back(TileDesc{L, i});
+        const uint32_t te = kEmitStage / (L + 1);
+        for (uint32_t i = 0; i < (b.n + te - 1) / te; i++) emit_tiles.push_back(TileDesc{L, i});
+    }
+    // buffers: keys-only -> X = keys_b, Y = keys_a (K3 output is consumed by the tile sort);
+    // with src_off -> interleaved (key words + payload) buffers.
+    int rc;
+    const uint64_t key_words = s.key_off[256];
+    const uint64_t W = s.n_words;
+    if ((rc = ensure(c, c->keys_a, key_words * 4 + 64, "keys_a"))) return rc;
+    if ((rc = ensure(c, c->keys_b, key_words * 4 + 64, "keys_b"))) return rc;
+    if (want_src) {
+        if ((rc = ensure(c, c->pay_a, W * 4 + 64, "pay_a"))) return rc;
+        if ((rc = ensure(c, c->src_off, W * 8 + 64, "src_off"))) return rc;
+        if ((rc = ensure(c, c->va_x, eoff * 4 + 64, "va_x"))) return rc;
+        if ((rc = ensure(c, c->va_y, eoff * 4 + 64, "va_y"))) return rc;
+    }
+    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    std::vector<uint8_t> plan;
+    append(plan, bk);
+    const size_t o_sort = append(plan, sort_tiles);
+    std::vector<size_t> o_merge(max_passes);
+    for (uint32_t m = 0; m < max_passes; m++) o_merge[m] = append(plan, merge_tiles[m]);
+    const size_t o_emit = append(plan, emit_tiles);
+    if ((rc = upload_plan(c, plan))) return rc;
+    uint8_t *dp = static_cast<uint8_t *>(c->plan.p);
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(dp);
+
+    uint32_t *ka = static_cast<uint32_t *>(c->keys_a.p), *kb = static_cast<uint32_t *>(c->keys_b.p);
+    uint32_t *pa = want_src ? static_cast<uint32_t *>(c->pay_a.p) : nullptr;
+    uint32_t *X = want_src ? static_cast<uint32_t *>(c->va_x.p) : kb;
+    uint32_t *Y = want_src ? static_cast<uint32_t *>(c->va_y.p) : ka;
+    TkArgs &tk = c->tk;
+    tk.buckets = d_bk;
+    tk.keys = ka;
+    tk.payload = pa;
+    const double key_bytes = (double)key_words * 4, elem_bytes = (double)eoff * 4;
+    rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes + (want_src ? 4.0 * W : 0.0),
+                [&] { return launch_pack_scatter(tk, c->stream); });
+    if (rc) return rc;
+    OetsArgs oa{};
+    oa.buckets = d_bk;
+    oa.tiles = reinterpret_cast<const TileDesc *>(dp + o_sort);
+    oa.ntiles = (uint32_t)sort_tiles.size();
+    oa.max_tile_words = max_tw;
+    oa.keys_in = ka;
+    oa.pay_in = pa;
+    oa.out = X;
+    rc = launch(c, "k4a_oets_tile_sort", key_bytes + (want_src ? 4.0 * W : 0.0) + (want_src ? elem_bytes : key_bytes),
+                [&] { return launch_oets_tile_sort(oa, c->stream); });
+    if (rc) return rc;
+    for (uint32_t m = 0; m < max_passes; m++) {
+        MergeArgs ma{};
+        ma.buckets = d_bk;
+        ma.tiles = reinterpret_cast<const TileDesc *>(dp + o_merge[m]);
+        ma.ntiles = (uint32_t)merge_tiles[m].size();
+        ma.pass = m;
+        ma.max_tile_words = max_tw;
+        ma.in = (m & 1u) ? Y : X;
+        ma.out = (m & 1u) ? X : Y;
+        double bytes = 0;
+        for (uint32_t L = 1; L <= lmax; L++)
+            if (npass[L] > m) bytes += 2.0 * bk[L].n * bk[L].estride * 4.0;
+        rc = launch(c, "k4b_merge_pass", bytes, [&] { return launch_merge_pass(ma, c->stream); });
+        if (rc) return rc;
+    }
+    EmitArgs ea{};
+    ea.buckets = d_bk;
+    ea.tiles = reinterpret_cast<const TileDesc *>(dp + o_emit);
+    ea.ntiles = (uint32_t)emit_tiles.size();
+    ea.keys_a = Y;
+    ea.keys_b = X;
+    ea.pay_a = nullptr;
+    ea.pay_b = nullptr;
+    ea.words = static_cast<uint8_t *>(c->words.p);
+    ea.src_off = want_src ? static_cast<uint64_t *>(c->src_off.p) : nullptr;
+    ea.global_base = c->global_base;
+    return launch(c, "k5_emit", (want_src ? elem_bytes : key_bytes) + (double)s.byte_off[256] + (want_src ? 8.0 * W : 0.0),
+                  [&] { return launch_emit(ea, c->stream); });
+}
+
 }  // namespace
 
 extern "C" {
@@ -574,8 +720,7 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     cudaSetDevice(c->device);
     const bool want_src = (flags & WSORT_FLAG_SRC_OFF) != 0;
     int rc;
-    if (algo == WSORT_ALGO_OETS_MERGE) return set_err(c, WSORT_E_INVALID_ARG, "OETS_MERGE not built yet");
-    rc = sort_radix(c, want_src);
+    rc = algo == WSORT_ALGO_OETS_MERGE ? sort_oets(c, want_src) : sort_radix(c, want_src);
     if (rc) {
         c->state = ST_TOKENIZED;
         return rc;

@@ -49,6 +49,10 @@ struct BucketInfo {                // per-length bucket, built on the host after
     uint32_t tile_keys;            // keys per radix / merge tile
     uint32_t dh_row;               // first row of this bucket's digit histograms (rows of 1024)
     uint32_t final_b;              // sorted keys end in buffer B (1) or A (0)
+    uint64_t elem_off;             // u32 words into the final buffer (element layout)
+    uint32_t estride;              // u32 words per element in the final buffer (kw, or kw+1 with an
+                                   // inline payload word)
+    uint32_t pad_;
 };
 
 struct TileDesc {
@@ -102,6 +106,33 @@ constexpr uint32_t kRadixRegMaxKw = 8;   // key widths sorted with keys held in 
 __host__ __device__ constexpr uint32_t radix_tile_keys(uint32_t kw) {
     return kRadixThreads * (kw >= 32 ? 1u : 32u / kw);
 }
+
+// ---------------- variant A: odd-even transposition tiles + merge path ----------------
+constexpr int kMergeThreads = 256;
+// elements per thread of an OETS tile: the largest power of two <= min(8, 32 / S), at least 1
+__host__ __device__ constexpr uint32_t oets_elems_per_thread(uint32_t S) {
+    return S * 8 <= 32 ? 8u : (S * 4 <= 32 ? 4u : (S * 2 <= 32 ? 2u : 1u));
+}
+struct OetsArgs {
+    const BucketInfo *buckets;
+    const TileDesc *tiles;
+    uint32_t ntiles;
+    uint32_t max_tile_words;       // max over buckets of tile_keys * estride
+    const uint32_t *keys_in;       // K3 output (key records, kw words)
+    const uint32_t *pay_in;        // K3 payload (nullable)
+    uint32_t *out;                 // element layout (estride words)
+};
+struct MergeArgs {
+    const BucketInfo *buckets;
+    const TileDesc *tiles;
+    uint32_t ntiles;
+    uint32_t pass;                 // runs of tile_keys << pass are merged pairwise
+    uint32_t max_tile_words;
+    const uint32_t *in;
+    uint32_t *out;
+};
+cudaError_t launch_oets_tile_sort(const OetsArgs &a, cudaStream_t s);
+cudaError_t launch_merge_pass(const MergeArgs &a, cudaStream_t s);
 
 struct EmitArgs {
     const BucketInfo *buckets;

@@ -20,7 +20,7 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["lsd_radix"]
+ALGOS = ["lsd_radix", "oets_merge"]
 
 
 @pytest.fixture(scope="module")
@@ -168,6 +168,15 @@ def test_auto_equals_radix(ws):
     assert gpu_sort(ws, text, "auto")[0] == gpu_sort(ws, text, "lsd_radix")[0]
 
 
+@pytest.mark.parametrize("algo", ALGOS)
+def test_keys_only_path(ws, algo):
+    """Without src_off the scatter and the sort take their keys-only (unordered-slot) paths."""
+    text, _ = gen.generate(2)
+    ref = oracle.sort(text, oracle.MERGE)
+    words, off, _ = gpu_sort(ws, text, algo, src=False)
+    assert words == ref.words and off == ref.off
+
+
 # ---------------------------------------------------------------- full-size (bench launch config)
 def _bucket_rows(words: np.ndarray, off: list, L: int) -> np.ndarray:
     """Bucket L of the output as an array of fixed-width byte strings (numpy 'S<L>')."""
@@ -178,12 +187,12 @@ def _bucket_rows(words: np.ndarray, off: list, L: int) -> np.ndarray:
     return np.ascontiguousarray(rows[:, :L]).view(f"S{L}").ravel()
 
 
-def _full_size_check(ws, text: np.ndarray, exact_from: int):
+def _full_size_check(ws, text: np.ndarray, exact_from: int, algo: str = "auto"):
     hist, ref_off, lmax = oracle.histogram(text)
     ref_off = [int(x) for x in ref_off[: lmax + 2]]
     ws.load_text(text)
     n = ws.tokenize()
-    ws.sort("auto")
+    ws.sort(algo)
     words, off = ws.fetch()
     assert n == ref_off[-1]
     assert off == ref_off                                                   # exact offsets
@@ -206,6 +215,12 @@ def _full_size_check(ws, text: np.ndarray, exact_from: int):
 def test_config4_full_size(ws):
     text, _ = gen.generate(4)
     _full_size_check(ws, text, exact_from=11)
+
+
+@pytest.mark.slow
+def test_config4_full_size_oets_merge(ws):
+    text, _ = gen.generate(4)
+    _full_size_check(ws, text, exact_from=13, algo="oets_merge")
 
 
 @pytest.mark.slow
