@@ -71,12 +71,139 @@ __device__ __forceinline__ void cmp_swap(uint32_t *x, uint32_t *y, uint32_t S) {
     }
 }
 
-// K4a: sort one tile of E * kMT elements of one bucket.
-__global__ void __launch_bounds__(kMT) k_oets_tile_sort(OetsArgs a) {
-    extern __shared__ __align__(16) uint32_t sm[];
+
+// ---------------- typed fast path: elements of S = 1 (u32) or S = 2 (u64, word 0 high) ----------------
+template <typename T>
+__device__ __forceinline__ T ld_elem(const uint32_t *p) {
+    if constexpr (sizeof(T) == 4) return *p;
+    else return ((uint64_t)p[0] << 32) | p[1];
+}
+template <typename T>
+__device__ __forceinline__ void st_elem(uint32_t *p, T v) {
+    if constexpr (sizeof(T) == 4) {
+        *p = v;
+    } else {
+        p[0] = (uint32_t)(v >> 32);
+        p[1] = (uint32_t)v;
+    }
+}
+template <typename T>
+__device__ __forceinline__ T shfl_elem(T v, int src) {
+    if constexpr (sizeof(T) == 4) {
+        return __shfl_sync(0xffffffffu, v, src);
+    } else {
+        const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
+        const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
+        return ((uint64_t)hi << 32) | lo;
+    }
+}
+template <typename T>
+__device__ __forceinline__ void ce(T &x, T &y) {
+    const T lo = x < y ? x : y, hi = x < y ? y : x;
+    x = lo;
+    y = hi;
+}
+template <typename T>
+__device__ __forceinline__ uint32_t merge_path_t(const T *a, uint32_t na, const T *b, uint32_t nb, uint32_t diag) {
+    uint32_t lo = diag > nb ? diag - nb : 0u, hi = diag < na ? diag : na;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] <= b[diag - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+template <typename T>
+__device__ __forceinline__ void serial_merge_t(const T *a, uint32_t na, const T *b, uint32_t nb, uint32_t i,
+                                               uint32_t j, uint32_t cnt, T *out) {
+    for (uint32_t k = 0; k < cnt; k++) {
+        const bool take_a = j >= nb || (i < na && a[i] <= b[j]);
+        out[k] = take_a ? a[i++] : b[j++];
+    }
+}
+
+// Tile sort with the 8 elements of each thread in registers: odd-even transposition inside the
+// thread, then odd-even merge-split across groups of 8 lanes through warp shuffles (the merge-split
+// of two sorted runs is min/max against the reversed partner run + a bitonic clean-up), then merge
+// paths in shared memory: 64 -> 128 -> ... -> 2048.
+template <typename T>
+__device__ __forceinline__ void tile_sort_reg(const OetsArgs &a, const BucketInfo &b, uint32_t tile, uint32_t *smem) {
+    constexpr int E = 8;
+    constexpr uint32_t TN = kMT * E;
+    const int t = threadIdx.x, lane = t & 31;
+    const uint32_t kw = b.kw, S = b.estride;
+    const uint32_t k0 = tile * TN, nk = min(TN, b.n - k0);
+    T v[E];
+    const uint32_t *ks = a.keys_in + b.key_off + (uint64_t)k0 * kw;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t idx = t * E + e;
+        if (idx < nk) {
+            if constexpr (sizeof(T) == 8) {
+                if (S == kw) v[e] = ld_elem<T>(ks + (size_t)idx * kw);          // two key words
+                else v[e] = ((T)__ldg(ks + idx) << 32) | __ldg(a.pay_in + b.word_off + k0 + idx);   // key, payload
+            } else {
+                v[e] = __ldg(ks + idx);                                          // one key word
+            }
+        } else {
+            v[e] = (T)~(T)0;
+        }
+    }
+    // (1) odd-even transposition within the thread
+#pragma unroll
+    for (int ph = 0; ph < E; ph++)
+#pragma unroll
+        for (int i = ph & 1; i + 1 < E; i += 2) ce(v[i], v[i + 1]);
+    // (2) odd-even merge-split across the 8 lanes of each lane group
+    const int g = lane & 7;
+#pragma unroll 1
+    for (int ph = 0; ph < 8; ph++) {
+        const bool lower = (g & 1) == (ph & 1);
+        const int pg = lower ? g + 1 : g - 1;
+        const bool active = pg >= 0 && pg < 8;
+        const int src = active ? (lane - g + pg) : lane;
+        T o[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) o[e] = shfl_elem(v[e], src);
+        if (active) {
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const T x = v[e], y = o[E - 1 - e];
+                v[e] = lower ? (x < y ? x : y) : (x < y ? y : x);
+            }
+            // v is bitonic: bitonic merge to ascending
+#pragma unroll
+            for (int d = E / 2; d >= 1; d >>= 1)
+#pragma unroll
+                for (int i = 0; i < E; i++)
+                    if ((i & d) == 0) ce(v[i], v[i + d]);
+        }
+    }
+    // (3) merge paths in shared memory
+    T *buf0 = reinterpret_cast<T *>(smem), *buf1 = buf0 + TN;
+#pragma unroll
+    for (int e = 0; e < E; e++) buf0[t * E + e] = v[e];
+    __syncthreads();
+    T *src = buf0, *dst = buf1;
+    for (uint32_t run = 8 * E; run < TN; run *= 2) {
+        const uint32_t o = t * E;
+        const uint32_t pair = o / (2 * run), d = o - pair * 2 * run;
+        const T *ra = src + pair * 2 * run, *rb = ra + run;
+        const uint32_t i = merge_path_t(ra, run, rb, run, d);
+        serial_merge_t(ra, run, rb, run, i, d - i, E, dst + o);
+        __syncthreads();
+        T *sw = src;
+        src = dst;
+        dst = sw;
+    }
+    uint32_t *out = a.out + b.elem_off + (uint64_t)k0 * S;
+    for (uint32_t i = t; i < nk; i += kMT) st_elem<T>(out + (size_t)i * S, src[i]);
+}
+
+// K4a: sort one tile of E * kMT elements of one bucket (generic element width).
+__device__ __forceinline__ void tile_sort_generic(const OetsArgs &a, const TileDesc td, const BucketInfo &b,
+                                                  uint32_t *sm) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const TileDesc td = a.tiles[blockIdx.x];
-    const BucketInfo b = a.buckets[td.L];
     const uint32_t kw = b.kw, S = b.estride, E = b.tile_keys / kMT;
     const uint32_t T = b.tile_keys, k0 = td.tile * T, nk = min(T, b.n - k0);
     uint32_t *X = sm, *Y = sm + (size_t)T * S;
@@ -145,11 +272,39 @@ __global__ void __launch_bounds__(kMT) k_oets_tile_sort(OetsArgs a) {
     for (uint32_t i = t; i < nk * S; i += kMT) out[i] = src[i];
 }
 
+__global__ void __launch_bounds__(kMT) k_oets_tile_sort(OetsArgs a) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const TileDesc td = a.tiles[blockIdx.x];
+    const BucketInfo b = a.buckets[td.L];
+    if (b.estride == 1) tile_sort_reg<uint32_t>(a, b, td.tile, sm);
+    else if (b.estride == 2) tile_sort_reg<uint64_t>(a, b, td.tile, sm);
+    else tile_sort_generic(a, td, b, sm);
+}
+
+// Merge-path split of every merge tile's first output (one thread per tile, all in parallel, so the
+// dependent global-memory binary searches overlap instead of stalling each merge CTA).
+__global__ void __launch_bounds__(256) k_merge_split(MergeArgs a) {
+    const uint32_t j = blockIdx.x * 256 + threadIdx.x;
+    if (j >= a.ntiles) return;
+    const TileDesc td = a.tiles[j];
+    const BucketInfo b = a.buckets[td.L];
+    const uint32_t S = b.estride, n = b.n, run = b.tile_keys << a.pass;
+    const uint32_t o0 = td.tile * b.tile_keys;
+    const uint32_t p0 = (o0 / (2 * run)) * 2 * run;
+    const uint32_t na = min(run, n - p0);
+    const uint32_t nb = n - p0 > run ? min(run, n - p0 - run) : 0u;
+    const uint32_t *ra = a.in + b.elem_off + (uint64_t)p0 * S;
+    const uint32_t *rb = ra + (size_t)na * S;
+    uint32_t r;
+    if (S == 1) r = merge_path_t(ra, na, rb, nb, o0 - p0);
+    else r = merge_path(ra, na, rb, nb, o0 - p0, S);
+    a.splits[j] = r;
+}
+
 // K4b: one merge pass over every bucket with runs left: runs of `run_len(L)` elements are merged
 // pairwise; this CTA produces outputs [o0, o0 + TO) of the bucket.
 __global__ void __launch_bounds__(kMT) k_merge_pass(MergeArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
-    __shared__ uint32_t s_ij[2];
     const int t = threadIdx.x;
     const TileDesc td = a.tiles[blockIdx.x];
     const BucketInfo b = a.buckets[td.L];
@@ -163,10 +318,8 @@ __global__ void __launch_bounds__(kMT) k_merge_pass(MergeArgs a) {
     const uint32_t *base = a.in + b.elem_off + (uint64_t)p0 * S;
     const uint32_t *ra = base, *rb = base + (size_t)na * S;
     const uint32_t d0 = o0 - p0, d1 = o1 - p0;
-    if (t == 0) s_ij[0] = merge_path(ra, na, rb, nb, d0, S);
-    if (t == 1) s_ij[1] = merge_path(ra, na, rb, nb, d1, S);
-    __syncthreads();
-    const uint32_t i0 = s_ij[0], i1 = s_ij[1];
+    const uint32_t i0 = a.splits[blockIdx.x];
+    const uint32_t i1 = d1 == na + nb ? na : a.splits[blockIdx.x + 1];   // next tile: same pair
     const uint32_t j0 = d0 - i0, j1 = d1 - i1;
     const uint32_t ca = i1 - i0, cb = j1 - j0;
     // stage both pieces
@@ -198,6 +351,7 @@ cudaError_t launch_oets_tile_sort(const OetsArgs &a, cudaStream_t s) {
 
 cudaError_t launch_merge_pass(const MergeArgs &a, cudaStream_t s) {
     if (a.ntiles == 0) return cudaSuccess;
+    k_merge_split<<<(a.ntiles + 255) / 256, 256, 0, s>>>(a);
     const size_t smem = (size_t)a.max_tile_words * 2 * 4;
     cudaError_t e = cudaFuncSetAttribute(k_merge_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

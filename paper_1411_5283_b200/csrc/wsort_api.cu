@@ -66,7 +66,7 @@ struct wsort_ctx {
     Summary *h_sum = nullptr;   // pinned
 
     // sort
-    DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y;
+    DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y, splits;
     std::vector<uint8_t> hplan;
     uint8_t *h_plan_pinned = nullptr;
     size_t h_plan_cap = 0;
@@ -260,7 +260,7 @@ void wsort_destroy(wsort_ctx *c) {
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->text_alloc, &c->cta_hist, &c->cta_base, &c->d_sum, &c->keys_a, &c->keys_b,
                       &c->pay_a, &c->pay_b, &c->words, &c->src_off, &c->dh, &c->status0, &c->status1,
-                      &c->tickets, &c->plan, &c->va_x, &c->va_y};
+                      &c->tickets, &c->plan, &c->va_x, &c->va_y, &c->splits};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_sum) cudaFreeHost(c->h_sum);
@@ -644,6 +644,7 @@ int sort_oets(wsort_ctx *c, bool want_src) {
         if ((rc = ensure(c, c->va_y, eoff * 4 + 64, "va_y"))) return rc;
     }
     if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    if ((rc = ensure(c, c->splits, (sort_tiles.size() + 1) * 4, "splits"))) return rc;
     std::vector<uint8_t> plan;
     append(plan, bk);
     const size_t o_sort = append(plan, sort_tiles);
@@ -686,6 +687,7 @@ int sort_oets(wsort_ctx *c, bool want_src) {
         ma.max_tile_words = max_tw;
         ma.in = (m & 1u) ? Y : X;
         ma.out = (m & 1u) ? X : Y;
+        ma.splits = static_cast<uint32_t *>(c->splits.p);
         double bytes = 0;
         for (uint32_t L = 1; L <= lmax; L++)
             if (npass[L] > m) bytes += 2.0 * bk[L].n * bk[L].estride * 4.0;

@@ -130,6 +130,7 @@ struct MergeArgs {
     uint32_t max_tile_words;
     const uint32_t *in;
     uint32_t *out;
+    uint32_t *splits;              // [ntiles] merge-path split of each tile's first output
 };
 cudaError_t launch_oets_tile_sort(const OetsArgs &a, cudaStream_t s);
 cudaError_t launch_merge_pass(const MergeArgs &a, cudaStream_t s);
