@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cpu-sample-mb", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the N>1 path with several ranks on one GPU (tests)")
     return ap.parse_args()
 
 
@@ -201,7 +203,7 @@ def run_wsort(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     cfg = gen.CONFIGS[args.config]
     if world > 1:
-        raise SystemExit("multi-GPU bench path: see paper_1411_5283_b200/dist.py (not wired in this build)")
+        return run_wsort_dist(args, rank, world, local_rank)
 
     # host text in pinned memory (the e2e leg copies it every step)
     host = torch.empty(cfg.n, dtype=torch.uint8, pin_memory=True)
@@ -305,6 +307,95 @@ def run_wsort(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+def run_wsort_dist(args, rank, world, local_rank):
+    """N > 1: the config text sharded by byte range over the ranks (strong scaling: the total text is
+    fixed), one sample-sort exchange per step over NCCL (paper_1411_5283_b200/dist.py)."""
+    import numpy as np
+    import torch
+
+    import gen
+    from paper_1411_5283_b200 import WSort
+    from paper_1411_5283_b200.dist import TorchComm, shard_cuts, sort_distributed
+
+    dev = local_rank
+    stream = torch.cuda.current_stream(dev)
+    cfg = gen.CONFIGS[args.config]
+    text, _ = gen.generate(args.config)
+    cuts = shard_cuts(text, world)
+    a, b = cuts[rank], cuts[rank + 1]
+    host = torch.empty(b - a, dtype=torch.uint8, pin_memory=True)
+    host.numpy()[:] = text[a:b]
+    shard = host.to(f"cuda:{dev}")
+    del text
+    comm = TorchComm(f"cuda:{dev}")
+    ws = WSort(dev, stream=stream.cuda_stream)
+    res = sort_distributed(ws, shard, a, comm, args.algo)
+    for _ in range(args.warmup):
+        res = sort_distributed(ws, shard, a, comm, args.algo)
+    torch.cuda.synchronize(dev)
+    comm.barrier()
+    ws.reset_kernel_stats()
+    ws.set_profiling(True)
+    l0 = ws.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = sort_distributed(ws, shard, a, comm, args.algo)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ws.launch_count() - l0
+    stats = ws.kernel_stats()
+    ws.set_profiling(False)
+    t = torch.tensor([ms], device=comm.wire)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    tot = torch.tensor([res.n_words, res.words_len], dtype=torch.int64, device=comm.wire)
+    torch.distributed.all_reduce(tot)
+    W, out_bytes = int(tot[0]), int(tot[1])
+    peak, peak_src = measured_peaks()
+    dom = max(stats.items(), key=lambda kv: kv[1]["ms"])
+    dname, d = dom
+    achieved = d["bytes"] / d["launches"] / (d["ms"] / d["launches"] / 1000) / 1e9
+    line = {
+        "metric": METRIC, "value": W / (ms / 1000), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": cfg.name, "n_bytes": cfg.n, "seed": cfg.seed, "words": W, "output_bytes": out_bytes,
+                   "algo": args.algo, "parallelism": f"byte-range shards x{world}, sample sort + NCCL all-to-all",
+                   "l2": "inputs larger than L2; no extra flush"},
+        "input_gbs": cfg.n / (ms / 1000) / 1e9,
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(dname), "peak_source": peak_src,
+                     "rank": 0},
+        "kernels": {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
+                    for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_e2e:
+        out = torch.empty(max(res.words_len, 1) + 64, dtype=torch.uint8, pin_memory=True).numpy()
+        comm.barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            r = sort_distributed(ws, host, a, comm, args.algo)
+            ws.fetch(out=out)
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = torch.tensor([f0.elapsed_time(f1) / args.e2e_steps], device=comm.wire)
+        torch.distributed.all_reduce(ems, op=torch.distributed.ReduceOp.MAX)
+        line["e2e"] = {"value": W / (float(ems.item()) / 1000), "unit": UNIT, "h2d_bytes_per_step": cfg.n,
+                       "d2h_bytes_per_step": out_bytes, "ms_per_step": float(ems.item()),
+                       "path": "per rank: pinned host shard -> sort_distributed -> wsort_fetch(pinned host)"}
+    ws.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = env_int("WORLD_SIZE", 1)
@@ -316,8 +407,9 @@ def main():
     if world > 1:
         import torch
 
+        local_rank = local_rank % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
+        torch.distributed.init_process_group(args.dist_backend)
     try:
         run_wsort(args, rank, world, local_rank)
     finally:

@@ -52,7 +52,7 @@ extern "C" {
 #define WSORT_E_STATE (-2)             /* call out of order (see the state machine below) */
 #define WSORT_E_NOMEM (-3)             /* device or pinned-host allocation failed */
 #define WSORT_E_CUDA (-4)              /* a CUDA runtime error; message in wsort_last_error */
-#define WSORT_E_NCCL (-5)              /* reserved for the multi-GPU exchange */
+#define WSORT_E_NCCL (-5)              /* reserved (the exchange runs in torch.distributed/NCCL) */
 #define WSORT_E_TOO_LARGE (-6)         /* a shard of more than WSORT_MAX_SHARD_BYTES bytes */
 #define WSORT_E_WORD_TOO_LONG (-7)     /* some word has more than WSORT_MAX_WORD_LEN letters (A7) */
 #define WSORT_E_BUFFER_TOO_SMALL (-8)  /* wsort_fetch: a cap is short; sizes are still filled in */
@@ -163,6 +163,47 @@ int wsort_kernel_stats(wsort_ctx *c, wsort_kernel_stat *out, int cap, int *n);
 int wsort_reset_kernel_stats(wsort_ctx *c);
 /* Number of kernel launches enqueued by this context since creation. */
 uint64_t wsort_launch_count(const wsort_ctx *c);
+
+
+/* ---- multi-GPU stages (keys only, no src_off) ----
+ * One context per rank. The text shard of rank r is [cut_r, cut_{r+1}) with cuts moved forward
+ * while both neighbouring bytes are letters (reading A13). Per step:
+ *   wsort_load_text(shard, global_base = cut_r); wsort_tokenize; wsort_histogram -> all-reduce;
+ *   wsort_pack (K3 only); wsort_sample -> all-gather; wsort_select_splitters (host, identical on
+ *   every rank); wsort_partition -> all-to-all of counts and of the send buffer (NCCL, outside the
+ *   library); wsort_load_keys(received); wsort_sort; wsort_set_global(global histogram, word_base,
+ *   byte_base); wsort_fetch returns this rank's slice of the global output.
+ * Global order = (length, key, source rank): the concatenation of the ranks' outputs in rank
+ * order equals the one-GPU output. */
+
+/* Local length histogram hist[0..255] (state >= TOKENIZED). */
+int wsort_histogram(wsort_ctx *c, uint64_t *hist);
+
+/* K3 only: pack and scatter the tokenized words into per-length buckets (state TOKENIZED -> PACKED). */
+int wsort_pack(wsort_ctx *c);
+
+/* Regular sample of the packed keys: nsamples records of rec_words u32 (device memory, caller
+ * owned): [length, rank, key words..., 0 padding]. rec_words >= 2 + ceil(Lmax_global / 6). */
+int wsort_sample(wsort_ctx *c, uint32_t nsamples, uint32_t rank, uint32_t rec_words, uint32_t *dev_records);
+
+/* Host only (no context): sort the all-gathered samples by (length, key, rank) and write the
+ * nparts-1 splitters (records at quantiles d*n/nparts) into host memory. Deterministic. */
+int wsort_select_splitters(const uint32_t *samples, uint64_t nsamples, uint32_t rec_words, uint32_t nparts,
+                           uint32_t *splitters);
+
+/* Partition the packed keys by the (host) splitters into dev_send (caller-owned device buffer of at
+ * least the local key words), laid out [dest][length][keys]. counts[dest*256 + L] (host, keys) and
+ * send_words[dest] (u32 words per destination) are filled. Synchronises once (the counts). */
+int wsort_partition(wsort_ctx *c, const uint32_t *splitters, uint32_t nparts, uint32_t rec_words, uint32_t rank,
+                    uint32_t *dev_send, uint64_t send_cap_words, uint64_t *counts, uint64_t *send_words);
+
+/* Adopt received keys: dev_recv holds, for src = 0..nparts-1, the ranges [length][keys] whose key
+ * counts are counts[src*256 + L] (host). State -> PACKED; wsort_sort then sorts and emits them. */
+int wsort_load_keys(wsort_ctx *c, const uint32_t *dev_recv, const uint64_t *counts, uint32_t nparts);
+
+/* Make wsort_fetch report the GLOBAL bucket offsets (from the all-reduced histogram ghist[256]) and
+ * this rank's word_base / byte_base. */
+int wsort_set_global(wsort_ctx *c, const uint64_t *ghist, uint64_t word_base, uint64_t byte_base);
 
 #ifdef __cplusplus
 }

@@ -35,7 +35,8 @@ EXPORTS = [
     "wsort_create", "wsort_set_stream", "wsort_load_text", "wsort_load_file", "wsort_tokenize",
     "wsort_sort", "wsort_fetch", "wsort_device_results", "wsort_last_error", "wsort_strerror",
     "wsort_destroy", "wsort_set_profiling", "wsort_kernel_stats", "wsort_reset_kernel_stats",
-    "wsort_launch_count",
+    "wsort_launch_count", "wsort_histogram", "wsort_pack", "wsort_sample", "wsort_select_splitters",
+    "wsort_partition", "wsort_load_keys", "wsort_set_global",
 ]
 
 
@@ -97,6 +98,13 @@ def load():
     L.wsort_reset_kernel_stats.argtypes = [P]
     L.wsort_launch_count.argtypes = [P]
     L.wsort_launch_count.restype = U64
+    L.wsort_histogram.argtypes = [P, P]
+    L.wsort_pack.argtypes = [P]
+    L.wsort_sample.argtypes = [P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, P]
+    L.wsort_select_splitters.argtypes = [P, U64, ctypes.c_uint32, ctypes.c_uint32, P]
+    L.wsort_partition.argtypes = [P, P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, P, U64, P, P]
+    L.wsort_load_keys.argtypes = [P, P, P, ctypes.c_uint32]
+    L.wsort_set_global.argtypes = [P, P, U64, U64]
     for name in EXPORTS:
         if name not in ("wsort_strerror", "wsort_destroy", "wsort_launch_count"):
             getattr(L, name).restype = I

@@ -146,6 +146,41 @@ class WSort:
         self._check(self._lib.wsort_fetch(self._h, ctypes.byref(rr)), "wsort_fetch(device)")
         return words[: r.words_len], self.offsets()
 
+    # ------------------------------------------------------------------ multi-GPU stages (dist.py)
+    torch_device = property(lambda self: f"cuda:{self.device}")
+
+    def histogram(self) -> np.ndarray:
+        h = np.zeros(256, np.uint64)
+        self._check(self._lib.wsort_histogram(self._h, h.ctypes.data), "wsort_histogram")
+        return h
+
+    def pack(self):
+        self._check(self._lib.wsort_pack(self._h), "wsort_pack")
+
+    def sample(self, nsamples: int, rank: int, rec_words: int, out):
+        """Write nsamples sample records into `out` (cuda int32/uint32 tensor [nsamples, rec_words])."""
+        assert out.is_cuda and out.numel() >= nsamples * rec_words
+        self._check(self._lib.wsort_sample(self._h, nsamples, rank, rec_words, out.data_ptr()), "wsort_sample")
+
+    def partition(self, splitters: np.ndarray, nparts: int, rec_words: int, rank: int, send):
+        """Partition packed keys into `send` (cuda int32 tensor); returns (counts[P,256], send_words[P])."""
+        sp = np.ascontiguousarray(splitters, dtype=np.uint32)
+        counts = np.zeros((nparts, 256), np.uint64)
+        sw = np.zeros(nparts, np.uint64)
+        self._check(self._lib.wsort_partition(self._h, sp.ctypes.data if sp.size else None, nparts, rec_words, rank,
+                                              send.data_ptr(), send.numel(), counts.ctypes.data, sw.ctypes.data),
+                    "wsort_partition")
+        return counts, sw
+
+    def load_keys(self, recv, counts: np.ndarray):
+        c = np.ascontiguousarray(counts, dtype=np.uint64)
+        self._check(self._lib.wsort_load_keys(self._h, recv.data_ptr() if recv.numel() else None, c.ctypes.data,
+                                              c.shape[0]), "wsort_load_keys")
+
+    def set_global(self, ghist: np.ndarray, word_base: int, byte_base: int):
+        g = np.ascontiguousarray(ghist, dtype=np.uint64)
+        self._check(self._lib.wsort_set_global(self._h, g.ctypes.data, int(word_base), int(byte_base)), "wsort_set_global")
+
     # ------------------------------------------------------------------ measurement
     def set_profiling(self, on: bool):
         self._check(self._lib.wsort_set_profiling(self._h, 1 if on else 0), "wsort_set_profiling")
@@ -162,6 +197,19 @@ class WSort:
 
     def launch_count(self) -> int:
         return int(self._lib.wsort_launch_count(self._h))
+
+
+def select_splitters(samples: np.ndarray, nparts: int) -> np.ndarray:
+    """Host-side splitter choice (libwsort wsort_select_splitters): records sorted by (L, key, rank)."""
+    lib = L.load()
+    smp = np.ascontiguousarray(samples, dtype=np.uint32)
+    n, rw = smp.shape
+    out = np.zeros((max(nparts - 1, 0), rw), np.uint32)
+    if nparts > 1:
+        rc = lib.wsort_select_splitters(smp.ctypes.data, n, rw, nparts, out.ctypes.data)
+        if rc != L.OK:
+            raise WSortError(rc, "wsort_select_splitters")
+    return out
 
 
 def _as_buffer(text):

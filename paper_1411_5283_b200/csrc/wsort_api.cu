@@ -24,7 +24,7 @@ using namespace wsort;
 
 namespace {
 
-enum State { ST_CREATED = 0, ST_LOADED = 1, ST_TOKENIZED = 2, ST_SORTED = 3 };
+enum State { ST_CREATED = 0, ST_LOADED = 1, ST_TOKENIZED = 2, ST_PACKED = 3, ST_SORTED = 4 };
 
 struct DevBuf {
     void *p = nullptr;
@@ -72,6 +72,15 @@ struct wsort_ctx {
     size_t h_plan_cap = 0;
     bool sorted_with_src = false;
     int last_algo = 0;
+    bool packed_pending = false;   // keys_a holds packed, not yet sorted keys (wsort_pack / load_keys)
+    bool keys_external = false;    // the keys came from wsort_load_keys (no local text behind them)
+
+    // multi-GPU: global view for wsort_fetch
+    bool has_global = false;
+    uint64_t goff[kHistBins + 1] = {0};
+    uint32_t gmax = 0;
+    uint64_t word_base = 0, byte_base = 0;
+    DevBuf bk, d_counts, d_cursor, d_sbase, d_split, d_lohi, d_tiles, d_ranges;
 
     // profiling
     bool prof = false;
@@ -260,7 +269,8 @@ void wsort_destroy(wsort_ctx *c) {
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->text_alloc, &c->cta_hist, &c->cta_base, &c->d_sum, &c->keys_a, &c->keys_b,
                       &c->pay_a, &c->pay_b, &c->words, &c->src_off, &c->dh, &c->status0, &c->status1,
-                      &c->tickets, &c->plan, &c->va_x, &c->va_y, &c->splits};
+                      &c->tickets, &c->plan, &c->va_x, &c->va_y, &c->splits, &c->bk, &c->d_counts,
+                      &c->d_cursor, &c->d_sbase, &c->d_split, &c->d_lohi, &c->d_tiles, &c->d_ranges};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_sum) cudaFreeHost(c->h_sum);
@@ -289,6 +299,10 @@ int wsort_load_text(wsort_ctx *c, const void *bytes, uint64_t n, int mem, uint64
                        (unsigned long long)WSORT_MAX_SHARD_BYTES);
     cudaSetDevice(c->device);
     c->state = ST_CREATED;
+    c->packed_pending = false;
+    c->keys_external = false;
+    c->has_global = false;
+    c->word_base = c->byte_base = 0;
     uint64_t nsteps = (n + kTkStep - 1) / kTkStep;
     size_t need = kTextFrontPad + nsteps * kTkStep + kTkHalo + 64;
     int rc = ensure(c, c->text_alloc, need, "text");
@@ -490,9 +504,11 @@ int sort_radix(wsort_ctx *c, bool want_src) {
     tk.keys = ka;
     tk.payload = pa;
     const double key_bytes = (double)key_words * 4;
-    rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes + (want_src ? 4.0 * W : 0.0),
-                [&] { return launch_pack_scatter(tk, c->stream); });
-    if (rc) return rc;
+    if (!c->packed_pending) {
+        rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes + (want_src ? 4.0 * W : 0.0),
+                    [&] { return launch_pack_scatter(tk, c->stream); });
+        if (rc) return rc;
+    }
 
     if (npasses) {
         CK(cudaMemsetAsync(c->dh.p, 0, (size_t)P.dh_rows * kRadixBins * 4, c->stream), "memset dh");
@@ -664,9 +680,11 @@ int sort_oets(wsort_ctx *c, bool want_src) {
     tk.keys = ka;
     tk.payload = pa;
     const double key_bytes = (double)key_words * 4, elem_bytes = (double)eoff * 4;
-    rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes + (want_src ? 4.0 * W : 0.0),
-                [&] { return launch_pack_scatter(tk, c->stream); });
-    if (rc) return rc;
+    if (!c->packed_pending) {
+        rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes + (want_src ? 4.0 * W : 0.0),
+                    [&] { return launch_pack_scatter(tk, c->stream); });
+        if (rc) return rc;
+    }
     OetsArgs oa{};
     oa.buckets = d_bk;
     oa.tiles = reinterpret_cast<const TileDesc *>(dp + o_sort);
@@ -719,12 +737,16 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     if (algo != WSORT_ALGO_AUTO && algo != WSORT_ALGO_LSD_RADIX && algo != WSORT_ALGO_OETS_MERGE)
         return set_err(c, WSORT_E_INVALID_ARG, "bad algo %d", algo);
     if (flags & ~WSORT_FLAG_SRC_OFF) return set_err(c, WSORT_E_INVALID_ARG, "bad flags 0x%x", flags);
+    if (c->keys_external && !c->packed_pending)
+        return set_err(c, WSORT_E_STATE, "keys from wsort_load_keys were already sorted; load them again");
+    if (c->packed_pending && (flags & WSORT_FLAG_SRC_OFF))
+        return set_err(c, WSORT_E_INVALID_ARG, "src_off is not available for packed / exchanged keys");
     cudaSetDevice(c->device);
     const bool want_src = (flags & WSORT_FLAG_SRC_OFF) != 0;
-    int rc;
-    rc = algo == WSORT_ALGO_OETS_MERGE ? sort_oets(c, want_src) : sort_radix(c, want_src);
+    const int rc = algo == WSORT_ALGO_OETS_MERGE ? sort_oets(c, want_src) : sort_radix(c, want_src);
+    c->packed_pending = false;
     if (rc) {
-        c->state = ST_TOKENIZED;
+        c->state = c->keys_external ? ST_CREATED : ST_TOKENIZED;
         return rc;
     }
     c->sorted_with_src = want_src;
@@ -741,14 +763,15 @@ int wsort_fetch(wsort_ctx *c, wsort_result *r) {
     const Summary &s = *c->h_sum;
     r->n_words = s.n_words;
     r->words_len = s.byte_off[256];
-    r->max_len = s.max_len;
-    r->word_base = 0;
-    r->byte_base = 0;
+    r->max_len = c->has_global ? c->gmax : s.max_len;
+    r->word_base = c->word_base;
+    r->byte_base = c->byte_base;
     const bool sorted = c->state == ST_SORTED;
     if (!sorted && (r->words || r->src_off))
         return set_err(c, WSORT_E_STATE, "words/src_off requested before wsort_sort");
     if (r->src_off && !c->sorted_with_src) return set_err(c, WSORT_E_STATE, "src_off needs WSORT_FLAG_SRC_OFF");
-    const uint32_t noff = s.max_len + 2;
+    const uint32_t noff = r->max_len + 2;
+    const uint64_t *offs = c->has_global ? c->goff : s.off;
     if ((r->bucket_off && r->bucket_cap < noff) || (r->words && r->words_cap < r->words_len) ||
         (r->src_off && r->src_cap < r->n_words))
         return set_err(c, WSORT_E_BUFFER_TOO_SMALL, "fetch: buffer too small");
@@ -760,9 +783,9 @@ int wsort_fetch(wsort_ctx *c, wsort_result *r) {
     CK(cudaStreamSynchronize(c->stream), "fetch");
     if (r->bucket_off) {
         if (r->mem == WSORT_MEM_HOST) {
-            memcpy(r->bucket_off, s.off, noff * sizeof(uint64_t));
+            memcpy(r->bucket_off, offs, noff * sizeof(uint64_t));
         } else {
-            CK(cudaMemcpy(r->bucket_off, s.off, noff * sizeof(uint64_t), cudaMemcpyHostToDevice), "fetch off");
+            CK(cudaMemcpy(r->bucket_off, offs, noff * sizeof(uint64_t), cudaMemcpyHostToDevice), "fetch off");
         }
     }
     return WSORT_OK;
@@ -817,5 +840,276 @@ int wsort_reset_kernel_stats(wsort_ctx *c) {
 }
 
 uint64_t wsort_launch_count(const wsort_ctx *c) { return c ? c->launches : 0; }
+
+}  // extern "C"
+
+// ====================================================================================
+// Multi-GPU stages: pack -> sample -> [all-gather] -> select splitters ->
+// partition -> [all-to-all] -> load_keys -> sort -> set_global -> fetch. Keys-only.
+// The collectives run outside the library (torch.distributed / NCCL over NVLink); every data step
+// between them is a kernel here.
+// ====================================================================================
+namespace {
+
+std::vector<BucketInfo> bucket_table(const Summary &s) {
+    std::vector<BucketInfo> bk(256, BucketInfo{});
+    for (uint32_t L = 1; L <= s.max_len && L < 256; L++) {
+        BucketInfo &b = bk[L];
+        b.key_off = s.key_off[L];
+        b.word_off = s.off[L];
+        b.byte_off = s.byte_off[L];
+        b.n = (uint32_t)(s.off[L + 1] - s.off[L]);
+        b.kw = kw_of(L);
+        b.elem_off = b.key_off;
+        b.estride = b.kw;
+    }
+    return bk;
+}
+
+int upload_small(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const char *what) {
+    int rc = ensure(c, dst, bytes, what);
+    if (rc) return rc;
+    if (bytes) CK(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, c->stream), what);
+    return WSORT_OK;
+}
+
+// Fill the host summary from per-length counts (local bucket layout of packed keys).
+void summary_from_counts(Summary &s, const uint64_t *n_per_len) {
+    memset(&s, 0, sizeof s);
+    uint64_t o = 0, ko = 0, bo = 0, letters = 0;
+    uint32_t lmax = 0;
+    for (int L = 0; L < 256; L++) {
+        s.off[L] = o;
+        s.key_off[L] = ko;
+        s.byte_off[L] = bo;
+        const uint64_t h = L ? n_per_len[L] : 0;
+        o += h;
+        ko += h * (uint64_t)kw_of(L);
+        bo += h * (uint64_t)(L + 1);
+        letters += h * (uint64_t)L;
+        if (h) lmax = (uint32_t)L;
+    }
+    s.off[256] = o;
+    s.key_off[256] = ko;
+    s.byte_off[256] = bo;
+    s.n_words = o;
+    s.letters = letters;
+    s.max_len = lmax;
+}
+
+}  // namespace
+
+extern "C" {
+
+int wsort_histogram(wsort_ctx *c, uint64_t *hist) {
+    if (!c || !hist) return WSORT_E_INVALID_ARG;
+    if (c->state < ST_TOKENIZED) return set_err(c, WSORT_E_STATE, "wsort_histogram before wsort_tokenize");
+    const Summary &s = *c->h_sum;
+    for (int L = 0; L < 256; L++) hist[L] = s.off[L + 1] - s.off[L];
+    return WSORT_OK;
+}
+
+int wsort_pack(wsort_ctx *c) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    if (c->state != ST_TOKENIZED || c->keys_external)
+        return set_err(c, WSORT_E_STATE, "wsort_pack needs a freshly tokenized text");
+    cudaSetDevice(c->device);
+    const Summary &s = *c->h_sum;
+    std::vector<BucketInfo> bk = bucket_table(s);
+    int rc;
+    if ((rc = upload_small(c, c->bk, bk.data(), bk.size() * sizeof(BucketInfo), "bucket table"))) return rc;
+    if ((rc = ensure(c, c->keys_a, s.key_off[256] * 4 + 64, "keys_a"))) return rc;
+    TkArgs &tk = c->tk;
+    tk.buckets = static_cast<const BucketInfo *>(c->bk.p);
+    tk.keys = static_cast<uint32_t *>(c->keys_a.p);
+    tk.payload = nullptr;
+    rc = launch(c, "k3_pack_scatter", (double)c->n + (double)s.key_off[256] * 4,
+                [&] { return launch_pack_scatter(tk, c->stream); });
+    if (rc) return rc;
+    c->packed_pending = true;
+    c->state = ST_PACKED;
+    return WSORT_OK;
+}
+
+int wsort_sample(wsort_ctx *c, uint32_t nsamples, uint32_t rank, uint32_t rec_words, uint32_t *dev_records) {
+    if (!c || (nsamples && !dev_records) || rec_words < 3) return WSORT_E_INVALID_ARG;
+    if (c->state != ST_PACKED || !c->packed_pending) return set_err(c, WSORT_E_STATE, "wsort_sample needs packed keys");
+    const Summary &s = *c->h_sum;
+    if (rec_words < 2 + (uint32_t)kw_of((int)s.max_len))
+        return set_err(c, WSORT_E_INVALID_ARG, "rec_words %u < 2 + kw(%u)", rec_words, s.max_len);
+    cudaSetDevice(c->device);
+    DistArgs a{};
+    a.buckets = static_cast<const BucketInfo *>(c->bk.p);
+    a.off = reinterpret_cast<const uint64_t *>(static_cast<const uint8_t *>(c->d_sum.p) + offsetof(Summary, off));
+    a.keys = static_cast<const uint32_t *>(c->keys_a.p);
+    a.n_words = s.n_words;
+    a.rank = rank;
+    a.rec_words = rec_words;
+    a.nsamples = nsamples;
+    a.records = dev_records;
+    return launch(c, "k6a_sample", (double)nsamples * rec_words * 8, [&] { return launch_sample(a, c->stream); });
+}
+
+static int cmp_records(const uint32_t *x, const uint32_t *y, uint32_t rec_words) {
+    if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;              // length
+    for (uint32_t u = 2; u < rec_words; u++)                     // key words
+        if (x[u] != y[u]) return x[u] < y[u] ? -1 : 1;
+    if (x[1] != y[1]) return x[1] < y[1] ? -1 : 1;              // source rank
+    return 0;
+}
+
+int wsort_select_splitters(const uint32_t *samples, uint64_t nsamples, uint32_t rec_words, uint32_t nparts,
+                           uint32_t *splitters) {
+    if (!samples || !splitters || nparts < 1 || nparts > kMaxRanks || rec_words < 3 || nsamples < nparts)
+        return WSORT_E_INVALID_ARG;
+    std::vector<uint64_t> idx(nsamples);
+    for (uint64_t i = 0; i < nsamples; i++) idx[i] = i;
+    std::sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) {
+        const int r = cmp_records(samples + a * rec_words, samples + b * rec_words, rec_words);
+        return r < 0 || (r == 0 && a < b);
+    });
+    for (uint32_t d = 1; d < nparts; d++) {
+        const uint64_t k = (d * nsamples) / nparts;
+        memcpy(splitters + (size_t)(d - 1) * rec_words, samples + idx[k] * rec_words, rec_words * 4);
+    }
+    return WSORT_OK;
+}
+
+int wsort_partition(wsort_ctx *c, const uint32_t *splitters, uint32_t nparts, uint32_t rec_words, uint32_t rank,
+                    uint32_t *dev_send, uint64_t send_cap_words, uint64_t *counts, uint64_t *send_words) {
+    if (!c || !counts || !send_words || nparts < 1 || nparts > kMaxRanks || (nparts > 1 && !splitters) ||
+        rank >= nparts)
+        return WSORT_E_INVALID_ARG;
+    if (c->state != ST_PACKED || !c->packed_pending) return set_err(c, WSORT_E_STATE, "wsort_partition needs packed keys");
+    const Summary &s = *c->h_sum;
+    if (send_cap_words < s.key_off[256] || (s.key_off[256] && !dev_send))
+        return set_err(c, WSORT_E_BUFFER_TOO_SMALL, "send buffer needs %llu words", (unsigned long long)s.key_off[256]);
+    cudaSetDevice(c->device);
+    int rc;
+    // splitter lookup ranges per length
+    std::vector<uint32_t> lohi(512, 0);
+    for (uint32_t L = 0; L < 256; L++) {
+        uint32_t lo = 0, hi = 0;
+        for (uint32_t d = 0; d + 1 < nparts; d++) {
+            const uint32_t sl = splitters[(size_t)d * rec_words];   // splitter length
+            lo += sl < L;
+            hi += sl <= L;
+        }
+        lohi[L] = lo;
+        lohi[256 + L] = hi;
+    }
+    std::vector<TileDesc> tiles;
+    for (uint32_t L = 1; L <= s.max_len; L++) {
+        const uint64_t n = s.off[L + 1] - s.off[L];
+        for (uint64_t i = 0; i * kDistTileKeys < n; i++) tiles.push_back(TileDesc{L, (uint32_t)i});
+    }
+    if (nparts > 1 && (rc = upload_small(c, c->d_split, splitters, (size_t)(nparts - 1) * rec_words * 4, "splitters")))
+        return rc;
+    if ((rc = ensure(c, c->d_split, 16, "splitters"))) return rc;
+    if ((rc = upload_small(c, c->d_lohi, lohi.data(), lohi.size() * 4, "split ranges"))) return rc;
+    if ((rc = upload_small(c, c->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc) + 8, "partition tiles"))) return rc;
+    if ((rc = ensure(c, c->d_counts, (size_t)nparts * 256 * 4, "counts"))) return rc;
+    if ((rc = ensure(c, c->d_cursor, (size_t)nparts * 256 * 4, "cursor"))) return rc;
+    if ((rc = ensure(c, c->d_sbase, (size_t)nparts * 256 * 8, "send base"))) return rc;
+    CK(cudaMemsetAsync(c->d_counts.p, 0, (size_t)nparts * 256 * 4, c->stream), "memset counts");
+    CK(cudaMemsetAsync(c->d_cursor.p, 0, (size_t)nparts * 256 * 4, c->stream), "memset cursor");
+    DistArgs a{};
+    a.buckets = static_cast<const BucketInfo *>(c->bk.p);
+    a.tiles = static_cast<const TileDesc *>(c->d_tiles.p);
+    a.ntiles = (uint32_t)tiles.size();
+    a.keys = static_cast<const uint32_t *>(c->keys_a.p);
+    a.n_words = s.n_words;
+    a.rank = rank;
+    a.nparts = nparts;
+    a.rec_words = rec_words;
+    a.splitters = static_cast<const uint32_t *>(c->d_split.p);
+    a.split_lo = static_cast<const uint32_t *>(c->d_lohi.p);
+    a.split_hi = a.split_lo + 256;
+    a.counts = static_cast<uint32_t *>(c->d_counts.p);
+    a.cursor = static_cast<uint32_t *>(c->d_cursor.p);
+    a.send_base = static_cast<const uint64_t *>(c->d_sbase.p);
+    a.send = dev_send;
+    rc = launch(c, "k6b_part_count", (double)s.key_off[256] * 4, [&] { return launch_part_count(a, c->stream); });
+    if (rc) return rc;
+    std::vector<uint32_t> hc((size_t)nparts * 256);
+    CK(cudaMemcpyAsync(hc.data(), c->d_counts.p, hc.size() * 4, cudaMemcpyDeviceToHost, c->stream), "counts D2H");
+    CK(cudaStreamSynchronize(c->stream), "partition counts");
+    std::vector<uint64_t> base((size_t)nparts * 256);
+    uint64_t w = 0;
+    for (uint32_t d = 0; d < nparts; d++) {
+        const uint64_t w0 = w;
+        for (uint32_t L = 0; L < 256; L++) {
+            counts[(size_t)d * 256 + L] = hc[(size_t)d * 256 + L];
+            base[(size_t)d * 256 + L] = w;
+            w += (uint64_t)hc[(size_t)d * 256 + L] * (uint64_t)kw_of((int)L);
+        }
+        send_words[d] = w - w0;
+    }
+    if ((rc = upload_small(c, c->d_sbase, base.data(), base.size() * 8, "send base"))) return rc;
+    return launch(c, "k6b_part_scatter", (double)s.key_off[256] * 8, [&] { return launch_part_scatter(a, c->stream); });
+}
+
+int wsort_load_keys(wsort_ctx *c, const uint32_t *dev_recv, const uint64_t *counts, uint32_t nparts) {
+    if (!c || !counts || nparts < 1 || nparts > kMaxRanks) return WSORT_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    std::vector<uint64_t> n(256, 0);
+    for (uint32_t src = 0; src < nparts; src++)
+        for (uint32_t L = 1; L < 256; L++) n[L] += counts[(size_t)src * 256 + L];
+    for (uint32_t src = 0; src < nparts; src++)
+        if (counts[(size_t)src * 256] != 0) return set_err(c, WSORT_E_INVALID_ARG, "counts of length 0");
+    Summary &s = *c->h_sum;
+    summary_from_counts(s, n.data());
+    if (s.key_off[256] && !dev_recv) return WSORT_E_INVALID_ARG;
+    int rc;
+    if ((rc = ensure(c, c->keys_a, s.key_off[256] * 4 + 64, "keys_a"))) return rc;
+    // received layout: [src][L][keys]; local bucket L = src-ordered concatenation
+    std::vector<CopyRange> ranges;
+    std::vector<uint64_t> fill(256, 0);
+    uint64_t from = 0;
+    for (uint32_t src = 0; src < nparts; src++)
+        for (uint32_t L = 1; L < 256; L++) {
+            const uint64_t cnt = counts[(size_t)src * 256 + L];
+            if (!cnt) continue;
+            const uint64_t words = cnt * (uint64_t)kw_of((int)L);
+            uint64_t to = s.key_off[L] + fill[L];
+            for (uint64_t o = 0; o < words; o += 16384) {
+                const uint32_t len = (uint32_t)std::min<uint64_t>(16384, words - o);
+                ranges.push_back(CopyRange{from + o, to + o, len, 0});
+            }
+            fill[L] += words;
+            from += words;
+        }
+    if ((rc = upload_small(c, c->d_ranges, ranges.data(), ranges.size() * sizeof(CopyRange) + 8, "ranges"))) return rc;
+    rc = launch(c, "k6c_regroup", (double)s.key_off[256] * 8, [&] {
+        return launch_regroup(static_cast<const CopyRange *>(c->d_ranges.p), (uint32_t)ranges.size(), dev_recv,
+                              static_cast<uint32_t *>(c->keys_a.p), c->stream);
+    });
+    if (rc) return rc;
+    c->n = 0;
+    c->packed_pending = true;
+    c->keys_external = true;
+    c->has_global = false;
+    c->state = ST_PACKED;
+    return WSORT_OK;
+}
+
+int wsort_set_global(wsort_ctx *c, const uint64_t *ghist, uint64_t word_base, uint64_t byte_base) {
+    if (!c || !ghist) return WSORT_E_INVALID_ARG;
+    uint64_t o = 0;
+    uint32_t lmax = 0;
+    for (int L = 0; L < 256; L++) {
+        c->goff[L] = o;
+        o += L ? ghist[L] : 0;
+        if (L && ghist[L]) lmax = (uint32_t)L;
+    }
+    c->goff[256] = o;
+    c->gmax = lmax;
+    // off[] has max_len + 2 entries: off[lmax + 1] = W
+    c->goff[lmax + 1] = o;
+    c->word_base = word_base;
+    c->byte_base = byte_base;
+    c->has_global = true;
+    return WSORT_OK;
+}
 
 }  // extern "C"

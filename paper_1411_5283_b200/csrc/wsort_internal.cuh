@@ -135,6 +135,36 @@ struct MergeArgs {
 cudaError_t launch_oets_tile_sort(const OetsArgs &a, cudaStream_t s);
 cudaError_t launch_merge_pass(const MergeArgs &a, cudaStream_t s);
 
+// ---------------- multi-GPU exchange (sample sort) ----------------
+constexpr uint32_t kMaxRanks = 64;
+constexpr uint32_t kDistTileKeys = 4096;
+struct CopyRange {
+    uint64_t from, to;             // u32 words
+    uint32_t len, pad_;
+};
+struct DistArgs {
+    const BucketInfo *buckets;
+    const uint64_t *off;           // off[0..256] (device)
+    const TileDesc *tiles;         // partition tiles (kDistTileKeys keys)
+    uint32_t ntiles;
+    const uint32_t *keys;          // packed keys (K3 output)
+    uint64_t n_words;
+    uint32_t rank, nparts, rec_words, nsamples;
+    uint32_t *records;             // sample records out [nsamples][rec_words]
+    const uint32_t *splitters;     // [nparts-1][rec_words], sorted
+    const uint32_t *split_lo;      // [256] #splitters with length < L
+    const uint32_t *split_hi;      // [256] #splitters with length <= L
+    uint32_t *counts;              // [nparts][256] keys per (dest, L)
+    uint32_t *cursor;              // [nparts][256] scatter cursors
+    const uint64_t *send_base;     // [nparts][256] u32-word offset of each (dest, L) range
+    uint32_t *send;
+};
+cudaError_t launch_sample(const DistArgs &a, cudaStream_t s);
+cudaError_t launch_part_count(const DistArgs &a, cudaStream_t s);
+cudaError_t launch_part_scatter(const DistArgs &a, cudaStream_t s);
+cudaError_t launch_regroup(const CopyRange *ranges, uint32_t nranges, const uint32_t *recv, uint32_t *keys,
+                           cudaStream_t s);
+
 struct EmitArgs {
     const BucketInfo *buckets;
     const TileDesc *tiles;

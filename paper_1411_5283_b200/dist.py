@@ -1,0 +1,190 @@
+"""Multi-GPU orchestration: byte-range shards + one sample-sort exchange.
+
+One process per GPU (torchrun); torch.distributed (NCCL over NVLink on B200, gloo on CPU for the
+host-logic tests) carries the four collectives; every data step between them is a libwsort kernel:
+
+    rank r:  load_text(shard_r, global_base=cut_r) -> tokenize (K1, K2) -> histogram
+             all_reduce(histogram)                                   -> global bucket offsets
+             pack (K3) -> sample (K6a)  ->  all_gather(samples)      -> select_splitters (host, same on all ranks)
+             partition (K6b)            ->  all_to_all(counts), all_to_all_v(keys)
+             load_keys (K6c regroup) -> sort (K4, K5)
+             all_gather(local sizes)                                 -> word_base, byte_base
+
+The global order is (length, key, source rank): the concatenation of the ranks' outputs in rank
+order is byte-identical to the one-GPU output (tests/test_gpu_dist.py, tests/test_dist_cpu.py).
+This replaces the paper's MPI master/slave scatter-gather by a symmetric exchange.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def kw_of(L):
+    return (np.asarray(L) + 5) // 6
+
+
+KW = kw_of(np.arange(256)).astype(np.uint64)
+
+
+def _is_letter(c: int) -> bool:
+    return ((c | 0x20) - 0x61) & 0xFF < 26
+
+
+def shard_cuts(text, nparts: int) -> list:
+    """Reading A13: nominal cut g*N/P moved forward while text[cut-1] and text[cut] are both letters."""
+    n = len(text)
+    cuts = [0]
+    for g in range(1, nparts):
+        c = max(cuts[-1], (g * n) // nparts)
+        while 0 < c < n and _is_letter(int(text[c - 1])) and _is_letter(int(text[c])):
+            c += 1
+        cuts.append(c)
+    cuts.append(n)
+    return cuts
+
+
+# ---------------------------------------------------------------------------------------- comms
+class TorchComm:
+    """The four collectives over torch.distributed (NCCL for cuda tensors, gloo for cpu tensors)."""
+
+    def __init__(self, device: str):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.device = torch, dist, device
+        self.rank, self.size = dist.get_rank(), dist.get_world_size()
+        # gloo carries cpu tensors only: stage device data through host memory (host-logic tests)
+        self.wire = "cpu" if dist.get_backend() == "gloo" else device
+
+    def all_reduce_u64(self, x: np.ndarray) -> np.ndarray:
+        t = self.torch.from_numpy(x.astype(np.int64)).to(self.wire)
+        self.dist.all_reduce(t)
+        return t.cpu().numpy().astype(np.uint64)
+
+    def all_gather_rows(self, x):
+        """x: tensor [n, w] -> numpy [size*n, w]."""
+        x = x.contiguous().to(self.wire)
+        out = self.torch.empty((self.size * x.shape[0], x.shape[1]), dtype=x.dtype, device=x.device)
+        self.dist.all_gather_into_tensor(out, x)
+        return out.cpu().numpy()
+
+    def all_to_all_counts(self, counts: np.ndarray) -> np.ndarray:
+        """counts[dest, L] (this rank's) -> recv[src, L] (what every src sends to this rank)."""
+        t = self.torch.from_numpy(counts.astype(np.int64)).to(self.wire)
+        out = self.torch.empty_like(t)
+        self.dist.all_to_all_single(out, t)
+        return out.cpu().numpy().astype(np.uint64)
+
+    def all_to_all_v(self, send, send_words, recv_words):
+        dev = send.device
+        src = send[: int(sum(send_words))].to(self.wire)
+        out = self.torch.empty(int(sum(recv_words)), dtype=send.dtype, device=self.wire)
+        self.dist.all_to_all_single(out, src, [int(x) for x in recv_words], [int(x) for x in send_words])
+        return out.to(dev)
+
+    def barrier(self):
+        self.dist.barrier()
+
+
+# ---------------------------------------------------------------------------------------- stages
+@dataclass
+class RankResult:
+    n_words: int
+    words_len: int
+    word_base: int
+    byte_base: int
+
+
+class DistSorter:
+    """The per-rank stages between collectives (a small state machine over one WSort context)."""
+
+    def __init__(self, ws, rank: int, nparts: int, nsamples: int = 1024):
+        import torch
+
+        self.torch = torch
+        self.ws, self.rank, self.nparts, self.nsamples = ws, rank, nparts, nsamples
+        self.device = ws.torch_device
+
+    def stage_tokenize(self, shard, global_base: int) -> np.ndarray:
+        self.ws.load_text(shard, global_base)
+        self.ws.tokenize()
+        return self.ws.histogram()
+
+    def stage_sample(self, ghist: np.ndarray):
+        self.ghist = ghist
+        nz = np.nonzero(ghist[1:])[0]
+        lmax = int(nz[-1]) + 1 if nz.size else 1
+        self.rec_words = 2 + int(kw_of(lmax))
+        self.ws.pack()
+        rec = self.torch.zeros((self.nsamples, self.rec_words), dtype=self.torch.int32, device=self.device)
+        self.ws.sample(self.nsamples, self.rank, self.rec_words, rec)
+        return rec
+
+    def stage_partition(self, all_samples: np.ndarray):
+        from .api import select_splitters
+
+        spl = select_splitters(all_samples.view(np.uint32), self.nparts)
+        local_words = int((self.ws.histogram() * KW).sum())
+        send = self.torch.empty(max(local_words, 1), dtype=self.torch.int32, device=self.device)
+        counts, send_words = self.ws.partition(spl, self.nparts, self.rec_words, self.rank, send)
+        return counts, send, send_words
+
+    @staticmethod
+    def recv_words(recv_counts: np.ndarray) -> np.ndarray:
+        return (recv_counts.astype(np.uint64) * KW[None, :]).sum(axis=1)
+
+    def stage_sort(self, recv, recv_counts: np.ndarray, algo: str = "auto"):
+        self.ws.load_keys(recv, recv_counts)
+        self.ws.sort(algo)
+        s = self.ws.sizes()
+        return np.array([s.n_words, s.words_len], np.uint64)
+
+    def stage_finish(self, all_sizes: np.ndarray) -> RankResult:
+        wb = int(all_sizes[: self.rank, 0].sum())
+        bb = int(all_sizes[: self.rank, 1].sum())
+        self.ws.set_global(self.ghist, wb, bb)
+        return RankResult(int(all_sizes[self.rank, 0]), int(all_sizes[self.rank, 1]), wb, bb)
+
+
+def sort_distributed(ws, shard, global_base: int, comm, algo: str = "auto", nsamples: int = 1024) -> RankResult:
+    """One distributed sort step on this rank (all ranks must call it)."""
+    ds = DistSorter(ws, comm.rank, comm.size, nsamples)
+    hist = ds.stage_tokenize(shard, global_base)
+    ghist = comm.all_reduce_u64(hist)
+    rec = ds.stage_sample(ghist)
+    all_samples = comm.all_gather_rows(rec)
+    counts, send, send_words = ds.stage_partition(all_samples)
+    recv_counts = comm.all_to_all_counts(counts)
+    recv = comm.all_to_all_v(send, send_words, ds.recv_words(recv_counts))
+    sizes = ds.stage_sort(recv, recv_counts, algo)
+    all_sizes = comm.all_gather_rows(ds.torch.from_numpy(sizes.astype(np.int64)).view(1, 2).to(comm.device))
+    return ds.stage_finish(all_sizes.astype(np.uint64))
+
+
+def sort_emulated(make_ws, text: np.ndarray, nparts: int, algo: str = "auto", nsamples: int = 1024):
+    """Run the P-rank pipeline for P virtual ranks in one process (one GPU), performing the
+    collectives by host-side concatenation. No kernel waits on another: stages run in lockstep.
+    Returns (list of (ws, RankResult), cuts)."""
+    import torch
+
+    cuts = shard_cuts(text, nparts)
+    sorters = [DistSorter(make_ws(), r, nparts, nsamples) for r in range(nparts)]
+    hists = [s.stage_tokenize(np.ascontiguousarray(text[cuts[r]: cuts[r + 1]]), cuts[r]) for r, s in enumerate(sorters)]
+    ghist = np.sum(hists, axis=0).astype(np.uint64)
+    recs = [s.stage_sample(ghist) for s in sorters]
+    all_samples = torch.cat(recs).cpu().numpy()
+    parts = [s.stage_partition(all_samples) for s in sorters]
+    sizes = []
+    for r, s in enumerate(sorters):
+        recv_counts = np.stack([parts[src][0][r] for src in range(nparts)]).astype(np.uint64)
+        pieces = []
+        for src in range(nparts):
+            counts_src, send_src, sw_src = parts[src]
+            start = int(sw_src[:r].sum())
+            pieces.append(send_src[start: start + int(sw_src[r])])
+        recv = torch.cat(pieces) if pieces else torch.empty(0, dtype=torch.int32, device=s.device)
+        sizes.append(s.stage_sort(recv, recv_counts, algo))
+    all_sizes = np.stack(sizes).astype(np.uint64)
+    return [(s.ws, s.stage_finish(all_sizes)) for s in sorters], cuts
