@@ -867,9 +867,9 @@ std::vector<BucketInfo> bucket_table(const Summary &s) {
 }
 
 int upload_small(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const char *what) {
-    int rc = ensure(c, dst, bytes, what);
+    int rc = ensure(c, dst, bytes, what);   // ensure() allocates at least 16 bytes
     if (rc) return rc;
-    if (bytes) CK(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, c->stream), what);
+    if (bytes && src) CK(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, c->stream), what);
     return WSORT_OK;
 }
 
@@ -1007,7 +1007,7 @@ int wsort_partition(wsort_ctx *c, const uint32_t *splitters, uint32_t nparts, ui
         return rc;
     if ((rc = ensure(c, c->d_split, 16, "splitters"))) return rc;
     if ((rc = upload_small(c, c->d_lohi, lohi.data(), lohi.size() * 4, "split ranges"))) return rc;
-    if ((rc = upload_small(c, c->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc) + 8, "partition tiles"))) return rc;
+    if ((rc = upload_small(c, c->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc), "partition tiles"))) return rc;
     if ((rc = ensure(c, c->d_counts, (size_t)nparts * 256 * 4, "counts"))) return rc;
     if ((rc = ensure(c, c->d_cursor, (size_t)nparts * 256 * 4, "cursor"))) return rc;
     if ((rc = ensure(c, c->d_sbase, (size_t)nparts * 256 * 8, "send base"))) return rc;
@@ -1079,7 +1079,7 @@ int wsort_load_keys(wsort_ctx *c, const uint32_t *dev_recv, const uint64_t *coun
             fill[L] += words;
             from += words;
         }
-    if ((rc = upload_small(c, c->d_ranges, ranges.data(), ranges.size() * sizeof(CopyRange) + 8, "ranges"))) return rc;
+    if ((rc = upload_small(c, c->d_ranges, ranges.data(), ranges.size() * sizeof(CopyRange), "ranges"))) return rc;
     rc = launch(c, "k6c_regroup", (double)s.key_off[256] * 8, [&] {
         return launch_regroup(static_cast<const CopyRange *>(c->d_ranges.p), (uint32_t)ranges.size(), dev_recv,
                               static_cast<uint32_t *>(c->keys_a.p), c->stream);
