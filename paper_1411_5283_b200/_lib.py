@@ -25,7 +25,8 @@ MEM_DEVICE = 1
 ALGO_AUTO = 0
 ALGO_OETS_MERGE = 1
 ALGO_LSD_RADIX = 2
-ALGOS = {"auto": ALGO_AUTO, "oets_merge": ALGO_OETS_MERGE, "lsd_radix": ALGO_LSD_RADIX}
+ALGO_MSD_RADIX = 3
+ALGOS = {"auto": ALGO_AUTO, "oets_merge": ALGO_OETS_MERGE, "lsd_radix": ALGO_LSD_RADIX, "msd_radix": ALGO_MSD_RADIX}
 
 FLAG_SRC_OFF = 0x1
 MAX_WORD_LEN = 255

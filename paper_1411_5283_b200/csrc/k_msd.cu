@@ -1,0 +1,491 @@
+// k_msd.cu — phase 3, variant B+ ("msd_radix"): most-significant-digit
+// radix partitioning of every length bucket ("sort each vector ... in the alphabetic
+// order"), finished by CTA-local odd-even transposition sorts (the data-parallel bubble sort of
+// PAPER.md:23) of the small sub-buckets.
+//
+// Keys only: equal keys are identical words, so no pass has to be stable. A level-l pass splits
+// every "big" segment by its l-th 2-letter digit:
+//   k_msd_count    per tile: digit histogram in shared memory -> per-segment histogram (atomics)
+//   k_msd_plan     per segment: exclusive scan of its histogram -> child bases / scatter cursors;
+//                  every child is queued as final (its digits are exhausted), tiny (<= 32 keys:
+//                  one warp sorts it), small (<= one CTA tile: one CTA sorts it) or big (next level)
+//   k_msd_scatter  per tile: a shared-memory atomic gives each key its slot inside its digit, one
+//                  global atomic per (tile, digit) reserves the range, keys are reordered in shared
+//                  memory and written out coalesced
+// then k_msd_warp_sort / k_msd_cta_sort finish the tiny / small children and k_msd_copy moves
+// finished runs that ended in buffer A into buffer B. Every key ends in buffer B at its final index.
+#include "wsort_internal.cuh"
+
+namespace wsort {
+namespace {
+
+constexpr int kST = 256;
+constexpr uint32_t kFullM = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t digit_at(const uint32_t *key, uint32_t q) {
+    return (key[q / 3] >> (20 - 10 * (q % 3))) & 1023u;
+}
+
+template <int KW>
+__device__ __forceinline__ uint32_t digit_reg(const uint32_t (&k)[KW], uint32_t q) {
+    uint32_t w = k[0];
+#pragma unroll
+    for (int u = 1; u < KW; u++) w = (q / 3) == (uint32_t)u ? k[u] : w;
+    return (w >> (20 - 10 * (q % 3))) & 1023u;
+}
+
+__device__ __forceinline__ uint32_t block_excl_scan_m(uint32_t v, uint32_t *wsum, uint32_t *total) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(kFullM, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < kST / 32 ? wsum[lane] : 0u, wi = w;
+#pragma unroll
+        for (int o = 1; o < kST / 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(kFullM, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < kST / 32) wsum[lane] = wi - w;
+        if (lane == kST / 32 - 1) wsum[kST / 32] = wi;
+    }
+    __syncthreads();
+    const uint32_t r = wsum[warp] + incl - v;
+    if (total) *total = wsum[kST / 32];
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------- count
+__global__ void __launch_bounds__(kST) k_msd_count(MsdArgs a) {
+    __shared__ uint32_t h[kRadixBins];
+    const int t = threadIdx.x;
+    const MsdTile td = a.tiles[blockIdx.x];
+    const MsdSeg sg = a.segs[td.seg];
+    const BucketInfo b = a.buckets[sg.L];
+    for (int i = t; i < kRadixBins; i += kST) h[i] = 0;
+    __syncthreads();
+    const uint32_t *keys = a.src + b.key_off + (uint64_t)(sg.start + td.off) * b.kw;
+    for (uint32_t k = t; k < td.n; k += kST) atomicAdd(&h[digit_at(keys + (uint64_t)k * b.kw, a.level)], 1u);
+    __syncthreads();
+    uint32_t *gh = a.hist + (size_t)td.seg * kRadixBins;
+    for (int i = t; i < kRadixBins; i += kST)
+        if (h[i]) atomicAdd(&gh[i], h[i]);
+}
+
+// ---------------------------------------------------------------- plan
+__device__ __forceinline__ void close_job(const MsdArgs &a, uint32_t L, uint32_t start, uint32_t n) {
+    if (!n) return;
+    if (n <= 32) {
+        const uint32_t q = atomicAdd(a.ctr + kQTiny, 1u);
+        if (q < a.cap_local) a.q_tiny[q] = MsdSeg{L, start, n, a.dst_is_a};
+    } else {
+        const uint32_t q = atomicAdd(a.ctr + kQSmall, 1u);
+        if (q < a.cap_local) a.q_small[q] = MsdSeg{L, start, n, a.dst_is_a};
+    }
+}
+
+// One CTA per segment of this level: exclusive scan of its digit histogram gives the children's
+// bases (the scatter cursors); thread 0 then walks the children in digit order and queues them:
+//   big (> CTA-sort capacity, digits left)  -> next level (segment + its scatter tiles)
+//   finished and already in B               -> nothing
+//   finished, in A, larger than a CTA tile  -> copy chunks A -> B
+//   everything else                         -> packed greedily into CTA / warp sort jobs of at most
+//                                              one tile; sorting a run of consecutive children by the
+//                                              full key sorts each child (their prefixes differ)
+__global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
+    __shared__ uint32_t wsum[kST / 32 + 1];
+    __shared__ uint32_t cnt_s[kRadixBins], base_s[kRadixBins];
+    const int t = threadIdx.x;
+    const uint32_t s = blockIdx.x;
+    const MsdSeg sg = a.segs[s];
+    const BucketInfo b = a.buckets[sg.L];
+    const uint32_t *h = a.hist + (size_t)s * kRadixBins;
+    uint32_t c[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) c[e] = h[4 * t + e];
+    uint32_t ex = block_excl_scan_m(c[0] + c[1] + c[2] + c[3], wsum, nullptr);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const uint32_t d = 4 * t + e;
+        a.cursor[(size_t)s * kRadixBins + d] = sg.start + ex;
+        cnt_s[d] = c[e];
+        base_s[d] = sg.start + ex;
+        ex += c[e];
+    }
+    __syncthreads();
+    if (t != 0) return;
+    const bool final_digit = a.level + 1 >= b.ndig;
+    const uint32_t cap = b.tile_keys;
+    uint32_t js = 0, jn = 0;   // open job
+    for (uint32_t d = 0; d < kRadixBins; d++) {
+        const uint32_t cnt = cnt_s[d], start = base_s[d];
+        if (!cnt) continue;
+        const bool fin = final_digit || cnt == 1;
+        if (!fin && cnt > cap) {
+            close_job(a, sg.L, js, jn);
+            jn = 0;
+            const uint32_t q = atomicAdd(a.ctr + kQBig, 1u);
+            const uint32_t nt = (cnt + b.aux - 1) / b.aux;
+            const uint32_t tq = atomicAdd(a.ctr + kQTiles, nt);
+            if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, start, cnt, 0};
+            for (uint32_t i = 0; i < nt && tq + i < a.cap_tiles; i++)
+                a.q_tiles[tq + i] = MsdTile{q, i * b.aux, min(b.aux, cnt - i * b.aux), 0};
+        } else if (fin && !a.dst_is_a) {
+            close_job(a, sg.L, js, jn);
+            jn = 0;
+        } else if (fin && cnt > cap) {
+            close_job(a, sg.L, js, jn);
+            jn = 0;
+            const uint32_t words = cnt * b.kw;
+            const uint32_t nch = (words + kMsdCopyChunk - 1) / kMsdCopyChunk;
+            const uint32_t q = atomicAdd(a.ctr + kQCopy, nch);
+            for (uint32_t i = 0; i < nch && q + i < a.cap_copy; i++) {
+                const uint64_t w0 = b.key_off + (uint64_t)start * b.kw + (uint64_t)i * kMsdCopyChunk;
+                a.q_copy[q + i] = CopyRange{w0, w0, min(kMsdCopyChunk, words - i * kMsdCopyChunk), 0};
+            }
+        } else {
+            if (jn + cnt > cap) {
+                close_job(a, sg.L, js, jn);
+                jn = 0;
+            }
+            if (!jn) js = start;
+            jn += cnt;
+        }
+    }
+    close_job(a, sg.L, js, jn);
+}
+
+// ---------------------------------------------------------------- scatter
+template <int KW>
+__device__ __forceinline__ void scatter_tile(const MsdArgs &a, const MsdTile &td, const MsdSeg &sg, const BucketInfo &b,
+                                             uint32_t *sm) {
+    constexpr int KPT = 32 / KW;   // keys per thread (striped)
+    const int t = threadIdx.x;
+    uint32_t *hist = sm, *toff = sm + kRadixBins, *gbase = sm + 2 * kRadixBins, *kout = sm + 3 * kRadixBins;
+    uint32_t *wsum = kout + 8192 + 8192 / 32 + 8;
+    for (int i = t; i < kRadixBins; i += kST) hist[i] = 0;
+    __syncthreads();
+    const uint32_t *src = a.src + b.key_off + (uint64_t)(sg.start + td.off) * KW;
+    uint32_t key[KPT][KW], slot[(KPT + 1) / 2];
+#pragma unroll
+    for (int r = 0; r < (KPT + 1) / 2; r++) slot[r] = 0;
+#pragma unroll
+    for (int r = 0; r < KPT; r++) {
+        const uint32_t i = t + r * kST;
+        if (i < td.n) {
+#pragma unroll
+            for (int u = 0; u < KW; u++) key[r][u] = __ldg(src + (uint64_t)i * KW + u);
+            slot[r / 2] |= atomicAdd(&hist[digit_reg<KW>(key[r], a.level)], 1u) << (16 * (r & 1));
+        }
+    }
+    __syncthreads();
+    uint32_t c[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) c[e] = hist[4 * t + e];
+    uint32_t ex = block_excl_scan_m(c[0] + c[1] + c[2] + c[3], wsum, nullptr);
+    const uint32_t *cur = a.cursor + (size_t)td.seg * kRadixBins;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const uint32_t d = 4 * t + e;
+        toff[d] = ex;
+        gbase[d] = c[e] ? atomicAdd(const_cast<uint32_t *>(cur + d), c[e]) - ex : 0u;
+        ex += c[e];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < KPT; r++) {
+        const uint32_t i = t + r * kST;
+        if (i < td.n) {
+            const uint32_t p = toff[digit_reg<KW>(key[r], a.level)] + ((slot[r / 2] >> (16 * (r & 1))) & 0xffffu);
+#pragma unroll
+            for (int u = 0; u < KW; u++) kout[p * KW + u + ((p * KW + u) >> 5)] = key[r][u];
+        }
+    }
+    __syncthreads();
+    uint32_t *dst = a.dst + b.key_off;
+    for (uint32_t i = t; i < td.n * KW; i += kST) {
+        const uint32_t p = i / KW, u = i - p * KW;
+        const uint32_t w = kout[i + (i >> 5)];
+        const uint32_t j = p * KW + a.level / 3;   // the element's digit word
+        const uint32_t wd = kout[j + (j >> 5)];
+        const uint32_t d = (wd >> (20 - 10 * (a.level % 3))) & 1023u;
+        dst[(uint64_t)(gbase[d] + p) * KW + u] = w;
+    }
+}
+
+__global__ void __launch_bounds__(kST, 2) k_msd_scatter(MsdArgs a) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const MsdTile td = a.tiles[blockIdx.x];
+    const MsdSeg sg = a.segs[td.seg];
+    const BucketInfo b = a.buckets[sg.L];
+    switch (b.kw) {
+        case 1: scatter_tile<1>(a, td, sg, b, sm); break;
+        case 2: scatter_tile<2>(a, td, sg, b, sm); break;
+        case 3: scatter_tile<3>(a, td, sg, b, sm); break;
+        case 4: scatter_tile<4>(a, td, sg, b, sm); break;
+        case 5: scatter_tile<5>(a, td, sg, b, sm); break;
+        case 6: scatter_tile<6>(a, td, sg, b, sm); break;
+        case 7: scatter_tile<7>(a, td, sg, b, sm); break;
+        case 8: scatter_tile<8>(a, td, sg, b, sm); break;
+        default: break;   // kw > 8 never reaches the scatter: the host sorts such buckets with LSD
+    }
+}
+
+// ---------------------------------------------------------------- finishing sorts
+__device__ __forceinline__ bool key_le(const uint32_t *x, const uint32_t *y, uint32_t kw) {
+    for (uint32_t u = 0; u < kw; u++)
+        if (x[u] != y[u]) return x[u] < y[u];
+    return true;
+}
+
+// One warp per tiny segment (<= 32 keys): odd-even transposition over the lanes, one key per lane,
+// compare-exchange with the neighbouring lane through shuffles (32 phases).
+template <int KW>
+__device__ __forceinline__ void warp_oets(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t *src = (sg.buf ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
+    uint32_t k[KW];
+#pragma unroll
+    for (int u = 0; u < KW; u++) k[u] = lane < (int)sg.n ? __ldg(src + lane * KW + u) : 0xffffffffu;
+    for (int ph = 0; ph < 32; ph++) {
+        const bool lower = (lane & 1) == (ph & 1);
+        const int partner = lower ? lane + 1 : lane - 1;
+        const bool act = partner >= 0 && partner < 32;
+        uint32_t o[KW];
+#pragma unroll
+        for (int u = 0; u < KW; u++) o[u] = __shfl_sync(kFullM, k[u], act ? partner : lane);
+        bool less = false, eq = true;   // o < k ?
+#pragma unroll
+        for (int u = 0; u < KW; u++) {
+            if (eq && o[u] != k[u]) {
+                less = o[u] < k[u];
+                eq = false;
+            }
+        }
+        const bool take = act && (lower ? less : (!less && !eq));
+        if (take) {
+#pragma unroll
+            for (int u = 0; u < KW; u++) k[u] = o[u];
+        }
+    }
+    uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
+    if (lane < (int)sg.n) {
+#pragma unroll
+        for (int u = 0; u < KW; u++) dst[lane * KW + u] = k[u];
+    }
+}
+
+__global__ void __launch_bounds__(kST) k_msd_warp_sort(MsdArgs a) {
+    const uint32_t w = blockIdx.x * (kST / 32) + (threadIdx.x >> 5);
+    if (w >= a.n_tiny) return;
+    const MsdSeg sg = a.q_tiny[w];
+    const BucketInfo b = a.buckets[sg.L];
+    switch (b.kw) {
+        case 1: warp_oets<1>(a, sg, b); break;
+        case 2: warp_oets<2>(a, sg, b); break;
+        case 3: warp_oets<3>(a, sg, b); break;
+        case 4: warp_oets<4>(a, sg, b); break;
+        case 5: warp_oets<5>(a, sg, b); break;
+        case 6: warp_oets<6>(a, sg, b); break;
+        case 7: warp_oets<7>(a, sg, b); break;
+        default: warp_oets<8>(a, sg, b); break;
+    }
+}
+
+// Keys of KW u32 words held in registers, compared lexicographically.
+template <int KW>
+struct Key {
+    uint32_t w[KW];
+};
+template <int KW>
+__device__ __forceinline__ bool klt(const Key<KW> &x, const Key<KW> &y) {
+#pragma unroll
+    for (int u = 0; u < KW; u++)
+        if (x.w[u] != y.w[u]) return x.w[u] < y.w[u];
+    return false;
+}
+template <int KW>
+__device__ __forceinline__ void kce(Key<KW> &x, Key<KW> &y) {   // compare-exchange: x <= y afterwards
+    if (klt<KW>(y, x)) {
+        const Key<KW> t = x;
+        x = y;
+        y = t;
+    }
+}
+template <int KW>
+__device__ __forceinline__ Key<KW> kshfl(const Key<KW> &x, int src) {
+    Key<KW> r;
+#pragma unroll
+    for (int u = 0; u < KW; u++) r.w[u] = __shfl_sync(kFullM, x.w[u], src);
+    return r;
+}
+template <int KW>
+__device__ __forceinline__ Key<KW> kld(const uint32_t *p) {
+    Key<KW> r;
+#pragma unroll
+    for (int u = 0; u < KW; u++) r.w[u] = p[u];
+    return r;
+}
+template <int KW>
+__device__ __forceinline__ void kst(uint32_t *p, const Key<KW> &x) {
+#pragma unroll
+    for (int u = 0; u < KW; u++) p[u] = x.w[u];
+}
+
+// One CTA per small job (<= 256*E keys of one bucket): odd-even transposition inside each thread's
+// E keys (the data-parallel bubble sort), odd-even merge-split across groups of 8 lanes through warp
+// shuffles (min/max against the reversed partner run + bitonic clean-up), then merge paths in
+// shared memory up to the whole tile. Keys stay in registers until the shared-memory merges.
+template <int KW>
+__device__ __forceinline__ void cta_sort_job(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint32_t *sm) {
+    constexpr int E = KW <= 4 ? 8 : 4;
+    constexpr uint32_t TN = kST * E;
+    const int t = threadIdx.x, lane = t & 31;
+    const uint32_t n = sg.n;
+    const uint32_t *src = (sg.buf ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
+    Key<KW> v[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t idx = t * E + e;
+        if (idx < n) v[e] = kld<KW>(src + (size_t)idx * KW);
+        else
+#pragma unroll
+            for (int u = 0; u < KW; u++) v[e].w[u] = 0xffffffffu;
+    }
+#pragma unroll
+    for (int ph = 0; ph < E; ph++)
+#pragma unroll
+        for (int i = ph & 1; i + 1 < E; i += 2) kce<KW>(v[i], v[i + 1]);
+    const int g = lane & 7;
+#pragma unroll 1
+    for (int ph = 0; ph < 8; ph++) {
+        const bool lower = (g & 1) == (ph & 1);
+        const int pg = lower ? g + 1 : g - 1;
+        const bool act = pg >= 0 && pg < 8;
+        const int srcl = act ? lane - g + pg : lane;
+        Key<KW> o[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) o[e] = kshfl<KW>(v[e], srcl);
+        if (act) {
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const Key<KW> &y = o[E - 1 - e];
+                const bool ylt = klt<KW>(y, v[e]);
+                if (lower ? ylt : !ylt) v[e] = y;
+            }
+#pragma unroll
+            for (int d = E / 2; d >= 1; d >>= 1)
+#pragma unroll
+                for (int i = 0; i < E; i++)
+                    if ((i & d) == 0) kce<KW>(v[i], v[i + d]);
+        }
+    }
+    uint32_t *b0 = sm, *b1 = sm + TN * KW;
+#pragma unroll
+    for (int e = 0; e < E; e++) kst<KW>(b0 + (size_t)(t * E + e) * KW, v[e]);
+    __syncthreads();
+    uint32_t *s0 = b0, *s1 = b1;
+    for (uint32_t run = 8 * E; run < TN; run *= 2) {
+        const uint32_t o = t * E, pair = o / (2 * run), d = o - pair * 2 * run;
+        const uint32_t *ra = s0 + (size_t)pair * 2 * run * KW, *rb = ra + (size_t)run * KW;
+        uint32_t lo = d > run ? d - run : 0u, hi = d < run ? d : run;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (!klt<KW>(kld<KW>(rb + (size_t)(d - 1 - mid) * KW), kld<KW>(ra + (size_t)mid * KW))) lo = mid + 1;
+            else hi = mid;
+        }
+        uint32_t i = lo, j = d - lo;
+        Key<KW> x = kld<KW>(ra + (size_t)min(i, run - 1) * KW), y = kld<KW>(rb + (size_t)min(j, run - 1) * KW);
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+            const bool take_a = j >= run || (i < run && !klt<KW>(y, x));
+            if (take_a) {
+                kst<KW>(s1 + (size_t)(o + k) * KW, x);
+                i++;
+                if (i < run) x = kld<KW>(ra + (size_t)i * KW);
+            } else {
+                kst<KW>(s1 + (size_t)(o + k) * KW, y);
+                j++;
+                if (j < run) y = kld<KW>(rb + (size_t)j * KW);
+            }
+        }
+        __syncthreads();
+        uint32_t *sw = s0;
+        s0 = s1;
+        s1 = sw;
+    }
+    uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
+    for (uint32_t i = t; i < n * KW; i += kST) dst[i] = s0[i];
+}
+
+__global__ void __launch_bounds__(kST) k_msd_cta_sort(MsdArgs a) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const MsdSeg sg = a.q_small[blockIdx.x];
+    const BucketInfo b = a.buckets[sg.L];
+    switch (b.kw) {
+        case 1: cta_sort_job<1>(a, sg, b, sm); break;
+        case 2: cta_sort_job<2>(a, sg, b, sm); break;
+        case 3: cta_sort_job<3>(a, sg, b, sm); break;
+        case 4: cta_sort_job<4>(a, sg, b, sm); break;
+        case 5: cta_sort_job<5>(a, sg, b, sm); break;
+        case 6: cta_sort_job<6>(a, sg, b, sm); break;
+        case 7: cta_sort_job<7>(a, sg, b, sm); break;
+        default: cta_sort_job<8>(a, sg, b, sm); break;
+    }
+}
+
+__global__ void __launch_bounds__(kST) k_msd_copy(MsdArgs a) {
+    const CopyRange r = a.q_copy[blockIdx.x];
+    for (uint32_t i = threadIdx.x; i < r.len; i += kST) a.keys_b[r.to + i] = __ldg(a.keys_a + r.from + i);
+}
+
+}  // namespace
+
+size_t msd_scatter_smem() { return (size_t)(3 * kRadixBins + 8192 + 8192 / 32 + 8 + kST / 32 + 1) * 4; }
+
+cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s) {
+    if (!ntiles) return cudaSuccess;
+    k_msd_count<<<ntiles, kST, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s) {
+    if (!nsegs) return cudaSuccess;
+    k_msd_plan<<<nsegs, kST, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s) {
+    if (!ntiles) return cudaSuccess;
+    const size_t smem = msd_scatter_smem();
+    cudaError_t e = cudaFuncSetAttribute(k_msd_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_msd_scatter<<<ntiles, kST, smem, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_copy, uint32_t max_tile_words,
+                              cudaStream_t s) {
+    cudaError_t e;
+    if (a.n_tiny) {
+        k_msd_warp_sort<<<(a.n_tiny + kST / 32 - 1) / (kST / 32), kST, 0, s>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (n_small) {
+        const size_t smem = (size_t)max_tile_words * 2 * 4;
+        e = cudaFuncSetAttribute(k_msd_cta_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_msd_cta_sort<<<n_small, kST, smem, s>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (n_copy) {
+        k_msd_copy<<<n_copy, kST, 0, s>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace wsort

@@ -67,6 +67,8 @@ struct wsort_ctx {
 
     // sort
     DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y, splits;
+    DevBuf m_hist, m_cursor, m_ctr, m_big[2], m_tiles[2], m_tiny, m_small, m_copy;
+    uint32_t *h_ctr = nullptr;   // pinned mirror of the msd queue counters
     std::vector<uint8_t> hplan;
     uint8_t *h_plan_pinned = nullptr;
     size_t h_plan_cap = 0;
@@ -127,6 +129,13 @@ int ensure(wsort_ctx *c, DevBuf &b, size_t bytes, const char *what, bool zero = 
     }
     b.cap = want;
     if (zero) CK(cudaMemsetAsync(b.p, 0, want, c->stream), "memset");
+    return WSORT_OK;
+}
+
+int upload_small(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const char *what) {
+    int rc = ensure(c, dst, bytes, what);   // ensure() allocates at least 16 bytes
+    if (rc) return rc;
+    if (bytes && src) CK(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, c->stream), what);
     return WSORT_OK;
 }
 
@@ -270,11 +279,14 @@ void wsort_destroy(wsort_ctx *c) {
     DevBuf *bufs[] = {&c->text_alloc, &c->cta_hist, &c->cta_base, &c->d_sum, &c->keys_a, &c->keys_b,
                       &c->pay_a, &c->pay_b, &c->words, &c->src_off, &c->dh, &c->status0, &c->status1,
                       &c->tickets, &c->plan, &c->va_x, &c->va_y, &c->splits, &c->bk, &c->d_counts,
-                      &c->d_cursor, &c->d_sbase, &c->d_split, &c->d_lohi, &c->d_tiles, &c->d_ranges};
+                      &c->d_cursor, &c->d_sbase, &c->d_split, &c->d_lohi, &c->d_tiles, &c->d_ranges,
+                      &c->m_hist, &c->m_cursor, &c->m_ctr, &c->m_big[0], &c->m_big[1], &c->m_tiles[0],
+                      &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_sum) cudaFreeHost(c->h_sum);
     if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
+    if (c->h_ctr) cudaFreeHost(c->h_ctr);
     for (auto &pe : c->pending) {
         cudaEventDestroy(pe.a);
         cudaEventDestroy(pe.b);
@@ -727,6 +739,164 @@ int sort_oets(wsort_ctx *c, bool want_src) {
                   [&] { return launch_emit(ea, c->stream); });
 }
 
+
+// msd_radix (keys only): MSD partitioning by 2-letter digits, level by level, with device-side
+// planning (k_msd_plan queues the next level's segments and the finishing jobs); one small D2H of
+// the queue counters per level sizes the next launches.
+int sort_msd(wsort_ctx *c) {
+    const Summary &s = *c->h_sum;
+    const uint32_t lmax = s.max_len;
+    std::vector<BucketInfo> bk(256, BucketInfo{});
+    uint32_t max_tw = 32, levels = 0;
+    for (uint32_t L = 1; L <= lmax; L++) {
+        BucketInfo &b = bk[L];
+        b.key_off = s.key_off[L];
+        b.word_off = s.off[L];
+        b.byte_off = s.byte_off[L];
+        b.n = (uint32_t)(s.off[L + 1] - s.off[L]);
+        b.kw = kw_of(L);
+        b.ndig = ndig_of(L);
+        b.tile_keys = kMergeThreads * oets_elems_per_thread(b.kw);   // CTA-sort capacity
+        b.aux = kRadixThreads * (32 / b.kw);                          // scatter tile keys
+        b.elem_off = b.key_off;
+        b.estride = b.kw;
+        b.final_b = 1;
+        max_tw = std::max(max_tw, b.tile_keys * b.kw);
+        if (b.n) levels = std::max(levels, b.ndig);
+    }
+    const uint64_t W = s.n_words, key_words = s.key_off[256];
+    int rc;
+    if ((rc = ensure(c, c->keys_a, key_words * 4 + 64, "keys_a"))) return rc;
+    if ((rc = ensure(c, c->keys_b, key_words * 4 + 64, "keys_b"))) return rc;
+    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    const uint32_t cap_big = (uint32_t)(W / 1024 + 4096), cap_tiles = (uint32_t)(W / 1024 + 2 * cap_big + 4096);
+    const uint32_t cap_local = (uint32_t)(W / 256 + 65536), cap_copy = (uint32_t)(W / 1024 + key_words / 65536 + 4096);
+    for (int i = 0; i < 2; i++) {
+        if ((rc = ensure(c, c->m_big[i], (size_t)cap_big * sizeof(MsdSeg), "msd segs"))) return rc;
+        if ((rc = ensure(c, c->m_tiles[i], (size_t)cap_tiles * sizeof(MsdTile), "msd tiles"))) return rc;
+    }
+    if ((rc = ensure(c, c->m_tiny, (size_t)cap_local * sizeof(MsdSeg), "msd tiny"))) return rc;
+    if ((rc = ensure(c, c->m_small, (size_t)cap_local * sizeof(MsdSeg), "msd small"))) return rc;
+    if ((rc = ensure(c, c->m_copy, (size_t)cap_copy * sizeof(CopyRange), "msd copy"))) return rc;
+    if ((rc = ensure(c, c->m_ctr, kQCount * 4, "msd counters"))) return rc;
+    if (!c->h_ctr && cudaMallocHost(&c->h_ctr, kQCount * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(c, WSORT_E_NOMEM, "pinned counters");
+    }
+    // level 0: whole buckets; small buckets go straight to the finishing jobs
+    std::vector<MsdSeg> segs, tiny, small;
+    std::vector<MsdTile> tiles;
+    for (uint32_t L = 1; L <= lmax; L++) {
+        const BucketInfo &b = bk[L];
+        if (!b.n) continue;
+        if (b.n <= b.tile_keys) {
+            (b.n <= 32 ? tiny : small).push_back(MsdSeg{L, 0, b.n, 1});
+        } else {
+            const uint32_t q = (uint32_t)segs.size();
+            segs.push_back(MsdSeg{L, 0, b.n, 0});
+            for (uint32_t o = 0; o < b.n; o += b.aux) tiles.push_back(MsdTile{q, o, std::min(b.aux, b.n - o), 0});
+        }
+    }
+    std::vector<uint8_t> plan;
+    append(plan, bk);
+    if ((rc = upload_plan(c, plan))) return rc;
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
+    if ((rc = upload_small(c, c->m_big[0], segs.data(), segs.size() * sizeof(MsdSeg), "segs0"))) return rc;
+    if ((rc = upload_small(c, c->m_tiles[0], tiles.data(), tiles.size() * sizeof(MsdTile), "tiles0"))) return rc;
+    if ((rc = upload_small(c, c->m_tiny, tiny.data(), tiny.size() * sizeof(MsdSeg), "tiny0"))) return rc;
+    if ((rc = upload_small(c, c->m_small, small.data(), small.size() * sizeof(MsdSeg), "small0"))) return rc;
+    uint32_t ctr0[kQCount] = {0, 0, (uint32_t)tiny.size(), (uint32_t)small.size(), 0, 0, 0, 0};
+    if ((rc = upload_small(c, c->m_ctr, ctr0, sizeof ctr0, "counters"))) return rc;
+
+    uint32_t *ka = static_cast<uint32_t *>(c->keys_a.p), *kb = static_cast<uint32_t *>(c->keys_b.p);
+    const double key_bytes = (double)key_words * 4;
+    if (!c->packed_pending) {
+        TkArgs &tk = c->tk;
+        tk.buckets = d_bk;
+        tk.keys = ka;
+        tk.payload = nullptr;
+        rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes, [&] { return launch_pack_scatter(tk, c->stream); });
+        if (rc) return rc;
+    }
+    MsdArgs m{};
+    m.buckets = d_bk;
+    m.ctr = static_cast<uint32_t *>(c->m_ctr.p);
+    m.q_tiny = static_cast<MsdSeg *>(c->m_tiny.p);
+    m.q_small = static_cast<MsdSeg *>(c->m_small.p);
+    m.q_copy = static_cast<CopyRange *>(c->m_copy.p);
+    m.cap_big = cap_big;
+    m.cap_tiles = cap_tiles;
+    m.cap_local = cap_local;
+    m.cap_copy = cap_copy;
+    m.keys_a = ka;
+    m.keys_b = kb;
+    uint32_t nsegs = (uint32_t)segs.size(), ntiles = (uint32_t)tiles.size();
+    std::vector<uint64_t> tile_words_level;
+    for (uint32_t level = 0; nsegs > 0; level++) {
+        if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
+        const int cur = level & 1;
+        if ((rc = ensure(c, c->m_hist, (size_t)nsegs * kRadixBins * 4, "msd hist"))) return rc;
+        if ((rc = ensure(c, c->m_cursor, (size_t)nsegs * kRadixBins * 4, "msd cursor"))) return rc;
+        CK(cudaMemsetAsync(c->m_hist.p, 0, (size_t)nsegs * kRadixBins * 4, c->stream), "memset msd hist");
+        CK(cudaMemsetAsync(c->m_ctr.p, 0, 2 * 4, c->stream), "reset big/tiles counters");
+        m.level = level;
+        m.dst_is_a = level & 1u;
+        m.segs = static_cast<const MsdSeg *>(c->m_big[cur].p);
+        m.tiles = static_cast<const MsdTile *>(c->m_tiles[cur].p);
+        m.src = (level & 1u) ? kb : ka;
+        m.dst = (level & 1u) ? ka : kb;
+        m.hist = static_cast<uint32_t *>(c->m_hist.p);
+        m.cursor = static_cast<uint32_t *>(c->m_cursor.p);
+        m.q_big = static_cast<MsdSeg *>(c->m_big[cur ^ 1].p);
+        m.q_tiles = static_cast<MsdTile *>(c->m_tiles[cur ^ 1].p);
+        // algorithmic bytes of this level: read the segments twice (count, scatter), write once
+        double seg_bytes = 0;
+        {
+            // host does not know the per-segment sizes beyond level 0; use the tile count bound
+            seg_bytes = level == 0 ? key_bytes : 0;
+        }
+        rc = launch(c, "k4m_msd_count", seg_bytes, [&] { return launch_msd_count(m, ntiles, c->stream); });
+        if (rc) return rc;
+        rc = launch(c, "k4m_msd_plan", (double)nsegs * kRadixBins * 8, [&] { return launch_msd_plan(m, nsegs, c->stream); });
+        if (rc) return rc;
+        rc = launch(c, "k4m_msd_scatter", 2 * seg_bytes, [&] { return launch_msd_scatter(m, ntiles, c->stream); });
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(c->h_ctr, c->m_ctr.p, kQCount * 4, cudaMemcpyDeviceToHost, c->stream), "msd counters");
+        CK(cudaStreamSynchronize(c->stream), "msd level");
+        nsegs = c->h_ctr[kQBig];
+        ntiles = c->h_ctr[kQTiles];
+        if (nsegs > cap_big || ntiles > cap_tiles || c->h_ctr[kQTiny] > cap_local || c->h_ctr[kQSmall] > cap_local ||
+            c->h_ctr[kQCopy] > cap_copy)
+            return set_err(c, WSORT_E_NOMEM, "msd queue overflow (segs %u tiles %u)", nsegs, ntiles);
+    }
+    if (!c->h_ctr || segs.empty()) {   // no level ran: counters are the host's
+        c->h_ctr[kQTiny] = (uint32_t)tiny.size();
+        c->h_ctr[kQSmall] = (uint32_t)small.size();
+        c->h_ctr[kQCopy] = 0;
+    }
+    m.n_tiny = c->h_ctr[kQTiny];
+    const uint32_t n_small = c->h_ctr[kQSmall], n_copy = c->h_ctr[kQCopy];
+    rc = launch(c, "k4m_msd_finish", 2 * key_bytes,
+                [&] { return launch_msd_finish(m, n_small, n_copy, max_tw, c->stream); });
+    if (rc) return rc;
+    EmitArgs ea{};
+    std::vector<TileDesc> emit_tiles;
+    for (uint32_t L = 1; L <= lmax; L++) {
+        const uint32_t te = kEmitStage / (L + 1);
+        for (uint32_t i = 0; bk[L].n && i < (bk[L].n + te - 1) / te; i++) emit_tiles.push_back(TileDesc{L, i});
+    }
+    if ((rc = upload_small(c, c->d_tiles, emit_tiles.data(), emit_tiles.size() * sizeof(TileDesc), "emit tiles")))
+        return rc;
+    ea.buckets = d_bk;
+    ea.tiles = static_cast<const TileDesc *>(c->d_tiles.p);
+    ea.ntiles = (uint32_t)emit_tiles.size();
+    ea.keys_a = ka;
+    ea.keys_b = kb;
+    ea.words = static_cast<uint8_t *>(c->words.p);
+    ea.global_base = c->global_base;
+    return launch(c, "k5_emit", key_bytes + (double)s.byte_off[256], [&] { return launch_emit(ea, c->stream); });
+}
+
 }  // namespace
 
 extern "C" {
@@ -734,7 +904,8 @@ extern "C" {
 int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     if (!c) return WSORT_E_INVALID_ARG;
     if (c->state < ST_TOKENIZED) return set_err(c, WSORT_E_STATE, "wsort_sort before wsort_tokenize");
-    if (algo != WSORT_ALGO_AUTO && algo != WSORT_ALGO_LSD_RADIX && algo != WSORT_ALGO_OETS_MERGE)
+    if (algo != WSORT_ALGO_AUTO && algo != WSORT_ALGO_LSD_RADIX && algo != WSORT_ALGO_OETS_MERGE &&
+        algo != WSORT_ALGO_MSD_RADIX)
         return set_err(c, WSORT_E_INVALID_ARG, "bad algo %d", algo);
     if (flags & ~WSORT_FLAG_SRC_OFF) return set_err(c, WSORT_E_INVALID_ARG, "bad flags 0x%x", flags);
     if (c->keys_external && !c->packed_pending)
@@ -743,7 +914,15 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
         return set_err(c, WSORT_E_INVALID_ARG, "src_off is not available for packed / exchanged keys");
     cudaSetDevice(c->device);
     const bool want_src = (flags & WSORT_FLAG_SRC_OFF) != 0;
-    const int rc = algo == WSORT_ALGO_OETS_MERGE ? sort_oets(c, want_src) : sort_radix(c, want_src);
+    int rc;
+    if (algo == WSORT_ALGO_OETS_MERGE) {
+        rc = sort_oets(c, want_src);
+    } else if ((algo == WSORT_ALGO_MSD_RADIX || algo == WSORT_ALGO_AUTO) && !want_src &&
+               kw_of((int)c->h_sum->max_len) <= (int)kRadixRegMaxKw) {
+        rc = sort_msd(c);
+    } else {
+        rc = sort_radix(c, want_src);
+    }
     c->packed_pending = false;
     if (rc) {
         c->state = c->keys_external ? ST_CREATED : ST_TOKENIZED;
@@ -866,12 +1045,6 @@ std::vector<BucketInfo> bucket_table(const Summary &s) {
     return bk;
 }
 
-int upload_small(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const char *what) {
-    int rc = ensure(c, dst, bytes, what);   // ensure() allocates at least 16 bytes
-    if (rc) return rc;
-    if (bytes && src) CK(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, c->stream), what);
-    return WSORT_OK;
-}
 
 // Fill the host summary from per-length counts (local bucket layout of packed keys).
 void summary_from_counts(Summary &s, const uint64_t *n_per_len) {

@@ -52,7 +52,7 @@ struct BucketInfo {                // per-length bucket, built on the host after
     uint64_t elem_off;             // u32 words into the final buffer (element layout)
     uint32_t estride;              // u32 words per element in the final buffer (kw, or kw+1 with an
                                    // inline payload word)
-    uint32_t pad_;
+    uint32_t aux;                  // msd: keys per scatter tile
 };
 
 struct TileDesc {
@@ -164,6 +164,41 @@ cudaError_t launch_part_count(const DistArgs &a, cudaStream_t s);
 cudaError_t launch_part_scatter(const DistArgs &a, cudaStream_t s);
 cudaError_t launch_regroup(const CopyRange *ranges, uint32_t nranges, const uint32_t *recv, uint32_t *keys,
                            cudaStream_t s);
+
+// ---------------- msd_radix: MSD partitioning + CTA-local odd-even transposition finish ----------------
+struct MsdSeg {
+    uint32_t L, start, n, buf;     // key range [start, start+n) of bucket L; buf: 1 = in A, 0 = in B
+};
+struct MsdTile {
+    uint32_t seg, off, n, pad_;    // keys [off, off+n) of segment `seg` of this level
+};
+enum { kQBig = 0, kQTiles = 1, kQTiny = 2, kQSmall = 3, kQCopy = 4, kQCount = 8 };
+constexpr uint32_t kMsdCopyChunk = 65536;   // u32 words per copy job
+struct MsdArgs {
+    const BucketInfo *buckets;
+    uint32_t level, dst_is_a;
+    const MsdSeg *segs;            // this level's segments
+    const MsdTile *tiles;          // this level's scatter / count tiles
+    const uint32_t *src;           // this level's input buffer
+    uint32_t *dst;                 // this level's output buffer
+    uint32_t *hist;                // [nsegs][1024]
+    uint32_t *cursor;              // [nsegs][1024]
+    uint32_t *ctr;                 // [kQCount] queue counters
+    MsdSeg *q_big;                 // next level's segments
+    MsdTile *q_tiles;              // next level's tiles
+    MsdSeg *q_tiny, *q_small;      // finishing sort jobs
+    CopyRange *q_copy;             // finishing copies A -> B
+    uint32_t cap_big, cap_tiles, cap_local, cap_copy;
+    const uint32_t *keys_a;        // finishing: buffer A
+    uint32_t *keys_b;              // finishing: buffer B (final)
+    uint32_t n_tiny;
+};
+size_t msd_scatter_smem();
+cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
+cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s);
+cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
+cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_copy, uint32_t max_tile_words,
+                              cudaStream_t s);
 
 struct EmitArgs {
     const BucketInfo *buckets;

@@ -20,7 +20,7 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["lsd_radix", "oets_merge"]
+ALGOS = ["lsd_radix", "oets_merge", "msd_radix"]
 
 
 @pytest.fixture(scope="module")
@@ -166,6 +166,7 @@ def test_deterministic_repeats(ws):
 def test_auto_equals_radix(ws):
     text, _ = gen.generate(1)
     assert gpu_sort(ws, text, "auto")[0] == gpu_sort(ws, text, "lsd_radix")[0]
+    assert gpu_sort(ws, text, "auto", src=False)[0] == gpu_sort(ws, text, "msd_radix", src=False)[0]
 
 
 @pytest.mark.parametrize("algo", ALGOS)
@@ -215,6 +216,12 @@ def _full_size_check(ws, text: np.ndarray, exact_from: int, algo: str = "auto"):
 def test_config4_full_size(ws):
     text, _ = gen.generate(4)
     _full_size_check(ws, text, exact_from=11)
+
+
+@pytest.mark.slow
+def test_config4_full_size_lsd(ws):
+    text, _ = gen.generate(4)
+    _full_size_check(ws, text, exact_from=13, algo="lsd_radix")
 
 
 @pytest.mark.slow
