@@ -79,28 +79,23 @@ __global__ void __launch_bounds__(kST) k_msd_count(MsdArgs a) {
 }
 
 // ---------------------------------------------------------------- plan
-__device__ __forceinline__ void close_job(const MsdArgs &a, uint32_t L, uint32_t start, uint32_t n) {
-    if (!n) return;
-    if (n <= 32) {
-        const uint32_t q = atomicAdd(a.ctr + kQTiny, 1u);
-        if (q < a.cap_local) a.q_tiny[q] = MsdSeg{L, start, n, a.dst_is_a};
-    } else {
-        const uint32_t q = atomicAdd(a.ctr + kQSmall, 1u);
-        if (q < a.cap_local) a.q_small[q] = MsdSeg{L, start, n, a.dst_is_a};
-    }
-}
-
 // One CTA per segment of this level: exclusive scan of its digit histogram gives the children's
-// bases (the scatter cursors); thread 0 then walks the children in digit order and queues them:
+// bases (the scatter cursors). The non-empty children are compacted, then thread 0 walks them in
+// digit order and classifies each (writing shared memory only):
 //   big (> CTA-sort capacity, digits left)  -> next level (segment + its scatter tiles)
 //   finished and already in B               -> nothing
 //   finished, in A, larger than a CTA tile  -> copy chunks A -> B
 //   everything else                         -> packed greedily into CTA / warp sort jobs of at most
 //                                              one tile; sorting a run of consecutive children by the
 //                                              full key sorts each child (their prefixes differ)
+// One atomic per queue then reserves the slots and all threads write the entries.
+constexpr int kPlanMax = 2048;   // >= 2 x the non-empty digits of a segment (<= 27*26)
 __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
     __shared__ uint32_t wsum[kST / 32 + 1];
-    __shared__ uint32_t cnt_s[kRadixBins], base_s[kRadixBins];
+    __shared__ uint32_t nz_d[kRadixBins];
+    __shared__ MsdSeg jobs[kPlanMax];        // sort jobs from the bottom, big/copy children from the top
+    __shared__ uint32_t big_t0[kPlanMax];
+    __shared__ uint32_t s_n[4], s_q[4];
     const int t = threadIdx.x;
     const uint32_t s = blockIdx.x;
     const MsdSeg sg = a.segs[s];
@@ -109,56 +104,103 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
     uint32_t c[4];
 #pragma unroll
     for (int e = 0; e < 4; e++) c[e] = h[4 * t + e];
+    const uint32_t nzc = (c[0] != 0) + (c[1] != 0) + (c[2] != 0) + (c[3] != 0);
     uint32_t ex = block_excl_scan_m(c[0] + c[1] + c[2] + c[3], wsum, nullptr);
+    uint32_t nzt = 0;
+    uint32_t nzx = block_excl_scan_m(nzc, wsum, &nzt);
 #pragma unroll
     for (int e = 0; e < 4; e++) {
         const uint32_t d = 4 * t + e;
         a.cursor[(size_t)s * kRadixBins + d] = sg.start + ex;
-        cnt_s[d] = c[e];
-        base_s[d] = sg.start + ex;
+        if (c[e]) nz_d[nzx++] = sg.start + ex;
         ex += c[e];
     }
     __syncthreads();
-    if (t != 0) return;
-    const bool final_digit = a.level + 1 >= b.ndig;
-    const uint32_t cap = b.tile_keys;
-    uint32_t js = 0, jn = 0;   // open job
-    for (uint32_t d = 0; d < kRadixBins; d++) {
-        const uint32_t cnt = cnt_s[d], start = base_s[d];
-        if (!cnt) continue;
-        const bool fin = final_digit || cnt == 1;
-        if (!fin && cnt > cap) {
-            close_job(a, sg.L, js, jn);
-            jn = 0;
-            const uint32_t q = atomicAdd(a.ctr + kQBig, 1u);
-            const uint32_t nt = (cnt + b.aux - 1) / b.aux;
-            const uint32_t tq = atomicAdd(a.ctr + kQTiles, nt);
-            if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, start, cnt, 0};
-            for (uint32_t i = 0; i < nt && tq + i < a.cap_tiles; i++)
-                a.q_tiles[tq + i] = MsdTile{q, i * b.aux, min(b.aux, cnt - i * b.aux), 0};
-        } else if (fin && !a.dst_is_a) {
-            close_job(a, sg.L, js, jn);
-            jn = 0;
-        } else if (fin && cnt > cap) {
-            close_job(a, sg.L, js, jn);
-            jn = 0;
-            const uint32_t words = cnt * b.kw;
-            const uint32_t nch = (words + kMsdCopyChunk - 1) / kMsdCopyChunk;
-            const uint32_t q = atomicAdd(a.ctr + kQCopy, nch);
-            for (uint32_t i = 0; i < nch && q + i < a.cap_copy; i++) {
-                const uint64_t w0 = b.key_off + (uint64_t)start * b.kw + (uint64_t)i * kMsdCopyChunk;
-                a.q_copy[q + i] = CopyRange{w0, w0, min(kMsdCopyChunk, words - i * kMsdCopyChunk), 0};
-            }
-        } else {
-            if (jn + cnt > cap) {
-                close_job(a, sg.L, js, jn);
+    if (t == 0) {
+        const bool final_digit = a.level + 1 >= b.ndig;
+        const uint32_t cap = b.tile_keys, seg_end = sg.start + sg.n;
+        uint32_t nj = 0, ntop = 0, ntiles = 0;
+        uint32_t js = 0, jn = 0;
+        for (uint32_t k = 0; k < nzt; k++) {
+            const uint32_t start = nz_d[k], cnt = (k + 1 < nzt ? nz_d[k + 1] : seg_end) - start;
+            const bool fin = final_digit || cnt == 1;
+            const bool big = !fin && cnt > cap, skip = fin && !a.dst_is_a, copy = fin && a.dst_is_a && cnt > cap;
+            if (big || skip || copy) {
+                if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a};
                 jn = 0;
+                if (big) {
+                    big_t0[ntop] = ntiles;
+                    jobs[kPlanMax - 1 - ntop++] = MsdSeg{sg.L, start, cnt, 1u};
+                    ntiles += (cnt + b.aux - 1) / b.aux;
+                } else if (copy) {
+                    big_t0[ntop] = 0;
+                    jobs[kPlanMax - 1 - ntop++] = MsdSeg{sg.L, start, cnt, 2u};
+                }
+            } else {
+                if (jn + cnt > cap) {
+                    jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a};
+                    jn = 0;
+                }
+                if (!jn) js = start;
+                jn += cnt;
             }
-            if (!jn) js = start;
-            jn += cnt;
+        }
+        if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a};
+        uint32_t ntiny = 0, nbig = 0, nch = 0;
+        for (uint32_t k = 0; k < nj; k++) ntiny += jobs[k].n <= 32;
+        for (uint32_t k = 0; k < ntop; k++) {
+            const MsdSeg &x = jobs[kPlanMax - 1 - k];
+            if (x.buf == 1u) nbig++;
+            else nch += (x.n * b.kw + kMsdCopyChunk - 1) / kMsdCopyChunk;
+        }
+        s_n[0] = nj;
+        s_n[1] = ntop;
+        s_q[0] = ntiny ? atomicAdd(a.ctr + kQTiny, ntiny) : 0u;
+        s_q[1] = nj - ntiny ? atomicAdd(a.ctr + kQSmall, nj - ntiny) : 0u;
+        s_q[2] = nbig ? atomicAdd(a.ctr + kQBig, nbig) : 0u;
+        s_q[3] = ntiles ? atomicAdd(a.ctr + kQTiles, ntiles) : 0u;
+        const uint32_t cq = nch ? atomicAdd(a.ctr + kQCopy, nch) : 0u;
+        // copies are few: written here; big children get their queue index in buf
+        uint32_t ci = 0, bi = 0;
+        for (uint32_t k = 0; k < ntop; k++) {
+            MsdSeg &x = jobs[kPlanMax - 1 - k];
+            if (x.buf == 2u) {
+                const uint32_t words = x.n * b.kw;
+                for (uint32_t i = 0; i < words; i += kMsdCopyChunk) {
+                    const uint64_t w0 = b.key_off + (uint64_t)x.start * b.kw + i;
+                    const uint32_t q = cq + ci++;
+                    if (q < a.cap_copy) a.q_copy[q] = CopyRange{w0, w0, min(kMsdCopyChunk, words - i), 0};
+                }
+            } else {
+                x.buf = 16u + bi++;   // big: index among this segment's big children
+            }
         }
     }
-    close_job(a, sg.L, js, jn);
+    __syncthreads();
+    const uint32_t nj = s_n[0], ntop = s_n[1];
+    // sort jobs, order-preserving split into tiny / small (each thread recounts its prefix)
+    for (uint32_t k = t; k < nj; k += kST) {
+        uint32_t before_tiny = 0;
+        for (uint32_t i = 0; i < k; i++) before_tiny += jobs[i].n <= 32;
+        const MsdSeg x = jobs[k];
+        if (x.n <= 32) {
+            const uint32_t q = s_q[0] + before_tiny;
+            if (q < a.cap_local) a.q_tiny[q] = x;
+        } else {
+            const uint32_t q = s_q[1] + (k - before_tiny);
+            if (q < a.cap_local) a.q_small[q] = x;
+        }
+    }
+    for (uint32_t k = t; k < ntop; k += kST) {
+        MsdSeg x = jobs[kPlanMax - 1 - k];
+        if (x.buf < 16u) continue;
+        const uint32_t q = s_q[2] + (x.buf - 16u), t0 = s_q[3] + big_t0[k];
+        const uint32_t nt = (x.n + b.aux - 1) / b.aux;
+        x.buf = 0;
+        if (q < a.cap_big) a.q_big[q] = x;
+        for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++)
+            a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, x.n - i * b.aux), 0};
+    }
 }
 
 // ---------------------------------------------------------------- scatter
@@ -238,12 +280,6 @@ __global__ void __launch_bounds__(kST, 2) k_msd_scatter(MsdArgs a) {
 }
 
 // ---------------------------------------------------------------- finishing sorts
-__device__ __forceinline__ bool key_le(const uint32_t *x, const uint32_t *y, uint32_t kw) {
-    for (uint32_t u = 0; u < kw; u++)
-        if (x[u] != y[u]) return x[u] < y[u];
-    return true;
-}
-
 // One warp per tiny segment (<= 32 keys): odd-even transposition over the lanes, one key per lane,
 // compare-exchange with the neighbouring lane through shuffles (32 phases).
 template <int KW>
@@ -386,33 +422,51 @@ __device__ __forceinline__ void cta_sort_job(const MsdArgs &a, const MsdSeg &sg,
                     if ((i & d) == 0) kce<KW>(v[i], v[i + d]);
         }
     }
-    uint32_t *b0 = sm, *b1 = sm + TN * KW;
+    // shared memory: two padded buffers (word w at w + w/32: conflict-free blocked access)
+    constexpr uint32_t PW = TN * KW + TN * KW / 32 + 1;
+    uint32_t *b0 = sm, *b1 = sm + PW;
+    auto lds = [](const uint32_t *base, uint32_t elem) {
+        Key<KW> r;
 #pragma unroll
-    for (int e = 0; e < E; e++) kst<KW>(b0 + (size_t)(t * E + e) * KW, v[e]);
+        for (int u = 0; u < KW; u++) {
+            const uint32_t w = elem * KW + u;
+            r.w[u] = base[w + (w >> 5)];
+        }
+        return r;
+    };
+    auto sts = [](uint32_t *base, uint32_t elem, const Key<KW> &x) {
+#pragma unroll
+        for (int u = 0; u < KW; u++) {
+            const uint32_t w = elem * KW + u;
+            base[w + (w >> 5)] = x.w[u];
+        }
+    };
+#pragma unroll
+    for (int e = 0; e < E; e++) sts(b0, t * E + e, v[e]);
     __syncthreads();
     uint32_t *s0 = b0, *s1 = b1;
     for (uint32_t run = 8 * E; run < TN; run *= 2) {
         const uint32_t o = t * E, pair = o / (2 * run), d = o - pair * 2 * run;
-        const uint32_t *ra = s0 + (size_t)pair * 2 * run * KW, *rb = ra + (size_t)run * KW;
+        const uint32_t ra = pair * 2 * run, rb = ra + run;   // element indices
         uint32_t lo = d > run ? d - run : 0u, hi = d < run ? d : run;
         while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (!klt<KW>(kld<KW>(rb + (size_t)(d - 1 - mid) * KW), kld<KW>(ra + (size_t)mid * KW))) lo = mid + 1;
+            if (!klt<KW>(lds(s0, rb + d - 1 - mid), lds(s0, ra + mid))) lo = mid + 1;
             else hi = mid;
         }
         uint32_t i = lo, j = d - lo;
-        Key<KW> x = kld<KW>(ra + (size_t)min(i, run - 1) * KW), y = kld<KW>(rb + (size_t)min(j, run - 1) * KW);
+        Key<KW> x = lds(s0, ra + min(i, run - 1)), y = lds(s0, rb + min(j, run - 1));
 #pragma unroll
         for (int k = 0; k < E; k++) {
             const bool take_a = j >= run || (i < run && !klt<KW>(y, x));
             if (take_a) {
-                kst<KW>(s1 + (size_t)(o + k) * KW, x);
+                sts(s1, o + k, x);
                 i++;
-                if (i < run) x = kld<KW>(ra + (size_t)i * KW);
+                if (i < run) x = lds(s0, ra + i);
             } else {
-                kst<KW>(s1 + (size_t)(o + k) * KW, y);
+                sts(s1, o + k, y);
                 j++;
-                if (j < run) y = kld<KW>(rb + (size_t)j * KW);
+                if (j < run) y = lds(s0, rb + j);
             }
         }
         __syncthreads();
@@ -421,7 +475,7 @@ __device__ __forceinline__ void cta_sort_job(const MsdArgs &a, const MsdSeg &sg,
         s1 = sw;
     }
     uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
-    for (uint32_t i = t; i < n * KW; i += kST) dst[i] = s0[i];
+    for (uint32_t i = t; i < n * KW; i += kST) dst[i] = s0[i + (i >> 5)];
 }
 
 __global__ void __launch_bounds__(kST) k_msd_cta_sort(MsdArgs a) {
@@ -475,7 +529,7 @@ cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_cop
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (n_small) {
-        const size_t smem = (size_t)max_tile_words * 2 * 4;
+        const size_t smem = ((size_t)max_tile_words + max_tile_words / 32 + 1) * 2 * 4;
         e = cudaFuncSetAttribute(k_msd_cta_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         k_msd_cta_sort<<<n_small, kST, smem, s>>>(a);
