@@ -70,8 +70,20 @@ __global__ void __launch_bounds__(kST) k_msd_count(MsdArgs a) {
     const BucketInfo b = a.buckets[sg.L];
     for (int i = t; i < kRadixBins; i += kST) h[i] = 0;
     __syncthreads();
-    const uint32_t *keys = a.src + b.key_off + (uint64_t)(sg.start + td.off) * b.kw;
-    for (uint32_t k = t; k < td.n; k += kST) atomicAdd(&h[digit_at(keys + (uint64_t)k * b.kw, a.level)], 1u);
+    // only the digit's key word is read; a batch of loads is issued before its atomics
+    const uint32_t *keys = a.src + b.key_off + (uint64_t)(sg.start + td.off) * b.kw + a.level / 3;
+    const uint32_t sh = 20 - 10 * (a.level % 3);
+    for (uint32_t k0 = t; k0 < td.n; k0 += 8 * kST) {
+        uint32_t w[8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const uint32_t k = k0 + r * kST;
+            w[r] = k < td.n ? __ldg(keys + (uint64_t)k * b.kw) : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+            if (k0 + r * kST < td.n) atomicAdd(&h[(w[r] >> sh) & 1023u], 1u);
+    }
     __syncthreads();
     uint32_t *gh = a.hist + (size_t)td.seg * kRadixBins;
     for (int i = t; i < kRadixBins; i += kST)
@@ -217,14 +229,17 @@ __device__ __forceinline__ void scatter_tile(const MsdArgs &a, const MsdTile &td
     uint32_t key[KPT][KW], slot[(KPT + 1) / 2];
 #pragma unroll
     for (int r = 0; r < (KPT + 1) / 2; r++) slot[r] = 0;
+    // all loads first (a shared-memory atomic between them would serialise them)
 #pragma unroll
     for (int r = 0; r < KPT; r++) {
         const uint32_t i = t + r * kST;
-        if (i < td.n) {
 #pragma unroll
-            for (int u = 0; u < KW; u++) key[r][u] = __ldg(src + (uint64_t)i * KW + u);
-            slot[r / 2] |= atomicAdd(&hist[digit_reg<KW>(key[r], a.level)], 1u) << (16 * (r & 1));
-        }
+        for (int u = 0; u < KW; u++) key[r][u] = i < td.n ? __ldg(src + (uint64_t)i * KW + u) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < KPT; r++) {
+        const uint32_t i = t + r * kST;
+        if (i < td.n) slot[r / 2] |= atomicAdd(&hist[digit_reg<KW>(key[r], a.level)], 1u) << (16 * (r & 1));
     }
     __syncthreads();
     uint32_t c[4];

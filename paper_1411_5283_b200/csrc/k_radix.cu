@@ -359,9 +359,14 @@ __global__ void __launch_bounds__(kNT) k_digit_hist(RadixArgs a) {
     __syncthreads();
     const uint32_t *kin = a.kin + b.key_off;
     if (kw == 1) {
-        for (uint32_t k = k0 + t; k < k1; k += kNT) {
-            const uint32_t w = __ldg(kin + k);
-            for (uint32_t q = 0; q < nd; q++) atomicAdd(&h[q * kRadixBins + digit_of(w, 20 - 10 * q)], 1u);
+        for (uint32_t kb = k0 + t; kb < k1; kb += 8 * kNT) {   // batch the loads before the atomics
+            uint32_t w[8];
+#pragma unroll
+            for (int r = 0; r < 8; r++) w[r] = kb + r * kNT < k1 ? __ldg(kin + kb + r * kNT) : 0u;
+#pragma unroll
+            for (int r = 0; r < 8; r++)
+                if (kb + r * kNT < k1)
+                    for (uint32_t q = 0; q < nd; q++) atomicAdd(&h[q * kRadixBins + digit_of(w[r], 20 - 10 * q)], 1u);
         }
     } else {
         for (uint32_t k = k0 + t; k < k1; k += kNT) {

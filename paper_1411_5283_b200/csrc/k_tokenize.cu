@@ -82,12 +82,31 @@ struct TkScatterSmem {
 
 // Stage step `st` and build its ordered word start / end lists. Returns the number of words whose
 // first letter lies in the step (S); send[k + skip] is the last letter of word k.
-__device__ __forceinline__ uint32_t stage_step(TkCommon &sm, const uint8_t *__restrict__ text, uint64_t s0) {
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+constexpr int kTkPf = (kTkBuf / 16 + kTkThreads - 1) / kTkThreads;   // uint4 per thread per step
+
+// Issue the global loads of step `st` into registers (consumed by the next stage_step).
+__device__ __forceinline__ void prefetch_step(uint4 (&pf)[kTkPf], const uint8_t *__restrict__ text, uint64_t s0) {
+    const int t = threadIdx.x;
     const uint4 *src = reinterpret_cast<const uint4 *>(text + s0 - kTkPre);
 #pragma unroll
-    for (int i = t; i < kTkBuf / 16; i += kTkThreads) sm.buf[i] = __ldg(src + i);
+    for (int r = 0; r < kTkPf; r++) {
+        const int i = t + r * kTkThreads;
+        if (i < kTkBuf / 16) pf[r] = __ldg(src + i);
+    }
+}
+
+// Store a prefetched step into shared memory, then prefetch the next one (in flight while this step
+// is processed).
+__device__ __forceinline__ uint32_t stage_step(TkCommon &sm, uint4 (&pf)[kTkPf], const uint8_t *__restrict__ text,
+                                               uint64_t next_s0, bool has_next) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+#pragma unroll
+    for (int r = 0; r < kTkPf; r++) {
+        const int i = t + r * kTkThreads;
+        if (i < kTkBuf / 16) sm.buf[i] = pf[r];
+    }
     __syncthreads();
+    if (has_next) prefetch_step(pf, text, next_s0);
 
     const uint8_t *sb = reinterpret_cast<const uint8_t *>(sm.buf) + kTkPre;
     uint4 a = sm.buf[1 + 2 * t], b = sm.buf[2 + 2 * t];
@@ -170,9 +189,11 @@ __global__ void __launch_bounds__(kTkThreads) k_tokenize(TkArgs a) {
     }
     // (the first stage_step's __syncthreads orders these initialisations)
 
+    uint4 pf[kTkPf];
+    if (st0 < st1) prefetch_step(pf, a.text, (uint64_t)st0 * kTkStep);
     for (uint32_t st = st0; st < st1; st++) {
         const uint64_t s0 = (uint64_t)st * kTkStep;
-        const uint32_t S = stage_step(sm.c, a.text, s0);
+        const uint32_t S = stage_step(sm.c, pf, a.text, s0 + kTkStep, st + 1 < st1);
         const uint32_t skip = sm.c.skip;
         if constexpr (!kScatter) {
             for (uint32_t k = t; k < S; k += kTkThreads)
