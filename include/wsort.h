@@ -67,13 +67,15 @@ enum wsort_mem { WSORT_MEM_HOST = 0, WSORT_MEM_DEVICE = 1 };
 
 /* in-bucket sort (phase 3) */
 enum wsort_algo {
-    WSORT_ALGO_AUTO = 0,       /* library picks: MSD radix for keys-only sorts with L <= 48, else LSD radix
+    WSORT_ALGO_AUTO = 0,       /* library picks: MSD_OETS for keys-only sorts with L <= 48, else LSD radix
                                   (measured) */
     WSORT_ALGO_OETS_MERGE = 1, /* odd-even transposition tiles (the data-parallel bubble sort,
                                   PAPER.md:23) + merge-path merging (the paper's merge) */
     WSORT_ALGO_LSD_RADIX = 2,  /* segmented LSD radix over 2-letter (10-bit) digits (stable; src_off) */
-    WSORT_ALGO_MSD_RADIX = 3   /* MSD radix partitioning by 2-letter digits + CTA-local odd-even
-                                  transposition finish (keys only, L <= 48; else falls back to LSD) */
+    WSORT_ALGO_MSD_RADIX = 3,  /* MSD radix partitioning by 2-letter digits; small sub-buckets finished by
+                                  a CTA-local LSD radix in shared memory (keys only, L <= 48; else LSD) */
+    WSORT_ALGO_MSD_OETS = 4    /* as MSD_RADIX, but the small sub-buckets are finished by CTA-local
+                                  odd-even transposition (data-parallel bubble sort) + merge paths */
 };
 
 /* wsort_sort flags */

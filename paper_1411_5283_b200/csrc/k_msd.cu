@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
             const bool fin = final_digit || cnt == 1;
             const bool big = !fin && cnt > cap, skip = fin && !a.dst_is_a, copy = fin && a.dst_is_a && cnt > cap;
             if (big || skip || copy) {
-                if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a};
+                if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
                 jn = 0;
                 if (big) {
                     big_t0[ntop] = ntiles;
@@ -150,14 +150,14 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
                 }
             } else {
                 if (jn + cnt > cap) {
-                    jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a};
+                    jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
                     jn = 0;
                 }
                 if (!jn) js = start;
                 jn += cnt;
             }
         }
-        if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a};
+        if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
         uint32_t ntiny = 0, nbig = 0, nch = 0;
         for (uint32_t k = 0; k < nj; k++) ntiny += jobs[k].n <= 32;
         for (uint32_t k = 0; k < ntop; k++) {
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kST, 2) k_msd_scatter(MsdArgs a) {
 template <int KW>
 __device__ __forceinline__ void warp_oets(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b) {
     const int lane = threadIdx.x & 31;
-    const uint32_t *src = (sg.buf ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
+    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
     uint32_t k[KW];
 #pragma unroll
     for (int u = 0; u < KW; u++) k[u] = lane < (int)sg.n ? __ldg(src + lane * KW + u) : 0xffffffffu;
@@ -356,17 +356,25 @@ struct Key {
 };
 template <int KW>
 __device__ __forceinline__ bool klt(const Key<KW> &x, const Key<KW> &y) {
+    if constexpr (KW == 1) {
+        return x.w[0] < y.w[0];
+    } else if constexpr (KW == 2) {
+        return (((uint64_t)x.w[0] << 32) | x.w[1]) < (((uint64_t)y.w[0] << 32) | y.w[1]);
+    } else {
 #pragma unroll
-    for (int u = 0; u < KW; u++)
-        if (x.w[u] != y.w[u]) return x.w[u] < y.w[u];
-    return false;
+        for (int u = 0; u < KW; u++)
+            if (x.w[u] != y.w[u]) return x.w[u] < y.w[u];
+        return false;
+    }
 }
 template <int KW>
 __device__ __forceinline__ void kce(Key<KW> &x, Key<KW> &y) {   // compare-exchange: x <= y afterwards
-    if (klt<KW>(y, x)) {
-        const Key<KW> t = x;
-        x = y;
-        y = t;
+    const bool sw = klt<KW>(y, x);
+#pragma unroll
+    for (int u = 0; u < KW; u++) {   // branch-free select
+        const uint32_t a = x.w[u], b = y.w[u];
+        x.w[u] = sw ? b : a;
+        y.w[u] = sw ? a : b;
     }
 }
 template <int KW>
@@ -399,7 +407,7 @@ __device__ __forceinline__ void cta_sort_job(const MsdArgs &a, const MsdSeg &sg,
     constexpr uint32_t TN = kST * E;
     const int t = threadIdx.x, lane = t & 31;
     const uint32_t n = sg.n;
-    const uint32_t *src = (sg.buf ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
+    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
     Key<KW> v[E];
 #pragma unroll
     for (int e = 0; e < E; e++) {
@@ -493,10 +501,96 @@ __device__ __forceinline__ void cta_sort_job(const MsdArgs &a, const MsdSeg &sg,
     for (uint32_t i = t; i < n * KW; i += kST) dst[i] = s0[i + (i >> 5)];
 }
 
+// Local LSD radix finish (optional): a job's keys share the digits above `level` (a job packs
+// consecutive children of one segment, which differ first at digit `level`), so sorting it by
+// digits ndig-1 .. level (least significant first) sorts it. Each 10-bit digit is two stable 5-bit
+// counting sub-passes over the tile in shared memory: thread-private 16-bit counters over 32 bins,
+// one block scan, scatter (blocked key ownership keeps the order stable).
+__device__ __forceinline__ uint32_t padm(uint32_t i) { return i + (i >> 5); }
+
+template <int KW>
+__device__ __forceinline__ void radix_job(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint32_t *sm) {
+    constexpr int KPT = 8;                         // keys per thread (blocked)
+    constexpr uint32_t TN = kST * KPT;             // 2048 = CTA-sort capacity for kw <= 4
+    const int t = threadIdx.x;
+    const uint32_t n = sg.n, level = sg.buf >> 8;
+    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
+    constexpr uint32_t PW = TN * KW + TN * KW / 32 + 1;
+    uint32_t *A = sm, *B = sm + PW;
+    uint32_t *cnt = B + PW;                        // 32 bins x 256 threads, u32, padded
+    uint32_t *wsum = cnt + 32 * kST + 32 * kST / 32 + 1;
+    for (uint32_t i = t; i < TN * KW; i += kST) A[padm(i)] = i < n * KW ? __ldg(src + i) : 0xffffffffu;
+    __syncthreads();
+    for (int q = (int)b.ndig - 1; q >= (int)level; q--) {
+        const uint32_t wi = q / 3, sh = 20 - 10 * (q % 3);
+        for (int half = 0; half < 2; half++) {
+            const uint32_t fs = sh + (half ? 5 : 0);   // 5-bit field: low letter first
+            uint32_t key[KPT][KW], rk[KPT];
+#pragma unroll
+            for (int f = 0; f < 32; f++) cnt[padm(f * kST + t)] = 0;
+#pragma unroll
+            for (int k = 0; k < KPT; k++) {
+#pragma unroll
+                for (int u = 0; u < KW; u++) key[k][u] = A[padm((t * KPT + k) * KW + u)];
+                uint32_t w = key[k][0];
+#pragma unroll
+                for (int u = 1; u < KW; u++) w = wi == (uint32_t)u ? key[k][u] : w;
+                const uint32_t f = (w >> fs) & 31u;
+                uint32_t *cp = cnt + padm(f * kST + t);
+                rk[k] = *cp;
+                *cp = rk[k] + 1;
+            }
+            __syncthreads();
+            {   // exclusive scan in (bin, thread) order; thread t owns linear entries [32t, 32t+32)
+                uint32_t sum = 0;
+#pragma unroll
+                for (int i = 0; i < 32; i++) sum += cnt[padm(32 * t + i)];
+                uint32_t run = block_excl_scan_m(sum, wsum, nullptr);
+#pragma unroll
+                for (int i = 0; i < 32; i++) {
+                    const uint32_t x = cnt[padm(32 * t + i)];
+                    cnt[padm(32 * t + i)] = run;
+                    run += x;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < KPT; k++) {
+                uint32_t w = key[k][0];
+#pragma unroll
+                for (int u = 1; u < KW; u++) w = wi == (uint32_t)u ? key[k][u] : w;
+                const uint32_t pos = cnt[padm(((w >> fs) & 31u) * kST + t)] + rk[k];
+#pragma unroll
+                for (int u = 0; u < KW; u++) B[padm(pos * KW + u)] = key[k][u];
+            }
+            __syncthreads();
+            uint32_t *sw = A;
+            A = B;
+            B = sw;
+        }
+    }
+    uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
+    for (uint32_t i = t; i < n * KW; i += kST) dst[i] = A[padm(i)];
+}
+
+__global__ void __launch_bounds__(kST) k_msd_radix_job(MsdArgs a) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const MsdSeg sg = a.q_small[blockIdx.x];
+    const BucketInfo b = a.buckets[sg.L];
+    switch (b.kw) {
+        case 1: radix_job<1>(a, sg, b, sm); break;
+        case 2: radix_job<2>(a, sg, b, sm); break;
+        case 3: radix_job<3>(a, sg, b, sm); break;
+        case 4: radix_job<4>(a, sg, b, sm); break;
+        default: break;   // wider keys use the odd-even transposition finish
+    }
+}
+
 __global__ void __launch_bounds__(kST) k_msd_cta_sort(MsdArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     const MsdSeg sg = a.q_small[blockIdx.x];
     const BucketInfo b = a.buckets[sg.L];
+    if (a.finish_radix && b.kw <= 4) return;   // done by k_msd_radix_job
     switch (b.kw) {
         case 1: cta_sort_job<1>(a, sg, b, sm); break;
         case 2: cta_sort_job<2>(a, sg, b, sm); break;
@@ -541,6 +635,13 @@ cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_cop
     cudaError_t e;
     if (a.n_tiny) {
         k_msd_warp_sort<<<(a.n_tiny + kST / 32 - 1) / (kST / 32), kST, 0, s>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (n_small && a.finish_radix) {
+        const size_t smem = ((size_t)2 * (2048 * 4 + 2048 * 4 / 32 + 1) + 32 * kST + 32 * kST / 32 + 1 + kST / 32 + 1) * 4;
+        e = cudaFuncSetAttribute(k_msd_radix_job, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_msd_radix_job<<<n_small, kST, smem, s>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (n_small) {

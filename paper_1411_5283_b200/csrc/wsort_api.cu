@@ -743,7 +743,7 @@ int sort_oets(wsort_ctx *c, bool want_src) {
 // msd_radix (keys only): MSD partitioning by 2-letter digits, level by level, with device-side
 // planning (k_msd_plan queues the next level's segments and the finishing jobs); one small D2H of
 // the queue counters per level sizes the next launches.
-int sort_msd(wsort_ctx *c) {
+int sort_msd(wsort_ctx *c, bool finish_radix) {
     const Summary &s = *c->h_sum;
     const uint32_t lmax = s.max_len;
     std::vector<BucketInfo> bk(256, BucketInfo{});
@@ -830,6 +830,7 @@ int sort_msd(wsort_ctx *c) {
     m.cap_copy = cap_copy;
     m.keys_a = ka;
     m.keys_b = kb;
+    m.finish_radix = finish_radix ? 1u : 0u;
     uint32_t nsegs = (uint32_t)segs.size(), ntiles = (uint32_t)tiles.size();
     std::vector<uint64_t> tile_words_level;
     for (uint32_t level = 0; nsegs > 0; level++) {
@@ -905,7 +906,7 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     if (!c) return WSORT_E_INVALID_ARG;
     if (c->state < ST_TOKENIZED) return set_err(c, WSORT_E_STATE, "wsort_sort before wsort_tokenize");
     if (algo != WSORT_ALGO_AUTO && algo != WSORT_ALGO_LSD_RADIX && algo != WSORT_ALGO_OETS_MERGE &&
-        algo != WSORT_ALGO_MSD_RADIX)
+        algo != WSORT_ALGO_MSD_RADIX && algo != WSORT_ALGO_MSD_OETS)
         return set_err(c, WSORT_E_INVALID_ARG, "bad algo %d", algo);
     if (flags & ~WSORT_FLAG_SRC_OFF) return set_err(c, WSORT_E_INVALID_ARG, "bad flags 0x%x", flags);
     if (c->keys_external && !c->packed_pending)
@@ -917,9 +918,9 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     int rc;
     if (algo == WSORT_ALGO_OETS_MERGE) {
         rc = sort_oets(c, want_src);
-    } else if ((algo == WSORT_ALGO_MSD_RADIX || algo == WSORT_ALGO_AUTO) && !want_src &&
+    } else if ((algo == WSORT_ALGO_MSD_RADIX || algo == WSORT_ALGO_MSD_OETS || algo == WSORT_ALGO_AUTO) && !want_src &&
                kw_of((int)c->h_sum->max_len) <= (int)kRadixRegMaxKw) {
-        rc = sort_msd(c);
+        rc = sort_msd(c, algo == WSORT_ALGO_MSD_RADIX);   // AUTO: odd-even transposition finish (measured faster)
     } else {
         rc = sort_radix(c, want_src);
     }

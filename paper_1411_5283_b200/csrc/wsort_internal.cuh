@@ -167,7 +167,8 @@ cudaError_t launch_regroup(const CopyRange *ranges, uint32_t nranges, const uint
 
 // ---------------- msd_radix: MSD partitioning + CTA-local odd-even transposition finish ----------------
 struct MsdSeg {
-    uint32_t L, start, n, buf;     // key range [start, start+n) of bucket L; buf: 1 = in A, 0 = in B
+    uint32_t L, start, n, buf;     // key range [start, start+n) of bucket L; buf bit 0: 1 = in A, 0 = in B;
+                                   // buf >> 8: first digit still to sort (sort jobs)
 };
 struct MsdTile {
     uint32_t seg, off, n, pad_;    // keys [off, off+n) of segment `seg` of this level
@@ -192,6 +193,7 @@ struct MsdArgs {
     const uint32_t *keys_a;        // finishing: buffer A
     uint32_t *keys_b;              // finishing: buffer B (final)
     uint32_t n_tiny;
+    uint32_t finish_radix;         // 1: small jobs with kw <= 4 by local LSD radix, else odd-even transposition
 };
 size_t msd_scatter_smem();
 cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);

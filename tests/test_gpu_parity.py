@@ -20,7 +20,7 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["lsd_radix", "oets_merge", "msd_radix"]
+ALGOS = ["lsd_radix", "oets_merge", "msd_radix", "msd_oets"]
 
 
 @pytest.fixture(scope="module")
