@@ -64,6 +64,7 @@ struct TkCommon {
     uint32_t warp_tot[kTkThreads / 32];
     uint32_t totals;
     uint32_t skip;
+    uint32_t qw[2 * (kTkThreads / 32) + 1];
 };
 
 struct TkCountSmem {
@@ -164,6 +165,75 @@ __device__ __forceinline__ uint32_t stage_step(TkCommon &sm, uint4 (&pf)[kTkPf],
 // kMode: 0 = K1 count; 1 = K3 scatter, any order within a (CTA, length) run (keys only: the sort
 // that follows fixes the order of distinct keys, and equal keys are identical words);
 // 2 = K3 scatter, stable (text order within each length; needed for the src_off payload).
+// List-free variant for K1 and the unordered K3: each thread keeps its own segment's word-start and
+// word-end masks; a word that runs past the segment end takes its remaining length from `carry`, the
+// length of the letter run that starts at the next segment's first byte (a suffix scan over the
+// threads of the run-combining operator (l1,f1)+(l2,f2) = (l1 + f1*l2, f1 & f2), where l is the
+// number of leading letters of a segment and f says the segment is all letters).
+struct SegRuns {
+    uint32_t starts, ends, carry;
+};
+
+__device__ __forceinline__ SegRuns stage_step_runs(TkCommon &sm, uint32_t *qw, uint4 (&pf)[kTkPf],
+                                                   const uint8_t *__restrict__ text, uint64_t next_s0, bool has_next) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+#pragma unroll
+    for (int r = 0; r < kTkPf; r++) {
+        const int i = t + r * kTkThreads;
+        if (i < kTkBuf / 16) sm.buf[i] = pf[r];
+    }
+    __syncthreads();
+    if (has_next) prefetch_step(pf, text, next_s0);
+    const uint8_t *sb = reinterpret_cast<const uint8_t *>(sm.buf) + kTkPre;
+    const uint32_t M = letter_mask32(sm.buf[1 + 2 * t], sm.buf[2 + 2 * t]);
+    const uint32_t p = is_letter(sb[32 * t - 1]), nx = is_letter(sb[32 * t + 32]);
+    SegRuns r;
+    r.starts = M & ~((M << 1) | p);
+    r.ends = M & ~((M >> 1) | (nx << 31));
+    const uint32_t full = M == 0xffffffffu;
+    uint32_t l = full ? 32u : (uint32_t)(__ffs(~M) - 1), f = full;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t l2 = __shfl_down_sync(kFull, l, o), f2 = __shfl_down_sync(kFull, f, o);
+        if (lane + o < 32 && f) {
+            l += l2;
+            f = f2;
+        }
+    }
+    if (lane == 0) qw[warp] = l | (f << 31);
+    __syncthreads();
+    if (t == 0) {   // chain the warps from the right, starting from the letters at the halo's head
+        uint32_t i = kTkStep;
+        while (i < kTkStep + kTkHalo && is_letter(sb[i])) i++;
+        uint32_t q = i - kTkStep;
+        qw[kTkThreads / 32 * 2] = q;
+        for (int w = kTkThreads / 32 - 1; w >= 0; w--) {
+            const uint32_t x = qw[w];
+            q = (x & 0x7fffffffu) + ((x >> 31) ? q : 0u);
+            qw[kTkThreads / 32 + w] = q;   // run starting at warp w's first byte
+        }
+    }
+    __syncthreads();
+    const uint32_t qnext = warp + 1 < kTkThreads / 32 ? qw[kTkThreads / 32 + warp + 1] : qw[kTkThreads / 32 * 2];
+    const uint32_t l1 = __shfl_down_sync(kFull, l, 1), f1 = __shfl_down_sync(kFull, f, 1);
+    r.carry = lane < 31 ? l1 + (f1 ? qnext : 0u) : qnext;
+    return r;
+}
+
+// Visit the words that start in this thread's segment: fn(start byte within the step, length).
+template <class F>
+__device__ __forceinline__ void for_each_word(const SegRuns &r, F fn) {
+    const int t = threadIdx.x;
+    uint32_t m = r.starts;
+    while (m) {
+        const uint32_t s = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t em = r.ends & (0xffffffffu << s);
+        const uint32_t L = em ? (uint32_t)(__ffs(em) - 1) - s + 1u : (32u - s) + r.carry;
+        fn(32u * t + s, L);
+    }
+}
+
 template <int kMode>
 struct SmemOf { using type = TkScatterSmem; };
 template <>
@@ -193,13 +263,16 @@ __global__ void __launch_bounds__(kTkThreads) k_tokenize(TkArgs a) {
     if (st0 < st1) prefetch_step(pf, a.text, (uint64_t)st0 * kTkStep);
     for (uint32_t st = st0; st < st1; st++) {
         const uint64_t s0 = (uint64_t)st * kTkStep;
+        if constexpr (kMode == 0) {
+            const SegRuns r = stage_step_runs(sm.c, sm.c.qw, pf, a.text, s0 + kTkStep, st + 1 < st1);
+            for_each_word(r, [&](uint32_t, uint32_t L) { atomicAdd(&sm.hist[min(L, 256u)], 1u); });
+            __syncthreads();   // the stage buffer is rewritten by the next step
+        } else {
+        // K3: words are dealt round-robin from the ordered lists (even load per thread; the per-word
+        // work is heavy, so this balances better than the list-free per-segment walk of K1)
         const uint32_t S = stage_step(sm.c, pf, a.text, s0 + kTkStep, st + 1 < st1);
         const uint32_t skip = sm.c.skip;
-        if constexpr (!kScatter) {
-            for (uint32_t k = t; k < S; k += kTkThreads)
-                atomicAdd(&sm.hist[min((uint32_t)sm.c.send[k + skip] - sm.c.sstart[k] + 1u, 256u)], 1u);
-            __syncthreads();   // lists are rewritten by the next step
-        } else if constexpr (kMode == 1) {
+        if constexpr (kMode == 1) {
             const uint32_t *buf32 = reinterpret_cast<const uint32_t *>(sm.c.buf);
             for (uint32_t k = t; k < S; k += kTkThreads) {
                 const uint32_t start = sm.c.sstart[k];
@@ -253,6 +326,7 @@ __global__ void __launch_bounds__(kTkThreads) k_tokenize(TkArgs a) {
             __syncthreads();
             for (int w = 0; w < kTkThreads / 32; w++) sm.wcnt[w][t] = 0;
             // the next stage_step's first __syncthreads orders this reset before phase A
+        }
         }
     }
     if constexpr (!kScatter) {
