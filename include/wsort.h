@@ -67,15 +67,20 @@ enum wsort_mem { WSORT_MEM_HOST = 0, WSORT_MEM_DEVICE = 1 };
 
 /* in-bucket sort (phase 3) */
 enum wsort_algo {
-    WSORT_ALGO_AUTO = 0,       /* library picks: MSD_OETS for keys-only sorts with L <= 48, else LSD radix
+    WSORT_ALGO_AUTO = 0,       /* library picks: DENSE_MSD for keys-only sorts of a tokenized text with every
+                                  word <= 48 letters, else MSD_OETS (keys only, L <= 48), else LSD radix
                                   (measured) */
     WSORT_ALGO_OETS_MERGE = 1, /* odd-even transposition tiles (the data-parallel bubble sort,
                                   PAPER.md:23) + merge-path merging (the paper's merge) */
     WSORT_ALGO_LSD_RADIX = 2,  /* segmented LSD radix over 2-letter (10-bit) digits (stable; src_off) */
     WSORT_ALGO_MSD_RADIX = 3,  /* MSD radix partitioning by 2-letter digits; small sub-buckets finished by
                                   a CTA-local LSD radix in shared memory (keys only, L <= 48; else LSD) */
-    WSORT_ALGO_MSD_OETS = 4    /* as MSD_RADIX, but the small sub-buckets are finished by CTA-local
+    WSORT_ALGO_MSD_OETS = 4,   /* as MSD_RADIX, but the small sub-buckets are finished by CTA-local
                                   odd-even transposition (data-parallel bubble sort) + merge paths */
+    WSORT_ALGO_DENSE_MSD = 5   /* words of L <= 5 counted in dense tables during wsort_tokenize (the sorted
+                                  sub-array is the counting sort of the word's base-26 value); longer words
+                                  staged as keys by the same text pass and sorted by MSD_OETS from there.
+                                  Keys only; falls back like AUTO when it does not apply */
 };
 
 /* wsort_sort flags */

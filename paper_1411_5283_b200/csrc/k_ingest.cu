@@ -1,0 +1,683 @@
+// k_ingest.cu — the one-pass text front end of the keys-only path and its two consumers.
+//
+// K1 k_ingest: phases 1-2 of the method (§3 Methodology, Pre-processing) in ONE read
+//   of the text. Every maximal run of ASCII letters is a word (reading A1, "removing / ignoring the
+//   special characters"); per word of length L:
+//     * the length histogram ("the number of elements with the same number of characters",
+//       PAPER.md:13) — per CTA (the byte ranges K3 uses) and global;
+//     * L <= 5 (dense-key counting): the word IS its dense index
+//       idx = sum c_j 26^(L-1-j) (c_j = letter code 0..25), so its sub-array sorted alphabetically
+//       is the counting sort of idx. L <= 2 count in shared memory; L = 3..5 go through a small
+//       shared-memory hash cache (hot words) and fall back to global atomics (cold words);
+//     * 6 <= L <= 48: the word is packed into its fixed-width key (kw = ceil(L/6) u32, the paper's
+//       "array char 3D") and appended to a staging chunk of its key-width class.
+//       Chunks (16 KiB) come from the CTA's own region of the pool (bounded: key bytes <= text bytes);
+//       order inside a chunk is arbitrary (keys only: equal keys are identical words).
+// K2d k_dense_reduce / k_dense_scan / k_dense_compact: exclusive scan of the dense counts (which is
+//   the global word index, since buckets 1..5 come first) and compaction of the non-zero entries.
+// K3c k_lscatter: the staged keys, chunk by chunk, into their length buckets (buffer A); the MSD
+//   levels of k_msd.cu sort the buckets from there.
+// K5d k_emit_dense: "prints the results" for L <= 5: word w of the dense buckets is
+//   the entry whose count range holds w; written as "word\n" (reading A12).
+#include "k_text.cuh"
+#include "wsort_internal.cuh"
+
+namespace wsort {
+namespace {
+
+using namespace text;
+
+constexpr int kIgWarps = kIgThreads / 32;
+constexpr int kCacheSlots = 2048;
+
+// entries of the dense tables of lengths < L: (26^L - 26) / 25
+__host__ __device__ constexpr uint32_t dense_base(uint32_t L) {
+    return L <= 1 ? 0u : L == 2 ? 26u : L == 3 ? 702u : L == 4 ? 18278u : L == 5 ? 475254u : 12356630u;
+}
+
+constexpr int kSub = 1024;                   // bytes per warp sub-step (32 per lane)
+constexpr int kSubTail = 128;                // staged bytes past it (a staged word: <= 48 letters + slack)
+constexpr int kWBuf = kSub + kSubTail;
+constexpr int kWList = kSub / 2;             // at most one word start per two bytes
+constexpr uint16_t kNoChunk16 = 0xffffu, kTrash16 = 0xfffeu;
+
+// keys per chunk of class k: the largest power of two <= kChunkWords / k
+__host__ __device__ constexpr uint32_t cls_lg(uint32_t k) { return k == 1 ? 12u : k == 2 ? 11u : k <= 4 ? 10u : 9u; }
+
+struct IgSmem {
+    uint4 wbuf[kIgWarps][kWBuf / 16 + 1];  // per warp: its sub-step + tail (+16 B: packing reads whole words)
+    uint16_t wlist[kIgWarps][kWList];      // per warp: s | (L-3) << 10; L = 3..5 from the front, 6..48 from the back
+    uint32_t d12[702];                     // dense counts of L = 1, 2
+    uint32_t ctag[kCacheSlots];            // hash cache for L = 3..5: tag = L << 24 | idx, 0 = empty
+    uint32_t ccnt[kCacheSlots];
+    uint32_t hist[kHistBins];
+    uint32_t nchunk;                       // chunks this CTA took from its region
+    uint32_t cls_fill[kMaxStageKw];        // keys of class k staged so far
+    // dynamic: uint16_t chunk_of[kMaxStageKw][cta_chunks]: local chunk of (class, sequence number)
+};
+
+// dense index of the word of length L <= 5 at byte boff of a staged buffer
+__device__ __forceinline__ uint32_t dense_index(const uint32_t *buf32, uint32_t boff, uint32_t L) {
+    const uint32_t a = boff >> 2, sh = 8u * (boff & 3u);
+    const uint32_t w0 = buf32[a], w1 = buf32[a + 1], w2 = buf32[a + 2];
+    const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+    uint32_t idx = (lo & 31u) - 1u;
+    if (L > 1) idx = idx * 26u + ((lo >> 8) & 31u) - 1u;
+    if (L > 2) idx = idx * 26u + ((lo >> 16) & 31u) - 1u;
+    if (L > 3) idx = idx * 26u + ((lo >> 24) & 31u) - 1u;
+    if (L > 4) idx = idx * 26u + (hi & 31u) - 1u;
+    return idx;
+}
+
+// one probe of the hash cache: true if the word was counted in slot h
+__device__ __forceinline__ bool cache_try(IgSmem &sm, uint32_t h, uint32_t tag) {
+    uint32_t cur = *reinterpret_cast<volatile uint32_t *>(&sm.ctag[h]);
+    if (cur == 0u) {
+        cur = atomicCAS(&sm.ctag[h], 0u, tag);
+        if (cur == 0u) cur = tag;
+    }
+    if (cur != tag) return false;
+    atomicAdd(&sm.ccnt[h], 1u);
+    return true;
+}
+
+// two-choice hash cache (hot words stay in shared memory); a word whose slots are both taken by other
+// words is counted in the global table directly
+__device__ __forceinline__ void cache_add(IgSmem &sm, uint32_t *dense, uint32_t L, uint32_t idx) {
+    const uint32_t tag = (L << 24) | idx;
+    const uint32_t hh = tag * 0x9E3779B1u;
+    if (cache_try(sm, hh >> 21, tag)) return;
+    if (cache_try(sm, (hh >> 10) & (kCacheSlots - 1), tag)) return;
+    atomicAdd(&dense[dense_base(L) + idx], 1u);
+}
+
+__device__ __forceinline__ uint32_t inclusive_scan_warp(uint32_t v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += y;
+    }
+    return v;
+}
+
+// letters leading a 32-bit letter mask, and whether all 32 are letters
+__device__ __forceinline__ uint32_t lead_run(uint32_t M) { return M == 0xffffffffu ? 32u : (uint32_t)(__ffs(~M) - 1); }
+
+// K1. The CTA's byte range is split into 16 contiguous warp ranges of 1 KiB sub-steps; each warp
+// streams its sub-steps with no block barrier: every lane classifies 32 bytes (SWAR letter mask, loaded
+// one sub-step ahead), word starts / ends come from mask shifts, the letter runs crossing lane
+// boundaries from a suffix scan of (l1,f1)+(l2,f2) = (l1 + f1*l2, f1 & f2) (l = letters leading a
+// segment, f = all letters). Words of L <= 2 are counted by their owner lane; L = 3..5 and 6..48 are
+// listed by category (warp scan) and then taken round-robin by the lanes: hash-cache count / key
+// packing into the class's chunk. Chunk (class, seq) is allocated by the lane that receives its
+// first rank; the others read its id from shared memory (written once).
+__global__ void __launch_bounds__(kIgThreads, 3) k_ingest(IngestArgs a) {
+    extern __shared__ __align__(16) uint8_t ig_smem[];
+    IgSmem &sm = *reinterpret_cast<IgSmem *>(ig_smem);
+    uint16_t *chunk_of = reinterpret_cast<uint16_t *>(ig_smem + sizeof(IgSmem));
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t c = blockIdx.x;
+    const uint64_t b0 = (uint64_t)c * a.steps_per_cta * kTkStep;
+    const uint64_t b1 = min((uint64_t)(c + 1) * a.steps_per_cta, (uint64_t)a.nsteps) * kTkStep;
+    const uint32_t cbase = c * a.cta_chunks;
+    const uint32_t trash = a.grid * a.cta_chunks;
+
+    for (int i = t; i < 702; i += kIgThreads) sm.d12[i] = 0;
+    for (int i = t; i < kCacheSlots; i += kIgThreads) sm.ctag[i] = sm.ccnt[i] = 0;
+    for (int i = t; i < kHistBins; i += kIgThreads) sm.hist[i] = 0;
+    for (uint32_t i = t; i < kMaxStageKw * a.cta_chunks; i += kIgThreads) chunk_of[i] = kNoChunk16;
+    if (t < (int)kMaxStageKw) sm.cls_fill[t] = 0;
+    if (t == 0) sm.nchunk = 0;
+    __syncthreads();
+
+    const uint32_t nsub = b0 < b1 ? (uint32_t)((b1 - b0) / kSub) : 0u;
+    const uint32_t w0 = (uint32_t)((uint64_t)nsub * warp / kIgWarps), w1 = (uint32_t)((uint64_t)nsub * (warp + 1) / kIgWarps);
+    uint8_t *wb = reinterpret_cast<uint8_t *>(sm.wbuf[warp]);
+    const uint32_t *wb32 = reinterpret_cast<const uint32_t *>(sm.wbuf[warp]);
+    uint16_t *wlst = sm.wlist[warp];
+    uint4 va, vb, ta, tb;
+    uint32_t prev_last = 0;
+    if (w0 < w1) {
+        const uint8_t *p = a.text + b0 + (uint64_t)w0 * kSub;
+        va = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane);
+        vb = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1);
+        if (lane < kSubTail / 32) {
+            ta = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane);
+            tb = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane + 1);
+        }
+        prev_last = is_letter(p[-1]);
+    }
+    for (uint32_t sub = w0; sub < w1; sub++) {
+        const uint64_t base = b0 + (uint64_t)sub * kSub;
+        reinterpret_cast<uint4 *>(wb)[2 * lane] = va;
+        reinterpret_cast<uint4 *>(wb)[2 * lane + 1] = vb;
+        const uint32_t M = letter_mask32(va, vb);
+        uint32_t Mt = 0;
+        if (lane < kSubTail / 32) {
+            reinterpret_cast<uint4 *>(wb + kSub)[2 * lane] = ta;
+            reinterpret_cast<uint4 *>(wb + kSub)[2 * lane + 1] = tb;
+            Mt = letter_mask32(ta, tb);
+        }
+        if (sub + 1 < w1) {   // prefetch the next sub-step
+            const uint8_t *p = a.text + base + kSub;
+            va = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane);
+            vb = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1);
+            if (lane < kSubTail / 32) {
+                ta = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane);
+                tb = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane + 1);
+            }
+        }
+        const uint32_t pm = __shfl_up_sync(kFull, M, 1), nm = __shfl_down_sync(kFull, M, 1);
+        const uint32_t pl = lane ? (pm >> 31) : prev_last;
+        const uint32_t mt0 = __shfl_sync(kFull, Mt, 0);   // (every lane shuffles: full-mask shuffles must not diverge)
+        const uint32_t nx = lane < 31 ? (nm & 1u) : (mt0 & 1u);
+        prev_last = __shfl_sync(kFull, M, 31) >> 31;
+        const uint32_t starts = M & ~((M << 1) | pl);
+        const uint32_t ends = M & ~((M >> 1) | (nx << 31));
+        // letters at the head of the tail (the run a word crossing the sub-step continues with)
+        uint32_t qh;
+        {
+            uint32_t tl = lane < kSubTail / 32 ? lead_run(Mt) : 0u, tf = lane < kSubTail / 32 ? (uint32_t)(Mt == 0xffffffffu) : 0u;
+#pragma unroll
+            for (int o = 1; o < kSubTail / 32; o <<= 1) {
+                const uint32_t l2 = __shfl_down_sync(kFull, tl, o), f2 = __shfl_down_sync(kFull, tf, o);
+                if (lane + o < kSubTail / 32 && tf) {
+                    tl += l2;
+                    tf = f2;
+                }
+            }
+            qh = __shfl_sync(kFull, tl, 0);
+            if (qh == (uint32_t)kSubTail) {   // rare: a run of >= 128 letters; count on (it is > 48 letters anyway)
+                const uint8_t *p = a.text + base + kSub;
+                uint32_t i = kSubTail;
+                while (i < 300u && is_letter(p[i])) i++;
+                qh = i;
+            }
+        }
+        uint32_t l = lead_run(M), f = M == 0xffffffffu;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t l2 = __shfl_down_sync(kFull, l, o), f2 = __shfl_down_sync(kFull, f, o);
+            if (lane + o < 32 && f) {
+                l += l2;
+                f = f2;
+            }
+        }
+        const uint32_t l1 = __shfl_down_sync(kFull, l, 1), f1 = __shfl_down_sync(kFull, f, 1);
+        const uint32_t carry = lane < 31 ? l1 + (f1 ? qh : 0u) : qh;
+        const uint32_t seg0 = 32u * lane;
+        // categories from the masks: a word starting at bit i has L >= j iff bytes i..i+j-1 are letters
+        // (X = this lane's letters followed by the next lane's / the tail's)
+        uint32_t n345, nlong;
+        {
+            const uint32_t N = lane < 31 ? nm : mt0;
+            const uint64_t X = (uint64_t)M | ((uint64_t)N << 32);
+            const uint32_t ge3 = starts & (uint32_t)(X >> 1) & (uint32_t)(X >> 2);
+            const uint32_t ge6 = ge3 & (uint32_t)(X >> 3) & (uint32_t)(X >> 4) & (uint32_t)(X >> 5);
+            nlong = __popc(ge6);
+            n345 = __popc(ge3) - nlong;
+        }
+        const uint32_t cnt = n345 | (nlong << 16);
+        const uint32_t ci = inclusive_scan_warp(cnt, lane);
+        const uint32_t tot = __shfl_sync(kFull, ci, 31);
+        uint32_t p3 = (ci - cnt) & 0xffffu, plg = (ci - cnt) >> 16;
+        for (uint32_t m = starts; m; m &= m - 1) {
+            const uint32_t bit = __ffs(m) - 1;
+            const uint32_t em = ends & (0xffffffffu << bit);
+            const uint32_t L = em ? (uint32_t)(__ffs(em) - 1) - bit + 1u : (32u - bit) + carry;
+            const uint32_t s = seg0 + bit;
+            if (L <= 2u) {   // L = 1, 2: count now (shared-memory table)
+                const uint32_t lo = __funnelshift_r(wb32[s >> 2], wb32[(s >> 2) + 1], 8u * (s & 3u));
+                const uint32_t idx = L == 1u ? (lo & 31u) - 1u : 26u + ((lo & 31u) - 1u) * 26u + ((lo >> 8) & 31u) - 1u;
+                if (!(a.debug & 1)) atomicAdd(&sm.d12[idx], 1u);
+            } else if (L <= kDenseMaxLen) {
+                wlst[p3++] = (uint16_t)(s | ((L - 3u) << 10));
+            } else {   // L >= 6; lengths above 48 are kept as 49 (not staged) and counted too long if > 255
+                wlst[kWList - 1 - plg++] = (uint16_t)(s | ((min(L, 49u) - 6u) << 10));
+                if (L > (uint32_t)kMaxLen) atomicAdd(&sm.hist[256], 1u);
+            }
+        }
+        __syncwarp();
+        const uint32_t n3 = tot & 0xffffu, nlg = tot >> 16;
+        for (uint32_t i = lane; i < ((a.debug & 17) ? 0u : n3); i += 32) {   // L = 3..5: hash cache
+            const uint32_t x = wlst[i];
+            const uint32_t s = x & 1023u, L = (x >> 10) + 3u;
+            cache_add(sm, a.dense, L, dense_index(wb32, s, L));
+        }
+        for (uint32_t i0 = 0; i0 < ((a.debug & 8) ? 0u : nlg); i0 += 32) {   // L = 6..48: key into its class's chunk
+            const uint32_t i = i0 + lane;
+            const uint32_t x = i < nlg ? wlst[kWList - 1 - i] : 0u;
+            const uint32_t s = x & 1023u, L = (x >> 10) + 6u;
+            const bool v = i < nlg && L <= 6u * kMaxStageKw;
+            if (i < nlg) {
+                if (v) atomicAdd(&sm.hist[L], 1u);
+                else atomicAdd(&a.ctr[kIgVeryLong], 1u);   // too long to stage: the host sorts with K3 + LSD
+            }
+            const uint32_t k = (L + 5u) / 6u, lg = cls_lg(k);
+            uint32_t r = 0;
+            if (v) r = atomicAdd(&sm.cls_fill[k - 1], 1u);
+            const uint32_t seq = r >> lg, pos = r & ((1u << lg) - 1u);
+            uint16_t *slot = chunk_of + (k - 1) * a.cta_chunks + min(seq, a.cta_chunks - 1);
+            if (v && pos == 0) {   // first key of chunk (k, seq): take a chunk from the region, publish its id
+                uint32_t id = atomicAdd(&sm.nchunk, 1u);
+                if (id >= a.cta_chunks || seq >= a.cta_chunks) {   // cannot happen (key bytes <= text bytes + 256)
+                    atomicExch(&a.ctr[kIgOverflow], 1u);
+                    id = kTrash16;
+                } else {
+                    a.chunk_cls[cbase + id] = k;
+                }
+                *reinterpret_cast<volatile uint16_t *>(slot) = (uint16_t)id;
+            }
+            __syncwarp();   // ids published by this warp are visible; other warps publish right after their atomic
+            if (!v || (a.debug & 2)) continue;
+            uint32_t id, spins = 0;
+            while ((id = *reinterpret_cast<volatile uint16_t *>(slot)) == kNoChunk16) {
+                if (++spins > (1u << 22)) {   // never expected: report instead of hanging
+                    atomicExch(&a.ctr[kIgOverflow], 2u);
+                    id = kTrash16;
+                    break;
+                }
+            }
+            uint32_t *dst = a.pool + (size_t)(id == kTrash16 ? trash : cbase + id) * kChunkWords + pos * k;
+            for (uint32_t q = 0; q < k; q++) dst[q] = pack6(wb32, s + 6u * q, L - 6u * q);
+        }
+        __syncwarp();   // the warp buffer and list are rewritten by the next sub-step
+    }
+    __syncthreads();
+    if (t == 0) atomicMax(&a.ctr[kIgMaxChunks], sm.nchunk);
+    if (t < (int)kMaxStageKw) {
+        const uint32_t fill = sm.cls_fill[t], lg = cls_lg(t + 1), cap = 1u << lg;
+        const uint32_t nseq = (fill + cap - 1) >> lg;
+        for (uint32_t q = 0; q < nseq && q < a.cta_chunks; q++) {
+            const uint32_t id = chunk_of[t * a.cta_chunks + q];
+            if (id < a.cta_chunks) a.chunk_fill[cbase + id] = q + 1 < nseq ? cap : fill - (q << lg);
+        }
+    }
+    for (int i = t; i < 702; i += kIgThreads)
+        if (sm.d12[i]) atomicAdd(&a.dense[i], sm.d12[i]);
+    for (int i = t; i < kCacheSlots; i += kIgThreads) {
+        const uint32_t tag = sm.ctag[i];
+        if (tag) atomicAdd(&a.dense[dense_base(tag >> 24) + (tag & 0xffffffu)], sm.ccnt[i]);
+    }
+    for (int i = t; i < kHistBins; i += kIgThreads) {   // lengths >= 6 (the dense ones come from the tables)
+        const uint32_t h = sm.hist[i];
+        if (h) atomicAdd(&a.ghist[i], h);
+    }
+}
+
+// ------------------------------------------------------------------ block scan helper (256 threads)
+__device__ __forceinline__ uint32_t excl_scan256(uint32_t v, uint32_t *wsum, uint32_t *total) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < 8 ? wsum[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < 8) wsum[lane] = wi - w;
+        if (lane == 7) wsum[8] = wi;
+    }
+    __syncthreads();
+    const uint32_t r = wsum[warp] + incl - v;
+    if (total) *total = wsum[8];
+    __syncthreads();
+    return r;
+}
+
+// ------------------------------------------------------------------ K2d: dense scan + compaction
+constexpr uint32_t kDenseBlk = 4096;   // entries per block (16 per thread)
+
+__global__ void __launch_bounds__(256) k_dense_reduce(DenseArgs a) {
+    __shared__ uint32_t wsum[9];
+    const uint32_t b = blockIdx.x, t = threadIdx.x;
+    uint32_t sum = 0, nnz = 0;
+    const uint32_t e0 = b * kDenseBlk + 16u * t;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        const uint32_t e = e0 + j;
+        const uint32_t v = e < a.n_entries ? a.dense[e] : 0u;
+        sum += v;
+        nnz += v != 0u;
+    }
+    uint32_t ts = 0, tn = 0;
+    excl_scan256(sum, wsum, &ts);
+    excl_scan256(nnz, wsum, &tn);
+    if (t == 0) {
+        a.blk_sum[b] = ts;
+        a.blk_nnz[b] = tn;
+    }
+}
+
+// words of each length L <= 5 = the sum of its dense table (the length histogram of the dense buckets)
+__global__ void __launch_bounds__(256) k_dense_lensum(const uint32_t *dense, uint32_t *ghist) {
+    __shared__ uint32_t h[kDenseMaxLen + 1];
+    const uint32_t t = threadIdx.x, e0 = blockIdx.x * kDenseBlk + 16u * t, ne = dense_base(kDenseMaxLen + 1);
+    if (t <= kDenseMaxLen) h[t] = 0;
+    __syncthreads();
+    uint32_t L = 1;
+    while (dense_base(L + 1) <= e0 && L < kDenseMaxLen) L++;
+    uint32_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        const uint32_t e = e0 + j;
+        if (e >= ne) break;
+        if (e == dense_base(L + 1)) {
+            if (sum) atomicAdd(&h[L], sum);
+            sum = 0;
+            L++;
+        }
+        sum += dense[e];
+    }
+    if (sum) atomicAdd(&h[L], sum);
+    __syncthreads();
+    if (t >= 1 && t <= kDenseMaxLen && h[t]) atomicAdd(&ghist[t], h[t]);
+}
+
+__global__ void __launch_bounds__(1024) k_dense_scan(DenseArgs a, uint32_t nblk) {
+    __shared__ uint32_t ws[33], wn[33];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    uint32_t run_s = 0, run_n = 0;
+    for (uint32_t b0 = 0; b0 < nblk; b0 += 1024) {
+        const uint32_t b = b0 + t;
+        const uint32_t vs = b < nblk ? a.blk_sum[b] : 0u, vn = b < nblk ? a.blk_nnz[b] : 0u;
+        uint32_t is = vs, in = vn;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ys = __shfl_up_sync(kFull, is, o), yn = __shfl_up_sync(kFull, in, o);
+            if (lane >= o) {
+                is += ys;
+                in += yn;
+            }
+        }
+        if (lane == 31) {
+            ws[warp] = is;
+            wn[warp] = in;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t xs = ws[lane], xn = wn[lane];
+            uint32_t ps = xs, pn = xn;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t ys = __shfl_up_sync(kFull, ps, o), yn = __shfl_up_sync(kFull, pn, o);
+                if (lane >= o) {
+                    ps += ys;
+                    pn += yn;
+                }
+            }
+            ws[lane] = ps - xs;
+            wn[lane] = pn - xn;
+            if (lane == 31) {
+                ws[32] = ps;
+                wn[32] = pn;
+            }
+        }
+        __syncthreads();
+        if (b < nblk) {
+            a.blk_sum[b] = run_s + ws[warp] + is - vs;
+            a.blk_nnz[b] = run_n + wn[warp] + in - vn;
+        }
+        run_s += ws[32];
+        run_n += wn[32];
+        __syncthreads();
+    }
+    if (t == 0) {
+        a.n_ent[0] = run_n;
+        a.n_ent[1] = run_s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_dense_compact(DenseArgs a) {
+    __shared__ uint32_t wsum[9];
+    const uint32_t b = blockIdx.x, t = threadIdx.x;
+    const uint32_t e0 = b * kDenseBlk + 16u * t;
+    uint32_t v[16], sum = 0, nnz = 0;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        const uint32_t e = e0 + j;
+        v[j] = e < a.n_entries ? a.dense[e] : 0u;
+        sum += v[j];
+        nnz += v[j] != 0u;
+    }
+    uint32_t ps = excl_scan256(sum, wsum, nullptr) + a.blk_sum[b];
+    uint32_t pn = excl_scan256(nnz, wsum, nullptr) + a.blk_nnz[b];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        if (v[j]) {
+            ps += v[j];
+            a.ent_idx[pn] = e0 + j;
+            a.ent_end[pn] = ps;   // inclusive end: global index of the entry's last word + 1
+            pn++;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K5d: emit the dense buckets
+constexpr uint32_t kDenseTile = 2048;                 // words per emit tile
+constexpr uint32_t kDenseStage = kDenseTile * 6 + 32; // <= 6 bytes per word (L <= 5)
+
+// first i in [0, n) with arr[i] > x (n if none): k-ary search, 256 probes per round
+__device__ __forceinline__ uint32_t block_first_greater(const uint32_t *arr, uint32_t n, uint32_t x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t stride = (hi - lo + 255u) / 256u;
+        const uint32_t p = lo + threadIdx.x * stride;
+        const bool le = p < hi && __ldg(arr + p) <= x;
+        const uint32_t m = (uint32_t)__syncthreads_count(le);
+        if (m == 0) return lo;
+        const uint32_t nlo = lo + (m - 1u) * stride + 1u, nhi = min(hi, lo + m * stride);
+        lo = nlo;
+        hi = nhi;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_emit_dense(DenseEmitArgs a) {
+    __shared__ __align__(16) uint8_t stage[kDenseStage];
+    __shared__ uint32_t s_end[kDenseTile], s_idx[kDenseTile];
+    const uint32_t t = threadIdx.x;
+    const TileDesc td = a.tiles[blockIdx.x];
+    const uint32_t L = td.L;
+    const BucketInfo b = a.buckets[L];
+    const uint32_t k0 = td.tile * kDenseTile;
+    const uint32_t nk = min(kDenseTile, b.n - k0);
+    const uint32_t w0 = (uint32_t)b.word_off + k0, w1 = w0 + nk;
+    const uint32_t E = a.n_ent[0];
+    const uint32_t e0 = block_first_greater(a.ent_end, E, w0);
+    const uint32_t e1 = block_first_greater(a.ent_end, E, w1 - 1u);
+    const uint32_t ne = e1 - e0 + 1u;   // <= nk: every entry holds >= 1 word
+    for (uint32_t j = t; j < ne; j += 256) {
+        s_end[j] = __ldg(a.ent_end + e0 + j);
+        s_idx[j] = __ldg(a.ent_idx + e0 + j) - dense_base(L);
+    }
+    const uint64_t ob = b.byte_off + (uint64_t)k0 * (L + 1);
+    const uint32_t head = (uint32_t)(ob & 15u);
+    __syncthreads();
+    constexpr uint32_t G = kDenseTile / 256;   // consecutive words per thread
+    const uint32_t i0 = G * t;
+    if (i0 < nk) {
+        const uint32_t wfirst = w0 + i0;
+        uint32_t lo = 0, hi = ne - 1;   // first j with s_end[j] > wfirst
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_end[mid] > wfirst) hi = mid;
+            else lo = mid + 1;
+        }
+        uint32_t j = lo, dec_j = 0xffffffffu;
+        uint8_t ch[5];
+        for (uint32_t i = i0; i < min(i0 + G, nk); i++) {
+            const uint32_t w = w0 + i;
+            while (s_end[j] <= w) j++;
+            if (j != dec_j) {
+                uint32_t x = s_idx[j];
+#pragma unroll
+                for (int q = 4; q >= 0; q--) {
+                    if ((uint32_t)q < L) {
+                        const uint32_t y = x / 26u;
+                        ch[q] = (uint8_t)('a' + (x - y * 26u));
+                        x = y;
+                    }
+                }
+                dec_j = j;
+            }
+            uint8_t *o = stage + head + i * (L + 1);
+#pragma unroll
+            for (int q = 0; q < 5; q++)
+                if ((uint32_t)q < L) o[q] = ch[q];
+            o[L] = '\n';
+        }
+    }
+    __syncthreads();
+    const uint64_t end = ob + (uint64_t)nk * (L + 1);
+    const uint64_t a0 = (ob + 15) & ~15ull, a1 = end & ~15ull;
+    if (a0 >= a1) {
+        for (uint64_t x = ob + t; x < end; x += 256) a.words[x] = stage[head + (x - ob)];
+        return;
+    }
+    for (uint64_t x = ob + t; x < a0; x += 256) a.words[x] = stage[head + (x - ob)];
+    for (uint64_t x = a1 + t; x < end; x += 256) a.words[x] = stage[head + (x - ob)];
+    const uint64_t base16 = ob & ~15ull;
+    uint4 *dst = reinterpret_cast<uint4 *>(a.words);
+    for (uint64_t x = a0 + 16ull * t; x < a1; x += 16ull * 256) dst[x >> 4] = *reinterpret_cast<const uint4 *>(stage + (x - base16));
+}
+
+// ------------------------------------------------------------------ K3c: chunks -> length buckets
+// Each staged key's length is recovered from its trailing zero 5-bit codes (letters are codes 1..26,
+// the pad is 0): L = 6K - (ctz(last key word) / 5). A chunk's keys (one key-width class K: lengths
+// 6K-5 .. 6K) are grouped by length in shared memory, one global atomic per (chunk, length) reserves
+// their range in the bucket, and they are written out coalesced. Order within a bucket is arbitrary
+// (keys only); the MSD levels sort it.
+__device__ __forceinline__ uint32_t key_len(uint32_t last, uint32_t K) {
+    return 6u * K - (uint32_t)(__ffs(last) - 1) / 5u;
+}
+
+template <int K>
+__device__ __forceinline__ void lscatter_chunk(const L0Args &a, uint32_t c, uint32_t n, uint32_t *sm) {
+    constexpr int KPT = (16 + K - 1) / K;   // 4096 / K keys per chunk, 256 threads
+    const uint32_t t = threadIdx.x;
+    uint32_t *cnt = sm, *lbase = sm + 8, *gbase = sm + 16;
+    uint64_t *koff = reinterpret_cast<uint64_t *>(sm + 24);
+    uint32_t *kout = sm + 40;
+    uint8_t *lof = reinterpret_cast<uint8_t *>(kout + kChunkWords + kChunkWords / 32 + 4);
+    if (t < 8) cnt[t] = 0;
+    if (t < 6) koff[t] = a.buckets[6 * K - 5 + t].key_off;
+    __syncthreads();
+    const uint32_t *src = a.pool + (size_t)c * kChunkWords;
+    uint32_t key[KPT][K], ll[KPT], slot[KPT];
+#pragma unroll
+    for (int r = 0; r < KPT; r++) {
+        const uint32_t i = t + r * 256;
+#pragma unroll
+        for (int u = 0; u < K; u++) key[r][u] = i < n ? __ldg(src + i * K + u) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < KPT; r++) {
+        const uint32_t i = t + r * 256;
+        if (i < n) {
+            ll[r] = key_len(key[r][K - 1], K) - (6u * K - 5u);
+            slot[r] = atomicAdd(&cnt[ll[r]], 1u);
+        }
+    }
+    __syncthreads();
+    if (t < 6) {
+        uint32_t ex = 0;
+        for (uint32_t j = 0; j < t; j++) ex += cnt[j];
+        lbase[t] = ex;
+        gbase[t] = cnt[t] ? atomicAdd(&a.lcursor[6 * K - 5 + t], cnt[t]) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < KPT; r++) {
+        const uint32_t i = t + r * 256;
+        if (i < n) {
+            const uint32_t p = lbase[ll[r]] + slot[r];
+#pragma unroll
+            for (int u = 0; u < K; u++) {
+                const uint32_t w = p * K + u;
+                kout[w + (w >> 5)] = key[r][u];
+            }
+            lof[p] = (uint8_t)ll[r];
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = t; i < n * K; i += 256) {
+        const uint32_t p = i / K, u = i - p * K;
+        const uint32_t l = lof[p];
+        a.dst[koff[l] + (uint64_t)(gbase[l] + p - lbase[l]) * K + u] = kout[i + (i >> 5)];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_lscatter(L0Args a) {
+    extern __shared__ __align__(16) uint32_t l0_smem[];
+    const uint32_t c = (blockIdx.x / a.used_chunks) * a.cta_chunks + blockIdx.x % a.used_chunks;
+    const uint32_t n = a.chunk_fill[c];
+    if (n == 0) return;
+    switch (a.chunk_cls[c]) {
+        case 1: lscatter_chunk<1>(a, c, n, l0_smem); break;
+        case 2: lscatter_chunk<2>(a, c, n, l0_smem); break;
+        case 3: lscatter_chunk<3>(a, c, n, l0_smem); break;
+        case 4: lscatter_chunk<4>(a, c, n, l0_smem); break;
+        case 5: lscatter_chunk<5>(a, c, n, l0_smem); break;
+        case 6: lscatter_chunk<6>(a, c, n, l0_smem); break;
+        case 7: lscatter_chunk<7>(a, c, n, l0_smem); break;
+        default: lscatter_chunk<8>(a, c, n, l0_smem); break;
+    }
+}
+
+constexpr size_t kLscatterSmem = (40 + kChunkWords + kChunkWords / 32 + 4) * 4 + kChunkWords;
+
+}  // namespace
+
+size_t ingest_smem(uint32_t cta_chunks) { return sizeof(IgSmem) + kMaxStageKw * cta_chunks * 2; }
+uint32_t dense_entries() { return dense_base(kDenseMaxLen + 1); }
+uint32_t dense_table_base(uint32_t L) { return dense_base(L); }
+
+cudaError_t launch_ingest(const IngestArgs &a, cudaStream_t s) {
+    if (a.grid == 0) return cudaSuccess;
+    const size_t smem = ingest_smem(a.cta_chunks);
+    cudaError_t e = cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_ingest<<<a.grid, kIgThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_scan(const DenseArgs &a, cudaStream_t s) {
+    const uint32_t nblk = (a.n_entries + kDenseBlk - 1) / kDenseBlk;
+    k_dense_reduce<<<nblk, 256, 0, s>>>(a);
+    k_dense_scan<<<1, 1024, 0, s>>>(a, nblk);
+    k_dense_compact<<<nblk, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+uint32_t dense_scan_blocks(uint32_t n_entries) { return (n_entries + kDenseBlk - 1) / kDenseBlk; }
+cudaError_t launch_dense_lensum(const uint32_t *dense, uint32_t *ghist, cudaStream_t s) {
+    k_dense_lensum<<<dense_scan_blocks(dense_base(kDenseMaxLen + 1)), 256, 0, s>>>(dense, ghist);
+    return cudaGetLastError();
+}
+
+uint32_t dense_emit_tile_words() { return kDenseTile; }
+cudaError_t launch_emit_dense(const DenseEmitArgs &a, cudaStream_t s) {
+    if (a.ntiles == 0) return cudaSuccess;
+    k_emit_dense<<<a.ntiles, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lscatter(const L0Args &a, uint32_t nctas, cudaStream_t s) {
+    const uint32_t nchunks = nctas * a.used_chunks;
+    if (!nchunks) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_lscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLscatterSmem);
+    if (e != cudaSuccess) return e;
+    k_lscatter<<<nchunks, 256, kLscatterSmem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace wsort

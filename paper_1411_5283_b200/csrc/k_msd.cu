@@ -22,10 +22,6 @@ namespace {
 constexpr int kST = 256;
 constexpr uint32_t kFullM = 0xffffffffu;
 
-__device__ __forceinline__ uint32_t digit_at(const uint32_t *key, uint32_t q) {
-    return (key[q / 3] >> (20 - 10 * (q % 3))) & 1023u;
-}
-
 template <int KW>
 __device__ __forceinline__ uint32_t digit_reg(const uint32_t (&k)[KW], uint32_t q) {
     uint32_t w = k[0];

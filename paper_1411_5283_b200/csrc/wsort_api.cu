@@ -13,6 +13,7 @@
 #include <cerrno>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -64,6 +65,14 @@ struct wsort_ctx {
     TkArgs tk{};
     DevBuf cta_hist, cta_base, d_sum;
     Summary *h_sum = nullptr;   // pinned
+    bool cta_bases_ready = false;  // K2b ran for the current tokenize (K3 needs it)
+    bool cta_counts_ready = false; // K1b's per-CTA histograms are in cta_hist (K2b needs them)
+
+    // K1 ingest: global histogram, dense counts, staging chunks
+    DevBuf ghist, dense, pool, chunk_cls, chunk_fill, ig_ctr;
+    uint32_t *h_ig = nullptr;   // pinned mirror of ig_ctr
+    uint32_t cta_chunks = 0, n_chunks = 0;
+    DevBuf d_blk_sum, d_blk_nnz, d_ent_idx, d_ent_end, d_n_ent, d_tiles2, d_lcursor;
 
     // sort
     DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y, splits;
@@ -192,13 +201,30 @@ void drain_events(wsort_ctx *c) {
     c->pending.clear();
 }
 
+// K3 (pack + scatter) needs K2b's per-(CTA, length) bases: computed once per tokenize, on demand.
+cudaError_t pack_scatter(wsort_ctx *c) {
+    if (!c->cta_counts_ready) {
+        cudaError_t e = launch_count_lengths(c->tk, nullptr, c->stream);
+        if (e != cudaSuccess) return e;
+        c->launches++;
+        c->cta_counts_ready = true;
+    }
+    if (!c->cta_bases_ready) {
+        cudaError_t e = launch_cta_bases(c->tk, c->h_sum->max_len, c->stream);
+        if (e != cudaSuccess) return e;
+        c->launches++;
+        c->cta_bases_ready = true;
+    }
+    return launch_pack_scatter(c->tk, c->stream);
+}
+
 // Tokenizer geometry: the same CTA -> byte-range mapping for K1 and K3.
 void plan_tokenizer(wsort_ctx *c) {
     TkArgs &a = c->tk;
     a.text = c->d_text;
     a.n = c->n;
     a.nsteps = (uint32_t)((c->n + kTkStep - 1) / kTkStep);
-    uint32_t want = (uint32_t)c->sms * 4;
+    uint32_t want = (uint32_t)c->sms * 3;   // one wave of K1 ingest (3 CTAs of 512 threads per SM)
     uint32_t g = std::min<uint32_t>(a.nsteps, want);
     a.steps_per_cta = g ? (a.nsteps + g - 1) / g : 0;
     a.grid = a.steps_per_cta ? (a.nsteps + a.steps_per_cta - 1) / a.steps_per_cta : 0;
@@ -281,12 +307,15 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->tickets, &c->plan, &c->va_x, &c->va_y, &c->splits, &c->bk, &c->d_counts,
                       &c->d_cursor, &c->d_sbase, &c->d_split, &c->d_lohi, &c->d_tiles, &c->d_ranges,
                       &c->m_hist, &c->m_cursor, &c->m_ctr, &c->m_big[0], &c->m_big[1], &c->m_tiles[0],
-                      &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy};
+                      &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->ghist, &c->dense,
+                      &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
+                      &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_sum) cudaFreeHost(c->h_sum);
     if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
+    if (c->h_ig) cudaFreeHost(c->h_ig);
     for (auto &pe : c->pending) {
         cudaEventDestroy(pe.a);
         cudaEventDestroy(pe.b);
@@ -316,7 +345,7 @@ int wsort_load_text(wsort_ctx *c, const void *bytes, uint64_t n, int mem, uint64
     c->has_global = false;
     c->word_base = c->byte_base = 0;
     uint64_t nsteps = (n + kTkStep - 1) / kTkStep;
-    size_t need = kTextFrontPad + nsteps * kTkStep + kTkHalo + 64;
+    size_t need = kTextFrontPad + nsteps * kTkStep + kIgStep + kTkHalo + 64;   // ingest reads up to 16 KiB + halo past a range
     int rc = ensure(c, c->text_alloc, need, "text");
     if (rc) return rc;
     uint8_t *base = static_cast<uint8_t *>(c->text_alloc.p);
@@ -360,15 +389,61 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     cudaSetDevice(c->device);
     TkArgs &a = c->tk;
     int rc;
-    if ((rc = ensure(c, c->cta_hist, (size_t)std::max<uint32_t>(a.grid, 1) * kHistBins * 4, "cta_hist"))) return rc;
-    if ((rc = ensure(c, c->cta_base, (size_t)std::max<uint32_t>(a.grid, 1) * 256 * 4, "cta_base"))) return rc;
+    const uint32_t G = std::max<uint32_t>(a.grid, 1);
+    if ((rc = ensure(c, c->cta_hist, (size_t)G * kHistBins * 4, "cta_hist"))) return rc;
+    if ((rc = ensure(c, c->cta_base, (size_t)G * 256 * 4, "cta_base"))) return rc;
     if ((rc = ensure(c, c->d_sum, sizeof(Summary), "summary"))) return rc;
+    if ((rc = ensure(c, c->ghist, kHistBins * 4, "ghist"))) return rc;
+    if ((rc = ensure(c, c->dense, (size_t)dense_entries() * 4, "dense counts"))) return rc;
+    if ((rc = ensure(c, c->ig_ctr, kIgCtrs * 4, "ingest counters"))) return rc;
+    // staging chunks: each CTA owns a region of the pool; a staged word of kw key words has >= 6kw-4
+    // letters plus a separator, so its key bytes <= its text bytes
+    c->cta_chunks = ingest_cta_chunks((uint64_t)a.steps_per_cta * kTkStep);
+    c->n_chunks = G * c->cta_chunks;
+    if ((rc = ensure(c, c->pool, ((size_t)c->n_chunks + 1) * kChunkWords * 4, "staging pool"))) return rc;
+    if ((rc = ensure(c, c->chunk_cls, (size_t)c->n_chunks * 4, "chunk classes"))) return rc;
+    if ((rc = ensure(c, c->chunk_fill, (size_t)c->n_chunks * 4, "chunk fills"))) return rc;
+    if (!c->h_ig && cudaMallocHost(&c->h_ig, kIgCtrs * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(c, WSORT_E_NOMEM, "pinned ingest counters");
+    }
     a.cta_hist = static_cast<uint32_t *>(c->cta_hist.p);
     a.cta_base = static_cast<uint32_t *>(c->cta_base.p);
-    rc = launch(c, "k1_tokenize_count", (double)c->n, [&] { return launch_tokenize_count(a, c->stream); });
+    CK(cudaMemsetAsync(c->ghist.p, 0, kHistBins * 4, c->stream), "memset ghist");
+    CK(cudaMemsetAsync(c->dense.p, 0, (size_t)dense_entries() * 4, c->stream), "memset dense");
+    CK(cudaMemsetAsync(c->ig_ctr.p, 0, kIgCtrs * 4, c->stream), "memset ingest counters");
+    CK(cudaMemsetAsync(c->chunk_fill.p, 0, (size_t)c->n_chunks * 4, c->stream), "memset chunk fills");
+    IngestArgs ia{};
+    ia.text = a.text;
+    ia.n = a.n;
+    ia.nsteps = a.nsteps;
+    ia.steps_per_cta = a.steps_per_cta;
+    ia.grid = a.grid;
+    ia.ghist = static_cast<uint32_t *>(c->ghist.p);
+    ia.dense = static_cast<uint32_t *>(c->dense.p);
+    ia.pool = static_cast<uint32_t *>(c->pool.p);
+    ia.chunk_cls = static_cast<uint32_t *>(c->chunk_cls.p);
+    ia.chunk_fill = static_cast<uint32_t *>(c->chunk_fill.p);
+    ia.cta_chunks = c->cta_chunks;
+    ia.ctr = static_cast<uint32_t *>(c->ig_ctr.p);
+    if (const char *dbg = getenv("WSORT_INGEST_DEBUG")) ia.debug = (uint32_t)atoi(dbg);
+    rc = launch(c, "k1_ingest", (double)c->n, [&] { return launch_ingest(ia, c->stream); });
     if (rc) return rc;
-    rc = launch(c, "k2_bucket_offsets", (double)a.grid * kHistBins * 4 * 2,
-                [&] { return launch_bucket_offsets(a, static_cast<Summary *>(c->d_sum.p), c->stream); });
+    rc = launch(c, "k2_dense_lensum", (double)dense_entries() * 4,
+                [&] { return launch_dense_lensum(ia.dense, ia.ghist, c->stream); });
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->h_ig, c->ig_ctr.p, kIgCtrs * 4, cudaMemcpyDeviceToHost, c->stream), "copy ingest counters");
+    CK(cudaStreamSynchronize(c->stream), "ingest");
+    c->cta_bases_ready = c->cta_counts_ready = false;
+    if (c->h_ig[kIgVeryLong]) {   // words of 49..255 letters were not staged: histogram them the K3 way
+        CK(cudaMemsetAsync(c->ghist.p, 0, kHistBins * 4, c->stream), "memset ghist");
+        rc = launch(c, "k1b_count_lengths", (double)c->n,
+                    [&] { return launch_count_lengths(a, ia.ghist, c->stream); });
+        if (rc) return rc;
+        c->cta_counts_ready = true;
+    }
+    rc = launch(c, "k2_bucket_offsets", (double)kHistBins * 4,
+                [&] { return launch_bucket_offsets(ia.ghist, static_cast<Summary *>(c->d_sum.p), c->stream); });
     if (rc) return rc;
     CK(cudaMemcpyAsync(c->h_sum, c->d_sum.p, sizeof(Summary), cudaMemcpyDeviceToHost, c->stream), "copy summary");
     CK(cudaStreamSynchronize(c->stream), "tokenize");
@@ -377,6 +452,9 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
         c->state = ST_LOADED;
         return set_err(c, WSORT_E_WORD_TOO_LONG, "%u word(s) longer than %d letters", s.too_long, kMaxLen);
     }
+    if (c->h_ig[kIgOverflow])
+        return set_err(c, WSORT_E_CUDA, "ingest: staging %s (internal error)",
+                       c->h_ig[kIgOverflow] == 2 ? "chunk id never published" : "pool overflow");
     if (n_words) *n_words = s.n_words;
     c->state = ST_TOKENIZED;
     return WSORT_OK;
@@ -518,7 +596,7 @@ int sort_radix(wsort_ctx *c, bool want_src) {
     const double key_bytes = (double)key_words * 4;
     if (!c->packed_pending) {
         rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes + (want_src ? 4.0 * W : 0.0),
-                    [&] { return launch_pack_scatter(tk, c->stream); });
+                    [&] { return pack_scatter(c); });
         if (rc) return rc;
     }
 
@@ -694,7 +772,7 @@ int sort_oets(wsort_ctx *c, bool want_src) {
     const double key_bytes = (double)key_words * 4, elem_bytes = (double)eoff * 4;
     if (!c->packed_pending) {
         rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes + (want_src ? 4.0 * W : 0.0),
-                    [&] { return launch_pack_scatter(tk, c->stream); });
+                    [&] { return pack_scatter(c); });
         if (rc) return rc;
     }
     OetsArgs oa{};
@@ -743,34 +821,11 @@ int sort_oets(wsort_ctx *c, bool want_src) {
 // msd_radix (keys only): MSD partitioning by 2-letter digits, level by level, with device-side
 // planning (k_msd_plan queues the next level's segments and the finishing jobs); one small D2H of
 // the queue counters per level sizes the next launches.
-int sort_msd(wsort_ctx *c, bool finish_radix) {
-    const Summary &s = *c->h_sum;
-    const uint32_t lmax = s.max_len;
-    std::vector<BucketInfo> bk(256, BucketInfo{});
-    uint32_t max_tw = 32, levels = 0;
-    for (uint32_t L = 1; L <= lmax; L++) {
-        BucketInfo &b = bk[L];
-        b.key_off = s.key_off[L];
-        b.word_off = s.off[L];
-        b.byte_off = s.byte_off[L];
-        b.n = (uint32_t)(s.off[L + 1] - s.off[L]);
-        b.kw = kw_of(L);
-        b.ndig = ndig_of(L);
-        b.tile_keys = kMergeThreads * oets_elems_per_thread(b.kw);   // CTA-sort capacity
-        b.aux = kRadixThreads * (32 / b.kw);                          // scatter tile keys
-        b.elem_off = b.key_off;
-        b.estride = b.kw;
-        b.final_b = 1;
-        max_tw = std::max(max_tw, b.tile_keys * b.kw);
-        if (b.n) levels = std::max(levels, b.ndig);
-    }
-    const uint64_t W = s.n_words, key_words = s.key_off[256];
-    int rc;
-    if ((rc = ensure(c, c->keys_a, key_words * 4 + 64, "keys_a"))) return rc;
-    if ((rc = ensure(c, c->keys_b, key_words * 4 + 64, "keys_b"))) return rc;
-    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+// MSD queues (segments, scatter tiles, finishing jobs, copies) sized for W words.
+int msd_alloc(wsort_ctx *c, MsdArgs &m, uint64_t W, uint64_t key_words) {
     const uint32_t cap_big = (uint32_t)(W / 1024 + 4096), cap_tiles = (uint32_t)(W / 1024 + 2 * cap_big + 4096);
     const uint32_t cap_local = (uint32_t)(W / 256 + 65536), cap_copy = (uint32_t)(W / 1024 + key_words / 65536 + 4096);
+    int rc;
     for (int i = 0; i < 2; i++) {
         if ((rc = ensure(c, c->m_big[i], (size_t)cap_big * sizeof(MsdSeg), "msd segs"))) return rc;
         if ((rc = ensure(c, c->m_tiles[i], (size_t)cap_tiles * sizeof(MsdTile), "msd tiles"))) return rc;
@@ -783,10 +838,143 @@ int sort_msd(wsort_ctx *c, bool finish_radix) {
         cudaGetLastError();
         return set_err(c, WSORT_E_NOMEM, "pinned counters");
     }
-    // level 0: whole buckets; small buckets go straight to the finishing jobs
+    m = MsdArgs{};
+    m.ctr = static_cast<uint32_t *>(c->m_ctr.p);
+    m.q_tiny = static_cast<MsdSeg *>(c->m_tiny.p);
+    m.q_small = static_cast<MsdSeg *>(c->m_small.p);
+    m.q_copy = static_cast<CopyRange *>(c->m_copy.p);
+    m.cap_big = cap_big;
+    m.cap_tiles = cap_tiles;
+    m.cap_local = cap_local;
+    m.cap_copy = cap_copy;
+    m.keys_a = static_cast<uint32_t *>(c->keys_a.p);
+    m.keys_b = static_cast<uint32_t *>(c->keys_b.p);
+    return WSORT_OK;
+}
+
+int msd_level_buffers(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nsegs) {
+    int rc;
+    if ((rc = ensure(c, c->m_hist, (size_t)nsegs * kRadixBins * 4, "msd hist"))) return rc;
+    if ((rc = ensure(c, c->m_cursor, (size_t)nsegs * kRadixBins * 4, "msd cursor"))) return rc;
+    CK(cudaMemsetAsync(c->m_hist.p, 0, (size_t)nsegs * kRadixBins * 4, c->stream), "memset msd hist");
+    CK(cudaMemsetAsync(c->m_ctr.p, 0, 2 * 4, c->stream), "reset big/tiles counters");
+    const int cur = level & 1;
+    uint32_t *ka = static_cast<uint32_t *>(c->keys_a.p), *kb = static_cast<uint32_t *>(c->keys_b.p);
+    m.level = level;
+    m.dst_is_a = level & 1u;
+    m.segs = static_cast<const MsdSeg *>(c->m_big[cur].p);
+    m.tiles = static_cast<const MsdTile *>(c->m_tiles[cur].p);
+    m.src = (level & 1u) ? kb : ka;
+    m.dst = (level & 1u) ? ka : kb;
+    m.hist = static_cast<uint32_t *>(c->m_hist.p);
+    m.cursor = static_cast<uint32_t *>(c->m_cursor.p);
+    m.q_big = static_cast<MsdSeg *>(c->m_big[cur ^ 1].p);
+    m.q_tiles = static_cast<MsdTile *>(c->m_tiles[cur ^ 1].p);
+    return WSORT_OK;
+}
+
+// After a level's plan + scatter: read the queue counters (one stream sync) for the next level.
+int msd_read_counters(wsort_ctx *c, const MsdArgs &m, uint32_t &nsegs, uint32_t &ntiles) {
+    CK(cudaMemcpyAsync(c->h_ctr, c->m_ctr.p, kQCount * 4, cudaMemcpyDeviceToHost, c->stream), "msd counters");
+    CK(cudaStreamSynchronize(c->stream), "msd level");
+    nsegs = c->h_ctr[kQBig];
+    ntiles = c->h_ctr[kQTiles];
+    if (nsegs > m.cap_big || ntiles > m.cap_tiles || c->h_ctr[kQTiny] > m.cap_local || c->h_ctr[kQSmall] > m.cap_local ||
+        c->h_ctr[kQCopy] > m.cap_copy)
+        return set_err(c, WSORT_E_NOMEM, "msd queue overflow (segs %u tiles %u)", nsegs, ntiles);
+    return WSORT_OK;
+}
+
+// MSD levels from `level` on (its segments / tiles are in m_big[level & 1] / m_tiles[level & 1]) until no
+// segment is left, then the finishing sorts: every key ends in buffer B at its final index.
+int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nsegs, uint32_t ntiles, uint32_t levels,
+                          double key_bytes, uint32_t max_tw) {
+    int rc;
+    for (; nsegs > 0; level++) {
+        if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
+        if ((rc = msd_level_buffers(c, m, level, nsegs))) return rc;
+        const double seg_bytes = level == 0 ? key_bytes : 0;   // later levels' sizes are device-side
+        rc = launch(c, "k4m_msd_count", seg_bytes, [&] { return launch_msd_count(m, ntiles, c->stream); });
+        if (rc) return rc;
+        rc = launch(c, "k4m_msd_plan", (double)nsegs * kRadixBins * 8, [&] { return launch_msd_plan(m, nsegs, c->stream); });
+        if (rc) return rc;
+        rc = launch(c, "k4m_msd_scatter", 2 * seg_bytes, [&] { return launch_msd_scatter(m, ntiles, c->stream); });
+        if (rc) return rc;
+        if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;
+    }
+    m.n_tiny = c->h_ctr[kQTiny];
+    const uint32_t n_small = c->h_ctr[kQSmall], n_copy = c->h_ctr[kQCopy];
+    return launch(c, "k4m_msd_finish", 2 * key_bytes,
+                  [&] { return launch_msd_finish(m, n_small, n_copy, max_tw, c->stream); });
+}
+
+int emit_keys(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketInfo *d_bk, uint32_t lmin, uint32_t lmax,
+              double bytes) {
+    std::vector<TileDesc> emit_tiles;
+    for (uint32_t L = lmin; L <= lmax; L++) {
+        const uint32_t te = kEmitStage / (L + 1);
+        for (uint32_t i = 0; bk[L].n && i < (bk[L].n + te - 1) / te; i++) emit_tiles.push_back(TileDesc{L, i});
+    }
+    if (emit_tiles.empty()) return WSORT_OK;
+    int rc;
+    if ((rc = upload_small(c, c->d_tiles, emit_tiles.data(), emit_tiles.size() * sizeof(TileDesc), "emit tiles")))
+        return rc;
+    EmitArgs ea{};
+    ea.buckets = d_bk;
+    ea.tiles = static_cast<const TileDesc *>(c->d_tiles.p);
+    ea.ntiles = (uint32_t)emit_tiles.size();
+    ea.keys_a = static_cast<uint32_t *>(c->keys_a.p);
+    ea.keys_b = static_cast<uint32_t *>(c->keys_b.p);
+    ea.words = static_cast<uint8_t *>(c->words.p);
+    ea.global_base = c->global_base;
+    return launch(c, "k5_emit", bytes, [&] { return launch_emit(ea, c->stream); });
+}
+
+// Buckets of the MSD paths: kw, digits, CTA-sort capacity, scatter tile; the keys of lengths >= lkey
+// are laid out contiguously in length order from key word 0.
+std::vector<BucketInfo> msd_buckets(const Summary &s, uint32_t lkey, uint32_t &max_tw, uint32_t &levels,
+                                    uint64_t &key_words) {
+    std::vector<BucketInfo> bk(256, BucketInfo{});
+    max_tw = 32;
+    levels = 0;
+    key_words = 0;
+    for (uint32_t L = 1; L <= s.max_len; L++) {
+        BucketInfo &b = bk[L];
+        b.word_off = s.off[L];
+        b.byte_off = s.byte_off[L];
+        b.n = (uint32_t)(s.off[L + 1] - s.off[L]);
+        b.kw = kw_of(L);
+        b.ndig = ndig_of(L);
+        b.tile_keys = kMergeThreads * oets_elems_per_thread(b.kw);   // CTA-sort capacity
+        b.aux = kRadixThreads * (32 / b.kw);                          // scatter tile keys
+        b.final_b = 1;
+        if (L < lkey) continue;
+        b.key_off = key_words;
+        b.elem_off = b.key_off;
+        b.estride = b.kw;
+        key_words += (uint64_t)b.n * b.kw;
+        max_tw = std::max(max_tw, b.tile_keys * b.kw);
+        if (b.n) levels = std::max(levels, b.ndig);
+    }
+    return bk;
+}
+
+// MSD over the key buckets of lengths >= lkey (keys laid out by msd_buckets). `pack` fills buffer A with
+// every bucket's keys (K3 from the text, or K3c from the ingest's chunks). Level 0 = whole buckets;
+// buckets of at most one CTA tile go straight to the finishing jobs. Ends with the keys emitted.
+template <class Pack>
+int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint32_t max_tw, uint32_t levels,
+                  uint64_t key_words, uint64_t W, bool finish_radix, Pack pack) {
+    const Summary &s = *c->h_sum;
+    const uint32_t lmax = s.max_len;
+    int rc;
+    if ((rc = ensure(c, c->keys_a, key_words * 4 + 64, "keys_a"))) return rc;
+    if ((rc = ensure(c, c->keys_b, key_words * 4 + 64, "keys_b"))) return rc;
+    MsdArgs m;
+    if ((rc = msd_alloc(c, m, W, key_words))) return rc;
     std::vector<MsdSeg> segs, tiny, small;
     std::vector<MsdTile> tiles;
-    for (uint32_t L = 1; L <= lmax; L++) {
+    for (uint32_t L = lkey; L <= lmax; L++) {
         const BucketInfo &b = bk[L];
         if (!b.n) continue;
         if (b.n <= b.tile_keys) {
@@ -807,95 +995,102 @@ int sort_msd(wsort_ctx *c, bool finish_radix) {
     if ((rc = upload_small(c, c->m_small, small.data(), small.size() * sizeof(MsdSeg), "small0"))) return rc;
     uint32_t ctr0[kQCount] = {0, 0, (uint32_t)tiny.size(), (uint32_t)small.size(), 0, 0, 0, 0};
     if ((rc = upload_small(c, c->m_ctr, ctr0, sizeof ctr0, "counters"))) return rc;
-
-    uint32_t *ka = static_cast<uint32_t *>(c->keys_a.p), *kb = static_cast<uint32_t *>(c->keys_b.p);
+    memcpy(c->h_ctr, ctr0, sizeof ctr0);   // if no level runs, these are the finishing counters
     const double key_bytes = (double)key_words * 4;
-    if (!c->packed_pending) {
-        TkArgs &tk = c->tk;
-        tk.buckets = d_bk;
-        tk.keys = ka;
-        tk.payload = nullptr;
-        rc = launch(c, "k3_pack_scatter", (double)c->n + key_bytes, [&] { return launch_pack_scatter(tk, c->stream); });
-        if (rc) return rc;
-    }
-    MsdArgs m{};
+    if ((rc = pack(d_bk, key_bytes))) return rc;
     m.buckets = d_bk;
-    m.ctr = static_cast<uint32_t *>(c->m_ctr.p);
-    m.q_tiny = static_cast<MsdSeg *>(c->m_tiny.p);
-    m.q_small = static_cast<MsdSeg *>(c->m_small.p);
-    m.q_copy = static_cast<CopyRange *>(c->m_copy.p);
-    m.cap_big = cap_big;
-    m.cap_tiles = cap_tiles;
-    m.cap_local = cap_local;
-    m.cap_copy = cap_copy;
-    m.keys_a = ka;
-    m.keys_b = kb;
     m.finish_radix = finish_radix ? 1u : 0u;
-    uint32_t nsegs = (uint32_t)segs.size(), ntiles = (uint32_t)tiles.size();
-    std::vector<uint64_t> tile_words_level;
-    for (uint32_t level = 0; nsegs > 0; level++) {
-        if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
-        const int cur = level & 1;
-        if ((rc = ensure(c, c->m_hist, (size_t)nsegs * kRadixBins * 4, "msd hist"))) return rc;
-        if ((rc = ensure(c, c->m_cursor, (size_t)nsegs * kRadixBins * 4, "msd cursor"))) return rc;
-        CK(cudaMemsetAsync(c->m_hist.p, 0, (size_t)nsegs * kRadixBins * 4, c->stream), "memset msd hist");
-        CK(cudaMemsetAsync(c->m_ctr.p, 0, 2 * 4, c->stream), "reset big/tiles counters");
-        m.level = level;
-        m.dst_is_a = level & 1u;
-        m.segs = static_cast<const MsdSeg *>(c->m_big[cur].p);
-        m.tiles = static_cast<const MsdTile *>(c->m_tiles[cur].p);
-        m.src = (level & 1u) ? kb : ka;
-        m.dst = (level & 1u) ? ka : kb;
-        m.hist = static_cast<uint32_t *>(c->m_hist.p);
-        m.cursor = static_cast<uint32_t *>(c->m_cursor.p);
-        m.q_big = static_cast<MsdSeg *>(c->m_big[cur ^ 1].p);
-        m.q_tiles = static_cast<MsdTile *>(c->m_tiles[cur ^ 1].p);
-        // algorithmic bytes of this level: read the segments twice (count, scatter), write once
-        double seg_bytes = 0;
-        {
-            // host does not know the per-segment sizes beyond level 0; use the tile count bound
-            seg_bytes = level == 0 ? key_bytes : 0;
-        }
-        rc = launch(c, "k4m_msd_count", seg_bytes, [&] { return launch_msd_count(m, ntiles, c->stream); });
-        if (rc) return rc;
-        rc = launch(c, "k4m_msd_plan", (double)nsegs * kRadixBins * 8, [&] { return launch_msd_plan(m, nsegs, c->stream); });
-        if (rc) return rc;
-        rc = launch(c, "k4m_msd_scatter", 2 * seg_bytes, [&] { return launch_msd_scatter(m, ntiles, c->stream); });
-        if (rc) return rc;
-        CK(cudaMemcpyAsync(c->h_ctr, c->m_ctr.p, kQCount * 4, cudaMemcpyDeviceToHost, c->stream), "msd counters");
-        CK(cudaStreamSynchronize(c->stream), "msd level");
-        nsegs = c->h_ctr[kQBig];
-        ntiles = c->h_ctr[kQTiles];
-        if (nsegs > cap_big || ntiles > cap_tiles || c->h_ctr[kQTiny] > cap_local || c->h_ctr[kQSmall] > cap_local ||
-            c->h_ctr[kQCopy] > cap_copy)
-            return set_err(c, WSORT_E_NOMEM, "msd queue overflow (segs %u tiles %u)", nsegs, ntiles);
-    }
-    if (!c->h_ctr || segs.empty()) {   // no level ran: counters are the host's
-        c->h_ctr[kQTiny] = (uint32_t)tiny.size();
-        c->h_ctr[kQSmall] = (uint32_t)small.size();
-        c->h_ctr[kQCopy] = 0;
-    }
-    m.n_tiny = c->h_ctr[kQTiny];
-    const uint32_t n_small = c->h_ctr[kQSmall], n_copy = c->h_ctr[kQCopy];
-    rc = launch(c, "k4m_msd_finish", 2 * key_bytes,
-                [&] { return launch_msd_finish(m, n_small, n_copy, max_tw, c->stream); });
-    if (rc) return rc;
-    EmitArgs ea{};
-    std::vector<TileDesc> emit_tiles;
-    for (uint32_t L = 1; L <= lmax; L++) {
-        const uint32_t te = kEmitStage / (L + 1);
-        for (uint32_t i = 0; bk[L].n && i < (bk[L].n + te - 1) / te; i++) emit_tiles.push_back(TileDesc{L, i});
-    }
-    if ((rc = upload_small(c, c->d_tiles, emit_tiles.data(), emit_tiles.size() * sizeof(TileDesc), "emit tiles")))
+    if ((rc = msd_levels_and_finish(c, m, 0, (uint32_t)segs.size(), (uint32_t)tiles.size(), levels, key_bytes, max_tw)))
         return rc;
+    return emit_keys(c, bk, d_bk, lkey, lmax, key_bytes + (double)(s.byte_off[256] - s.byte_off[lkey]));
+}
+
+int sort_msd(wsort_ctx *c, bool finish_radix) {
+    const Summary &s = *c->h_sum;
+    uint32_t max_tw, levels;
+    uint64_t key_words;
+    std::vector<BucketInfo> bk = msd_buckets(s, 1, max_tw, levels, key_words);
+    int rc;
+    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    return sort_msd_core(c, bk, 1, max_tw, levels, key_words, s.n_words, finish_radix,
+                         [&](const BucketInfo *d_bk, double key_bytes) {
+                             if (c->packed_pending) return (int)WSORT_OK;
+                             TkArgs &tk = c->tk;
+                             tk.buckets = d_bk;
+                             tk.keys = static_cast<uint32_t *>(c->keys_a.p);
+                             tk.payload = nullptr;
+                             return launch(c, "k3_pack_scatter", (double)c->n + key_bytes, [&] { return pack_scatter(c); });
+                         });
+}
+
+// AUTO (keys only, every word <= 48 letters): the one-pass ingest already counted the words of L <= 5
+// (dense tables) and staged the longer ones as keys in chunks. Dense buckets: scan + compact + emit.
+// Long buckets: K3c moves the staged keys into their length buckets, then MSD_OETS sorts them.
+int sort_dense_msd(wsort_ctx *c) {
+    const Summary &s = *c->h_sum;
+    const uint32_t lmax = s.max_len;
+    uint32_t max_tw, levels;
+    uint64_t key_words;
+    std::vector<BucketInfo> bk = msd_buckets(s, kDenseMaxLen + 1, max_tw, levels, key_words);
+    const uint64_t W = s.n_words, n_dense = s.off[kDenseMaxLen + 1];
+    int rc;
+    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    if (W > n_dense) {
+        if ((rc = ensure(c, c->d_lcursor, 256 * 4, "length cursors"))) return rc;
+        CK(cudaMemsetAsync(c->d_lcursor.p, 0, 256 * 4, c->stream), "memset length cursors");
+        rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, W - n_dense, false,
+                           [&](const BucketInfo *d_bk, double key_bytes) {
+                               L0Args la{};
+                               la.buckets = d_bk;
+                               la.pool = static_cast<const uint32_t *>(c->pool.p);
+                               la.chunk_cls = static_cast<const uint32_t *>(c->chunk_cls.p);
+                               la.chunk_fill = static_cast<const uint32_t *>(c->chunk_fill.p);
+                               la.lcursor = static_cast<uint32_t *>(c->d_lcursor.p);
+                               la.dst = static_cast<uint32_t *>(c->keys_a.p);
+                               la.cta_chunks = c->cta_chunks;
+                               la.used_chunks = std::min(c->h_ig[kIgMaxChunks], c->cta_chunks);
+                               return launch(c, "k3c_chunk_scatter", 2 * key_bytes,
+                                             [&] { return launch_lscatter(la, c->tk.grid, c->stream); });
+                           });
+        if (rc) return rc;
+    } else {
+        std::vector<uint8_t> plan;
+        append(plan, bk);
+        if ((rc = upload_plan(c, plan))) return rc;
+    }
+    if (!n_dense) return WSORT_OK;
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
+    std::vector<TileDesc> dtiles;
+    const uint32_t te = dense_emit_tile_words();
+    for (uint32_t L = 1; L <= std::min<uint32_t>(lmax, kDenseMaxLen); L++)
+        for (uint32_t i = 0; bk[L].n && i < (bk[L].n + te - 1) / te; i++) dtiles.push_back(TileDesc{L, i});
+    const uint32_t ne = dense_entries(), nblk = dense_scan_blocks(ne);
+    if ((rc = ensure(c, c->d_blk_sum, (size_t)nblk * 4, "dense block sums"))) return rc;
+    if ((rc = ensure(c, c->d_blk_nnz, (size_t)nblk * 4, "dense block nnz"))) return rc;
+    if ((rc = ensure(c, c->d_ent_idx, (size_t)ne * 4, "dense entries"))) return rc;
+    if ((rc = ensure(c, c->d_ent_end, (size_t)ne * 4, "dense entry ends"))) return rc;
+    if ((rc = ensure(c, c->d_n_ent, 16, "dense entry count"))) return rc;
+    DenseArgs da{};
+    da.dense = static_cast<const uint32_t *>(c->dense.p);
+    da.n_entries = ne;
+    da.blk_sum = static_cast<uint32_t *>(c->d_blk_sum.p);
+    da.blk_nnz = static_cast<uint32_t *>(c->d_blk_nnz.p);
+    da.ent_idx = static_cast<uint32_t *>(c->d_ent_idx.p);
+    da.ent_end = static_cast<uint32_t *>(c->d_ent_end.p);
+    da.n_ent = static_cast<uint32_t *>(c->d_n_ent.p);
+    rc = launch(c, "k2d_dense_scan", 2.0 * ne * 4, [&] { return launch_dense_scan(da, c->stream); });
+    if (rc) return rc;
+    if ((rc = upload_small(c, c->d_tiles2, dtiles.data(), dtiles.size() * sizeof(TileDesc), "dense tiles"))) return rc;
+    DenseEmitArgs ea{};
     ea.buckets = d_bk;
-    ea.tiles = static_cast<const TileDesc *>(c->d_tiles.p);
-    ea.ntiles = (uint32_t)emit_tiles.size();
-    ea.keys_a = ka;
-    ea.keys_b = kb;
+    ea.tiles = static_cast<const TileDesc *>(c->d_tiles2.p);
+    ea.ntiles = (uint32_t)dtiles.size();
+    ea.ent_idx = da.ent_idx;
+    ea.ent_end = da.ent_end;
+    ea.n_ent = da.n_ent;
     ea.words = static_cast<uint8_t *>(c->words.p);
-    ea.global_base = c->global_base;
-    return launch(c, "k5_emit", key_bytes + (double)s.byte_off[256], [&] { return launch_emit(ea, c->stream); });
+    return launch(c, "k5d_emit_dense", (double)s.byte_off[kDenseMaxLen + 1],
+                  [&] { return launch_emit_dense(ea, c->stream); });
 }
 
 }  // namespace
@@ -906,7 +1101,7 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     if (!c) return WSORT_E_INVALID_ARG;
     if (c->state < ST_TOKENIZED) return set_err(c, WSORT_E_STATE, "wsort_sort before wsort_tokenize");
     if (algo != WSORT_ALGO_AUTO && algo != WSORT_ALGO_LSD_RADIX && algo != WSORT_ALGO_OETS_MERGE &&
-        algo != WSORT_ALGO_MSD_RADIX && algo != WSORT_ALGO_MSD_OETS)
+        algo != WSORT_ALGO_MSD_RADIX && algo != WSORT_ALGO_MSD_OETS && algo != WSORT_ALGO_DENSE_MSD)
         return set_err(c, WSORT_E_INVALID_ARG, "bad algo %d", algo);
     if (flags & ~WSORT_FLAG_SRC_OFF) return set_err(c, WSORT_E_INVALID_ARG, "bad flags 0x%x", flags);
     if (c->keys_external && !c->packed_pending)
@@ -916,9 +1111,15 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     cudaSetDevice(c->device);
     const bool want_src = (flags & WSORT_FLAG_SRC_OFF) != 0;
     int rc;
+    // the dense + MSD path reads what K1 ingest left (dense counts, staged keys): a text this context
+    // tokenized, keys only, every word staged (<= 48 letters)
+    const bool ingest_ok = !want_src && !c->packed_pending && !c->keys_external && c->h_ig[kIgVeryLong] == 0;
     if (algo == WSORT_ALGO_OETS_MERGE) {
         rc = sort_oets(c, want_src);
-    } else if ((algo == WSORT_ALGO_MSD_RADIX || algo == WSORT_ALGO_MSD_OETS || algo == WSORT_ALGO_AUTO) && !want_src &&
+    } else if ((algo == WSORT_ALGO_AUTO || algo == WSORT_ALGO_DENSE_MSD) && ingest_ok) {
+        rc = sort_dense_msd(c);
+    } else if ((algo == WSORT_ALGO_MSD_RADIX || algo == WSORT_ALGO_MSD_OETS || algo == WSORT_ALGO_AUTO ||
+                algo == WSORT_ALGO_DENSE_MSD) && !want_src &&
                kw_of((int)c->h_sum->max_len) <= (int)kRadixRegMaxKw) {
         rc = sort_msd(c, algo == WSORT_ALGO_MSD_RADIX);   // AUTO: odd-even transposition finish (measured faster)
     } else {
@@ -1098,7 +1299,7 @@ int wsort_pack(wsort_ctx *c) {
     tk.keys = static_cast<uint32_t *>(c->keys_a.p);
     tk.payload = nullptr;
     rc = launch(c, "k3_pack_scatter", (double)c->n + (double)s.key_off[256] * 4,
-                [&] { return launch_pack_scatter(tk, c->stream); });
+                [&] { return pack_scatter(c); });
     if (rc) return rc;
     c->packed_pending = true;
     c->state = ST_PACKED;

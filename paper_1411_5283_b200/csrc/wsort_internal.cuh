@@ -74,9 +74,73 @@ struct TkArgs {
     uint32_t *payload;             // optional u32 local source offsets (bucket order)
 };
 
-cudaError_t launch_tokenize_count(const TkArgs &a, cudaStream_t s);
-cudaError_t launch_bucket_offsets(const TkArgs &a, Summary *d_sum, cudaStream_t s);
+cudaError_t launch_bucket_offsets(const uint32_t *ghist, Summary *d_sum, cudaStream_t s);
+cudaError_t launch_count_lengths(const TkArgs &a, uint32_t *ghist, cudaStream_t s);
+cudaError_t launch_cta_bases(const TkArgs &a, uint32_t max_len, cudaStream_t s);
 cudaError_t launch_pack_scatter(const TkArgs &a, cudaStream_t s);
+
+// ---------------- K1 ingest: one text pass (k_ingest.cu) ----------------
+constexpr int kIgThreads = 512;
+constexpr int kIgStep = 16384;                       // bytes per ingest step = 32 per thread
+constexpr int kIgBuf = kTkPre + kIgStep + kTkHalo;   // 16656 bytes
+constexpr uint32_t kDenseMaxLen = 5;                 // words of L <= 5 are counted, not sorted
+constexpr uint32_t kMaxStageKw = 8;                  // words of 6 <= L <= 48 are staged as keys
+constexpr uint32_t kChunkWords = 4096;               // u32 words per staging chunk (16 KiB)
+enum { kIgMaxChunks = 0, kIgOverflow = 1, kIgVeryLong = 2, kIgCtrs = 4 };
+// chunks per CTA region: a staged word's key bytes <= its text bytes (+256 for the last word), a full
+// chunk holds >= 2560 key words (class 5: 512 keys of 5 words), one partial chunk per class
+__host__ __device__ constexpr uint32_t ingest_cta_chunks(uint64_t range_bytes) {
+    return (uint32_t)((range_bytes + 256) / 10000 + 2 * kMaxStageKw + 10);
+}
+struct IngestArgs {
+    const uint8_t *text;
+    uint64_t n;
+    uint32_t nsteps, steps_per_cta, grid;   // the K3 geometry (8 KiB steps): same CTA byte ranges
+    uint32_t *ghist;                        // [257] histogram of lengths >= 6 and of > 255 (zeroed by the host)
+    uint32_t *dense;                        // [dense_entries()] counts (zeroed by the host)
+    uint32_t *pool;                         // [grid * cta_chunks + 1][kChunkWords]; the last is a trash chunk
+    uint32_t *chunk_cls, *chunk_fill;       // [grid * cta_chunks] key width (1..8) and keys of each chunk
+                                            // (fills zeroed by the host: unused chunks stay empty)
+    uint32_t cta_chunks;                    // chunks of one CTA's region
+    uint32_t *ctr;                          // [kIgCtrs] (zeroed by the host)
+    uint32_t debug;                         // timing experiments only (WSORT_INGEST_DEBUG): 1 = skip dense
+                                            // counting, 2 = skip key packing, 4 = direct L3-5 counts
+};
+size_t ingest_smem(uint32_t cta_chunks);
+uint32_t dense_entries();
+uint32_t dense_table_base(uint32_t L);
+cudaError_t launch_ingest(const IngestArgs &a, cudaStream_t s);
+
+struct DenseArgs {
+    const uint32_t *dense;
+    uint32_t n_entries;
+    uint32_t *blk_sum, *blk_nnz;            // [dense_scan_blocks()]
+    uint32_t *ent_idx, *ent_end;            // compacted non-zero entries: table index, inclusive word end
+    uint32_t *n_ent;                        // [2]: entries, words
+};
+uint32_t dense_scan_blocks(uint32_t n_entries);
+cudaError_t launch_dense_lensum(const uint32_t *dense, uint32_t *ghist, cudaStream_t s);   // ghist[1..5] += table sums
+cudaError_t launch_dense_scan(const DenseArgs &a, cudaStream_t s);
+
+struct DenseEmitArgs {
+    const BucketInfo *buckets;
+    const TileDesc *tiles;
+    uint32_t ntiles;
+    const uint32_t *ent_idx, *ent_end, *n_ent;
+    uint8_t *words;
+};
+uint32_t dense_emit_tile_words();
+cudaError_t launch_emit_dense(const DenseEmitArgs &a, cudaStream_t s);
+
+struct L0Args {
+    const BucketInfo *buckets;
+    const uint32_t *pool, *chunk_cls, *chunk_fill;
+    uint32_t *lcursor;                      // [256] keys placed per bucket so far (zeroed by the host)
+    uint32_t *dst;                          // buffer A
+    uint32_t cta_chunks;                    // chunks per CTA region of the pool
+    uint32_t used_chunks;                   // max chunks any CTA used (its first ids)
+};
+cudaError_t launch_lscatter(const L0Args &a, uint32_t nctas, cudaStream_t s);
 
 struct RadixArgs {
     const BucketInfo *buckets;

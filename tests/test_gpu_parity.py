@@ -20,7 +20,9 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["lsd_radix", "oets_merge", "msd_radix", "msd_oets"]
+ALGOS = ["lsd_radix", "oets_merge", "msd_radix", "msd_oets", "dense_msd"]
+# keys-only algorithms: without src_off (with it they fall back to the stable LSD path)
+KEYS_ONLY = {"msd_radix", "msd_oets", "dense_msd"}
 
 
 @pytest.fixture(scope="module")
@@ -48,13 +50,16 @@ def gpu_sort(ws, text, algo="lsd_radix", src=True):
 
 def check(ws, text, algo="lsd_radix"):
     ref = oracle.sort(text, oracle.MERGE, want_src=True)
-    words, off, src = gpu_sort(ws, text, algo)
+    keys_only = algo in KEYS_ONLY
+    words, off, src = gpu_sort(ws, text, algo, src=not keys_only)
     assert off == ref.off
     if words != ref.words:
         a, b = words.split(b"\n"), ref.words.split(b"\n")
-        i = next(i for i in range(min(len(a), len(b))) if a[i] != b[i])
-        pytest.fail(f"first differing word #{i}: gpu={a[i][:80]!r} oracle={b[i][:80]!r}")
-    assert np.array_equal(src, ref.src_off)
+        i = next((i for i in range(min(len(a), len(b))) if a[i] != b[i]), min(len(a), len(b)))
+        pytest.fail(f"first differing word #{i} of {len(b)}: gpu={a[i][:80] if i < len(a) else None!r} "
+                    f"oracle={b[i][:80] if i < len(b) else None!r}")
+    if not keys_only:
+        assert np.array_equal(src, ref.src_off)
     return ref
 
 
@@ -66,10 +71,11 @@ GOLD = [g for g in GOLD if "text_latin1" in g]
 @pytest.mark.parametrize("fx", GOLD, ids=[g["name"] for g in GOLD])
 def test_golden(ws, fx, algo):
     text = fx["text_latin1"].encode("latin-1")
-    words, off, src = gpu_sort(ws, text, algo)
+    words, off, src = gpu_sort(ws, text, algo, src=algo not in KEYS_ONLY)
     assert words == b"".join(w.encode() + b"\n" for w in fx["words"])
     assert off == fx["off"]
-    assert src.tolist() == fx["src_off"]
+    if algo not in KEYS_ONLY:
+        assert src.tolist() == fx["src_off"]
 
 
 def _edge_cases():
@@ -93,6 +99,19 @@ def _edge_cases():
         "mixed_case_dups": b"Apple APPLE apple aPPle " * 5000,
         "reverse_sorted_distinct": b" ".join(
             bytes([97 + (i // 676) % 26, 97 + (i // 26) % 26, 97 + i % 26]) for i in reversed(range(17576))),
+        # dense tables (L <= 5): every L=1/L=2 entry, first/last entries, cache overflow (many distinct
+        # L=5 words go to the global fallback), hot words hit in every CTA
+        "dense_all_l1_l2": b" ".join([bytes([97 + i]) for i in range(26)] +
+                                     [bytes([97 + i // 26, 97 + i % 26]) for i in range(676)]) * 3,
+        "dense_extremes": b"a aa aaa aaaa aaaaa z zz zzz zzzz zzzzz ZZZZZ Aaaaa " * 777,
+        "dense_l5_distinct": b" ".join(bytes([97 + (i * 7919 // 26 ** j) % 26 for j in range(5)])
+                                       for i in range(120_000)),
+        "dense_hot_l4_l5": b"that with those their there " * 60_000,
+        # staged classes: L = 6 (class 1), 7..12 (2), ..., 43..48 (class 8), enough to fill many chunks
+        "staged_l6_many": b" ".join(bytes([97 + (i * 31 // 26 ** j) % 26 for j in range(6)]) for i in range(150_000)),
+        "staged_classes_6_48": b" ".join(bytes([97 + (i * j + j * j) % 26 for j in range(6 + i % 43)])
+                                         for i in range(40_000)),
+        "staged_l48_dups": (b"q" * 47 + b"r ") * 5000 + (b"q" * 48 + b" ") * 3000,
     }
     # a word crossing every 8 KiB boundary of a multi-step text (CTA chunk boundaries too)
     t = bytearray(b"." * (S * 40))
@@ -167,6 +186,19 @@ def test_auto_equals_radix(ws):
     text, _ = gen.generate(1)
     assert gpu_sort(ws, text, "auto")[0] == gpu_sort(ws, text, "lsd_radix")[0]
     assert gpu_sort(ws, text, "auto", src=False)[0] == gpu_sort(ws, text, "msd_radix", src=False)[0]
+    assert gpu_sort(ws, text, "auto", src=False)[0] == gpu_sort(ws, text, "dense_msd", src=False)[0]
+
+
+def test_dense_msd_repeat_sorts(ws):
+    """One tokenize, several sorts: the dense tables and staged keys are read-only inputs of the sort."""
+    text, _ = gen.generate(2)
+    ref = oracle.sort(text, oracle.MERGE)
+    ws.load_text(text)
+    ws.tokenize()
+    for algo in ("dense_msd", "lsd_radix", "dense_msd", "msd_oets", "auto"):
+        ws.sort(algo)
+        w, off = ws.fetch()
+        assert w.tobytes() == ref.words and off == ref.off, algo
 
 
 @pytest.mark.parametrize("algo", ALGOS)
