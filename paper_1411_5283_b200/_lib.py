@@ -5,7 +5,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwsort.so")
+LIB_PATH = os.environ.get("WSORT_LIB", os.path.join(_HERE, "libwsort.so"))   # override: experiments only
 
 OK = 0
 E_INVALID_ARG = -1

@@ -35,6 +35,10 @@ __host__ __device__ constexpr uint32_t dense_base(uint32_t L) {
     return L <= 1 ? 0u : L == 2 ? 26u : L == 3 ? 702u : L == 4 ? 18278u : L == 5 ? 475254u : 12356630u;
 }
 
+#ifndef WSORT_IG_MINB
+#define WSORT_IG_MINB 2
+#endif
+constexpr int kIgMinBlocks = WSORT_IG_MINB;
 constexpr int kSub = 1024;                   // bytes per warp sub-step (32 per lane)
 constexpr int kSubTail = 128;                // staged bytes past it (a staged word: <= 48 letters + slack)
 constexpr int kWBuf = kSub + kSubTail;
@@ -111,7 +115,7 @@ __device__ __forceinline__ uint32_t lead_run(uint32_t M) { return M == 0xfffffff
 // listed by category (warp scan) and then taken round-robin by the lanes: hash-cache count / key
 // packing into the class's chunk. Chunk (class, seq) is allocated by the lane that receives its
 // first rank; the others read its id from shared memory (written once).
-__global__ void __launch_bounds__(kIgThreads, 3) k_ingest(IngestArgs a) {
+__global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs a) {
     extern __shared__ __align__(16) uint8_t ig_smem[];
     IgSmem &sm = *reinterpret_cast<IgSmem *>(ig_smem);
     uint16_t *chunk_of = reinterpret_cast<uint16_t *>(ig_smem + sizeof(IgSmem));
@@ -221,6 +225,7 @@ __global__ void __launch_bounds__(kIgThreads, 3) k_ingest(IngestArgs a) {
         const uint32_t ci = inclusive_scan_warp(cnt, lane);
         const uint32_t tot = __shfl_sync(kFull, ci, 31);
         uint32_t p3 = (ci - cnt) & 0xffffu, plg = (ci - cnt) >> 16;
+        uint32_t *d12 = sm.d12;
         for (uint32_t m = starts; m; m &= m - 1) {
             const uint32_t bit = __ffs(m) - 1;
             const uint32_t em = ends & (0xffffffffu << bit);
@@ -228,12 +233,13 @@ __global__ void __launch_bounds__(kIgThreads, 3) k_ingest(IngestArgs a) {
             const uint32_t s = seg0 + bit;
             if (L <= 2u) {   // L = 1, 2: count now (shared-memory table)
                 const uint32_t lo = __funnelshift_r(wb32[s >> 2], wb32[(s >> 2) + 1], 8u * (s & 3u));
-                const uint32_t idx = L == 1u ? (lo & 31u) - 1u : 26u + ((lo & 31u) - 1u) * 26u + ((lo >> 8) & 31u) - 1u;
-                if (!(a.debug & 1)) atomicAdd(&sm.d12[idx], 1u);
-            } else if (L <= kDenseMaxLen) {
-                wlst[p3++] = (uint16_t)(s | ((L - 3u) << 10));
-            } else {   // L >= 6; lengths above 48 are kept as 49 (not staged) and counted too long if > 255
-                wlst[kWList - 1 - plg++] = (uint16_t)(s | ((min(L, 49u) - 6u) << 10));
+                const uint32_t c0 = (lo & 31u) - 1u, c1 = ((lo >> 8) & 31u) - 1u;
+                if (!(a.debug & 1)) atomicAdd(&d12[L == 1u ? c0 : 26u + c0 * 26u + c1], 1u);
+            } else {   // listed: L = 3..5 from the front, L >= 6 from the back (above 48 kept as 49: not staged)
+                const bool d = L <= kDenseMaxLen;
+                wlst[d ? p3 : kWList - 1 - plg] = (uint16_t)(s | ((d ? L - 3u : min(L, 49u) - 6u) << 10));
+                p3 += d;
+                plg += !d;
                 if (L > (uint32_t)kMaxLen) atomicAdd(&sm.hist[256], 1u);
             }
         }
@@ -589,11 +595,12 @@ __device__ __forceinline__ void lscatter_chunk(const L0Args &a, uint32_t c, uint
         }
     }
     __syncthreads();
-    if (t < 6) {
+    uint32_t g = 0;
+    if (t < 6) {   // reserve this chunk's range of each length; the result is consumed after the reorder
         uint32_t ex = 0;
         for (uint32_t j = 0; j < t; j++) ex += cnt[j];
         lbase[t] = ex;
-        gbase[t] = cnt[t] ? atomicAdd(&a.lcursor[6 * K - 5 + t], cnt[t]) : 0u;
+        g = cnt[t] ? atomicAdd(&a.lcursor[6 * K - 5 + t], cnt[t]) : 0u;
     }
     __syncthreads();
 #pragma unroll
@@ -609,6 +616,7 @@ __device__ __forceinline__ void lscatter_chunk(const L0Args &a, uint32_t c, uint
             lof[p] = (uint8_t)ll[r];
         }
     }
+    if (t < 6) gbase[t] = g;
     __syncthreads();
     for (uint32_t i = t; i < n * K; i += 256) {
         const uint32_t p = i / K, u = i - p * K;
@@ -638,6 +646,7 @@ constexpr size_t kLscatterSmem = (40 + kChunkWords + kChunkWords / 32 + 4) * 4 +
 
 }  // namespace
 
+uint32_t ingest_ctas_per_sm() { return kIgMinBlocks; }
 size_t ingest_smem(uint32_t cta_chunks) { return sizeof(IgSmem) + kMaxStageKw * cta_chunks * 2; }
 uint32_t dense_entries() { return dense_base(kDenseMaxLen + 1); }
 uint32_t dense_table_base(uint32_t L) { return dense_base(L); }

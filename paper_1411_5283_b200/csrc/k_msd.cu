@@ -14,6 +14,8 @@
 //                  memory and written out coalesced
 // then k_msd_warp_sort / k_msd_cta_sort finish the tiny / small children and k_msd_copy moves
 // finished runs that ended in buffer A into buffer B. Every key ends in buffer B at its final index.
+#include <type_traits>
+
 #include "wsort_internal.cuh"
 
 namespace wsort {
@@ -243,11 +245,15 @@ __device__ __forceinline__ void scatter_tile(const MsdArgs &a, const MsdTile &td
     for (int e = 0; e < 4; e++) c[e] = hist[4 * t + e];
     uint32_t ex = block_excl_scan_m(c[0] + c[1] + c[2] + c[3], wsum, nullptr);
     const uint32_t *cur = a.cursor + (size_t)td.seg * kRadixBins;
+    // reserve the tile's range of every digit (global atomics), but consume the results only after the
+    // shared-memory reorder below: their latency overlaps it
+    uint32_t g[4], ex4[4];
 #pragma unroll
     for (int e = 0; e < 4; e++) {
         const uint32_t d = 4 * t + e;
         toff[d] = ex;
-        gbase[d] = c[e] ? atomicAdd(const_cast<uint32_t *>(cur + d), c[e]) - ex : 0u;
+        ex4[e] = ex;
+        g[e] = c[e] ? atomicAdd(const_cast<uint32_t *>(cur + d), c[e]) : 0u;
         ex += c[e];
     }
     __syncthreads();
@@ -260,6 +266,8 @@ __device__ __forceinline__ void scatter_tile(const MsdArgs &a, const MsdTile &td
             for (int u = 0; u < KW; u++) kout[p * KW + u + ((p * KW + u) >> 5)] = key[r][u];
         }
     }
+#pragma unroll
+    for (int e = 0; e < 4; e++) gbase[4 * t + e] = g[e] - ex4[e];
     __syncthreads();
     uint32_t *dst = a.dst + b.key_off;
     for (uint32_t i = t; i < td.n * KW; i += kST) {
@@ -399,7 +407,7 @@ __device__ __forceinline__ void kst(uint32_t *p, const Key<KW> &x) {
 // shared memory up to the whole tile. Keys stay in registers until the shared-memory merges.
 template <int KW>
 __device__ __forceinline__ void cta_sort_job(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint32_t *sm) {
-    constexpr int E = KW <= 4 ? 8 : 4;
+    constexpr int E = KW <= 4 ? kFinE : 4;
     constexpr uint32_t TN = kST * E;
     const int t = threadIdx.x, lane = t & 31;
     const uint32_t n = sg.n;
@@ -599,6 +607,234 @@ __global__ void __launch_bounds__(kST) k_msd_cta_sort(MsdArgs a) {
     }
 }
 
+// Keys of 1 or 2 words as one native integer (u32 / u64: word 0 is the most significant), so one
+// compare decides the order. One CTA per small job (<= 2048 keys): each thread sorts its 8 keys in
+// registers by odd-even transposition (the data-parallel bubble sort of PAPER.md:23), then merge-path
+// passes in shared memory merge the runs 8 -> 16 -> ... up to the job (the paper's merge).
+template <typename T, int KW>
+__device__ __forceinline__ T fin_load(const uint32_t *p) {
+    if constexpr (KW == 1) return p[0];
+    else return ((uint64_t)p[0] << 32) | p[1];
+}
+template <typename T, int KW>
+__device__ __forceinline__ void fin_store(uint32_t *p, T v) {
+    if constexpr (KW == 1) {
+        p[0] = (uint32_t)v;
+    } else {
+        p[0] = (uint32_t)(v >> 32);
+        p[1] = (uint32_t)v;
+    }
+}
+__device__ __forceinline__ uint32_t fpad(uint32_t i) { return i + (i >> 4); }   // bank spreading
+
+// Sort n <= 2048 keys of type T held in shared memory A (padded layout), using B as scratch: each
+// thread sorts its 8 keys in registers by odd-even transposition (the data-parallel bubble sort of
+// PAPER.md:23), then merge-path passes merge the runs 8 -> 16 -> ... up to n (the paper's merge,
+// PAPER.md:76). Returns the buffer holding the sorted keys. All threads of the CTA must call it.
+template <typename T>
+__device__ __forceinline__ T *block_sort_smem(T *A, T *B, uint32_t n) {
+    constexpr int E = 8;
+    const T kMax = ~(T)0;   // above every key (key words are < 2^30)
+    const uint32_t t = threadIdx.x;
+    T v[E];
+    __syncthreads();   // A was filled by other threads
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t idx = t * E + e;
+        v[e] = idx < n ? A[fpad(idx)] : kMax;
+    }
+#pragma unroll
+    for (int ph = 0; ph < E; ph++)
+#pragma unroll
+        for (int i = ph & 1; i + 1 < E; i += 2) {
+            const T x = v[i], y = v[i + 1];
+            v[i] = x < y ? x : y;
+            v[i + 1] = x < y ? y : x;
+        }
+    __syncthreads();   // (A is read above and rewritten below)
+#pragma unroll
+    for (int e = 0; e < E; e++) A[fpad(t * E + e)] = v[e];
+    __syncthreads();
+    uint32_t span = E;
+    while (span < n) span *= 2;   // merge only as far as the keys reach
+    for (uint32_t run = E; run < span; run *= 2) {
+        const uint32_t o = t * E;
+        if (o < span) {
+            const uint32_t ra = (o / (2 * run)) * 2 * run, rb = ra + run, d = o - ra;
+            uint32_t lo = d > run ? d - run : 0u, hi = d < run ? d : run;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (A[fpad(ra + mid)] <= A[fpad(rb + d - 1 - mid)]) lo = mid + 1;
+                else hi = mid;
+            }
+            uint32_t i = lo, j = d - lo;
+            T x = i < run ? A[fpad(ra + i)] : kMax, y = j < run ? A[fpad(rb + j)] : kMax;
+#pragma unroll
+            for (int k = 0; k < E; k++) {
+                const bool tx = j >= run || (i < run && x <= y);
+                B[fpad(o + k)] = tx ? x : y;
+                if (tx) {
+                    i++;
+                    x = i < run ? A[fpad(ra + i)] : kMax;
+                } else {
+                    j++;
+                    y = j < run ? A[fpad(rb + j)] : kMax;
+                }
+            }
+        }
+        __syncthreads();
+        T *sw = A;
+        A = B;
+        B = sw;
+    }
+    return A;
+}
+
+// Finishing job (a multiset of text words: equal keys are identical words, and the job's keys share
+// their leading digits). The keys are staged in shared memory and counted in a hash table whose
+// slots hold the index of a representative key (exact: keys are compared in full). If the job has
+// at most kFinRank distinct keys, each distinct key's rank is the number of distinct keys below it
+// and every key is written as many times as it occurs (the sorted multiset; ties are unobservable,
+// reading A6). Otherwise the job is sorted in full: odd-even transposition in registers + merge paths.
+constexpr uint32_t kFinSlots = 2048, kFinRank = 256;
+constexpr uint32_t kFinEmpty = 0xffffffffu;
+
+template <int KW>
+__device__ __forceinline__ bool kw_eq(const uint32_t *K, uint32_t i, uint32_t j) {
+    bool eq = true;
+#pragma unroll
+    for (int u = 0; u < KW; u++) eq &= K[i * KW + u] == K[j * KW + u];
+    return eq;
+}
+template <int KW>
+__device__ __forceinline__ bool kw_lt(const uint32_t *K, uint32_t i, uint32_t j) {   // key i < key j
+#pragma unroll
+    for (int u = 0; u < KW; u++) {
+        const uint32_t x = K[i * KW + u], y = K[j * KW + u];
+        if (x != y) return x < y;
+    }
+    return false;
+}
+template <int KW>
+__device__ __forceinline__ uint32_t kw_hash(const uint32_t *K, uint32_t i) {
+    uint32_t h = 0x811c9dc5u;
+#pragma unroll
+    for (int u = 0; u < KW; u++) h = (h ^ K[i * KW + u]) * 0x9E3779B1u;
+    return (h >> 16) & (kFinSlots - 1);
+}
+
+template <int KW>
+__device__ __forceinline__ void fin_job(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw) {
+    const uint32_t t = threadIdx.x, n = sg.n;
+    uint32_t *K = reinterpret_cast<uint32_t *>(smraw);             // [n * KW] the job's keys
+    uint32_t *slot = K + kST * 8 * 4;                               // [kFinSlots] representative key
+    uint32_t *cnt = slot + kFinSlots;                               // [kFinSlots]
+    uint32_t *D = cnt + kFinSlots;                                  // [kFinRank] distinct keys (rep)
+    uint32_t *R = D + kFinRank;                                     // [kFinRank] sorted distinct keys
+    uint32_t *pos = R + kFinRank;                                   // [kFinRank] run ends
+    uint32_t *wsum = pos + kFinRank;                                // [9 + 1]
+    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
+    for (uint32_t i = t; i < n * KW; i += kST) K[i] = __ldg(src + i);
+    for (uint32_t i = t; i < kFinSlots; i += kST) {
+        slot[i] = kFinEmpty;
+        cnt[i] = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = t; i < n; i += kST) {
+        uint32_t h = kw_hash<KW>(K, i);
+        for (;;) {
+            uint32_t r = slot[h];
+            if (r == kFinEmpty) {
+                r = atomicCAS(&slot[h], kFinEmpty, i);
+                if (r == kFinEmpty) r = i;
+            }
+            if (r == i || kw_eq<KW>(K, r, i)) {
+                atomicAdd(&cnt[h], 1u);
+                break;
+            }
+            h = (h + 1) & (kFinSlots - 1);
+        }
+    }
+    __syncthreads();
+    uint32_t occ = 0;
+#pragma unroll
+    for (int e = 0; e < (int)(kFinSlots / kST); e++) occ += cnt[(kFinSlots / kST) * t + e] != 0;
+    uint32_t nd = 0;
+    uint32_t p = block_excl_scan_m(occ, wsum, &nd);
+    if (t == 0) atomicAdd(a.ctr + 7, nd);   // (statistics: distinct keys over all finishing jobs)
+    if (nd > kFinRank) {   // many distinct keys: sort the job in full
+        __syncthreads();
+        if constexpr (KW <= 2) {
+            using T = typename std::conditional<KW == 1, uint32_t, uint64_t>::type;
+            T *A = reinterpret_cast<T *>(smraw), *B = A + fpad(kST * 8);
+            for (uint32_t i = t; i < kST * 8; i += kST) A[fpad(i)] = i < n ? fin_load<T, KW>(src + (size_t)i * KW) : ~(T)0;
+            T *S = block_sort_smem<T>(A, B, n);
+            uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
+            for (uint32_t i = t; i < n; i += kST) fin_store<T, KW>(dst + (size_t)i * KW, S[fpad(i)]);
+        } else {
+            cta_sort_job<KW>(a, sg, b, reinterpret_cast<uint32_t *>(smraw));
+        }
+        return;
+    }
+#pragma unroll
+    for (int e = 0; e < (int)(kFinSlots / kST); e++) {
+        const uint32_t h = (kFinSlots / kST) * t + e;
+        if (cnt[h]) {
+            D[p] = slot[h];
+            pos[p] = cnt[h];   // (count, for now)
+            p++;
+        }
+    }
+    __syncthreads();
+    if (t < nd) {   // rank among the distinct keys
+        const uint32_t me = D[t];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < nd; j++) rank += kw_lt<KW>(K, D[j], me);
+        R[rank] = t;
+    }
+    __syncthreads();
+    uint32_t c = t < nd ? pos[R[t]] : 0u;   // runs in sorted order -> their ends
+    uint32_t end = block_excl_scan_m(c, wsum, nullptr) + c;
+    const uint32_t rep = t < nd ? D[R[t]] : 0u;
+    __syncthreads();
+    if (t < nd) {
+        pos[t] = end;
+        D[t] = rep;   // D now: representative of the t-th smallest distinct key
+    }
+    __syncthreads();
+    uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
+    for (uint32_t j = t; j < n * KW; j += kST) {   // output word j: key j / KW of the sorted multiset
+        const uint32_t k = j / KW;
+        uint32_t lo = 0, hi = nd - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pos[mid] > k) hi = mid;
+            else lo = mid + 1;
+        }
+        dst[j] = K[D[lo] * KW + (j - k * KW)];
+    }
+}
+
+__global__ void __launch_bounds__(kST) k_msd_fin(MsdArgs a) {
+    extern __shared__ __align__(16) uint8_t fsm[];
+    const MsdSeg sg = a.q_small[blockIdx.x];
+    const BucketInfo b = a.buckets[sg.L];
+    switch (b.kw) {
+        case 1: fin_job<1>(a, sg, b, fsm); break;
+        case 2: fin_job<2>(a, sg, b, fsm); break;
+        case 3: fin_job<3>(a, sg, b, fsm); break;
+        case 4: fin_job<4>(a, sg, b, fsm); break;
+        case 5: fin_job<5>(a, sg, b, fsm); break;
+        case 6: fin_job<6>(a, sg, b, fsm); break;
+        case 7: fin_job<7>(a, sg, b, fsm); break;
+        default: fin_job<8>(a, sg, b, fsm); break;
+    }
+}
+// the fallbacks reuse the whole buffer: cta_sort_job needs two padded tiles of <= 8192 words
+constexpr size_t kFinSmem = (2 * (8192 + 8192 / 32 + 1)) * 4 > (kST * 8 * 4 + 2 * kFinSlots + 3 * kFinRank + 10) * 4
+                                ? (2 * (8192 + 8192 / 32 + 1)) * 4
+                                : (kST * 8 * 4 + 2 * kFinSlots + 3 * kFinRank + 10) * 4;
+
 __global__ void __launch_bounds__(kST) k_msd_copy(MsdArgs a) {
     const CopyRange r = a.q_copy[blockIdx.x];
     for (uint32_t i = threadIdx.x; i < r.len; i += kST) a.keys_b[r.to + i] = __ldg(a.keys_a + r.from + i);
@@ -640,7 +876,13 @@ cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_cop
         k_msd_radix_job<<<n_small, kST, smem, s>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    if (n_small) {
+    if (n_small && !a.finish_radix) {
+        e = cudaFuncSetAttribute(k_msd_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinSmem);
+        if (e != cudaSuccess) return e;
+        k_msd_fin<<<n_small, kST, kFinSmem, s>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (n_small && a.finish_radix) {
         const size_t smem = ((size_t)max_tile_words + max_tile_words / 32 + 1) * 2 * 4;
         e = cudaFuncSetAttribute(k_msd_cta_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

@@ -224,7 +224,7 @@ void plan_tokenizer(wsort_ctx *c) {
     a.text = c->d_text;
     a.n = c->n;
     a.nsteps = (uint32_t)((c->n + kTkStep - 1) / kTkStep);
-    uint32_t want = (uint32_t)c->sms * 3;   // one wave of K1 ingest (3 CTAs of 512 threads per SM)
+    uint32_t want = (uint32_t)c->sms * ingest_ctas_per_sm();   // one wave of K1 ingest
     uint32_t g = std::min<uint32_t>(a.nsteps, want);
     a.steps_per_cta = g ? (a.nsteps + g - 1) / g : 0;
     a.grid = a.steps_per_cta ? (a.nsteps + a.steps_per_cta - 1) / a.steps_per_cta : 0;
@@ -448,6 +448,17 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     CK(cudaMemcpyAsync(c->h_sum, c->d_sum.p, sizeof(Summary), cudaMemcpyDeviceToHost, c->stream), "copy summary");
     CK(cudaStreamSynchronize(c->stream), "tokenize");
     const Summary &s = *c->h_sum;
+    if (c->prof && !c->h_ig[kIgVeryLong]) {   // K1's algorithmic bytes: the text + the staged keys it wrote
+        double staged = 0;
+        for (uint32_t L = kDenseMaxLen + 1; L <= s.max_len && L <= 6 * kMaxStageKw; L++)
+            staged += 4.0 * kw_of((int)L) * (double)(s.off[L + 1] - s.off[L]);
+        const int k1 = class_id(c, "k1_ingest");
+        for (auto it = c->pending.rbegin(); it != c->pending.rend(); ++it)
+            if (it->cls == k1) {
+                it->bytes += staged;
+                break;
+            }
+    }
     if (s.too_long) {
         c->state = ST_LOADED;
         return set_err(c, WSORT_E_WORD_TOO_LONG, "%u word(s) longer than %d letters", s.too_long, kMaxLen);
@@ -901,11 +912,39 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         rc = launch(c, "k4m_msd_scatter", 2 * seg_bytes, [&] { return launch_msd_scatter(m, ntiles, c->stream); });
         if (rc) return rc;
         if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;
+        if (getenv("WSORT_DEBUG_MSD"))
+            fprintf(stderr, "msd level %u -> next segs %u tiles %u | tiny %u small %u copy %u\n", level, nsegs, ntiles,
+                    c->h_ctr[kQTiny], c->h_ctr[kQSmall], c->h_ctr[kQCopy]);
     }
     m.n_tiny = c->h_ctr[kQTiny];
     const uint32_t n_small = c->h_ctr[kQSmall], n_copy = c->h_ctr[kQCopy];
-    return launch(c, "k4m_msd_finish", 2 * key_bytes,
-                  [&] { return launch_msd_finish(m, n_small, n_copy, max_tw, c->stream); });
+    if (getenv("WSORT_DEBUG_MSD")) {   // finishing jobs by key width (experiments)
+        std::vector<MsdSeg> jobs(n_small);
+        cudaMemcpy(jobs.data(), c->m_small.p, n_small * sizeof(MsdSeg), cudaMemcpyDeviceToHost);
+        std::vector<CopyRange> cps(n_copy);
+        cudaMemcpy(cps.data(), c->m_copy.p, n_copy * sizeof(CopyRange), cudaMemcpyDeviceToHost);
+        uint64_t keys[9] = {0}, nj[9] = {0}, lv[8] = {0}, cw = 0;
+        for (auto &j : jobs) {
+            const uint32_t kw = kw_of((int)j.L) > 8 ? 8 : kw_of((int)j.L);
+            keys[kw] += j.n;
+            nj[kw]++;
+            lv[std::min<uint32_t>(j.buf >> 8, 7)] += j.n;
+        }
+        for (auto &r : cps) cw += r.len;
+        for (int k = 1; k <= 8; k++)
+            if (nj[k]) fprintf(stderr, "finish kw=%d: %llu jobs, %llu keys\n", k, (unsigned long long)nj[k], (unsigned long long)keys[k]);
+        for (int l = 0; l < 8; l++)
+            if (lv[l]) fprintf(stderr, "finish level %d: %llu keys\n", l, (unsigned long long)lv[l]);
+        fprintf(stderr, "copies: %u ranges, %llu words\n", n_copy, (unsigned long long)cw);
+    }
+    int rc2 = launch(c, "k4m_msd_finish", 2 * key_bytes,
+                     [&] { return launch_msd_finish(m, n_small, n_copy, max_tw, c->stream); });
+    if (!rc2 && getenv("WSORT_DEBUG_MSD")) {
+        uint32_t h[kQCount];
+        cudaMemcpy(h, m.ctr, sizeof h, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "finish: distinct keys in 1-2 word jobs: %u\n", h[7]);
+    }
+    return rc2;
 }
 
 int emit_keys(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketInfo *d_bk, uint32_t lmin, uint32_t lmax,
@@ -945,7 +984,7 @@ std::vector<BucketInfo> msd_buckets(const Summary &s, uint32_t lkey, uint32_t &m
         b.n = (uint32_t)(s.off[L + 1] - s.off[L]);
         b.kw = kw_of(L);
         b.ndig = ndig_of(L);
-        b.tile_keys = kMergeThreads * oets_elems_per_thread(b.kw);   // CTA-sort capacity
+        b.tile_keys = kMergeThreads * (b.kw <= 4 ? (uint32_t)kFinE : 4u);   // CTA-sort capacity
         b.aux = kRadixThreads * (32 / b.kw);                          // scatter tile keys
         b.final_b = 1;
         if (L < lkey) continue;

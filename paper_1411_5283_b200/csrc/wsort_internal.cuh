@@ -107,6 +107,7 @@ struct IngestArgs {
                                             // counting, 2 = skip key packing, 4 = direct L3-5 counts
 };
 size_t ingest_smem(uint32_t cta_chunks);
+uint32_t ingest_ctas_per_sm();   // resident K1 CTAs per SM (the tokenizer grid is one wave of them)
 uint32_t dense_entries();
 uint32_t dense_table_base(uint32_t L);
 cudaError_t launch_ingest(const IngestArgs &a, cudaStream_t s);
@@ -174,6 +175,10 @@ __host__ __device__ constexpr uint32_t radix_tile_keys(uint32_t kw) {
 // ---------------- variant A: odd-even transposition tiles + merge path ----------------
 constexpr int kMergeThreads = 256;
 // elements per thread of an OETS tile: the largest power of two <= min(8, 32 / S), at least 1
+#ifndef WSORT_FIN_E
+#define WSORT_FIN_E 8
+#endif
+constexpr int kFinE = WSORT_FIN_E;   // msd finishing CTA sort: keys per thread for key widths <= 4
 __host__ __device__ constexpr uint32_t oets_elems_per_thread(uint32_t S) {
     return S * 8 <= 32 ? 8u : (S * 4 <= 32 ? 4u : (S * 2 <= 32 ? 2u : 1u));
 }
