@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
         for (uint32_t k = 0; k < nzt; k++) {
             const uint32_t start = nz_d[k], cnt = (k + 1 < nzt ? nz_d[k + 1] : seg_end) - start;
             const bool fin = final_digit || cnt == 1;
-            const bool big = !fin && cnt > cap, skip = fin && !a.dst_is_a, copy = fin && a.dst_is_a && cnt > cap;
+            const bool stream = a.stream_fin && b.kw <= 2;   // any child size: k_msd_fin counts it
+            const bool big = !fin && cnt > cap && !stream, skip = fin && !a.dst_is_a, copy = fin && a.dst_is_a && cnt > cap;
             if (big || skip || copy) {
                 if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
                 jn = 0;
@@ -146,6 +147,10 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
                     big_t0[ntop] = 0;
                     jobs[kPlanMax - 1 - ntop++] = MsdSeg{sg.L, start, cnt, 2u};
                 }
+            } else if (cnt > cap) {   // (stream) a child larger than a CTA tile is a job of its own
+                if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
+                jn = 0;
+                jobs[nj++] = MsdSeg{sg.L, start, cnt, a.dst_is_a | (a.level << 8)};
             } else {
                 if (jn + cnt > cap) {
                     jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
@@ -815,13 +820,135 @@ __device__ __forceinline__ void fin_job(const MsdArgs &a, const MsdSeg &sg, cons
     }
 }
 
+// Finishing job of 1- or 2-word keys of any size (a whole MSD child): the keys are streamed from
+// global memory into a shared-memory table whose key is the key itself (u32 / u64: exact), the
+// distinct keys sorted (block_sort_smem), and each written as often as it occurs. More than
+// kStreamDistinct distinct keys: a job of <= 2048 keys is sorted in full; a larger one goes back to
+// the MSD as a segment of the next level.
+constexpr uint32_t kStreamSlots = 2048, kStreamDistinct = 1024;
+__device__ __forceinline__ uint32_t cas_t(uint32_t *p, uint32_t cmp, uint32_t v) { return atomicCAS(p, cmp, v); }
+__device__ __forceinline__ uint64_t cas_t(uint64_t *p, uint64_t cmp, uint64_t v) {
+    return atomicCAS(reinterpret_cast<unsigned long long *>(p), (unsigned long long)cmp, (unsigned long long)v);
+}
+template <typename T>
+__device__ __forceinline__ uint32_t st_hash(T k) { return (uint32_t)(((uint64_t)k * 0x9E3779B97F4A7C15ull) >> 53); }
+
+template <typename T, int KW>
+__device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw) {
+    const T kEmpty = ~(T)0;
+    const uint32_t t = threadIdx.x, n = sg.n;
+    T *slots = reinterpret_cast<T *>(smraw);
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(slots + kStreamSlots);
+    T *A = reinterpret_cast<T *>(cnt + kStreamSlots);
+    T *B = A + fpad(kStreamDistinct);
+    uint32_t *pos = reinterpret_cast<uint32_t *>(B + fpad(kStreamDistinct));
+    uint32_t *misc = pos + kStreamDistinct;   // [0] distinct keys, [1] overflow, [2..] scan scratch
+    for (uint32_t i = t; i < kStreamSlots; i += kST) {
+        slots[i] = kEmpty;
+        cnt[i] = 0;
+    }
+    if (t < 2) misc[t] = 0;
+    __syncthreads();
+    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
+    for (uint32_t i0 = 0; i0 < n; i0 += 4 * kST) {
+        T k[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const uint32_t i = i0 + r * kST + t;
+            k[r] = i < n ? fin_load<T, KW>(src + (size_t)i * KW) : kEmpty;
+        }
+        if (*reinterpret_cast<volatile uint32_t *>(misc + 1)) break;
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            if (k[r] == kEmpty) continue;
+            uint32_t h = st_hash(k[r]);
+            for (;;) {
+                T cur = slots[h];
+                if (cur == kEmpty) {
+                    if (atomicAdd(misc, 1u) >= kStreamDistinct) {   // table full: give up on this job
+                        atomicExch(misc + 1, 1u);
+                        break;
+                    }
+                    cur = cas_t(&slots[h], kEmpty, k[r]);
+                    if (cur == kEmpty) cur = k[r];
+                    else atomicSub(misc, 1u);   // lost the race for this slot
+                }
+                if (cur == k[r]) {
+                    atomicAdd(&cnt[h], 1u);
+                    break;
+                }
+                h = (h + 1) & (kStreamSlots - 1);
+            }
+        }
+    }
+    __syncthreads();
+    if (misc[1]) {   // too many distinct keys
+        if (n <= kST * 8) {   // sort the job in full (the whole buffer is free again)
+            __syncthreads();
+            T *FA = reinterpret_cast<T *>(smraw), *FB = FA + fpad(kST * 8);
+            for (uint32_t i = t; i < kST * 8; i += kST) FA[fpad(i)] = i < n ? fin_load<T, KW>(src + (size_t)i * KW) : kEmpty;
+            T *S = block_sort_smem<T>(FA, FB, n);
+            uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
+            for (uint32_t i = t; i < n; i += kST) fin_store<T, KW>(dst + (size_t)i * KW, S[fpad(i)]);
+        } else if (t == 0) {   // back to the MSD: a segment of the next level (its tiles too)
+            const uint32_t nt = (n + b.aux - 1) / b.aux;
+            const uint32_t q = atomicAdd(a.ctr + kQBig, 1u), t0 = atomicAdd(a.ctr + kQTiles, nt);
+            if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, n, 0u};
+            for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++) a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, n - i * b.aux), 0};
+        }
+        return;
+    }
+    // compact the distinct keys (8 slots per thread), sort them, look up their counts, scan
+    uint32_t occ = 0;
+#pragma unroll
+    for (int e = 0; e < (int)(kStreamSlots / kST); e++) occ += cnt[(kStreamSlots / kST) * t + e] != 0;
+    uint32_t nd = 0;
+    uint32_t p = block_excl_scan_m(occ, misc + 2, &nd);
+#pragma unroll
+    for (int e = 0; e < (int)(kStreamSlots / kST); e++) {
+        const uint32_t h = (kStreamSlots / kST) * t + e;
+        if (cnt[h]) A[fpad(p++)] = slots[h];
+    }
+    T *S = block_sort_smem<T>(A, B, nd);
+    uint32_t c4[4], tot = 0;   // nd <= 1024: 4 per thread
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const uint32_t i = 4 * t + e;
+        c4[e] = 0;
+        if (i < nd) {
+            const T k = S[fpad(i)];
+            uint32_t h = st_hash(k);
+            while (slots[h] != k) h = (h + 1) & (kStreamSlots - 1);
+            c4[e] = cnt[h];
+        }
+        tot += c4[e];
+    }
+    uint32_t run = block_excl_scan_m(tot, misc + 2, nullptr);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        run += c4[e];
+        if (4 * t + e < nd) pos[4 * t + e] = run;   // end (exclusive) of the run of distinct key 4t+e
+    }
+    __syncthreads();
+    uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
+    for (uint32_t j = t; j < n; j += kST) {
+        uint32_t lo = 0, hi = nd - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pos[mid] > j) hi = mid;
+            else lo = mid + 1;
+        }
+        fin_store<T, KW>(dst + (size_t)j * KW, S[fpad(lo)]);
+    }
+}
+
 __global__ void __launch_bounds__(kST) k_msd_fin(MsdArgs a) {
     extern __shared__ __align__(16) uint8_t fsm[];
-    const MsdSeg sg = a.q_small[blockIdx.x];
+    const MsdSeg sg = a.q_small[a.small_base + blockIdx.x];
     const BucketInfo b = a.buckets[sg.L];
     switch (b.kw) {
-        case 1: fin_job<1>(a, sg, b, fsm); break;
-        case 2: fin_job<2>(a, sg, b, fsm); break;
+        case 1: if (a.stream_fin) fin_stream<uint32_t, 1>(a, sg, b, fsm); else fin_job<1>(a, sg, b, fsm); break;
+        case 2: if (a.stream_fin) fin_stream<uint64_t, 2>(a, sg, b, fsm); else fin_job<2>(a, sg, b, fsm); break;
         case 3: fin_job<3>(a, sg, b, fsm); break;
         case 4: fin_job<4>(a, sg, b, fsm); break;
         case 5: fin_job<5>(a, sg, b, fsm); break;
@@ -862,6 +989,16 @@ cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s
     k_msd_scatter<<<ntiles, kST, smem, s>>>(a);
     return cudaGetLastError();
 }
+cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t count, cudaStream_t s) {
+    if (!count) return cudaSuccess;
+    MsdArgs b = a;
+    b.small_base = first;
+    cudaError_t e = cudaFuncSetAttribute(k_msd_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinSmem);
+    if (e != cudaSuccess) return e;
+    k_msd_fin<<<count, kST, kFinSmem, s>>>(b);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_copy, uint32_t max_tile_words,
                               cudaStream_t s) {
     cudaError_t e;
@@ -875,18 +1012,10 @@ cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_cop
         if (e != cudaSuccess) return e;
         k_msd_radix_job<<<n_small, kST, smem, s>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    if (n_small && !a.finish_radix) {
-        e = cudaFuncSetAttribute(k_msd_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinSmem);
+        const size_t smem2 = ((size_t)max_tile_words + max_tile_words / 32 + 1) * 2 * 4;
+        e = cudaFuncSetAttribute(k_msd_cta_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
         if (e != cudaSuccess) return e;
-        k_msd_fin<<<n_small, kST, kFinSmem, s>>>(a);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    if (n_small && a.finish_radix) {
-        const size_t smem = ((size_t)max_tile_words + max_tile_words / 32 + 1) * 2 * 4;
-        e = cudaFuncSetAttribute(k_msd_cta_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k_msd_cta_sort<<<n_small, kST, smem, s>>>(a);
+        k_msd_cta_sort<<<n_small, kST, smem2, s>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (n_copy) {

@@ -901,6 +901,13 @@ int msd_read_counters(wsort_ctx *c, const MsdArgs &m, uint32_t &nsegs, uint32_t 
 int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nsegs, uint32_t ntiles, uint32_t levels,
                           double key_bytes, uint32_t max_tw) {
     int rc;
+    m.stream_fin = m.finish_radix ? 0u : 1u;
+    uint32_t small_done = 0;
+    if (!m.finish_radix && c->h_ctr[kQSmall]) {   // jobs planned before the first level (whole small buckets)
+        small_done = c->h_ctr[kQSmall];
+        rc = launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_fin_jobs(m, 0, small_done, c->stream); });
+        if (rc) return rc;
+    }
     for (; nsegs > 0; level++) {
         if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
         if ((rc = msd_level_buffers(c, m, level, nsegs))) return rc;
@@ -912,39 +919,22 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         rc = launch(c, "k4m_msd_scatter", 2 * seg_bytes, [&] { return launch_msd_scatter(m, ntiles, c->stream); });
         if (rc) return rc;
         if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;
+        if (!m.finish_radix && c->h_ctr[kQSmall] > small_done) {
+            // this level's finishing jobs; a job with too many distinct keys re-enters the next level
+            const uint32_t n_new = std::min(c->h_ctr[kQSmall], m.cap_local) - small_done;
+            rc = launch(c, "k4m_msd_finish", level == 0 ? 2 * key_bytes : 0,
+                        [&] { return launch_msd_fin_jobs(m, small_done, n_new, c->stream); });
+            if (rc) return rc;
+            small_done += n_new;
+            if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;
+        }
         if (getenv("WSORT_DEBUG_MSD"))
             fprintf(stderr, "msd level %u -> next segs %u tiles %u | tiny %u small %u copy %u\n", level, nsegs, ntiles,
                     c->h_ctr[kQTiny], c->h_ctr[kQSmall], c->h_ctr[kQCopy]);
     }
     m.n_tiny = c->h_ctr[kQTiny];
     const uint32_t n_small = c->h_ctr[kQSmall], n_copy = c->h_ctr[kQCopy];
-    if (getenv("WSORT_DEBUG_MSD")) {   // finishing jobs by key width (experiments)
-        std::vector<MsdSeg> jobs(n_small);
-        cudaMemcpy(jobs.data(), c->m_small.p, n_small * sizeof(MsdSeg), cudaMemcpyDeviceToHost);
-        std::vector<CopyRange> cps(n_copy);
-        cudaMemcpy(cps.data(), c->m_copy.p, n_copy * sizeof(CopyRange), cudaMemcpyDeviceToHost);
-        uint64_t keys[9] = {0}, nj[9] = {0}, lv[8] = {0}, cw = 0;
-        for (auto &j : jobs) {
-            const uint32_t kw = kw_of((int)j.L) > 8 ? 8 : kw_of((int)j.L);
-            keys[kw] += j.n;
-            nj[kw]++;
-            lv[std::min<uint32_t>(j.buf >> 8, 7)] += j.n;
-        }
-        for (auto &r : cps) cw += r.len;
-        for (int k = 1; k <= 8; k++)
-            if (nj[k]) fprintf(stderr, "finish kw=%d: %llu jobs, %llu keys\n", k, (unsigned long long)nj[k], (unsigned long long)keys[k]);
-        for (int l = 0; l < 8; l++)
-            if (lv[l]) fprintf(stderr, "finish level %d: %llu keys\n", l, (unsigned long long)lv[l]);
-        fprintf(stderr, "copies: %u ranges, %llu words\n", n_copy, (unsigned long long)cw);
-    }
-    int rc2 = launch(c, "k4m_msd_finish", 2 * key_bytes,
-                     [&] { return launch_msd_finish(m, n_small, n_copy, max_tw, c->stream); });
-    if (!rc2 && getenv("WSORT_DEBUG_MSD")) {
-        uint32_t h[kQCount];
-        cudaMemcpy(h, m.ctr, sizeof h, cudaMemcpyDeviceToHost);
-        fprintf(stderr, "finish: distinct keys in 1-2 word jobs: %u\n", h[7]);
-    }
-    return rc2;
+    return launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_finish(m, n_small, n_copy, max_tw, c->stream); });
 }
 
 int emit_keys(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketInfo *d_bk, uint32_t lmin, uint32_t lmax,

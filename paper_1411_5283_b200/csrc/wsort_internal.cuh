@@ -263,13 +263,16 @@ struct MsdArgs {
     uint32_t *keys_b;              // finishing: buffer B (final)
     uint32_t n_tiny;
     uint32_t finish_radix;         // 1: small jobs with kw <= 4 by local LSD radix, else odd-even transposition
+    uint32_t stream_fin;           // 1: children of kw <= 2 buckets of any size become finishing jobs (k_msd_fin)
+    uint32_t small_base;           // k_msd_fin: first job of this launch in q_small
 };
 size_t msd_scatter_smem();
 cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
 cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s);
 cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
 cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_copy, uint32_t max_tile_words,
-                              cudaStream_t s);
+                              cudaStream_t s);   // tiny jobs, radix-finish jobs, copies (after the last level)
+cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t count, cudaStream_t s);   // per level
 
 struct EmitArgs {
     const BucketInfo *buckets;
