@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
         for (uint32_t k = 0; k < nzt; k++) {
             const uint32_t start = nz_d[k], cnt = (k + 1 < nzt ? nz_d[k + 1] : seg_end) - start;
             const bool fin = final_digit || cnt == 1;
-            const bool stream = a.stream_fin && b.kw <= 2;   // any child size: k_msd_fin counts it
+            const bool stream = a.stream_fin;   // any child size: k_msd_fin counts it
             const bool big = !fin && cnt > cap && !stream, skip = fin && !a.dst_is_a, copy = fin && a.dst_is_a && cnt > cap;
             if (big || skip || copy) {
                 if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
@@ -410,9 +410,8 @@ __device__ __forceinline__ void kst(uint32_t *p, const Key<KW> &x) {
 // E keys (the data-parallel bubble sort), odd-even merge-split across groups of 8 lanes through warp
 // shuffles (min/max against the reversed partner run + bitonic clean-up), then merge paths in
 // shared memory up to the whole tile. Keys stay in registers until the shared-memory merges.
-template <int KW>
+template <int KW, int E = (KW <= 4 ? kFinE : 4)>
 __device__ __forceinline__ void cta_sort_job(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint32_t *sm) {
-    constexpr int E = KW <= 4 ? kFinE : 4;
     constexpr uint32_t TN = kST * E;
     const int t = threadIdx.x, lane = t & 31;
     const uint32_t n = sg.n;
@@ -695,131 +694,6 @@ __device__ __forceinline__ T *block_sort_smem(T *A, T *B, uint32_t n) {
     return A;
 }
 
-// Finishing job (a multiset of text words: equal keys are identical words, and the job's keys share
-// their leading digits). The keys are staged in shared memory and counted in a hash table whose
-// slots hold the index of a representative key (exact: keys are compared in full). If the job has
-// at most kFinRank distinct keys, each distinct key's rank is the number of distinct keys below it
-// and every key is written as many times as it occurs (the sorted multiset; ties are unobservable,
-// reading A6). Otherwise the job is sorted in full: odd-even transposition in registers + merge paths.
-constexpr uint32_t kFinSlots = 2048, kFinRank = 256;
-constexpr uint32_t kFinEmpty = 0xffffffffu;
-
-template <int KW>
-__device__ __forceinline__ bool kw_eq(const uint32_t *K, uint32_t i, uint32_t j) {
-    bool eq = true;
-#pragma unroll
-    for (int u = 0; u < KW; u++) eq &= K[i * KW + u] == K[j * KW + u];
-    return eq;
-}
-template <int KW>
-__device__ __forceinline__ bool kw_lt(const uint32_t *K, uint32_t i, uint32_t j) {   // key i < key j
-#pragma unroll
-    for (int u = 0; u < KW; u++) {
-        const uint32_t x = K[i * KW + u], y = K[j * KW + u];
-        if (x != y) return x < y;
-    }
-    return false;
-}
-template <int KW>
-__device__ __forceinline__ uint32_t kw_hash(const uint32_t *K, uint32_t i) {
-    uint32_t h = 0x811c9dc5u;
-#pragma unroll
-    for (int u = 0; u < KW; u++) h = (h ^ K[i * KW + u]) * 0x9E3779B1u;
-    return (h >> 16) & (kFinSlots - 1);
-}
-
-template <int KW>
-__device__ __forceinline__ void fin_job(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw) {
-    const uint32_t t = threadIdx.x, n = sg.n;
-    uint32_t *K = reinterpret_cast<uint32_t *>(smraw);             // [n * KW] the job's keys
-    uint32_t *slot = K + kST * 8 * 4;                               // [kFinSlots] representative key
-    uint32_t *cnt = slot + kFinSlots;                               // [kFinSlots]
-    uint32_t *D = cnt + kFinSlots;                                  // [kFinRank] distinct keys (rep)
-    uint32_t *R = D + kFinRank;                                     // [kFinRank] sorted distinct keys
-    uint32_t *pos = R + kFinRank;                                   // [kFinRank] run ends
-    uint32_t *wsum = pos + kFinRank;                                // [9 + 1]
-    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
-    for (uint32_t i = t; i < n * KW; i += kST) K[i] = __ldg(src + i);
-    for (uint32_t i = t; i < kFinSlots; i += kST) {
-        slot[i] = kFinEmpty;
-        cnt[i] = 0;
-    }
-    __syncthreads();
-    for (uint32_t i = t; i < n; i += kST) {
-        uint32_t h = kw_hash<KW>(K, i);
-        for (;;) {
-            uint32_t r = slot[h];
-            if (r == kFinEmpty) {
-                r = atomicCAS(&slot[h], kFinEmpty, i);
-                if (r == kFinEmpty) r = i;
-            }
-            if (r == i || kw_eq<KW>(K, r, i)) {
-                atomicAdd(&cnt[h], 1u);
-                break;
-            }
-            h = (h + 1) & (kFinSlots - 1);
-        }
-    }
-    __syncthreads();
-    uint32_t occ = 0;
-#pragma unroll
-    for (int e = 0; e < (int)(kFinSlots / kST); e++) occ += cnt[(kFinSlots / kST) * t + e] != 0;
-    uint32_t nd = 0;
-    uint32_t p = block_excl_scan_m(occ, wsum, &nd);
-    if (t == 0) atomicAdd(a.ctr + 7, nd);   // (statistics: distinct keys over all finishing jobs)
-    if (nd > kFinRank) {   // many distinct keys: sort the job in full
-        __syncthreads();
-        if constexpr (KW <= 2) {
-            using T = typename std::conditional<KW == 1, uint32_t, uint64_t>::type;
-            T *A = reinterpret_cast<T *>(smraw), *B = A + fpad(kST * 8);
-            for (uint32_t i = t; i < kST * 8; i += kST) A[fpad(i)] = i < n ? fin_load<T, KW>(src + (size_t)i * KW) : ~(T)0;
-            T *S = block_sort_smem<T>(A, B, n);
-            uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
-            for (uint32_t i = t; i < n; i += kST) fin_store<T, KW>(dst + (size_t)i * KW, S[fpad(i)]);
-        } else {
-            cta_sort_job<KW>(a, sg, b, reinterpret_cast<uint32_t *>(smraw));
-        }
-        return;
-    }
-#pragma unroll
-    for (int e = 0; e < (int)(kFinSlots / kST); e++) {
-        const uint32_t h = (kFinSlots / kST) * t + e;
-        if (cnt[h]) {
-            D[p] = slot[h];
-            pos[p] = cnt[h];   // (count, for now)
-            p++;
-        }
-    }
-    __syncthreads();
-    if (t < nd) {   // rank among the distinct keys
-        const uint32_t me = D[t];
-        uint32_t rank = 0;
-        for (uint32_t j = 0; j < nd; j++) rank += kw_lt<KW>(K, D[j], me);
-        R[rank] = t;
-    }
-    __syncthreads();
-    uint32_t c = t < nd ? pos[R[t]] : 0u;   // runs in sorted order -> their ends
-    uint32_t end = block_excl_scan_m(c, wsum, nullptr) + c;
-    const uint32_t rep = t < nd ? D[R[t]] : 0u;
-    __syncthreads();
-    if (t < nd) {
-        pos[t] = end;
-        D[t] = rep;   // D now: representative of the t-th smallest distinct key
-    }
-    __syncthreads();
-    uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
-    for (uint32_t j = t; j < n * KW; j += kST) {   // output word j: key j / KW of the sorted multiset
-        const uint32_t k = j / KW;
-        uint32_t lo = 0, hi = nd - 1;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (pos[mid] > k) hi = mid;
-            else lo = mid + 1;
-        }
-        dst[j] = K[D[lo] * KW + (j - k * KW)];
-    }
-}
-
 // Finishing job of 1- or 2-word keys of any size (a whole MSD child): the keys are streamed from
 // global memory into a shared-memory table whose key is the key itself (u32 / u64: exact), the
 // distinct keys sorted (block_sort_smem), and each written as often as it occurs. More than
@@ -883,14 +757,15 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
     }
     __syncthreads();
     if (misc[1]) {   // too many distinct keys
-        if (n <= kST * 8) {   // sort the job in full (the whole buffer is free again)
+        if (n <= b.tile_keys) {   // (possibly several children): sort the job in full
             __syncthreads();
             T *FA = reinterpret_cast<T *>(smraw), *FB = FA + fpad(kST * 8);
             for (uint32_t i = t; i < kST * 8; i += kST) FA[fpad(i)] = i < n ? fin_load<T, KW>(src + (size_t)i * KW) : kEmpty;
             T *S = block_sort_smem<T>(FA, FB, n);
             uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
             for (uint32_t i = t; i < n; i += kST) fin_store<T, KW>(dst + (size_t)i * KW, S[fpad(i)]);
-        } else if (t == 0) {   // back to the MSD: a segment of the next level (its tiles too)
+        } else if (t == 0) {   // one child larger than a tile: back to the MSD as a segment of the next
+                               // level (a child without digits left holds one key only: this terminates)
             const uint32_t nt = (n + b.aux - 1) / b.aux;
             const uint32_t q = atomicAdd(a.ctr + kQBig, 1u), t0 = atomicAdd(a.ctr + kQTiles, nt);
             if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, n, 0u};
@@ -942,25 +817,158 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
     }
 }
 
-__global__ void __launch_bounds__(kST) k_msd_fin(MsdArgs a) {
+// Finishing job of KW >= 3-word keys of any size: as fin_stream, but the table key is a 64-bit
+// fingerprint of the key; the first key of each fingerprint is kept as its representative, and a
+// second pass compares every key with its representative word by word (exact: any mismatch sorts
+// the job in full / sends it to the next MSD level). At most kWideDistinct distinct keys, ranked by
+// counting the smaller ones.
+constexpr uint32_t kWideSlots = 1024, kWideDistinct = 256;
+template <int KW>
+__device__ __forceinline__ uint64_t fp64(const uint32_t (&k)[KW]) {
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+#pragma unroll
+    for (int u = 0; u < KW; u++) h = (h ^ k[u]) * 0xD6E8FEB86659FD93ull;
+    h ^= h >> 29;
+    return h == ~0ull ? 0x5555ull : h;   // never ~0 (= empty)
+}
+template <int KW>
+__device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw) {
+    const uint64_t kEmpty = ~0ull;
+    const uint32_t t = threadIdx.x, n = sg.n;
+    uint64_t *fps = reinterpret_cast<uint64_t *>(smraw);                 // [kWideSlots]
+    uint32_t *sid = reinterpret_cast<uint32_t *>(fps + kWideSlots);       // [kWideSlots] distinct id
+    uint32_t *cnt = sid + kWideSlots;                                     // [kWideSlots]
+    uint32_t *rep = cnt + kWideSlots;                                     // [kWideDistinct][KW]
+    uint32_t *dcnt = rep + kWideDistinct * KW;                            // [kWideDistinct] count by id
+    uint32_t *order = dcnt + kWideDistinct;                               // [kWideDistinct] id by rank
+    uint32_t *pos = order + kWideDistinct;                                // [kWideDistinct] run ends
+    uint32_t *misc = pos + kWideDistinct;                                 // [0] nd [1] overflow [2..] scan
+    for (uint32_t i = t; i < kWideSlots; i += kST) {
+        fps[i] = kEmpty;
+        sid[i] = 0xffffffffu;
+        cnt[i] = 0;
+    }
+    if (t < 2) misc[t] = 0;
+    __syncthreads();
+    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
+    for (uint32_t i = t; i < n; i += kST) {
+        if (*reinterpret_cast<volatile uint32_t *>(misc + 1)) break;
+        uint32_t k[KW];
+#pragma unroll
+        for (int u = 0; u < KW; u++) k[u] = __ldg(src + (size_t)i * KW + u);
+        const uint64_t f = fp64<KW>(k);
+        uint32_t h = (uint32_t)(f >> 40) & (kWideSlots - 1);
+        for (;;) {
+            uint64_t cur = fps[h];
+            if (cur == kEmpty) {
+                cur = atomicCAS(reinterpret_cast<unsigned long long *>(&fps[h]), kEmpty, (unsigned long long)f);
+                if (cur == kEmpty) {   // new fingerprint: this key is its representative
+                    const uint32_t id = atomicAdd(misc, 1u);
+                    if (id >= kWideDistinct) {
+                        atomicExch(misc + 1, 1u);
+                        break;
+                    }
+#pragma unroll
+                    for (int u = 0; u < KW; u++) rep[id * KW + u] = k[u];
+                    atomicExch(&sid[h], id);
+                    cur = f;
+                }
+            }
+            if (cur == f) {
+                atomicAdd(&cnt[h], 1u);
+                break;
+            }
+            h = (h + 1) & (kWideSlots - 1);
+        }
+    }
+    __syncthreads();
+    if (!misc[1]) {   // verify: every key equals its fingerprint's representative
+        for (uint32_t i = t; i < n; i += kST) {
+            uint32_t k[KW];
+#pragma unroll
+            for (int u = 0; u < KW; u++) k[u] = __ldg(src + (size_t)i * KW + u);
+            const uint64_t f = fp64<KW>(k);
+            uint32_t h = (uint32_t)(f >> 40) & (kWideSlots - 1);
+            while (fps[h] != f) h = (h + 1) & (kWideSlots - 1);
+            const uint32_t id = sid[h];
+            bool eq = true;
+#pragma unroll
+            for (int u = 0; u < KW; u++) eq &= rep[id * KW + u] == k[u];
+            if (!eq) misc[1] = 1u;   // a 64-bit fingerprint collision (never expected)
+        }
+    }
+    __syncthreads();
+    if (misc[1]) {   // too many distinct keys
+        if (n <= b.tile_keys) {   // (possibly several children): sort the job in full
+            __syncthreads();
+            cta_sort_job<KW, (KW <= 4 ? 4 : 2)>(a, sg, b, reinterpret_cast<uint32_t *>(smraw));
+        } else if (t == 0) {   // one child larger than a tile: back to the MSD as a segment of the next
+                               // level (a child without digits left holds one key only: this terminates)
+            const uint32_t nt = (n + b.aux - 1) / b.aux;
+            const uint32_t q = atomicAdd(a.ctr + kQBig, 1u), t0 = atomicAdd(a.ctr + kQTiles, nt);
+            if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, n, 0u};
+            for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++) a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, n - i * b.aux), 0};
+        }
+        return;
+    }
+    const uint32_t nd = misc[0];
+    for (uint32_t i = t; i < kWideSlots; i += kST)
+        if (cnt[i]) dcnt[sid[i]] = cnt[i];
+    __syncthreads();
+    if (t < nd) {   // rank = number of smaller distinct keys
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < nd; j++) {
+            bool lt = false, decided = false;
+#pragma unroll
+            for (int u = 0; u < KW; u++) {
+                const uint32_t x = rep[j * KW + u], y = rep[t * KW + u];
+                if (!decided && x != y) {
+                    lt = x < y;
+                    decided = true;
+                }
+            }
+            rank += lt;
+        }
+        order[rank] = t;
+    }
+    __syncthreads();
+    const uint32_t c = t < nd ? dcnt[order[t]] : 0u;
+    const uint32_t end = block_excl_scan_m(c, misc + 2, nullptr) + c;
+    if (t < nd) pos[t] = end;
+    __syncthreads();
+    uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
+    for (uint32_t j = t; j < n * KW; j += kST) {
+        const uint32_t kk = j / KW;
+        uint32_t lo = 0, hi = nd - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pos[mid] > kk) hi = mid;
+            else lo = mid + 1;
+        }
+        dst[j] = rep[order[lo] * KW + (j - kk * KW)];
+    }
+}
+
+__global__ void __launch_bounds__(kST, 4) k_msd_fin(MsdArgs a) {
     extern __shared__ __align__(16) uint8_t fsm[];
     const MsdSeg sg = a.q_small[a.small_base + blockIdx.x];
     const BucketInfo b = a.buckets[sg.L];
     switch (b.kw) {
-        case 1: if (a.stream_fin) fin_stream<uint32_t, 1>(a, sg, b, fsm); else fin_job<1>(a, sg, b, fsm); break;
-        case 2: if (a.stream_fin) fin_stream<uint64_t, 2>(a, sg, b, fsm); else fin_job<2>(a, sg, b, fsm); break;
-        case 3: fin_job<3>(a, sg, b, fsm); break;
-        case 4: fin_job<4>(a, sg, b, fsm); break;
-        case 5: fin_job<5>(a, sg, b, fsm); break;
-        case 6: fin_job<6>(a, sg, b, fsm); break;
-        case 7: fin_job<7>(a, sg, b, fsm); break;
-        default: fin_job<8>(a, sg, b, fsm); break;
+        case 1: fin_stream<uint32_t, 1>(a, sg, b, fsm); break;
+        case 2: fin_stream<uint64_t, 2>(a, sg, b, fsm); break;
+        case 3: fin_stream_wide<3>(a, sg, b, fsm); break;
+        case 4: fin_stream_wide<4>(a, sg, b, fsm); break;
+        case 5: fin_stream_wide<5>(a, sg, b, fsm); break;
+        case 6: fin_stream_wide<6>(a, sg, b, fsm); break;
+        case 7: fin_stream_wide<7>(a, sg, b, fsm); break;
+        default: fin_stream_wide<8>(a, sg, b, fsm); break;
     }
 }
-// the fallbacks reuse the whole buffer: cta_sort_job needs two padded tiles of <= 8192 words
-constexpr size_t kFinSmem = (2 * (8192 + 8192 / 32 + 1)) * 4 > (kST * 8 * 4 + 2 * kFinSlots + 3 * kFinRank + 10) * 4
-                                ? (2 * (8192 + 8192 / 32 + 1)) * 4
-                                : (kST * 8 * 4 + 2 * kFinSlots + 3 * kFinRank + 10) * 4;
+constexpr size_t kFinSmemStream = kStreamSlots * 12 + 2 * (kStreamDistinct + kStreamDistinct / 16) * 8 + (kStreamDistinct + 16) * 4;
+constexpr size_t kFinSmemWide = kWideSlots * 16 + (kWideDistinct * 8 + 3 * kWideDistinct + 16) * 4;
+constexpr size_t kFinSmemSort = 2 * (kST * 4 * 4 + kST * 4 * 4 / 32 + 1) * 4;   // cta_sort_job fallback: TN*KW <= 4096
+constexpr size_t kFinSmem0 = kFinSmemStream > kFinSmemWide ? kFinSmemStream : kFinSmemWide;
+constexpr size_t kFinSmem = kFinSmem0 > kFinSmemSort ? kFinSmem0 : kFinSmemSort;
 
 __global__ void __launch_bounds__(kST) k_msd_copy(MsdArgs a) {
     const CopyRange r = a.q_copy[blockIdx.x];
@@ -1012,7 +1020,10 @@ cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_cop
         if (e != cudaSuccess) return e;
         k_msd_radix_job<<<n_small, kST, smem, s>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        const size_t smem2 = ((size_t)max_tile_words + max_tile_words / 32 + 1) * 2 * 4;
+        // cta_sort_job's default tile: 256 * E keys of kw words <= 8192 words (jobs are at most tile_keys)
+        const size_t tw = 8192;
+        (void)max_tile_words;
+        const size_t smem2 = (tw + tw / 32 + 1) * 2 * 4;
         e = cudaFuncSetAttribute(k_msd_cta_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
         if (e != cudaSuccess) return e;
         k_msd_cta_sort<<<n_small, kST, smem2, s>>>(a);

@@ -974,7 +974,8 @@ std::vector<BucketInfo> msd_buckets(const Summary &s, uint32_t lkey, uint32_t &m
         b.n = (uint32_t)(s.off[L + 1] - s.off[L]);
         b.kw = kw_of(L);
         b.ndig = ndig_of(L);
-        b.tile_keys = kMergeThreads * (b.kw <= 4 ? (uint32_t)kFinE : 4u);   // CTA-sort capacity
+        // finishing-job capacity: its full-sort fallback holds <= 4096 key words (<= 2048 keys)
+        b.tile_keys = b.kw <= 2 ? 2048u : (b.kw <= 4 ? 1024u : 512u);
         b.aux = kRadixThreads * (32 / b.kw);                          // scatter tile keys
         b.final_b = 1;
         if (L < lkey) continue;
