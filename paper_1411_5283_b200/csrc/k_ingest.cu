@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(256) k_emit_dense(DenseEmitArgs a) {
     __shared__ __align__(16) uint8_t stage[kDenseStage];
     __shared__ uint32_t s_end[kDenseTile], s_idx[kDenseTile];
     const uint32_t t = threadIdx.x;
-    const TileDesc td = a.tiles[blockIdx.x];
+    const TileDesc td = tile_from_prefix(a.tile_pfx, blockIdx.x);
     const uint32_t L = td.L;
     const BucketInfo b = a.buckets[L];
     const uint32_t k0 = td.tile * kDenseTile;

@@ -949,9 +949,18 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     }
 }
 
+// Persistent: jobs [small_base, ctr[kQSmall]) — the end is read on the device (this level's plan
+// appended them), so the host needs no sync before the launch.
 __global__ void __launch_bounds__(kST, 4) k_msd_fin(MsdArgs a) {
     extern __shared__ __align__(16) uint8_t fsm[];
-    const MsdSeg sg = a.q_small[a.small_base + blockIdx.x];
+    __shared__ uint32_t s_job;
+    const uint32_t end = min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQSmall), a.cap_local);
+    for (;;) {   // jobs are taken dynamically (their sizes differ by orders of magnitude)
+    if (threadIdx.x == 0) s_job = a.small_base + atomicAdd(a.ctr + kQFinTicket, 1u);
+    __syncthreads();
+    const uint32_t j = s_job;
+    if (j >= end) break;
+    const MsdSeg sg = a.q_small[j];
     const BucketInfo b = a.buckets[sg.L];
     switch (b.kw) {
         case 1: fin_stream<uint32_t, 1>(a, sg, b, fsm); break;
@@ -962,6 +971,8 @@ __global__ void __launch_bounds__(kST, 4) k_msd_fin(MsdArgs a) {
         case 6: fin_stream_wide<6>(a, sg, b, fsm); break;
         case 7: fin_stream_wide<7>(a, sg, b, fsm); break;
         default: fin_stream_wide<8>(a, sg, b, fsm); break;
+    }
+    __syncthreads();   // shared memory is reused by the next job
     }
 }
 constexpr size_t kFinSmemStream = kStreamSlots * 12 + 2 * (kStreamDistinct + kStreamDistinct / 16) * 8 + (kStreamDistinct + 16) * 4;
@@ -997,13 +1008,15 @@ cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s
     k_msd_scatter<<<ntiles, kST, smem, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t count, cudaStream_t s) {
-    if (!count) return cudaSuccess;
+cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t grid, cudaStream_t s) {
+    if (!grid) return cudaSuccess;
     MsdArgs b = a;
     b.small_base = first;
-    cudaError_t e = cudaFuncSetAttribute(k_msd_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinSmem);
+    cudaError_t e = cudaMemsetAsync(a.ctr + kQFinTicket, 0, 4, s);
     if (e != cudaSuccess) return e;
-    k_msd_fin<<<count, kST, kFinSmem, s>>>(b);
+    e = cudaFuncSetAttribute(k_msd_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinSmem);
+    if (e != cudaSuccess) return e;
+    k_msd_fin<<<grid, kST, kFinSmem, s>>>(b);
     return cudaGetLastError();
 }
 

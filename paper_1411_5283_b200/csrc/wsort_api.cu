@@ -51,6 +51,8 @@ struct wsort_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
+    cudaStream_t aux = nullptr;                  // second stream: the dense buckets run beside the MSD
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int sms = 148;
     State state = ST_CREATED;
     char err[512] = {0};
@@ -81,6 +83,11 @@ struct wsort_ctx {
     std::vector<uint8_t> hplan;
     uint8_t *h_plan_pinned = nullptr;
     size_t h_plan_cap = 0;
+    // pinned staging arena for the host-built tables of one sort (one region per upload, reused by the
+    // next sort once `arena_done` has passed)
+    uint8_t *arena = nullptr;
+    size_t arena_cap = 0, arena_off = 0;
+    cudaEvent_t arena_done = nullptr;
     bool sorted_with_src = false;
     int last_algo = 0;
     bool packed_pending = false;   // keys_a holds packed, not yet sorted keys (wsort_pack / load_keys)
@@ -148,6 +155,42 @@ int upload_small(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const
     return WSORT_OK;
 }
 
+// Staged uploads: host tables are copied into the pinned arena and sent with one async copy each
+// (pageable cudaMemcpyAsync would stage through the driver); regions are not reused within a sort.
+int arena_begin(wsort_ctx *c) {
+    if (c->arena_done) CK(cudaEventSynchronize(c->arena_done), "arena reuse");
+    c->arena_off = 0;
+    return WSORT_OK;
+}
+int arena_upload(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const char *what) {
+    int rc = ensure(c, dst, bytes, what);
+    if (rc || !bytes) return rc;
+    const size_t need = c->arena_off + ((bytes + 255) & ~(size_t)255);
+    if (need > c->arena_cap) {   // grow (rare): earlier copies of this sort read the old buffer
+        CK(cudaStreamSynchronize(c->stream), "arena grow");
+        uint8_t *nb = nullptr;
+        const size_t cap = std::max<size_t>(need * 2, 1 << 20);
+        if (cudaMallocHost(&nb, cap) != cudaSuccess) {
+            cudaGetLastError();
+            return set_err(c, WSORT_E_NOMEM, "pinned arena");
+        }
+        if (c->arena) cudaFreeHost(c->arena);
+        c->arena = nb;
+        c->arena_cap = cap;
+        c->arena_off = 0;
+    }
+    uint8_t *h = c->arena + c->arena_off;
+    memcpy(h, src, bytes);
+    c->arena_off += (bytes + 255) & ~(size_t)255;
+    CK(cudaMemcpyAsync(dst.p, h, bytes, cudaMemcpyHostToDevice, c->stream), what);
+    return WSORT_OK;
+}
+int arena_end(wsort_ctx *c) {
+    if (!c->arena_done) CK(cudaEventCreateWithFlags(&c->arena_done, cudaEventDisableTiming), "arena event");
+    CK(cudaEventRecord(c->arena_done, c->stream), "arena event");
+    return WSORT_OK;
+}
+
 int class_id(wsort_ctx *c, const char *name) {
     for (size_t i = 0; i < c->classes.size(); i++)
         if (c->classes[i].name == name) return (int)i;
@@ -167,26 +210,43 @@ cudaEvent_t get_event(wsort_ctx *c) {
 }
 
 template <class F>
-int launch(wsort_ctx *c, const char *name, double bytes, F f) {
+int launch_on(wsort_ctx *c, cudaStream_t s, const char *name, double bytes, F f) {
     PendingEv pe{};
     if (c->prof) {
         pe.cls = class_id(c, name);
         pe.a = get_event(c);
         pe.b = get_event(c);
         pe.bytes = bytes;
-        cudaEventRecord(pe.a, c->stream);
+        cudaEventRecord(pe.a, s);
     }
     cudaError_t e = f();
     if (e != cudaSuccess) return cuda_err(c, e, name);
     c->launches++;
     if (c->prof) {
-        cudaEventRecord(pe.b, c->stream);
+        cudaEventRecord(pe.b, s);
         c->pending.push_back(pe);
     }
     return WSORT_OK;
 }
+template <class F>
+int launch(wsort_ctx *c, const char *name, double bytes, F f) {
+    return launch_on(c, c->stream, name, bytes, f);
+}
 
 void drain_events(wsort_ctx *c) {
+    static const bool timeline = getenv("WSORT_DEBUG_TIMELINE") != nullptr;   // (experiments)
+    if (timeline && !c->pending.empty()) {
+        cudaEventSynchronize(c->pending.back().b);
+        float prev_end = 0;
+        for (auto &pe : c->pending) {
+            float t0 = 0, t1 = 0;
+            cudaEventElapsedTime(&t0, c->pending.front().a, pe.a);
+            cudaEventElapsedTime(&t1, c->pending.front().a, pe.b);
+            fprintf(stderr, "  %-22s start %8.3f  dur %7.3f  gap %7.3f ms\n", c->classes[pe.cls].name.c_str(), t0, t1 - t0,
+                    t0 - prev_end);
+            prev_end = t1;
+        }
+    }
     for (auto &pe : c->pending) {
         float ms = 0;
         cudaEventSynchronize(pe.b);
@@ -314,6 +374,8 @@ void wsort_destroy(wsort_ctx *c) {
         if (b->p) cudaFree(b->p);
     if (c->h_sum) cudaFreeHost(c->h_sum);
     if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
+    if (c->arena) cudaFreeHost(c->arena);
+    if (c->arena_done) cudaEventDestroy(c->arena_done);
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->h_ig) cudaFreeHost(c->h_ig);
     for (auto &pe : c->pending) {
@@ -321,6 +383,9 @@ void wsort_destroy(wsort_ctx *c) {
         cudaEventDestroy(pe.b);
     }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->aux && c->aux != c->stream) cudaStreamDestroy(c->aux);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -432,8 +497,12 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     rc = launch(c, "k2_dense_lensum", (double)dense_entries() * 4,
                 [&] { return launch_dense_lensum(ia.dense, ia.ghist, c->stream); });
     if (rc) return rc;
+    rc = launch(c, "k2_bucket_offsets", (double)kHistBins * 4,
+                [&] { return launch_bucket_offsets(ia.ghist, static_cast<Summary *>(c->d_sum.p), c->stream); });
+    if (rc) return rc;
     CK(cudaMemcpyAsync(c->h_ig, c->ig_ctr.p, kIgCtrs * 4, cudaMemcpyDeviceToHost, c->stream), "copy ingest counters");
-    CK(cudaStreamSynchronize(c->stream), "ingest");
+    CK(cudaMemcpyAsync(c->h_sum, c->d_sum.p, sizeof(Summary), cudaMemcpyDeviceToHost, c->stream), "copy summary");
+    CK(cudaStreamSynchronize(c->stream), "tokenize");
     c->cta_bases_ready = c->cta_counts_ready = false;
     if (c->h_ig[kIgVeryLong]) {   // words of 49..255 letters were not staged: histogram them the K3 way
         CK(cudaMemsetAsync(c->ghist.p, 0, kHistBins * 4, c->stream), "memset ghist");
@@ -441,12 +510,12 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
                     [&] { return launch_count_lengths(a, ia.ghist, c->stream); });
         if (rc) return rc;
         c->cta_counts_ready = true;
+        rc = launch(c, "k2_bucket_offsets", (double)kHistBins * 4,
+                    [&] { return launch_bucket_offsets(ia.ghist, static_cast<Summary *>(c->d_sum.p), c->stream); });
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(c->h_sum, c->d_sum.p, sizeof(Summary), cudaMemcpyDeviceToHost, c->stream), "copy summary");
+        CK(cudaStreamSynchronize(c->stream), "tokenize (long words)");
     }
-    rc = launch(c, "k2_bucket_offsets", (double)kHistBins * 4,
-                [&] { return launch_bucket_offsets(ia.ghist, static_cast<Summary *>(c->d_sum.p), c->stream); });
-    if (rc) return rc;
-    CK(cudaMemcpyAsync(c->h_sum, c->d_sum.p, sizeof(Summary), cudaMemcpyDeviceToHost, c->stream), "copy summary");
-    CK(cudaStreamSynchronize(c->stream), "tokenize");
     const Summary &s = *c->h_sum;
     if (c->prof && !c->h_ig[kIgVeryLong]) {   // K1's algorithmic bytes: the text + the staged keys it wrote
         double staged = 0;
@@ -902,11 +971,12 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
                           double key_bytes, uint32_t max_tw) {
     int rc;
     m.stream_fin = m.finish_radix ? 0u : 1u;
+    const uint32_t fin_grid = (uint32_t)c->sms * 4;   // k_msd_fin: 4 resident CTAs per SM
     uint32_t small_done = 0;
     if (!m.finish_radix && c->h_ctr[kQSmall]) {   // jobs planned before the first level (whole small buckets)
-        small_done = c->h_ctr[kQSmall];
-        rc = launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_fin_jobs(m, 0, small_done, c->stream); });
+        rc = launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_fin_jobs(m, 0, fin_grid, c->stream); });
         if (rc) return rc;
+        small_done = c->h_ctr[kQSmall];
     }
     for (; nsegs > 0; level++) {
         if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
@@ -918,16 +988,14 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         if (rc) return rc;
         rc = launch(c, "k4m_msd_scatter", 2 * seg_bytes, [&] { return launch_msd_scatter(m, ntiles, c->stream); });
         if (rc) return rc;
-        if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;
-        if (!m.finish_radix && c->h_ctr[kQSmall] > small_done) {
-            // this level's finishing jobs; a job with too many distinct keys re-enters the next level
-            const uint32_t n_new = std::min(c->h_ctr[kQSmall], m.cap_local) - small_done;
+        if (!m.finish_radix) {   // this level's finishing jobs (their count is on the device); a job with too
+                                 // many distinct keys re-enters the next level
             rc = launch(c, "k4m_msd_finish", level == 0 ? 2 * key_bytes : 0,
-                        [&] { return launch_msd_fin_jobs(m, small_done, n_new, c->stream); });
+                        [&] { return launch_msd_fin_jobs(m, small_done, fin_grid, c->stream); });
             if (rc) return rc;
-            small_done += n_new;
-            if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;
         }
+        if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;   // the level's one host sync
+        if (!m.finish_radix) small_done = std::min(c->h_ctr[kQSmall], m.cap_local);
         if (getenv("WSORT_DEBUG_MSD"))
             fprintf(stderr, "msd level %u -> next segs %u tiles %u | tiny %u small %u copy %u\n", level, nsegs, ntiles,
                     c->h_ctr[kQTiny], c->h_ctr[kQSmall], c->h_ctr[kQCopy]);
@@ -939,19 +1007,19 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
 
 int emit_keys(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketInfo *d_bk, uint32_t lmin, uint32_t lmax,
               double bytes) {
-    std::vector<TileDesc> emit_tiles;
-    for (uint32_t L = lmin; L <= lmax; L++) {
-        const uint32_t te = kEmitStage / (L + 1);
-        for (uint32_t i = 0; bk[L].n && i < (bk[L].n + te - 1) / te; i++) emit_tiles.push_back(TileDesc{L, i});
+    uint32_t pfx[257], nt = 0;   // tiles of bucket L: [pfx[L], pfx[L+1]); the kernel maps its block to (L, tile)
+    for (uint32_t L = 0; L < 256; L++) {
+        pfx[L] = nt;
+        if (L >= lmin && L <= lmax && bk[L].n) nt += (bk[L].n + kEmitStage / (L + 1) - 1) / (kEmitStage / (L + 1));
     }
-    if (emit_tiles.empty()) return WSORT_OK;
+    pfx[256] = nt;
+    if (!nt) return WSORT_OK;
     int rc;
-    if ((rc = upload_small(c, c->d_tiles, emit_tiles.data(), emit_tiles.size() * sizeof(TileDesc), "emit tiles")))
-        return rc;
+    if ((rc = arena_upload(c, c->d_tiles, pfx, sizeof pfx, "emit tile prefix"))) return rc;
     EmitArgs ea{};
     ea.buckets = d_bk;
-    ea.tiles = static_cast<const TileDesc *>(c->d_tiles.p);
-    ea.ntiles = (uint32_t)emit_tiles.size();
+    ea.tile_pfx = static_cast<const uint32_t *>(c->d_tiles.p);
+    ea.ntiles = nt;
     ea.keys_a = static_cast<uint32_t *>(c->keys_a.p);
     ea.keys_b = static_cast<uint32_t *>(c->keys_b.p);
     ea.words = static_cast<uint8_t *>(c->words.p);
@@ -994,7 +1062,7 @@ std::vector<BucketInfo> msd_buckets(const Summary &s, uint32_t lkey, uint32_t &m
 // buckets of at most one CTA tile go straight to the finishing jobs. Ends with the keys emitted.
 template <class Pack>
 int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint32_t max_tw, uint32_t levels,
-                  uint64_t key_words, uint64_t W, bool finish_radix, Pack pack) {
+                  uint64_t key_words, uint64_t W, bool finish_radix, Pack pack, const BucketInfo *d_bk_pre = nullptr) {
     const Summary &s = *c->h_sum;
     const uint32_t lmax = s.max_len;
     int rc;
@@ -1015,16 +1083,17 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
             for (uint32_t o = 0; o < b.n; o += b.aux) tiles.push_back(MsdTile{q, o, std::min(b.aux, b.n - o), 0});
         }
     }
-    std::vector<uint8_t> plan;
-    append(plan, bk);
-    if ((rc = upload_plan(c, plan))) return rc;
-    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
-    if ((rc = upload_small(c, c->m_big[0], segs.data(), segs.size() * sizeof(MsdSeg), "segs0"))) return rc;
-    if ((rc = upload_small(c, c->m_tiles[0], tiles.data(), tiles.size() * sizeof(MsdTile), "tiles0"))) return rc;
-    if ((rc = upload_small(c, c->m_tiny, tiny.data(), tiny.size() * sizeof(MsdSeg), "tiny0"))) return rc;
-    if ((rc = upload_small(c, c->m_small, small.data(), small.size() * sizeof(MsdSeg), "small0"))) return rc;
+    const BucketInfo *d_bk = d_bk_pre;
+    if (!d_bk) {
+        if ((rc = arena_upload(c, c->plan, bk.data(), bk.size() * sizeof(BucketInfo), "plan"))) return rc;
+        d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
+    }
+    if ((rc = arena_upload(c, c->m_big[0], segs.data(), segs.size() * sizeof(MsdSeg), "segs0"))) return rc;
+    if ((rc = arena_upload(c, c->m_tiles[0], tiles.data(), tiles.size() * sizeof(MsdTile), "tiles0"))) return rc;
+    if ((rc = arena_upload(c, c->m_tiny, tiny.data(), tiny.size() * sizeof(MsdSeg), "tiny0"))) return rc;
+    if ((rc = arena_upload(c, c->m_small, small.data(), small.size() * sizeof(MsdSeg), "small0"))) return rc;
     uint32_t ctr0[kQCount] = {0, 0, (uint32_t)tiny.size(), (uint32_t)small.size(), 0, 0, 0, 0};
-    if ((rc = upload_small(c, c->m_ctr, ctr0, sizeof ctr0, "counters"))) return rc;
+    if ((rc = arena_upload(c, c->m_ctr, ctr0, sizeof ctr0, "counters"))) return rc;
     memcpy(c->h_ctr, ctr0, sizeof ctr0);   // if no level runs, these are the finishing counters
     const double key_bytes = (double)key_words * 4;
     if ((rc = pack(d_bk, key_bytes))) return rc;
@@ -1065,13 +1134,62 @@ int sort_dense_msd(wsort_ctx *c) {
     const uint64_t W = s.n_words, n_dense = s.off[kDenseMaxLen + 1];
     int rc;
     if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    if ((rc = arena_upload(c, c->plan, bk.data(), bk.size() * sizeof(BucketInfo), "plan"))) return rc;
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
+    if (n_dense) {   // dense buckets (scan + compact + emit) on the second stream, beside the MSD
+        uint32_t dpfx[257], ndt = 0;   // dense emit tiles, bucket by bucket (tile_from_prefix)
+        const uint32_t te = dense_emit_tile_words();
+        for (uint32_t L = 0; L < 256; L++) {
+            dpfx[L] = ndt;
+            if (L >= 1 && L <= std::min<uint32_t>(lmax, kDenseMaxLen)) ndt += (bk[L].n + te - 1) / te;
+        }
+        dpfx[256] = ndt;
+        const uint32_t ne = dense_entries(), nblk = dense_scan_blocks(ne);
+        if ((rc = ensure(c, c->d_blk_sum, (size_t)nblk * 4, "dense block sums"))) return rc;
+        if ((rc = ensure(c, c->d_blk_nnz, (size_t)nblk * 4, "dense block nnz"))) return rc;
+        if ((rc = ensure(c, c->d_ent_idx, (size_t)ne * 4, "dense entries"))) return rc;
+        if ((rc = ensure(c, c->d_ent_end, (size_t)ne * 4, "dense entry ends"))) return rc;
+        if ((rc = ensure(c, c->d_n_ent, 16, "dense entry count"))) return rc;
+        if ((rc = arena_upload(c, c->d_tiles2, dpfx, sizeof dpfx, "dense tile prefix"))) return rc;
+        static const bool no_aux = getenv("WSORT_NO_AUX") != nullptr;   // (experiments: serial dense branch)
+        if (!c->aux) {
+            if (no_aux) c->aux = c->stream;
+            else CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking), "aux stream");
+            CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
+            CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
+        }
+        CK(cudaEventRecord(c->ev_fork, c->stream), "fork");
+        CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0), "fork wait");
+        DenseArgs da{};
+        da.dense = static_cast<const uint32_t *>(c->dense.p);
+        da.n_entries = ne;
+        da.blk_sum = static_cast<uint32_t *>(c->d_blk_sum.p);
+        da.blk_nnz = static_cast<uint32_t *>(c->d_blk_nnz.p);
+        da.ent_idx = static_cast<uint32_t *>(c->d_ent_idx.p);
+        da.ent_end = static_cast<uint32_t *>(c->d_ent_end.p);
+        da.n_ent = static_cast<uint32_t *>(c->d_n_ent.p);
+        rc = launch_on(c, c->aux, "k2d_dense_scan", 2.0 * ne * 4, [&] { return launch_dense_scan(da, c->aux); });
+        if (rc) return rc;
+        DenseEmitArgs ea{};
+        ea.buckets = d_bk;
+        ea.tile_pfx = static_cast<const uint32_t *>(c->d_tiles2.p);
+        ea.ntiles = ndt;
+        ea.ent_idx = da.ent_idx;
+        ea.ent_end = da.ent_end;
+        ea.n_ent = da.n_ent;
+        ea.words = static_cast<uint8_t *>(c->words.p);
+        rc = launch_on(c, c->aux, "k5d_emit_dense", (double)s.byte_off[kDenseMaxLen + 1],
+                       [&] { return launch_emit_dense(ea, c->aux); });
+        if (rc) return rc;
+        CK(cudaEventRecord(c->ev_join, c->aux), "join");
+    }
     if (W > n_dense) {
         if ((rc = ensure(c, c->d_lcursor, 256 * 4, "length cursors"))) return rc;
         CK(cudaMemsetAsync(c->d_lcursor.p, 0, 256 * 4, c->stream), "memset length cursors");
         rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, W - n_dense, false,
-                           [&](const BucketInfo *d_bk, double key_bytes) {
+                           [&](const BucketInfo *db, double key_bytes) {
                                L0Args la{};
-                               la.buckets = d_bk;
+                               la.buckets = db;
                                la.pool = static_cast<const uint32_t *>(c->pool.p);
                                la.chunk_cls = static_cast<const uint32_t *>(c->chunk_cls.p);
                                la.chunk_fill = static_cast<const uint32_t *>(c->chunk_fill.p);
@@ -1081,46 +1199,14 @@ int sort_dense_msd(wsort_ctx *c) {
                                la.used_chunks = std::min(c->h_ig[kIgMaxChunks], c->cta_chunks);
                                return launch(c, "k3c_chunk_scatter", 2 * key_bytes,
                                              [&] { return launch_lscatter(la, c->tk.grid, c->stream); });
-                           });
-        if (rc) return rc;
-    } else {
-        std::vector<uint8_t> plan;
-        append(plan, bk);
-        if ((rc = upload_plan(c, plan))) return rc;
+                           },
+                           d_bk);
     }
-    if (!n_dense) return WSORT_OK;
-    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
-    std::vector<TileDesc> dtiles;
-    const uint32_t te = dense_emit_tile_words();
-    for (uint32_t L = 1; L <= std::min<uint32_t>(lmax, kDenseMaxLen); L++)
-        for (uint32_t i = 0; bk[L].n && i < (bk[L].n + te - 1) / te; i++) dtiles.push_back(TileDesc{L, i});
-    const uint32_t ne = dense_entries(), nblk = dense_scan_blocks(ne);
-    if ((rc = ensure(c, c->d_blk_sum, (size_t)nblk * 4, "dense block sums"))) return rc;
-    if ((rc = ensure(c, c->d_blk_nnz, (size_t)nblk * 4, "dense block nnz"))) return rc;
-    if ((rc = ensure(c, c->d_ent_idx, (size_t)ne * 4, "dense entries"))) return rc;
-    if ((rc = ensure(c, c->d_ent_end, (size_t)ne * 4, "dense entry ends"))) return rc;
-    if ((rc = ensure(c, c->d_n_ent, 16, "dense entry count"))) return rc;
-    DenseArgs da{};
-    da.dense = static_cast<const uint32_t *>(c->dense.p);
-    da.n_entries = ne;
-    da.blk_sum = static_cast<uint32_t *>(c->d_blk_sum.p);
-    da.blk_nnz = static_cast<uint32_t *>(c->d_blk_nnz.p);
-    da.ent_idx = static_cast<uint32_t *>(c->d_ent_idx.p);
-    da.ent_end = static_cast<uint32_t *>(c->d_ent_end.p);
-    da.n_ent = static_cast<uint32_t *>(c->d_n_ent.p);
-    rc = launch(c, "k2d_dense_scan", 2.0 * ne * 4, [&] { return launch_dense_scan(da, c->stream); });
-    if (rc) return rc;
-    if ((rc = upload_small(c, c->d_tiles2, dtiles.data(), dtiles.size() * sizeof(TileDesc), "dense tiles"))) return rc;
-    DenseEmitArgs ea{};
-    ea.buckets = d_bk;
-    ea.tiles = static_cast<const TileDesc *>(c->d_tiles2.p);
-    ea.ntiles = (uint32_t)dtiles.size();
-    ea.ent_idx = da.ent_idx;
-    ea.ent_end = da.ent_end;
-    ea.n_ent = da.n_ent;
-    ea.words = static_cast<uint8_t *>(c->words.p);
-    return launch(c, "k5d_emit_dense", (double)s.byte_off[kDenseMaxLen + 1],
-                  [&] { return launch_emit_dense(ea, c->stream); });
+    if (n_dense) {   // join: the sort is complete when both streams are
+        const cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+        if (!rc && e != cudaSuccess) return cuda_err(c, e, "join wait");
+    }
+    return rc;
 }
 
 }  // namespace
@@ -1140,7 +1226,8 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
         return set_err(c, WSORT_E_INVALID_ARG, "src_off is not available for packed / exchanged keys");
     cudaSetDevice(c->device);
     const bool want_src = (flags & WSORT_FLAG_SRC_OFF) != 0;
-    int rc;
+    int rc = arena_begin(c);
+    if (rc) return rc;
     // the dense + MSD path reads what K1 ingest left (dense counts, staged keys): a text this context
     // tokenized, keys only, every word staged (<= 48 letters)
     const bool ingest_ok = !want_src && !c->packed_pending && !c->keys_external && c->h_ig[kIgVeryLong] == 0;
@@ -1156,6 +1243,7 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
         rc = sort_radix(c, want_src);
     }
     c->packed_pending = false;
+    if (!rc) rc = arena_end(c);
     if (rc) {
         c->state = c->keys_external ? ST_CREATED : ST_TOKENIZED;
         return rc;

@@ -60,6 +60,18 @@ struct TileDesc {
     uint32_t tile;                 // tile index within the bucket
 };
 
+// Tile b of a launch whose tiles are enumerated bucket by bucket: pfx[L] = first tile of bucket L
+// (pfx[256] = all tiles). Lets a kernel find its (bucket, tile) without a host-built tile array.
+__device__ __forceinline__ TileDesc tile_from_prefix(const uint32_t *pfx, uint32_t b) {
+    uint32_t lo = 0, hi = 255;   // largest L with pfx[L] <= b
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(pfx + mid) <= b) lo = mid;
+        else hi = mid - 1;
+    }
+    return TileDesc{lo, b - __ldg(pfx + lo)};
+}
+
 // ---------------- launchers (defined in the .cu files) ----------------
 struct TkArgs {
     const uint8_t *text;           // device copy, text[-kTextFrontPad..-1] = 0, zero tail padding
@@ -125,7 +137,7 @@ cudaError_t launch_dense_scan(const DenseArgs &a, cudaStream_t s);
 
 struct DenseEmitArgs {
     const BucketInfo *buckets;
-    const TileDesc *tiles;
+    const uint32_t *tile_pfx;      // [257] first tile of each dense bucket (tile_from_prefix)
     uint32_t ntiles;
     const uint32_t *ent_idx, *ent_end, *n_ent;
     uint8_t *words;
@@ -242,7 +254,7 @@ struct MsdSeg {
 struct MsdTile {
     uint32_t seg, off, n, pad_;    // keys [off, off+n) of segment `seg` of this level
 };
-enum { kQBig = 0, kQTiles = 1, kQTiny = 2, kQSmall = 3, kQCopy = 4, kQCount = 8 };
+enum { kQBig = 0, kQTiles = 1, kQTiny = 2, kQSmall = 3, kQCopy = 4, kQFinTicket = 5, kQCount = 8 };
 constexpr uint32_t kMsdCopyChunk = 65536;   // u32 words per copy job
 struct MsdArgs {
     const BucketInfo *buckets;
@@ -272,11 +284,13 @@ cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s);
 cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
 cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_copy, uint32_t max_tile_words,
                               cudaStream_t s);   // tiny jobs, radix-finish jobs, copies (after the last level)
-cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t count, cudaStream_t s);   // per level
+// per level: jobs [first, *ctr[kQSmall]) by `grid` persistent CTAs
+cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t grid, cudaStream_t s);
 
 struct EmitArgs {
     const BucketInfo *buckets;
-    const TileDesc *tiles;
+    const TileDesc *tiles;         // tile list, or (if tile_pfx) none: tiles enumerated bucket by bucket
+    const uint32_t *tile_pfx;      // [257] first tile of each bucket (nullable)
     uint32_t ntiles;
     const uint32_t *keys_a;
     const uint32_t *keys_b;
