@@ -134,8 +134,9 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
         for (uint32_t k = 0; k < nzt; k++) {
             const uint32_t start = nz_d[k], cnt = (k + 1 < nzt ? nz_d[k + 1] : seg_end) - start;
             const bool fin = final_digit || cnt == 1;
-            const bool stream = a.stream_fin;   // any child size: k_msd_fin counts it
-            const bool big = !fin && cnt > cap && !stream, skip = fin && !a.dst_is_a, copy = fin && a.dst_is_a && cnt > cap;
+            const bool stream = a.stream_fin;   // every child is a finishing job of k_msd_fin (it writes the text)
+            const bool big = !fin && cnt > cap && !stream, skip = fin && !a.dst_is_a && !stream,
+                       copy = fin && a.dst_is_a && cnt > cap && !stream;
             if (big || skip || copy) {
                 if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
                 jn = 0;
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
         }
         if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
         uint32_t ntiny = 0, nbig = 0, nch = 0;
-        for (uint32_t k = 0; k < nj; k++) ntiny += jobs[k].n <= 32;
+        for (uint32_t k = 0; k < nj; k++) ntiny += jobs[k].n <= 32 && !a.stream_fin;
         for (uint32_t k = 0; k < ntop; k++) {
             const MsdSeg &x = jobs[kPlanMax - 1 - k];
             if (x.buf == 1u) nbig++;
@@ -196,9 +197,9 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
     // sort jobs, order-preserving split into tiny / small (each thread recounts its prefix)
     for (uint32_t k = t; k < nj; k += kST) {
         uint32_t before_tiny = 0;
-        for (uint32_t i = 0; i < k; i++) before_tiny += jobs[i].n <= 32;
+        for (uint32_t i = 0; i < k; i++) before_tiny += jobs[i].n <= 32 && !a.stream_fin;
         const MsdSeg x = jobs[k];
-        if (x.n <= 32) {
+        if (x.n <= 32 && !a.stream_fin) {
             const uint32_t q = s_q[0] + before_tiny;
             if (q < a.cap_local) a.q_tiny[q] = x;
         } else {
@@ -694,6 +695,62 @@ __device__ __forceinline__ T *block_sort_smem(T *A, T *B, uint32_t n) {
     return A;
 }
 
+// K5 fused into the finish (streaming mode): write the text of a finished job — word i of the job
+// (bucket L, first word `start`) is `word_of(i)`'s letters + '\n' at byte_off[L] + (start + i)(L + 1)
+// (reading A12). Pieces of kFinStage bytes are built in shared memory at the destination's 16-byte
+// phase and stored with aligned 16-byte stores.
+constexpr uint32_t kFinStage = 8192;   // text bytes staged per piece (+32: the 16-byte phase)
+template <int KW, class WordOf>
+__device__ __forceinline__ void emit_job_text(const MsdArgs &a, const BucketInfo &b, uint32_t L, uint32_t start, uint32_t n,
+                                              uint8_t *stage, WordOf word_of) {
+    const uint32_t t = threadIdx.x;
+    const uint32_t te = kFinStage / (L + 1);
+    for (uint32_t w0 = 0; w0 < n; w0 += te) {
+        const uint32_t nk = min(te, n - w0);
+        const uint64_t ob = b.byte_off + (uint64_t)(start + w0) * (L + 1);
+        const uint32_t head = (uint32_t)(ob & 15u);
+        for (uint32_t k = t; k < nk; k += kST) {
+            uint32_t key[KW];
+            word_of(w0 + k, key);
+            uint8_t *o = stage + head + k * (L + 1);
+#pragma unroll
+            for (int q = 0; q < KW; q++) {
+#pragma unroll
+                for (int j = 0; j < 6; j++) {
+                    const uint32_t li = q * 6 + j;
+                    if (li < L) o[li] = (uint8_t)(((key[q] >> (25 - 5 * j)) & 31u) | 0x60u);
+                }
+            }
+            o[L] = '\n';
+        }
+        __syncthreads();
+        const uint64_t end = ob + (uint64_t)nk * (L + 1);
+        const uint64_t a0 = (ob + 15) & ~15ull, a1 = end & ~15ull;
+        if (a0 >= a1) {
+            for (uint64_t x = ob + t; x < end; x += kST) a.words[x] = stage[head + (x - ob)];
+        } else {
+            for (uint64_t x = ob + t; x < a0; x += kST) a.words[x] = stage[head + (x - ob)];
+            for (uint64_t x = a1 + t; x < end; x += kST) a.words[x] = stage[head + (x - ob)];
+            const uint64_t base16 = ob & ~15ull;
+            uint4 *dst = reinterpret_cast<uint4 *>(a.words);
+            for (uint64_t x = a0 + 16ull * t; x < a1; x += 16ull * kST)
+                dst[x >> 4] = *reinterpret_cast<const uint4 *>(stage + (x - base16));
+        }
+        __syncthreads();
+    }
+}
+
+// index of the run holding output word j: first i with ends[i] > j
+__device__ __forceinline__ uint32_t run_of(const uint32_t *ends, uint32_t nd, uint32_t j) {
+    uint32_t lo = 0, hi = nd - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (ends[mid] > j) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
 // Finishing job of 1- or 2-word keys of any size (a whole MSD child): the keys are streamed from
 // global memory into a shared-memory table whose key is the key itself (u32 / u64: exact), the
 // distinct keys sorted (block_sort_smem), and each written as often as it occurs. More than
@@ -762,8 +819,15 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
             T *FA = reinterpret_cast<T *>(smraw), *FB = FA + fpad(kST * 8);
             for (uint32_t i = t; i < kST * 8; i += kST) FA[fpad(i)] = i < n ? fin_load<T, KW>(src + (size_t)i * KW) : kEmpty;
             T *S = block_sort_smem<T>(FA, FB, n);
-            uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
-            for (uint32_t i = t; i < n; i += kST) fin_store<T, KW>(dst + (size_t)i * KW, S[fpad(i)]);
+            uint8_t *stage = reinterpret_cast<uint8_t *>(S == FA ? FB : FA);   // (>= kFinStage + 32 bytes)
+            emit_job_text<KW>(a, b, sg.L, sg.start, n, stage, [&](uint32_t i, uint32_t (&k)[KW]) {
+                const T v = S[fpad(i)];
+                if constexpr (KW == 1) k[0] = (uint32_t)v;
+                else {
+                    k[0] = (uint32_t)((uint64_t)v >> 32);
+                    k[1] = (uint32_t)v;
+                }
+            });
         } else if (t == 0) {   // one child larger than a tile: back to the MSD as a segment of the next
                                // level (a child without digits left holds one key only: this terminates)
             const uint32_t nt = (n + b.aux - 1) / b.aux;
@@ -805,16 +869,15 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
         if (4 * t + e < nd) pos[4 * t + e] = run;   // end (exclusive) of the run of distinct key 4t+e
     }
     __syncthreads();
-    uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
-    for (uint32_t j = t; j < n; j += kST) {
-        uint32_t lo = 0, hi = nd - 1;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (pos[mid] > j) hi = mid;
-            else lo = mid + 1;
+    // the table is no longer needed: its space stages the text
+    emit_job_text<KW>(a, b, sg.L, sg.start, n, reinterpret_cast<uint8_t *>(slots), [&](uint32_t i, uint32_t (&k)[KW]) {
+        const T v = S[fpad(run_of(pos, nd, i))];
+        if constexpr (KW == 1) k[0] = (uint32_t)v;
+        else {
+            k[0] = (uint32_t)((uint64_t)v >> 32);
+            k[1] = (uint32_t)v;
         }
-        fin_store<T, KW>(dst + (size_t)j * KW, S[fpad(lo)]);
-    }
+    });
 }
 
 // Finishing job of KW >= 3-word keys of any size: as fin_stream, but the table key is a 64-bit
@@ -902,6 +965,12 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
         if (n <= b.tile_keys) {   // (possibly several children): sort the job in full
             __syncthreads();
             cta_sort_job<KW, (KW <= 4 ? 4 : 2)>(a, sg, b, reinterpret_cast<uint32_t *>(smraw));
+            __syncthreads();   // the sorted keys are in buffer B (written by this CTA)
+            const uint32_t *kb = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
+            emit_job_text<KW>(a, b, sg.L, sg.start, n, smraw, [&](uint32_t i, uint32_t (&k)[KW]) {
+#pragma unroll
+                for (int u = 0; u < KW; u++) k[u] = kb[(size_t)i * KW + u];
+            });
         } else if (t == 0) {   // one child larger than a tile: back to the MSD as a segment of the next
                                // level (a child without digits left holds one key only: this terminates)
             const uint32_t nt = (n + b.aux - 1) / b.aux;
@@ -936,17 +1005,12 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     const uint32_t end = block_excl_scan_m(c, misc + 2, nullptr) + c;
     if (t < nd) pos[t] = end;
     __syncthreads();
-    uint32_t *dst = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
-    for (uint32_t j = t; j < n * KW; j += kST) {
-        const uint32_t kk = j / KW;
-        uint32_t lo = 0, hi = nd - 1;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (pos[mid] > kk) hi = mid;
-            else lo = mid + 1;
-        }
-        dst[j] = rep[order[lo] * KW + (j - kk * KW)];
-    }
+    // the fingerprint table is no longer needed: its space (16 KiB) stages the text
+    emit_job_text<KW>(a, b, sg.L, sg.start, n, smraw, [&](uint32_t i, uint32_t (&k)[KW]) {
+        const uint32_t id = order[run_of(pos, nd, i)];
+#pragma unroll
+        for (int u = 0; u < KW; u++) k[u] = rep[id * KW + u];
+    });
 }
 
 // Persistent: jobs [small_base, ctr[kQSmall]) — the end is read on the device (this level's plan

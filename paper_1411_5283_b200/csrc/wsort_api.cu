@@ -1076,7 +1076,7 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
         const BucketInfo &b = bk[L];
         if (!b.n) continue;
         if (b.n <= b.tile_keys) {
-            (b.n <= 32 ? tiny : small).push_back(MsdSeg{L, 0, b.n, 1});
+            (b.n <= 32 && finish_radix ? tiny : small).push_back(MsdSeg{L, 0, b.n, 1});
         } else {
             const uint32_t q = (uint32_t)segs.size();
             segs.push_back(MsdSeg{L, 0, b.n, 0});
@@ -1099,8 +1099,10 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
     if ((rc = pack(d_bk, key_bytes))) return rc;
     m.buckets = d_bk;
     m.finish_radix = finish_radix ? 1u : 0u;
+    m.words = static_cast<uint8_t *>(c->words.p);
     if ((rc = msd_levels_and_finish(c, m, 0, (uint32_t)segs.size(), (uint32_t)tiles.size(), levels, key_bytes, max_tw)))
         return rc;
+    if (!finish_radix) return WSORT_OK;   // the streaming finish wrote the text (K5 fused)
     return emit_keys(c, bk, d_bk, lkey, lmax, key_bytes + (double)(s.byte_off[256] - s.byte_off[lkey]));
 }
 

@@ -275,7 +275,8 @@ struct MsdArgs {
     uint32_t *keys_b;              // finishing: buffer B (final)
     uint32_t n_tiny;
     uint32_t finish_radix;         // 1: small jobs with kw <= 4 by local LSD radix, else odd-even transposition
-    uint32_t stream_fin;           // 1: children of kw <= 2 buckets of any size become finishing jobs (k_msd_fin)
+    uint32_t stream_fin;           // 1: every child is a finishing job of k_msd_fin, which writes the text
+    uint8_t *words;                // (stream_fin) output text
     uint32_t small_base;           // k_msd_fin: first job of this launch in q_small
 };
 size_t msd_scatter_smem();
