@@ -19,7 +19,10 @@
 //   levels of k_msd.cu sort the buckets from there.
 // K5d k_emit_dense: "prints the results" for L <= 5: word w of the dense buckets is
 //   the entry whose count range holds w; written as "word\n" (reading A12).
+#include <algorithm>
+
 #include "k_text.cuh"
+#include "k_tma.cuh"
 #include "wsort_internal.cuh"
 
 namespace wsort {
@@ -568,7 +571,7 @@ __device__ __forceinline__ uint32_t key_len(uint32_t last, uint32_t K) {
 }
 
 template <int K>
-__device__ __forceinline__ void lscatter_chunk(const L0Args &a, uint32_t c, uint32_t n, uint32_t *sm) {
+__device__ __forceinline__ void lscatter_chunk(const L0Args &a, const uint32_t *src, uint32_t n, uint32_t *sm) {
     constexpr int KPT = (16 + K - 1) / K;   // 4096 / K keys per chunk, 256 threads
     const uint32_t t = threadIdx.x;
     uint32_t *cnt = sm, *lbase = sm + 8, *gbase = sm + 16;
@@ -578,20 +581,13 @@ __device__ __forceinline__ void lscatter_chunk(const L0Args &a, uint32_t c, uint
     if (t < 8) cnt[t] = 0;
     if (t < 6) koff[t] = a.buckets[6 * K - 5 + t].key_off;
     __syncthreads();
-    const uint32_t *src = a.pool + (size_t)c * kChunkWords;
-    uint32_t key[KPT][K], ll[KPT], slot[KPT];
-#pragma unroll
-    for (int r = 0; r < KPT; r++) {
-        const uint32_t i = t + r * 256;
-#pragma unroll
-        for (int u = 0; u < K; u++) key[r][u] = i < n ? __ldg(src + i * K + u) : 0u;
-    }
+    uint32_t ls[KPT];   // length offset (3 bits) | slot within the length (<< 3); keys stay in shared memory
 #pragma unroll
     for (int r = 0; r < KPT; r++) {
         const uint32_t i = t + r * 256;
         if (i < n) {
-            ll[r] = key_len(key[r][K - 1], K) - (6u * K - 5u);
-            slot[r] = atomicAdd(&cnt[ll[r]], 1u);
+            const uint32_t l = key_len(src[i * K + K - 1], K) - (6u * K - 5u);
+            ls[r] = l | (atomicAdd(&cnt[l], 1u) << 3);
         }
     }
     __syncthreads();
@@ -607,13 +603,13 @@ __device__ __forceinline__ void lscatter_chunk(const L0Args &a, uint32_t c, uint
     for (int r = 0; r < KPT; r++) {
         const uint32_t i = t + r * 256;
         if (i < n) {
-            const uint32_t p = lbase[ll[r]] + slot[r];
+            const uint32_t l = ls[r] & 7u, p = lbase[l] + (ls[r] >> 3);
 #pragma unroll
             for (int u = 0; u < K; u++) {
                 const uint32_t w = p * K + u;
-                kout[w + (w >> 5)] = key[r][u];
+                kout[w + (w >> 5)] = src[i * K + u];
             }
-            lof[p] = (uint8_t)ll[r];
+            lof[p] = (uint8_t)l;
         }
     }
     if (t < 6) gbase[t] = g;
@@ -625,24 +621,63 @@ __device__ __forceinline__ void lscatter_chunk(const L0Args &a, uint32_t c, uint
     }
 }
 
-__global__ void __launch_bounds__(256) k_lscatter(L0Args a) {
-    extern __shared__ __align__(16) uint32_t l0_smem[];
-    const uint32_t c = (blockIdx.x / a.used_chunks) * a.cta_chunks + blockIdx.x % a.used_chunks;
-    const uint32_t n = a.chunk_fill[c];
-    if (n == 0) return;
-    switch (a.chunk_cls[c]) {
-        case 1: lscatter_chunk<1>(a, c, n, l0_smem); break;
-        case 2: lscatter_chunk<2>(a, c, n, l0_smem); break;
-        case 3: lscatter_chunk<3>(a, c, n, l0_smem); break;
-        case 4: lscatter_chunk<4>(a, c, n, l0_smem); break;
-        case 5: lscatter_chunk<5>(a, c, n, l0_smem); break;
-        case 6: lscatter_chunk<6>(a, c, n, l0_smem); break;
-        case 7: lscatter_chunk<7>(a, c, n, l0_smem); break;
-        default: lscatter_chunk<8>(a, c, n, l0_smem); break;
+// Persistent: CTA b takes chunks b, b + grid, ... (skipping empty ones); the next chunk is fetched by
+// a TMA bulk copy into the other shared-memory buffer while this one is scattered.
+constexpr int kLsCtasPerSm = 3;
+constexpr uint32_t kLsWork = (40 + kChunkWords + kChunkWords / 32 + 4) * 4 + kChunkWords;
+__global__ void __launch_bounds__(256, kLsCtasPerSm) k_lscatter(L0Args a) {
+    extern __shared__ __align__(128) uint8_t ls_raw[];
+    uint32_t *inb = reinterpret_cast<uint32_t *>(ls_raw);                       // [2][kChunkWords]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(ls_raw + 2 * kChunkWords * 4);  // [2]
+    uint32_t *sj = reinterpret_cast<uint32_t *>(bar + 2);                        // [2] chunk, [2] keys, [2] class
+    uint32_t *work = sj + 8;
+    const uint32_t t = threadIdx.x;
+    const uint32_t total = a.nctas * a.used_chunks;
+    auto chunk_id = [&](uint32_t j) { return (j / a.used_chunks) * a.cta_chunks + j % a.used_chunks; };
+    // thread 0: the first non-empty chunk at or after j (stride grid) -> buffer b
+    auto fetch = [&](uint32_t j, uint32_t b) {
+        uint32_t n = 0;
+        while (j < total && (n = a.chunk_fill[chunk_id(j)]) == 0) j += gridDim.x;
+        sj[b] = j;
+        if (j < total) {
+            const uint32_t c = chunk_id(j), K = a.chunk_cls[c];
+            sj[2 + b] = n;
+            sj[4 + b] = K;
+            const uint32_t bytes = (n * K * 4 + 15) & ~15u;
+            tma::mbar_expect_tx(&bar[b], bytes);
+            tma::bulk_g2s(inb + b * kChunkWords, a.pool + (size_t)c * kChunkWords, bytes, &bar[b]);
+        }
+    };
+    if (t == 0) {
+        tma::mbar_init(&bar[0], 1);
+        tma::mbar_init(&bar[1], 1);
+        tma::fence_mbar_init();
+        fetch(blockIdx.x, 0);
+    }
+    __syncthreads();
+    for (uint32_t it = 0;; it++) {
+        const uint32_t cur = it & 1;
+        const uint32_t j = sj[cur];
+        if (j >= total) break;
+        const uint32_t n = sj[2 + cur], K = sj[4 + cur];
+        if (t == 0) fetch(j + gridDim.x, cur ^ 1);   // (buffer cur^1 was released at the last barrier)
+        tma::mbar_wait(&bar[cur], (it >> 1) & 1);
+        const uint32_t *src = inb + cur * kChunkWords;
+        switch (K) {
+            case 1: lscatter_chunk<1>(a, src, n, work); break;
+            case 2: lscatter_chunk<2>(a, src, n, work); break;
+            case 3: lscatter_chunk<3>(a, src, n, work); break;
+            case 4: lscatter_chunk<4>(a, src, n, work); break;
+            case 5: lscatter_chunk<5>(a, src, n, work); break;
+            case 6: lscatter_chunk<6>(a, src, n, work); break;
+            case 7: lscatter_chunk<7>(a, src, n, work); break;
+            default: lscatter_chunk<8>(a, src, n, work); break;
+        }
+        __syncthreads();
     }
 }
 
-constexpr size_t kLscatterSmem = (40 + kChunkWords + kChunkWords / 32 + 4) * 4 + kChunkWords;
+constexpr size_t kLscatterSmem = 2 * kChunkWords * 4 + 16 + 32 + kLsWork;
 
 }  // namespace
 
@@ -681,11 +716,16 @@ cudaError_t launch_emit_dense(const DenseEmitArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_lscatter(const L0Args &a, uint32_t nctas, cudaStream_t s) {
-    const uint32_t nchunks = nctas * a.used_chunks;
-    if (!nchunks) return cudaSuccess;
+    if (!nctas || !a.used_chunks) return cudaSuccess;
+    L0Args b = a;
+    b.nctas = nctas;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t grid = std::min<uint32_t>(nctas * a.used_chunks, (uint32_t)sms * kLsCtasPerSm);
     cudaError_t e = cudaFuncSetAttribute(k_lscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLscatterSmem);
     if (e != cudaSuccess) return e;
-    k_lscatter<<<nchunks, 256, kLscatterSmem, s>>>(a);
+    k_lscatter<<<grid, 256, kLscatterSmem, s>>>(b);
     return cudaGetLastError();
 }
 

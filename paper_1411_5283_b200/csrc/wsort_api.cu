@@ -996,9 +996,24 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         }
         if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;   // the level's one host sync
         if (!m.finish_radix) small_done = std::min(c->h_ctr[kQSmall], m.cap_local);
-        if (getenv("WSORT_DEBUG_MSD"))
+        if (getenv("WSORT_DEBUG_MSD")) {
             fprintf(stderr, "msd level %u -> next segs %u tiles %u | tiny %u small %u copy %u\n", level, nsegs, ntiles,
                     c->h_ctr[kQTiny], c->h_ctr[kQSmall], c->h_ctr[kQCopy]);
+            std::vector<MsdSeg> jobs(c->h_ctr[kQSmall]);
+            cudaMemcpy(jobs.data(), c->m_small.p, jobs.size() * sizeof(MsdSeg), cudaMemcpyDeviceToHost);
+            std::vector<uint32_t> sz;
+            uint64_t tot = 0;
+            for (auto &j : jobs) {
+                sz.push_back(j.n);
+                tot += j.n;
+            }
+            std::sort(sz.rbegin(), sz.rend());
+            fprintf(stderr, "  jobs so far %zu keys %llu; largest:", sz.size(), (unsigned long long)tot);
+            for (size_t i = 0; i < sz.size() && i < 12; i++) fprintf(stderr, " %u", sz[i]);
+            uint64_t big = 0;
+            for (auto x : sz) big += x > 65536 ? x : 0;
+            fprintf(stderr, " | keys in jobs > 64k: %llu\n", (unsigned long long)big);
+        }
     }
     m.n_tiny = c->h_ctr[kQTiny];
     const uint32_t n_small = c->h_ctr[kQSmall], n_copy = c->h_ctr[kQCopy];

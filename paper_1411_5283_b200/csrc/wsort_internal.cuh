@@ -152,6 +152,7 @@ struct L0Args {
     uint32_t *dst;                          // buffer A
     uint32_t cta_chunks;                    // chunks per CTA region of the pool
     uint32_t used_chunks;                   // max chunks any CTA used (its first ids)
+    uint32_t nctas;                         // K1 CTAs (regions)
 };
 cudaError_t launch_lscatter(const L0Args &a, uint32_t nctas, cudaStream_t s);
 
