@@ -751,6 +751,105 @@ __device__ __forceinline__ uint32_t run_of(const uint32_t *ends, uint32_t nd, ui
     return lo;
 }
 
+// Text of a job made of runs (the streaming finish): distinct word r (sorted) occupies output words
+// [ends[r-1], ends[r]). Its text `letters\n` is laid out repeated in R[r] (W bytes, W >= L+1+16), so
+// the 16 output bytes starting at phase f of the pattern are R[r][f .. f+16). Aligned 16-byte chunks
+// of the job's byte range are written straight to global memory (one warp takes a contiguous range of
+// chunks, so each lane's run index only moves forward); a chunk that crosses a run boundary, and the
+// unaligned head / tail bytes, are assembled byte by byte.
+__device__ __forceinline__ uint32_t div_by(uint32_t n, uint32_t d, uint32_t m) {   // n / d, m = 2^32/d + 1
+    uint32_t q = __umulhi(n, m);
+    if ((q + 1) * d <= n) q++;
+    if (q * d > n) q--;
+    return q;
+}
+__device__ __forceinline__ uint8_t run_byte(const uint8_t *R, uint32_t W, const uint32_t *ends, uint32_t nd, uint32_t L1,
+                                            uint32_t rel, uint32_t m) {
+    const uint32_t w = div_by(rel, L1, m);
+    const uint32_t r = run_of(ends, nd, w);
+    return R[r * W + (rel - w * L1)];
+}
+__device__ __forceinline__ void emit_runs_text(const MsdArgs &a, const BucketInfo &b, uint32_t L, uint32_t start, uint32_t n,
+                                               const uint8_t *R, uint32_t W, const uint32_t *ends, uint32_t nd) {
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t L1 = L + 1, m = (uint32_t)(0x100000000ull / L1) + 1u;
+    const uint64_t B0 = b.byte_off + (uint64_t)start * L1, B1 = B0 + (uint64_t)n * L1;
+    const uint64_t A0 = (B0 + 15) & ~15ull, A1 = B1 & ~15ull;
+    if (A0 >= A1) {
+        for (uint64_t x = B0 + t; x < B1; x += kST) a.words[x] = run_byte(R, W, ends, nd, L1, (uint32_t)(x - B0), m);
+        return;
+    }
+    if (t < A0 - B0) a.words[B0 + t] = run_byte(R, W, ends, nd, L1, t, m);
+    if (t < B1 - A1) a.words[A1 + t] = run_byte(R, W, ends, nd, L1, (uint32_t)(A1 - B0) + t, m);
+    const uint32_t nch = (uint32_t)((A1 - A0) >> 4);
+    const uint32_t per = (nch + (kST / 32) - 1) / (kST / 32);   // chunks per warp (contiguous)
+    const uint32_t c0 = warp * per, c1 = min(c0 + per, nch);
+    uint32_t r = 0;
+    bool first = true;
+    uint4 *dst = reinterpret_cast<uint4 *>(a.words + A0);
+    const uint32_t rel0 = (uint32_t)(A0 - B0);
+    for (uint32_t c = c0 + lane; c < c1; c += 32) {
+        const uint32_t rel = rel0 + 16 * c;
+        const uint32_t w = div_by(rel, L1, m), f = rel - w * L1;
+        if (first) {
+            r = run_of(ends, nd, w);
+            first = false;
+        } else {
+            while (ends[r] <= w) r++;
+        }
+        const uint32_t wl = div_by(rel + 15, L1, m);
+        uint32_t v[4];
+        if (wl < ends[r]) {   // inside one run: a window of its repeated pattern
+            const uint8_t *p = R + r * W + f;
+            const uint32_t al = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3u);
+            const uint32_t *p4 = reinterpret_cast<const uint32_t *>(p - al);
+            const uint32_t x0 = p4[0], x1 = p4[1], x2 = p4[2], x3 = p4[3], x4 = p4[4];
+            v[0] = __funnelshift_r(x0, x1, 8 * al);
+            v[1] = __funnelshift_r(x1, x2, 8 * al);
+            v[2] = __funnelshift_r(x2, x3, 8 * al);
+            v[3] = __funnelshift_r(x3, x4, 8 * al);
+        } else {   // crosses a run boundary: byte by byte
+            uint32_t rr = r, ww = w, ff = f;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    acc |= (uint32_t)R[rr * W + ff] << (8 * k);
+                    if (++ff == L1) {
+                        ff = 0;
+                        ww++;
+                        while (rr + 1 < nd && ends[rr] <= ww) rr++;
+                    }
+                }
+                v[q] = acc;
+            }
+        }
+        dst[c] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+// Lay out distinct word r's text repeated in R[r] (W bytes): pattern byte i = letter i (i < L) or '\n'.
+template <int KW, class KeyOf>
+__device__ __forceinline__ void build_run_patterns(uint8_t *R, uint32_t W, uint32_t L, uint32_t nd, KeyOf key_of) {
+    for (uint32_t r = threadIdx.x; r < nd; r += kST) {
+        uint32_t k[KW];
+        key_of(r, k);
+        uint8_t pat[6 * KW + 1];
+#pragma unroll
+        for (int q = 0; q < KW; q++)
+#pragma unroll
+            for (int j = 0; j < 6; j++) pat[q * 6 + j] = (uint8_t)(((k[q] >> (25 - 5 * j)) & 31u) | 0x60u);
+        pat[L] = '\n';
+        uint32_t f = 0;
+        for (uint32_t i = 0; i < W; i++) {
+            R[r * W + i] = pat[f];
+            f = f == L ? 0u : f + 1u;
+        }
+    }
+    __syncthreads();
+}
+
 // Finishing job of 1- or 2-word keys of any size (a whole MSD child): the keys are streamed from
 // global memory into a shared-memory table whose key is the key itself (u32 / u64: exact), the
 // distinct keys sorted (block_sort_smem), and each written as often as it occurs. More than
@@ -869,15 +968,23 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
         if (4 * t + e < nd) pos[4 * t + e] = run;   // end (exclusive) of the run of distinct key 4t+e
     }
     __syncthreads();
-    // the table is no longer needed: its space stages the text
-    emit_job_text<KW>(a, b, sg.L, sg.start, n, reinterpret_cast<uint8_t *>(slots), [&](uint32_t i, uint32_t (&k)[KW]) {
-        const T v = S[fpad(run_of(pos, nd, i))];
+    // the table is no longer needed: its space holds the runs' repeated patterns (or stages the text)
+    auto key_of = [&](uint32_t r, uint32_t (&k)[KW]) {
+        const T v = S[fpad(r)];
         if constexpr (KW == 1) k[0] = (uint32_t)v;
         else {
             k[0] = (uint32_t)((uint64_t)v >> 32);
             k[1] = (uint32_t)v;
         }
-    });
+    };
+    const uint32_t W = (sg.L + 1 + 16 + 3) & ~3u;
+    uint8_t *R = reinterpret_cast<uint8_t *>(slots);
+    if (nd * W + 4 <= kStreamSlots * (sizeof(T) + 4)) {
+        build_run_patterns<KW>(R, W, sg.L, nd, key_of);
+        emit_runs_text(a, b, sg.L, sg.start, n, R, W, pos, nd);
+    } else {
+        emit_job_text<KW>(a, b, sg.L, sg.start, n, R, [&](uint32_t i, uint32_t (&k)[KW]) { key_of(run_of(pos, nd, i), k); });
+    }
 }
 
 // Finishing job of KW >= 3-word keys of any size: as fin_stream, but the table key is a 64-bit
@@ -1005,12 +1112,20 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     const uint32_t end = block_excl_scan_m(c, misc + 2, nullptr) + c;
     if (t < nd) pos[t] = end;
     __syncthreads();
-    // the fingerprint table is no longer needed: its space (16 KiB) stages the text
-    emit_job_text<KW>(a, b, sg.L, sg.start, n, smraw, [&](uint32_t i, uint32_t (&k)[KW]) {
-        const uint32_t id = order[run_of(pos, nd, i)];
+    // the fingerprint table is no longer needed: its space (16 KiB) holds the runs' repeated patterns
+    // (or stages the text)
+    auto key_of = [&](uint32_t r, uint32_t (&k)[KW]) {
+        const uint32_t id = order[r];
 #pragma unroll
         for (int u = 0; u < KW; u++) k[u] = rep[id * KW + u];
-    });
+    };
+    const uint32_t W = (sg.L + 1 + 16 + 3) & ~3u;
+    if (nd * W + 4 <= kWideSlots * 16) {
+        build_run_patterns<KW>(smraw, W, sg.L, nd, key_of);
+        emit_runs_text(a, b, sg.L, sg.start, n, smraw, W, pos, nd);
+    } else {
+        emit_job_text<KW>(a, b, sg.L, sg.start, n, smraw, [&](uint32_t i, uint32_t (&k)[KW]) { key_of(run_of(pos, nd, i), k); });
+    }
 }
 
 // Persistent: jobs [small_base, ctr[kQSmall]) — the end is read on the device (this level's plan
