@@ -214,37 +214,35 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
         const uint32_t carry = lane < 31 ? l1 + (f1 ? qh : 0u) : qh;
         const uint32_t seg0 = 32u * lane;
         // categories from the masks: a word starting at bit i has L >= j iff bytes i..i+j-1 are letters
-        // (X = this lane's letters followed by the next lane's / the tail's)
-        uint32_t n345, nlong;
-        {
-            const uint32_t N = lane < 31 ? nm : mt0;
-            const uint64_t X = (uint64_t)M | ((uint64_t)N << 32);
-            const uint32_t ge3 = starts & (uint32_t)(X >> 1) & (uint32_t)(X >> 2);
-            const uint32_t ge6 = ge3 & (uint32_t)(X >> 3) & (uint32_t)(X >> 4) & (uint32_t)(X >> 5);
-            nlong = __popc(ge6);
-            n345 = __popc(ge3) - nlong;
-        }
+        // (X = this lane's letters followed by the next lane's / the tail's); one branch-free loop each
+        const uint64_t X = (uint64_t)M | ((uint64_t)(lane < 31 ? nm : mt0) << 32);
+        const uint32_t ge3 = starts & (uint32_t)(X >> 1) & (uint32_t)(X >> 2);
+        const uint32_t ge6 = ge3 & (uint32_t)(X >> 3) & (uint32_t)(X >> 4) & (uint32_t)(X >> 5);
+        const uint32_t s12 = starts & ~ge3, s345 = ge3 & ~ge6;
+        const uint32_t nlong = __popc(ge6), n345 = __popc(s345);
         const uint32_t cnt = n345 | (nlong << 16);
         const uint32_t ci = inclusive_scan_warp(cnt, lane);
         const uint32_t tot = __shfl_sync(kFull, ci, 31);
         uint32_t p3 = (ci - cnt) & 0xffffu, plg = (ci - cnt) >> 16;
         uint32_t *d12 = sm.d12;
-        for (uint32_t m = starts; m; m &= m - 1) {
+        for (uint32_t m = s12; m; m &= m - 1) {   // L = 1, 2: count now (shared-memory table)
+            const uint32_t bit = __ffs(m) - 1, s = seg0 + bit;
+            const uint32_t two = (uint32_t)(X >> (bit + 1)) & 1u;
+            const uint32_t lo = __funnelshift_r(wb32[s >> 2], wb32[(s >> 2) + 1], 8u * (s & 3u));
+            const uint32_t c0 = (lo & 31u) - 1u, c1 = ((lo >> 8) & 31u) - 1u;
+            if (!(a.debug & 1)) atomicAdd(&d12[two ? 26u + c0 * 26u + c1 : c0], 1u);
+        }
+        for (uint32_t m = s345; m; m &= m - 1) {   // L = 3..5: listed for the hash cache
+            const uint32_t bit = __ffs(m) - 1;
+            const uint32_t y = (uint32_t)(X >> (bit + 3));
+            wlst[p3++] = (uint16_t)((seg0 + bit) | (((y & 1u) + (y & (y >> 1) & 1u)) << 10));
+        }
+        for (uint32_t m = ge6; m; m &= m - 1) {   // L >= 6: listed for packing (above 48 kept as 49: not staged)
             const uint32_t bit = __ffs(m) - 1;
             const uint32_t em = ends & (0xffffffffu << bit);
             const uint32_t L = em ? (uint32_t)(__ffs(em) - 1) - bit + 1u : (32u - bit) + carry;
-            const uint32_t s = seg0 + bit;
-            if (L <= 2u) {   // L = 1, 2: count now (shared-memory table)
-                const uint32_t lo = __funnelshift_r(wb32[s >> 2], wb32[(s >> 2) + 1], 8u * (s & 3u));
-                const uint32_t c0 = (lo & 31u) - 1u, c1 = ((lo >> 8) & 31u) - 1u;
-                if (!(a.debug & 1)) atomicAdd(&d12[L == 1u ? c0 : 26u + c0 * 26u + c1], 1u);
-            } else {   // listed: L = 3..5 from the front, L >= 6 from the back (above 48 kept as 49: not staged)
-                const bool d = L <= kDenseMaxLen;
-                wlst[d ? p3 : kWList - 1 - plg] = (uint16_t)(s | ((d ? L - 3u : min(L, 49u) - 6u) << 10));
-                p3 += d;
-                plg += !d;
-                if (L > (uint32_t)kMaxLen) atomicAdd(&sm.hist[256], 1u);
-            }
+            wlst[kWList - 1 - plg++] = (uint16_t)((seg0 + bit) | ((min(L, 49u) - 6u) << 10));
+            if (L > (uint32_t)kMaxLen) atomicAdd(&sm.hist[256], 1u);
         }
         __syncwarp();
         const uint32_t n3 = tot & 0xffffu, nlg = tot >> 16;
