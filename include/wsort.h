@@ -143,6 +143,16 @@ typedef struct {
  * BUFFER_TOO_SMALL (sizes filled, nothing copied). src_off without WSORT_FLAG_SRC_OFF -> STATE. */
 int wsort_fetch(wsort_ctx *c, wsort_result *r);
 
+/* As wsort_fetch, but the copies of words/src_off are only enqueued on the context's stream: the
+ * caller's buffers hold the results once wsort_sync(c) returns (or the stream has been synchronised);
+ * they must stay valid until then. Sizes and bucket_off are filled in before it returns. Lets a caller
+ * overlap one text's device->host copy with the next text's host->device copy and sort (e.g. two
+ * contexts in a pipeline). Errors as wsort_fetch. */
+int wsort_fetch_async(wsort_ctx *c, wsort_result *r);
+
+/* Wait until all work enqueued by this context has completed. Errors: CUDA. */
+int wsort_sync(wsort_ctx *c);
+
 /* Device pointers of the context-owned results (valid until the next load/sort/destroy), for
  * zero-copy consumers. Any out pointer may be NULL. State: SORTED (words, src_off) or
  * TOKENIZED (bucket_off only). */

@@ -40,7 +40,7 @@ EXPORTS = [
     "wsort_sort", "wsort_fetch", "wsort_device_results", "wsort_last_error", "wsort_strerror",
     "wsort_destroy", "wsort_set_profiling", "wsort_kernel_stats", "wsort_reset_kernel_stats",
     "wsort_launch_count", "wsort_histogram", "wsort_pack", "wsort_sample", "wsort_select_splitters",
-    "wsort_partition", "wsort_load_keys", "wsort_set_global",
+    "wsort_partition", "wsort_load_keys", "wsort_set_global", "wsort_fetch_async", "wsort_sync",
 ]
 
 
@@ -91,6 +91,8 @@ def load():
     L.wsort_tokenize.argtypes = [P, ctypes.POINTER(U64)]
     L.wsort_sort.argtypes = [P, I, ctypes.c_uint]
     L.wsort_fetch.argtypes = [P, ctypes.POINTER(Result)]
+    L.wsort_fetch_async.argtypes = [P, ctypes.POINTER(Result)]
+    L.wsort_sync.argtypes = [P]
     L.wsort_device_results.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]
     L.wsort_last_error.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
     L.wsort_strerror.argtypes = [I]

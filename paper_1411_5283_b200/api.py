@@ -133,6 +133,21 @@ class WSort:
             return w, offl, src[: r.n_words]
         return w, offl
 
+    def fetch_async(self, out: np.ndarray):
+        """Enqueue the copy of the sorted words into `out` (pinned host or any host uint8 array of at least
+        words_len bytes); returns (words view, off). `out` holds the words after sync()."""
+        r = self.sizes()
+        off = np.zeros(r.max_len + 2, np.uint64)
+        r.words = out.ctypes.data
+        r.words_cap = out.size
+        r.bucket_off = off.ctypes.data
+        r.bucket_cap = off.size
+        self._check(self._lib.wsort_fetch_async(self._h, ctypes.byref(r)), "wsort_fetch_async")
+        return out[: r.words_len], [int(x) for x in off]
+
+    def sync(self):
+        self._check(self._lib.wsort_sync(self._h), "wsort_sync")
+
     def fetch_device(self):
         """(words: torch.uint8 cuda tensor (a copy), off: list[int])."""
         torch = _torch()

@@ -3,6 +3,8 @@
 // one word per line). Word i of bucket L lands at byte byte_off[L] + (i - off[L]) * (L + 1), so no
 // scan is needed. A tile decodes its keys into a shared-memory stage placed at the same 16-byte
 // phase as its global destination and writes it out with aligned 16-byte stores.
+#include <algorithm>
+
 #include "wsort_internal.cuh"
 
 namespace wsort {
@@ -65,9 +67,30 @@ __global__ void __launch_bounds__(kEThreads) k_emit(EmitArgs a) {
 
 }  // namespace
 
+// Small host<->device copies done by SM loads/stores through UVA-mapped pinned host memory instead of
+// a copy engine: the copy engines stay free for the bulk text / output transfers (whose queue a
+// few-KB table would otherwise wait behind).
+__global__ void k_copy_small(uint8_t *dst, const uint8_t *src, size_t n) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)dst | (uintptr_t)src | n) & 15u) == 0) {
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        for (size_t i = t; i < n / 16; i += stride) d4[i] = s4[i];
+    } else {
+        for (size_t i = t; i < n; i += stride) dst[i] = src[i];
+    }
+}
+
 cudaError_t launch_emit(const EmitArgs &a, cudaStream_t s) {
     if (a.ntiles == 0) return cudaSuccess;
     k_emit<<<a.ntiles, kEThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t copy_small(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    if (!bytes) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<size_t>((bytes + 4095) / 4096, 64);
+    k_copy_small<<<grid, 256, 0, s>>>(static_cast<uint8_t *>(dst), static_cast<const uint8_t *>(src), bytes);
     return cudaGetLastError();
 }
 

@@ -182,7 +182,7 @@ int arena_upload(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const
     uint8_t *h = c->arena + c->arena_off;
     memcpy(h, src, bytes);
     c->arena_off += (bytes + 255) & ~(size_t)255;
-    CK(cudaMemcpyAsync(dst.p, h, bytes, cudaMemcpyHostToDevice, c->stream), what);
+    CK(copy_small(dst.p, h, bytes, c->stream), what);   // (pinned arena: no copy-engine queue)
     return WSORT_OK;
 }
 int arena_end(wsort_ctx *c) {
@@ -500,8 +500,8 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     rc = launch(c, "k2_bucket_offsets", (double)kHistBins * 4,
                 [&] { return launch_bucket_offsets(ia.ghist, static_cast<Summary *>(c->d_sum.p), c->stream); });
     if (rc) return rc;
-    CK(cudaMemcpyAsync(c->h_ig, c->ig_ctr.p, kIgCtrs * 4, cudaMemcpyDeviceToHost, c->stream), "copy ingest counters");
-    CK(cudaMemcpyAsync(c->h_sum, c->d_sum.p, sizeof(Summary), cudaMemcpyDeviceToHost, c->stream), "copy summary");
+    CK(copy_small(c->h_ig, c->ig_ctr.p, kIgCtrs * 4, c->stream), "copy ingest counters");
+    CK(copy_small(c->h_sum, c->d_sum.p, sizeof(Summary), c->stream), "copy summary");
     CK(cudaStreamSynchronize(c->stream), "tokenize");
     c->cta_bases_ready = c->cta_counts_ready = false;
     if (c->h_ig[kIgVeryLong]) {   // words of 49..255 letters were not staged: histogram them the K3 way
@@ -513,7 +513,7 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
         rc = launch(c, "k2_bucket_offsets", (double)kHistBins * 4,
                     [&] { return launch_bucket_offsets(ia.ghist, static_cast<Summary *>(c->d_sum.p), c->stream); });
         if (rc) return rc;
-        CK(cudaMemcpyAsync(c->h_sum, c->d_sum.p, sizeof(Summary), cudaMemcpyDeviceToHost, c->stream), "copy summary");
+        CK(copy_small(c->h_sum, c->d_sum.p, sizeof(Summary), c->stream), "copy summary");
         CK(cudaStreamSynchronize(c->stream), "tokenize (long words)");
     }
     const Summary &s = *c->h_sum;
@@ -955,7 +955,7 @@ int msd_level_buffers(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nsegs) 
 
 // After a level's plan + scatter: read the queue counters (one stream sync) for the next level.
 int msd_read_counters(wsort_ctx *c, const MsdArgs &m, uint32_t &nsegs, uint32_t &ntiles) {
-    CK(cudaMemcpyAsync(c->h_ctr, c->m_ctr.p, kQCount * 4, cudaMemcpyDeviceToHost, c->stream), "msd counters");
+    CK(copy_small(c->h_ctr, c->m_ctr.p, kQCount * 4, c->stream), "msd counters");
     CK(cudaStreamSynchronize(c->stream), "msd level");
     nsegs = c->h_ctr[kQBig];
     ntiles = c->h_ctr[kQTiles];
@@ -1271,7 +1271,18 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     return WSORT_OK;
 }
 
-int wsort_fetch(wsort_ctx *c, wsort_result *r) {
+int fetch_impl(wsort_ctx *c, wsort_result *r, bool wait);
+
+int wsort_fetch(wsort_ctx *c, wsort_result *r) { return fetch_impl(c, r, true); }
+int wsort_fetch_async(wsort_ctx *c, wsort_result *r) { return fetch_impl(c, r, false); }
+int wsort_sync(wsort_ctx *c) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    CK(cudaStreamSynchronize(c->stream), "sync");
+    return WSORT_OK;
+}
+
+int fetch_impl(wsort_ctx *c, wsort_result *r, bool wait) {
     if (!c || !r) return WSORT_E_INVALID_ARG;
     if (c->state < ST_TOKENIZED) return set_err(c, WSORT_E_STATE, "wsort_fetch before wsort_tokenize");
     if (r->mem != WSORT_MEM_HOST && r->mem != WSORT_MEM_DEVICE) return set_err(c, WSORT_E_INVALID_ARG, "bad mem");
@@ -1296,7 +1307,7 @@ int wsort_fetch(wsort_ctx *c, wsort_result *r) {
         CK(cudaMemcpyAsync(r->words, c->words.p, r->words_len, k, c->stream), "fetch words");
     if (r->src_off && r->n_words)
         CK(cudaMemcpyAsync(r->src_off, c->src_off.p, r->n_words * 8, k, c->stream), "fetch src_off");
-    CK(cudaStreamSynchronize(c->stream), "fetch");
+    if (wait) CK(cudaStreamSynchronize(c->stream), "fetch");
     if (r->bucket_off) {
         if (r->mem == WSORT_MEM_HOST) {
             memcpy(r->bucket_off, offs, noff * sizeof(uint64_t));

@@ -304,5 +304,7 @@ struct EmitArgs {
 };
 constexpr int kEmitStage = 16384;  // smem bytes of output staged per emit tile
 cudaError_t launch_emit(const EmitArgs &a, cudaStream_t s);
+// small (KB) host<->device copy by a kernel through UVA-mapped pinned host memory (no copy engine)
+cudaError_t copy_small(void *dst, const void *src, size_t bytes, cudaStream_t s);
 
 }  // namespace wsort

@@ -323,3 +323,35 @@ def test_device_text_and_device_fetch(ws):
     dw, off = ws.fetch_device()
     ref = oracle.sort(text, oracle.MERGE)
     assert dw.cpu().numpy().tobytes() == ref.words and off == ref.off
+
+
+def test_fetch_async_pipeline(ws):
+    """wsort_fetch_async + wsort_sync: two contexts in a pipeline (the e2e bench pattern) give the
+    oracle's output for every text."""
+    import torch
+
+    from paper_1411_5283_b200 import WSort
+
+    texts = [gen.generate(1)[0], gen.generate(2)[0], gen.generate(1)[0]]
+    refs = [oracle.sort(t, oracle.MERGE) for t in texts]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    ctxs = [WSort(0, stream=s.cuda_stream) for s in streams]
+    outs = [np.empty(len(r.words) + 64, np.uint8) for r in refs]
+    got = []
+    try:
+        ctxs[0].load_text(texts[0])
+        for i, t in enumerate(texts):
+            cur = ctxs[i % 2]
+            cur.tokenize()
+            if i + 1 < len(texts):
+                ctxs[(i + 1) % 2].load_text(texts[i + 1])
+            cur.sort("auto")
+            got.append(cur.fetch_async(outs[i]))
+        for c in ctxs:
+            c.sync()
+        for (w, off), r in zip(got, refs):
+            assert off == r.off
+            assert w.tobytes() == r.words
+    finally:
+        for c in ctxs:
+            c.close()
