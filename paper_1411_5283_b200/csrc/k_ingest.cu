@@ -49,7 +49,7 @@ constexpr int kWList = kSub / 2;             // at most one word start per two b
 constexpr uint16_t kNoChunk16 = 0xffffu, kTrash16 = 0xfffeu;
 
 // keys per chunk of class k: the largest power of two <= kChunkWords / k
-__host__ __device__ constexpr uint32_t cls_lg(uint32_t k) { return k == 1 ? 12u : k == 2 ? 11u : k <= 4 ? 10u : 9u; }
+__host__ __device__ constexpr uint32_t cls_lg(uint32_t k) { return k == 1 ? 12u : k == 2 ? 11u : k <= 4 ? 10u : k <= 8 ? 9u : 8u; }
 
 struct IgSmem {
     uint4 wbuf[kIgWarps][kWBuf / 16 + 1];  // per warp: its sub-step + tail (+16 B: packing reads whole words)
@@ -237,11 +237,11 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
             const uint32_t y = (uint32_t)(X >> (bit + 3));
             wlst[p3++] = (uint16_t)((seg0 + bit) | (((y & 1u) + (y & (y >> 1) & 1u)) << 10));
         }
-        for (uint32_t m = ge6; m; m &= m - 1) {   // L >= 6: listed for packing (above 48 kept as 49: not staged)
+        for (uint32_t m = ge6; m; m &= m - 1) {   // L >= 6: listed for packing (above 66 kept as 67: not staged)
             const uint32_t bit = __ffs(m) - 1;
             const uint32_t em = ends & (0xffffffffu << bit);
             const uint32_t L = em ? (uint32_t)(__ffs(em) - 1) - bit + 1u : (32u - bit) + carry;
-            wlst[kWList - 1 - plg++] = (uint16_t)((seg0 + bit) | ((min(L, 49u) - 6u) << 10));
+            wlst[kWList - 1 - plg++] = (uint16_t)((seg0 + bit) | ((min(L, 6u * kMaxStageKw + 1u) - 6u) << 10));
             if (L > (uint32_t)kMaxLen) atomicAdd(&sm.hist[256], 1u);
         }
         __syncwarp();
@@ -669,7 +669,10 @@ __global__ void __launch_bounds__(256, kLsCtasPerSm) k_lscatter(L0Args a) {
             case 5: lscatter_chunk<5>(a, src, n, work); break;
             case 6: lscatter_chunk<6>(a, src, n, work); break;
             case 7: lscatter_chunk<7>(a, src, n, work); break;
-            default: lscatter_chunk<8>(a, src, n, work); break;
+            case 8: lscatter_chunk<8>(a, src, n, work); break;
+            case 9: lscatter_chunk<9>(a, src, n, work); break;
+            case 10: lscatter_chunk<10>(a, src, n, work); break;
+            default: lscatter_chunk<11>(a, src, n, work); break;
         }
         __syncthreads();
     }

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kST) k_msd_count(MsdArgs a) {
     for (int i = t; i < kRadixBins; i += kST) h[i] = 0;
     __syncthreads();
     // only the digit's key word is read; a batch of loads is issued before its atomics
-    const uint32_t *keys = a.src + b.key_off + (uint64_t)(sg.start + td.off) * b.kw + a.level / 3;
+    const uint32_t *keys = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)(sg.start + td.off) * b.kw + a.level / 3;
     const uint32_t sh = 20 - 10 * (a.level % 3);
     for (uint32_t k0 = t; k0 < td.n; k0 += 8 * kST) {
         uint32_t w[8];
@@ -99,7 +99,11 @@ __global__ void __launch_bounds__(kST) k_msd_count(MsdArgs a) {
 //                                              one tile; sorting a run of consecutive children by the
 //                                              full key sorts each child (their prefixes differ)
 // One atomic per queue then reserves the slots and all threads write the entries.
-constexpr int kPlanMax = 2048;   // >= 2 x the non-empty digits of a segment (<= 27*26)
+constexpr int kPlanMax = 2048;
+// Jobs of the first queue (q_tiny): <= 32 keys (warp sorts), or in streaming mode the big jobs
+// (> kBigJobKeys), which the persistent finish takes before the others (longest first).
+constexpr uint32_t kBigJobKeys = 16384;
+__device__ __forceinline__ bool first_queue(const MsdArgs &a, uint32_t n) { return a.stream_fin ? n > kBigJobKeys : n <= 32; }   // >= 2 x the non-empty digits of a segment (<= 27*26)
 __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
     __shared__ uint32_t wsum[kST / 32 + 1];
     __shared__ uint32_t nz_d[kRadixBins];
@@ -126,6 +130,18 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
         ex += c[e];
     }
     __syncthreads();
+    const uint32_t src_a = sg.buf & 1u, dst_a = src_a ^ 1u;   // where the segment is / its children go
+    if (t == 0 && nzt == 1 && a.level + 1 < b.ndig && sg.n > 1) {
+        // every key shares this digit: no data movement; the segment goes to the next level as it is
+        a.seg_skip[s] = 1u;
+        const uint32_t nt = (sg.n + b.aux - 1) / b.aux;
+        const uint32_t q = atomicAdd(a.ctr + kQBig, 1u), t0 = atomicAdd(a.ctr + kQTiles, nt);
+        if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, sg.n, src_a};
+        for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++)
+            a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, sg.n - i * b.aux), 0};
+    }
+    if (nzt == 1 && a.level + 1 < b.ndig && sg.n > 1) return;
+    if (t == 0) a.seg_skip[s] = 0u;
     if (t == 0) {
         const bool final_digit = a.level + 1 >= b.ndig;
         const uint32_t cap = b.tile_keys, seg_end = sg.start + sg.n;
@@ -135,10 +151,10 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
             const uint32_t start = nz_d[k], cnt = (k + 1 < nzt ? nz_d[k + 1] : seg_end) - start;
             const bool fin = final_digit || cnt == 1;
             const bool stream = a.stream_fin;   // every child is a finishing job of k_msd_fin (it writes the text)
-            const bool big = !fin && cnt > cap && !stream, skip = fin && !a.dst_is_a && !stream,
-                       copy = fin && a.dst_is_a && cnt > cap && !stream;
+            const bool big = !fin && cnt > cap && !stream, skip = fin && !dst_a && !stream,
+                       copy = fin && dst_a && cnt > cap && !stream;
             if (big || skip || copy) {
-                if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
+                if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, dst_a | (a.level << 8)};
                 jn = 0;
                 if (big) {
                     big_t0[ntop] = ntiles;
@@ -149,21 +165,21 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
                     jobs[kPlanMax - 1 - ntop++] = MsdSeg{sg.L, start, cnt, 2u};
                 }
             } else if (cnt > cap) {   // (stream) a child larger than a CTA tile is a job of its own
-                if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
+                if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, dst_a | (a.level << 8)};
                 jn = 0;
-                jobs[nj++] = MsdSeg{sg.L, start, cnt, a.dst_is_a | (a.level << 8)};
+                jobs[nj++] = MsdSeg{sg.L, start, cnt, dst_a | (a.level << 8)};
             } else {
                 if (jn + cnt > cap) {
-                    jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
+                    jobs[nj++] = MsdSeg{sg.L, js, jn, dst_a | (a.level << 8)};
                     jn = 0;
                 }
                 if (!jn) js = start;
                 jn += cnt;
             }
         }
-        if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, a.dst_is_a | (a.level << 8)};
+        if (jn) jobs[nj++] = MsdSeg{sg.L, js, jn, dst_a | (a.level << 8)};
         uint32_t ntiny = 0, nbig = 0, nch = 0;
-        for (uint32_t k = 0; k < nj; k++) ntiny += jobs[k].n <= 32 && !a.stream_fin;
+        for (uint32_t k = 0; k < nj; k++) ntiny += first_queue(a, jobs[k].n);
         for (uint32_t k = 0; k < ntop; k++) {
             const MsdSeg &x = jobs[kPlanMax - 1 - k];
             if (x.buf == 1u) nbig++;
@@ -197,9 +213,9 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
     // sort jobs, order-preserving split into tiny / small (each thread recounts its prefix)
     for (uint32_t k = t; k < nj; k += kST) {
         uint32_t before_tiny = 0;
-        for (uint32_t i = 0; i < k; i++) before_tiny += jobs[i].n <= 32 && !a.stream_fin;
+        for (uint32_t i = 0; i < k; i++) before_tiny += first_queue(a, jobs[i].n);
         const MsdSeg x = jobs[k];
-        if (x.n <= 32 && !a.stream_fin) {
+        if (first_queue(a, x.n)) {
             const uint32_t q = s_q[0] + before_tiny;
             if (q < a.cap_local) a.q_tiny[q] = x;
         } else {
@@ -212,7 +228,7 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
         if (x.buf < 16u) continue;
         const uint32_t q = s_q[2] + (x.buf - 16u), t0 = s_q[3] + big_t0[k];
         const uint32_t nt = (x.n + b.aux - 1) / b.aux;
-        x.buf = 0;
+        x.buf = dst_a;   // the children of a scattered segment are in the other buffer
         if (q < a.cap_big) a.q_big[q] = x;
         for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++)
             a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, x.n - i * b.aux), 0};
@@ -229,7 +245,7 @@ __device__ __forceinline__ void scatter_tile(const MsdArgs &a, const MsdTile &td
     uint32_t *wsum = kout + 8192 + 8192 / 32 + 8;
     for (int i = t; i < kRadixBins; i += kST) hist[i] = 0;
     __syncthreads();
-    const uint32_t *src = a.src + b.key_off + (uint64_t)(sg.start + td.off) * KW;
+    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)(sg.start + td.off) * KW;
     uint32_t key[KPT][KW], slot[(KPT + 1) / 2];
 #pragma unroll
     for (int r = 0; r < (KPT + 1) / 2; r++) slot[r] = 0;
@@ -275,7 +291,7 @@ __device__ __forceinline__ void scatter_tile(const MsdArgs &a, const MsdTile &td
 #pragma unroll
     for (int e = 0; e < 4; e++) gbase[4 * t + e] = g[e] - ex4[e];
     __syncthreads();
-    uint32_t *dst = a.dst + b.key_off;
+    uint32_t *dst = ((sg.buf & 1u) ? a.keys_b : const_cast<uint32_t *>(a.keys_a)) + b.key_off;
     for (uint32_t i = t; i < td.n * KW; i += kST) {
         const uint32_t p = i / KW, u = i - p * KW;
         const uint32_t w = kout[i + (i >> 5)];
@@ -289,6 +305,7 @@ __device__ __forceinline__ void scatter_tile(const MsdArgs &a, const MsdTile &td
 __global__ void __launch_bounds__(kST, 2) k_msd_scatter(MsdArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     const MsdTile td = a.tiles[blockIdx.x];
+    if (a.seg_skip[td.seg]) return;   // all its keys share this digit: the segment moves on in place
     const MsdSeg sg = a.segs[td.seg];
     const BucketInfo b = a.buckets[sg.L];
     switch (b.kw) {
@@ -300,7 +317,10 @@ __global__ void __launch_bounds__(kST, 2) k_msd_scatter(MsdArgs a) {
         case 6: scatter_tile<6>(a, td, sg, b, sm); break;
         case 7: scatter_tile<7>(a, td, sg, b, sm); break;
         case 8: scatter_tile<8>(a, td, sg, b, sm); break;
-        default: break;   // kw > 8 never reaches the scatter: the host sorts such buckets with LSD
+        case 9: scatter_tile<9>(a, td, sg, b, sm); break;
+        case 10: scatter_tile<10>(a, td, sg, b, sm); break;
+        case 11: scatter_tile<11>(a, td, sg, b, sm); break;
+        default: break;   // kw > 11 never reaches the scatter: the host sorts such buckets with LSD
     }
 }
 
@@ -873,7 +893,11 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
     T *B = A + fpad(kStreamDistinct);
     uint32_t *pos = reinterpret_cast<uint32_t *>(B + fpad(kStreamDistinct));
     uint32_t *misc = pos + kStreamDistinct;   // [0] distinct keys, [1] overflow, [2..] scan scratch
-    for (uint32_t i = t; i < kStreamSlots; i += kST) {
+    // table size adapted to the job (a small job pays for a small table): >= 2n slots, <= kStreamSlots
+    uint32_t ns = 64;
+    while (ns < 2 * n && ns < kStreamSlots) ns *= 2;
+    const uint32_t smask = ns - 1, sshift = 32 - (31 - __clz(ns));
+    for (uint32_t i = t; i < ns; i += kST) {
         slots[i] = kEmpty;
         cnt[i] = 0;
     }
@@ -891,7 +915,7 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
 #pragma unroll
         for (int r = 0; r < 4; r++) {
             if (k[r] == kEmpty) continue;
-            uint32_t h = st_hash(k[r]);
+            uint32_t h = (uint32_t)(((uint64_t)k[r] * 0x9E3779B97F4A7C15ull) >> 32) >> sshift;
             for (;;) {
                 T cur = slots[h];
                 if (cur == kEmpty) {
@@ -907,7 +931,7 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
                     atomicAdd(&cnt[h], 1u);
                     break;
                 }
-                h = (h + 1) & (kStreamSlots - 1);
+                h = (h + 1) & smask;
             }
         }
     }
@@ -931,21 +955,20 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
                                // level (a child without digits left holds one key only: this terminates)
             const uint32_t nt = (n + b.aux - 1) / b.aux;
             const uint32_t q = atomicAdd(a.ctr + kQBig, 1u), t0 = atomicAdd(a.ctr + kQTiles, nt);
-            if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, n, 0u};
+            if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, n, sg.buf & 1u};
             for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++) a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, n - i * b.aux), 0};
         }
         return;
     }
     // compact the distinct keys (8 slots per thread), sort them, look up their counts, scan
+    const uint32_t per = (ns + kST - 1) / kST;   // slots per thread (contiguous)
     uint32_t occ = 0;
-#pragma unroll
-    for (int e = 0; e < (int)(kStreamSlots / kST); e++) occ += cnt[(kStreamSlots / kST) * t + e] != 0;
+    for (uint32_t e = 0; e < per; e++) occ += (per * t + e < ns) && cnt[per * t + e] != 0;
     uint32_t nd = 0;
     uint32_t p = block_excl_scan_m(occ, misc + 2, &nd);
-#pragma unroll
-    for (int e = 0; e < (int)(kStreamSlots / kST); e++) {
-        const uint32_t h = (kStreamSlots / kST) * t + e;
-        if (cnt[h]) A[fpad(p++)] = slots[h];
+    for (uint32_t e = 0; e < per; e++) {
+        const uint32_t h = per * t + e;
+        if (h < ns && cnt[h]) A[fpad(p++)] = slots[h];
     }
     T *S = block_sort_smem<T>(A, B, nd);
     uint32_t c4[4], tot = 0;   // nd <= 1024: 4 per thread
@@ -955,8 +978,8 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
         c4[e] = 0;
         if (i < nd) {
             const T k = S[fpad(i)];
-            uint32_t h = st_hash(k);
-            while (slots[h] != k) h = (h + 1) & (kStreamSlots - 1);
+            uint32_t h = (uint32_t)(((uint64_t)k * 0x9E3779B97F4A7C15ull) >> 32) >> sshift;
+            while (slots[h] != k) h = (h + 1) & smask;
             c4[e] = cnt[h];
         }
         tot += c4[e];
@@ -1071,7 +1094,7 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     if (misc[1]) {   // too many distinct keys
         if (n <= b.tile_keys) {   // (possibly several children): sort the job in full
             __syncthreads();
-            cta_sort_job<KW, (KW <= 4 ? 4 : 2)>(a, sg, b, reinterpret_cast<uint32_t *>(smraw));
+            cta_sort_job<KW, (KW <= 4 ? 4 : (KW <= 8 ? 2 : 1))>(a, sg, b, reinterpret_cast<uint32_t *>(smraw));
             __syncthreads();   // the sorted keys are in buffer B (written by this CTA)
             const uint32_t *kb = a.keys_b + b.key_off + (uint64_t)sg.start * KW;
             emit_job_text<KW>(a, b, sg.L, sg.start, n, smraw, [&](uint32_t i, uint32_t (&k)[KW]) {
@@ -1082,7 +1105,7 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
                                // level (a child without digits left holds one key only: this terminates)
             const uint32_t nt = (n + b.aux - 1) / b.aux;
             const uint32_t q = atomicAdd(a.ctr + kQBig, 1u), t0 = atomicAdd(a.ctr + kQTiles, nt);
-            if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, n, 0u};
+            if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, n, sg.buf & 1u};
             for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++) a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, n - i * b.aux), 0};
         }
         return;
@@ -1133,13 +1156,14 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
 __global__ void __launch_bounds__(kST, 4) k_msd_fin(MsdArgs a) {
     extern __shared__ __align__(16) uint8_t fsm[];
     __shared__ uint32_t s_job;
-    const uint32_t end = min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQSmall), a.cap_local);
-    for (;;) {   // jobs are taken dynamically (their sizes differ by orders of magnitude)
-    if (threadIdx.x == 0) s_job = a.small_base + atomicAdd(a.ctr + kQFinTicket, 1u);
+    const uint32_t nb = min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQTiny), a.cap_local) - a.big_base;
+    const uint32_t end = nb + min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQSmall), a.cap_local) - a.small_base;
+    for (;;) {   // jobs are taken dynamically, big ones first (their sizes differ by orders of magnitude)
+    if (threadIdx.x == 0) s_job = atomicAdd(a.ctr + kQFinTicket, 1u);
     __syncthreads();
     const uint32_t j = s_job;
     if (j >= end) break;
-    const MsdSeg sg = a.q_small[j];
+    const MsdSeg sg = j < nb ? a.q_tiny[a.big_base + j] : a.q_small[a.small_base + j - nb];
     const BucketInfo b = a.buckets[sg.L];
     switch (b.kw) {
         case 1: fin_stream<uint32_t, 1>(a, sg, b, fsm); break;
@@ -1149,13 +1173,16 @@ __global__ void __launch_bounds__(kST, 4) k_msd_fin(MsdArgs a) {
         case 5: fin_stream_wide<5>(a, sg, b, fsm); break;
         case 6: fin_stream_wide<6>(a, sg, b, fsm); break;
         case 7: fin_stream_wide<7>(a, sg, b, fsm); break;
-        default: fin_stream_wide<8>(a, sg, b, fsm); break;
+        case 8: fin_stream_wide<8>(a, sg, b, fsm); break;
+        case 9: fin_stream_wide<9>(a, sg, b, fsm); break;
+        case 10: fin_stream_wide<10>(a, sg, b, fsm); break;
+        default: fin_stream_wide<11>(a, sg, b, fsm); break;
     }
     __syncthreads();   // shared memory is reused by the next job
     }
 }
 constexpr size_t kFinSmemStream = kStreamSlots * 12 + 2 * (kStreamDistinct + kStreamDistinct / 16) * 8 + (kStreamDistinct + 16) * 4;
-constexpr size_t kFinSmemWide = kWideSlots * 16 + (kWideDistinct * 8 + 3 * kWideDistinct + 16) * 4;
+constexpr size_t kFinSmemWide = kWideSlots * 16 + (kWideDistinct * 11 + 3 * kWideDistinct + 16) * 4;   // KW <= 11
 constexpr size_t kFinSmemSort = 2 * (kST * 4 * 4 + kST * 4 * 4 / 32 + 1) * 4;   // cta_sort_job fallback: TN*KW <= 4096
 constexpr size_t kFinSmem0 = kFinSmemStream > kFinSmemWide ? kFinSmemStream : kFinSmemWide;
 constexpr size_t kFinSmem = kFinSmem0 > kFinSmemSort ? kFinSmem0 : kFinSmemSort;
@@ -1187,10 +1214,11 @@ cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s
     k_msd_scatter<<<ntiles, kST, smem, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t grid, cudaStream_t s) {
+cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t first_big, uint32_t grid, cudaStream_t s) {
     if (!grid) return cudaSuccess;
     MsdArgs b = a;
     b.small_base = first;
+    b.big_base = first_big;
     cudaError_t e = cudaMemsetAsync(a.ctr + kQFinTicket, 0, 4, s);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_msd_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinSmem);

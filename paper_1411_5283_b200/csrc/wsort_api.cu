@@ -78,7 +78,7 @@ struct wsort_ctx {
 
     // sort
     DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y, splits;
-    DevBuf m_hist, m_cursor, m_ctr, m_big[2], m_tiles[2], m_tiny, m_small, m_copy;
+    DevBuf m_hist, m_cursor, m_ctr, m_big[2], m_tiles[2], m_tiny, m_small, m_copy, m_skip;
     uint32_t *h_ctr = nullptr;   // pinned mirror of the msd queue counters
     std::vector<uint8_t> hplan;
     uint8_t *h_plan_pinned = nullptr;
@@ -367,7 +367,7 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->tickets, &c->plan, &c->va_x, &c->va_y, &c->splits, &c->bk, &c->d_counts,
                       &c->d_cursor, &c->d_sbase, &c->d_split, &c->d_lohi, &c->d_tiles, &c->d_ranges,
                       &c->m_hist, &c->m_cursor, &c->m_ctr, &c->m_big[0], &c->m_big[1], &c->m_tiles[0],
-                      &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->ghist, &c->dense,
+                      &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->ghist, &c->dense,
                       &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
                       &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor};
     for (DevBuf *b : bufs)
@@ -914,6 +914,7 @@ int msd_alloc(wsort_ctx *c, MsdArgs &m, uint64_t W, uint64_t key_words) {
     if ((rc = ensure(c, c->m_small, (size_t)cap_local * sizeof(MsdSeg), "msd small"))) return rc;
     if ((rc = ensure(c, c->m_copy, (size_t)cap_copy * sizeof(CopyRange), "msd copy"))) return rc;
     if ((rc = ensure(c, c->m_ctr, kQCount * 4, "msd counters"))) return rc;
+    if ((rc = ensure(c, c->m_skip, (size_t)cap_big * 4, "msd skip flags"))) return rc;
     if (!c->h_ctr && cudaMallocHost(&c->h_ctr, kQCount * 4) != cudaSuccess) {
         cudaGetLastError();
         return set_err(c, WSORT_E_NOMEM, "pinned counters");
@@ -929,6 +930,7 @@ int msd_alloc(wsort_ctx *c, MsdArgs &m, uint64_t W, uint64_t key_words) {
     m.cap_copy = cap_copy;
     m.keys_a = static_cast<uint32_t *>(c->keys_a.p);
     m.keys_b = static_cast<uint32_t *>(c->keys_b.p);
+    m.seg_skip = static_cast<uint32_t *>(c->m_skip.p);
     return WSORT_OK;
 }
 
@@ -972,11 +974,12 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
     int rc;
     m.stream_fin = m.finish_radix ? 0u : 1u;
     const uint32_t fin_grid = (uint32_t)c->sms * 4;   // k_msd_fin: 4 resident CTAs per SM
-    uint32_t small_done = 0;
-    if (!m.finish_radix && c->h_ctr[kQSmall]) {   // jobs planned before the first level (whole small buckets)
-        rc = launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_fin_jobs(m, 0, fin_grid, c->stream); });
+    uint32_t small_done = 0, big_done = 0;
+    if (!m.finish_radix && (c->h_ctr[kQSmall] || c->h_ctr[kQTiny])) {   // jobs planned before the first level
+        rc = launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_fin_jobs(m, 0, 0, fin_grid, c->stream); });
         if (rc) return rc;
         small_done = c->h_ctr[kQSmall];
+        big_done = c->h_ctr[kQTiny];
     }
     for (; nsegs > 0; level++) {
         if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
@@ -991,11 +994,14 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         if (!m.finish_radix) {   // this level's finishing jobs (their count is on the device); a job with too
                                  // many distinct keys re-enters the next level
             rc = launch(c, "k4m_msd_finish", level == 0 ? 2 * key_bytes : 0,
-                        [&] { return launch_msd_fin_jobs(m, small_done, fin_grid, c->stream); });
+                        [&] { return launch_msd_fin_jobs(m, small_done, big_done, fin_grid, c->stream); });
             if (rc) return rc;
         }
         if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;   // the level's one host sync
-        if (!m.finish_radix) small_done = std::min(c->h_ctr[kQSmall], m.cap_local);
+        if (!m.finish_radix) {
+            small_done = std::min(c->h_ctr[kQSmall], m.cap_local);
+            big_done = std::min(c->h_ctr[kQTiny], m.cap_local);
+        }
         if (getenv("WSORT_DEBUG_MSD")) {
             fprintf(stderr, "msd level %u -> next segs %u tiles %u | tiny %u small %u copy %u\n", level, nsegs, ntiles,
                     c->h_ctr[kQTiny], c->h_ctr[kQSmall], c->h_ctr[kQCopy]);
@@ -1015,7 +1021,7 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
             fprintf(stderr, " | keys in jobs > 64k: %llu\n", (unsigned long long)big);
         }
     }
-    m.n_tiny = c->h_ctr[kQTiny];
+    m.n_tiny = m.finish_radix ? c->h_ctr[kQTiny] : 0u;   // (streaming: q_tiny held the big jobs, finished)
     const uint32_t n_small = c->h_ctr[kQSmall], n_copy = c->h_ctr[kQCopy];
     return launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_finish(m, n_small, n_copy, max_tw, c->stream); });
 }
@@ -1058,7 +1064,7 @@ std::vector<BucketInfo> msd_buckets(const Summary &s, uint32_t lkey, uint32_t &m
         b.kw = kw_of(L);
         b.ndig = ndig_of(L);
         // finishing-job capacity: its full-sort fallback holds <= 4096 key words (<= 2048 keys)
-        b.tile_keys = b.kw <= 2 ? 2048u : (b.kw <= 4 ? 1024u : 512u);
+        b.tile_keys = b.kw <= 2 ? 2048u : (b.kw <= 4 ? 1024u : (b.kw <= 8 ? 512u : 256u));
         b.aux = kRadixThreads * (32 / b.kw);                          // scatter tile keys
         b.final_b = 1;
         if (L < lkey) continue;
@@ -1091,10 +1097,10 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
         const BucketInfo &b = bk[L];
         if (!b.n) continue;
         if (b.n <= b.tile_keys) {
-            (b.n <= 32 && finish_radix ? tiny : small).push_back(MsdSeg{L, 0, b.n, 1});
+            (finish_radix ? b.n <= 32 : b.n > 16384) ? tiny.push_back(MsdSeg{L, 0, b.n, 1}) : small.push_back(MsdSeg{L, 0, b.n, 1});
         } else {
             const uint32_t q = (uint32_t)segs.size();
-            segs.push_back(MsdSeg{L, 0, b.n, 0});
+            segs.push_back(MsdSeg{L, 0, b.n, 1});   // packed into buffer A
             for (uint32_t o = 0; o < b.n; o += b.aux) tiles.push_back(MsdTile{q, o, std::min(b.aux, b.n - o), 0});
         }
     }

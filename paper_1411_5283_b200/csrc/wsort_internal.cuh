@@ -96,13 +96,13 @@ constexpr int kIgThreads = 512;
 constexpr int kIgStep = 16384;                       // bytes per ingest step = 32 per thread
 constexpr int kIgBuf = kTkPre + kIgStep + kTkHalo;   // 16656 bytes
 constexpr uint32_t kDenseMaxLen = 5;                 // words of L <= 5 are counted, not sorted
-constexpr uint32_t kMaxStageKw = 8;                  // words of 6 <= L <= 48 are staged as keys
+constexpr uint32_t kMaxStageKw = 11;                 // words of 6 <= L <= 66 are staged as keys
 constexpr uint32_t kChunkWords = 4096;               // u32 words per staging chunk (16 KiB)
 enum { kIgMaxChunks = 0, kIgOverflow = 1, kIgVeryLong = 2, kIgCtrs = 4 };
 // chunks per CTA region: a staged word's key bytes <= its text bytes (+256 for the last word), a full
-// chunk holds >= 2560 key words (class 5: 512 keys of 5 words), one partial chunk per class
+// chunk holds >= 2304 key words (class 9: 256 keys of 9 words), one partial chunk per class
 __host__ __device__ constexpr uint32_t ingest_cta_chunks(uint64_t range_bytes) {
-    return (uint32_t)((range_bytes + 256) / 10000 + 2 * kMaxStageKw + 10);
+    return (uint32_t)((range_bytes + 256) / 9000 + 2 * kMaxStageKw + 10);
 }
 struct IngestArgs {
     const uint8_t *text;
@@ -249,8 +249,8 @@ cudaError_t launch_regroup(const CopyRange *ranges, uint32_t nranges, const uint
 
 // ---------------- msd_radix: MSD partitioning + CTA-local odd-even transposition finish ----------------
 struct MsdSeg {
-    uint32_t L, start, n, buf;     // key range [start, start+n) of bucket L; buf bit 0: 1 = in A, 0 = in B;
-                                   // buf >> 8: first digit still to sort (sort jobs)
+    uint32_t L, start, n, buf;     // key range [start, start+n) of bucket L; buf bit 0: 1 = in A, 0 = in B
+                                   // (segments and jobs alike); buf >> 8: the job's level (sort jobs)
 };
 struct MsdTile {
     uint32_t seg, off, n, pad_;    // keys [off, off+n) of segment `seg` of this level
@@ -277,8 +277,10 @@ struct MsdArgs {
     uint32_t n_tiny;
     uint32_t finish_radix;         // 1: small jobs with kw <= 4 by local LSD radix, else odd-even transposition
     uint32_t stream_fin;           // 1: every child is a finishing job of k_msd_fin, which writes the text
+    uint32_t *seg_skip;            // [segments of this level] 1: all keys share the digit (not scattered)
     uint8_t *words;                // (stream_fin) output text
     uint32_t small_base;           // k_msd_fin: first job of this launch in q_small
+    uint32_t big_base;             // k_msd_fin (streaming): first job of this launch in q_tiny (big jobs)
 };
 size_t msd_scatter_smem();
 cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
@@ -287,7 +289,7 @@ cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s
 cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_copy, uint32_t max_tile_words,
                               cudaStream_t s);   // tiny jobs, radix-finish jobs, copies (after the last level)
 // per level: jobs [first, *ctr[kQSmall]) by `grid` persistent CTAs
-cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t grid, cudaStream_t s);
+cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t first_big, uint32_t grid, cudaStream_t s);
 
 struct EmitArgs {
     const BucketInfo *buckets;

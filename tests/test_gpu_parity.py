@@ -112,6 +112,10 @@ def _edge_cases():
         "staged_classes_6_48": b" ".join(bytes([97 + (i * j + j * j) % 26 for j in range(6 + i % 43)])
                                          for i in range(40_000)),
         "staged_l48_dups": (b"q" * 47 + b"r ") * 5000 + (b"q" * 48 + b" ") * 3000,
+        # key-width classes 9..11 (49..66 letters, config 5's longest words) and the first unstaged length
+        "staged_classes_9_11": b" ".join(bytes([97 + (i * j + 3 * j) % 26 for j in range(49 + i % 18)])
+                                         for i in range(6_000)) + b" " + b"z" * 66 + b" " + b"a" * 66,
+        "unstaged_67": b"ab " * 1000 + b"m" * 67 + b" x",
     }
     # a word crossing every 8 KiB boundary of a multi-step text (CTA chunk boundaries too)
     t = bytearray(b"." * (S * 40))
