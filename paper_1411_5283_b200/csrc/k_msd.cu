@@ -1015,7 +1015,7 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
 // second pass compares every key with its representative word by word (exact: any mismatch sorts
 // the job in full / sends it to the next MSD level). At most kWideDistinct distinct keys, ranked by
 // counting the smaller ones.
-constexpr uint32_t kWideSlots = 1024, kWideDistinct = 256;
+constexpr uint32_t kWideSlots = 1024, kWideDistinct = 512;
 template <int KW>
 __device__ __forceinline__ uint64_t fp64(const uint32_t (&k)[KW]) {
     uint64_t h = 0x9E3779B97F4A7C15ull;
@@ -1114,13 +1114,13 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     for (uint32_t i = t; i < kWideSlots; i += kST)
         if (cnt[i]) dcnt[sid[i]] = cnt[i];
     __syncthreads();
-    if (t < nd) {   // rank = number of smaller distinct keys
+    for (uint32_t me = t; me < nd; me += kST) {   // rank = number of smaller distinct keys
         uint32_t rank = 0;
         for (uint32_t j = 0; j < nd; j++) {
             bool lt = false, decided = false;
 #pragma unroll
             for (int u = 0; u < KW; u++) {
-                const uint32_t x = rep[j * KW + u], y = rep[t * KW + u];
+                const uint32_t x = rep[j * KW + u], y = rep[me * KW + u];
                 if (!decided && x != y) {
                     lt = x < y;
                     decided = true;
@@ -1128,12 +1128,23 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
             }
             rank += lt;
         }
-        order[rank] = t;
+        order[rank] = me;
     }
     __syncthreads();
-    const uint32_t c = t < nd ? dcnt[order[t]] : 0u;
-    const uint32_t end = block_excl_scan_m(c, misc + 2, nullptr) + c;
-    if (t < nd) pos[t] = end;
+    constexpr int PT = kWideDistinct / kST;   // ranks per thread (contiguous)
+    uint32_t cc[PT], tot = 0;
+#pragma unroll
+    for (int e = 0; e < PT; e++) {
+        const uint32_t r = PT * t + e;
+        cc[e] = r < nd ? dcnt[order[r]] : 0u;
+        tot += cc[e];
+    }
+    uint32_t end = block_excl_scan_m(tot, misc + 2, nullptr);
+#pragma unroll
+    for (int e = 0; e < PT; e++) {
+        end += cc[e];
+        if (PT * t + e < nd) pos[PT * t + e] = end;
+    }
     __syncthreads();
     // the fingerprint table is no longer needed: its space (16 KiB) holds the runs' repeated patterns
     // (or stages the text)
