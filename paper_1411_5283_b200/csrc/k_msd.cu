@@ -661,6 +661,9 @@ __device__ __forceinline__ T *block_sort_smem(T *A, T *B, uint32_t n) {
     constexpr int E = 8;
     const T kMax = ~(T)0;   // above every key (key words are < 2^30)
     const uint32_t t = threadIdx.x;
+    uint32_t span = E;
+    while (span < n) span *= 2;   // only [0, span) is touched: A and B need fpad(span) entries
+    const bool mine = t * E < span;
     T v[E];
     __syncthreads();   // A was filled by other threads
 #pragma unroll
@@ -677,11 +680,10 @@ __device__ __forceinline__ T *block_sort_smem(T *A, T *B, uint32_t n) {
             v[i + 1] = x < y ? y : x;
         }
     __syncthreads();   // (A is read above and rewritten below)
+    if (mine)
 #pragma unroll
-    for (int e = 0; e < E; e++) A[fpad(t * E + e)] = v[e];
+        for (int e = 0; e < E; e++) A[fpad(t * E + e)] = v[e];
     __syncthreads();
-    uint32_t span = E;
-    while (span < n) span *= 2;   // merge only as far as the keys reach
     for (uint32_t run = E; run < span; run *= 2) {
         const uint32_t o = t * E;
         if (o < span) {
@@ -709,6 +711,72 @@ __device__ __forceinline__ T *block_sort_smem(T *A, T *B, uint32_t n) {
         }
         __syncthreads();
         T *sw = A;
+        A = B;
+        B = sw;
+    }
+    return A;
+}
+
+// block_sort_smem for u32 indices ordered by a comparator lt(a, b) ("key a < key b"): odd-even
+// transposition of each thread's 8 indices in registers, then merge-path passes in shared memory.
+template <class Lt>
+__device__ __forceinline__ uint32_t *block_sort_idx(uint32_t *A, uint32_t *B, uint32_t n, Lt lt) {
+    constexpr int E = 8;
+    const uint32_t kPad = 0xffffffffu;   // sorts after every index
+    auto less = [&](uint32_t x, uint32_t y) { return y == kPad ? x != kPad : (x == kPad ? false : lt(x, y)); };
+    const uint32_t t = threadIdx.x;
+    uint32_t span = E;
+    while (span < n) span *= 2;
+    const bool mine = t * E < span;
+    uint32_t v[E];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t idx = t * E + e;
+        v[e] = idx < n ? A[fpad(idx)] : kPad;
+    }
+    if (mine)
+#pragma unroll
+        for (int ph = 0; ph < E; ph++)
+#pragma unroll
+            for (int i = ph & 1; i + 1 < E; i += 2) {
+                const uint32_t x = v[i], y = v[i + 1];
+                const bool sw = less(y, x);
+                v[i] = sw ? y : x;
+                v[i + 1] = sw ? x : y;
+            }
+    __syncthreads();
+    if (mine)
+#pragma unroll
+        for (int e = 0; e < E; e++) A[fpad(t * E + e)] = v[e];
+    __syncthreads();
+    for (uint32_t run = E; run < span; run *= 2) {
+        const uint32_t o = t * E;
+        if (o < span) {
+            const uint32_t ra = (o / (2 * run)) * 2 * run, rb = ra + run, d = o - ra;
+            uint32_t lo = d > run ? d - run : 0u, hi = d < run ? d : run;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (!less(A[fpad(rb + d - 1 - mid)], A[fpad(ra + mid)])) lo = mid + 1;
+                else hi = mid;
+            }
+            uint32_t i = lo, j = d - lo;
+            uint32_t x = i < run ? A[fpad(ra + i)] : kPad, y = j < run ? A[fpad(rb + j)] : kPad;
+#pragma unroll
+            for (int k = 0; k < E; k++) {
+                const bool tx = j >= run || (i < run && !less(y, x));
+                B[fpad(o + k)] = tx ? x : y;
+                if (tx) {
+                    i++;
+                    x = i < run ? A[fpad(ra + i)] : kPad;
+                } else {
+                    j++;
+                    y = j < run ? A[fpad(rb + j)] : kPad;
+                }
+            }
+        }
+        __syncthreads();
+        uint32_t *sw = A;
         A = B;
         B = sw;
     }
@@ -1044,11 +1112,9 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     if (t < 2) misc[t] = 0;
     __syncthreads();
     const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
-    for (uint32_t i = t; i < n; i += kST) {
-        if (*reinterpret_cast<volatile uint32_t *>(misc + 1)) break;
-        uint32_t k[KW];
-#pragma unroll
-        for (int u = 0; u < KW; u++) k[u] = __ldg(src + (size_t)i * KW + u);
+    // keys are loaded BATCH at a time ahead of their inserts (independent loads in flight)
+    constexpr int BATCH = KW <= 4 ? 4 : (KW <= 8 ? 2 : 1);
+    auto insert = [&](const uint32_t (&k)[KW]) {
         const uint64_t f = fp64<KW>(k);
         uint32_t h = (uint32_t)(f >> 40) & (kWideSlots - 1);
         for (;;) {
@@ -1059,7 +1125,7 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
                     const uint32_t id = atomicAdd(misc, 1u);
                     if (id >= kWideDistinct) {
                         atomicExch(misc + 1, 1u);
-                        break;
+                        return;
                     }
 #pragma unroll
                     for (int u = 0; u < KW; u++) rep[id * KW + u] = k[u];
@@ -1069,25 +1135,46 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
             }
             if (cur == f) {
                 atomicAdd(&cnt[h], 1u);
-                break;
+                return;
             }
             h = (h + 1) & (kWideSlots - 1);
         }
+    };
+    for (uint32_t i0 = 0; i0 < n; i0 += BATCH * kST) {
+        if (*reinterpret_cast<volatile uint32_t *>(misc + 1)) break;
+        uint32_t k[BATCH][KW];
+#pragma unroll
+        for (int r = 0; r < BATCH; r++) {
+            const uint32_t i = i0 + r * kST + t;
+#pragma unroll
+            for (int u = 0; u < KW; u++) k[r][u] = i < n ? __ldg(src + (size_t)i * KW + u) : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < BATCH; r++)
+            if (i0 + r * kST + t < n) insert(k[r]);
     }
     __syncthreads();
     if (!misc[1]) {   // verify: every key equals its fingerprint's representative
-        for (uint32_t i = t; i < n; i += kST) {
-            uint32_t k[KW];
+        for (uint32_t i0 = 0; i0 < n; i0 += BATCH * kST) {
+            uint32_t k[BATCH][KW];
 #pragma unroll
-            for (int u = 0; u < KW; u++) k[u] = __ldg(src + (size_t)i * KW + u);
-            const uint64_t f = fp64<KW>(k);
-            uint32_t h = (uint32_t)(f >> 40) & (kWideSlots - 1);
-            while (fps[h] != f) h = (h + 1) & (kWideSlots - 1);
-            const uint32_t id = sid[h];
-            bool eq = true;
+            for (int r = 0; r < BATCH; r++) {
+                const uint32_t i = i0 + r * kST + t;
 #pragma unroll
-            for (int u = 0; u < KW; u++) eq &= rep[id * KW + u] == k[u];
-            if (!eq) misc[1] = 1u;   // a 64-bit fingerprint collision (never expected)
+                for (int u = 0; u < KW; u++) k[r][u] = i < n ? __ldg(src + (size_t)i * KW + u) : 0u;
+            }
+#pragma unroll
+            for (int r = 0; r < BATCH; r++) {
+                if (i0 + r * kST + t >= n) continue;
+                const uint64_t f = fp64<KW>(k[r]);
+                uint32_t h = (uint32_t)(f >> 40) & (kWideSlots - 1);
+                while (fps[h] != f) h = (h + 1) & (kWideSlots - 1);
+                const uint32_t id = sid[h];
+                bool eq = true;
+#pragma unroll
+                for (int u = 0; u < KW; u++) eq &= rep[id * KW + u] == k[r][u];
+                if (!eq) misc[1] = 1u;   // a 64-bit fingerprint collision (never expected)
+            }
         }
     }
     __syncthreads();
@@ -1114,23 +1201,44 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     for (uint32_t i = t; i < kWideSlots; i += kST)
         if (cnt[i]) dcnt[sid[i]] = cnt[i];
     __syncthreads();
-    for (uint32_t me = t; me < nd; me += kST) {   // rank = number of smaller distinct keys
-        uint32_t rank = 0;
-        for (uint32_t j = 0; j < nd; j++) {
-            bool lt = false, decided = false;
+    // sort the distinct keys: 64-bit sort key = the 11 letters from the job's first undecided position
+    // (its keys share the letters before 2*level) and the key's index, by the odd-even transposition +
+    // merge-path block sort; if keys agree on those 11 letters, the indices are sorted again with the
+    // full-key comparison (same block sort)
+    {
+        uint64_t *SA = reinterpret_cast<uint64_t *>(smraw), *SB = SA + fpad(kWideDistinct);   // (table space: free now)
+        const uint32_t p0 = 2u * (sg.buf >> 8);
+        for (uint32_t id = t; id < nd; id += kST) {
+            uint64_t acc = 0;
 #pragma unroll
-            for (int u = 0; u < KW; u++) {
-                const uint32_t x = rep[j * KW + u], y = rep[me * KW + u];
-                if (!decided && x != y) {
-                    lt = x < y;
-                    decided = true;
-                }
+            for (uint32_t q = 0; q < 11; q++) {
+                const uint32_t j = p0 + q;
+                const uint32_t code = j < sg.L ? (rep[id * KW + min(j / 6u, (uint32_t)KW - 1)] >> (25 - 5 * (j % 6))) & 31u : 0u;
+                acc = (acc << 5) | code;
             }
-            rank += lt;
+            SA[fpad(id)] = (acc << 9) | id;
         }
-        order[rank] = me;
+        uint64_t *S = block_sort_smem<uint64_t>(SA, SB, nd);
+        uint32_t ties = 0;
+        for (uint32_t r = t; r + 1 < nd; r += kST) ties += (S[fpad(r)] >> 9) == (S[fpad(r + 1)] >> 9);
+        ties = __syncthreads_count(ties != 0);
+        for (uint32_t r = t; r < nd; r += kST) order[r] = (uint32_t)(S[fpad(r)] & 511u);
+        __syncthreads();
+        if (ties) {
+            uint32_t *IA = reinterpret_cast<uint32_t *>(smraw), *IB = IA + fpad(kWideDistinct);
+            for (uint32_t r = t; r < nd; r += kST) IA[fpad(r)] = order[r];
+            uint32_t *SI = block_sort_idx(IA, IB, nd, [&](uint32_t x, uint32_t y) {
+#pragma unroll
+                for (int u = 0; u < KW; u++) {
+                    const uint32_t a2 = rep[x * KW + u], c2 = rep[y * KW + u];
+                    if (a2 != c2) return a2 < c2;
+                }
+                return false;
+            });
+            for (uint32_t r = t; r < nd; r += kST) order[r] = SI[fpad(r)];
+            __syncthreads();
+        }
     }
-    __syncthreads();
     constexpr int PT = kWideDistinct / kST;   // ranks per thread (contiguous)
     uint32_t cc[PT], tot = 0;
 #pragma unroll
@@ -1176,6 +1284,7 @@ __global__ void __launch_bounds__(kST, 4) k_msd_fin(MsdArgs a) {
     if (j >= end) break;
     const MsdSeg sg = j < nb ? a.q_tiny[a.big_base + j] : a.q_small[a.small_base + j - nb];
     const BucketInfo b = a.buckets[sg.L];
+    const long long c0 = a.dbg_jobs ? clock64() : 0;
     switch (b.kw) {
         case 1: fin_stream<uint32_t, 1>(a, sg, b, fsm); break;
         case 2: fin_stream<uint64_t, 2>(a, sg, b, fsm); break;
@@ -1190,6 +1299,12 @@ __global__ void __launch_bounds__(kST, 4) k_msd_fin(MsdArgs a) {
         default: fin_stream_wide<11>(a, sg, b, fsm); break;
     }
     __syncthreads();   // shared memory is reused by the next job
+    if (a.dbg_jobs && threadIdx.x == 0 && j < 65536) {   // (experiments: per-job cycles)
+        a.dbg_jobs[4 * j] = sg.n;
+        a.dbg_jobs[4 * j + 1] = b.kw | (sg.L << 8);
+        a.dbg_jobs[4 * j + 2] = (uint32_t)(clock64() - c0);
+        a.dbg_jobs[4 * j + 3] = a.buckets[sg.L].kw;
+    }
     }
 }
 constexpr size_t kFinSmemStream = kStreamSlots * 12 + 2 * (kStreamDistinct + kStreamDistinct / 16) * 8 + (kStreamDistinct + 16) * 4;

@@ -993,9 +993,35 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         if (rc) return rc;
         if (!m.finish_radix) {   // this level's finishing jobs (their count is on the device); a job with too
                                  // many distinct keys re-enters the next level
+            static const bool dbg = getenv("WSORT_DEBUG_JOBS") != nullptr;   // (experiments: slowest jobs)
+            uint32_t *dj = nullptr;
+            if (dbg) {
+                cudaMalloc(&dj, 65536 * 16);
+                cudaMemset(dj, 0, 65536 * 16);
+                m.dbg_jobs = dj;
+            }
             rc = launch(c, "k4m_msd_finish", level == 0 ? 2 * key_bytes : 0,
                         [&] { return launch_msd_fin_jobs(m, small_done, big_done, fin_grid, c->stream); });
             if (rc) return rc;
+            if (dbg) {
+                cudaStreamSynchronize(c->stream);
+                std::vector<uint32_t> h(65536 * 4);
+                cudaMemcpy(h.data(), dj, h.size() * 4, cudaMemcpyDeviceToHost);
+                std::vector<std::pair<uint32_t, uint32_t>> v;
+                uint64_t tot = 0;
+                for (uint32_t i = 0; i < 65536; i++)
+                    if (h[4 * i]) {
+                        v.push_back({h[4 * i + 2], i});
+                        tot += h[4 * i + 2];
+                    }
+                std::sort(v.rbegin(), v.rend());
+                fprintf(stderr, "level %u finish: %zu jobs, %.3f Gcycles total; slowest:\n", level, v.size(), tot / 1e9);
+                for (size_t q = 0; q < v.size() && q < 12; q++)
+                    fprintf(stderr, "   job %u: n %u kw %u L %u  %.1f Mcycles\n", v[q].second, h[4 * v[q].second],
+                            h[4 * v[q].second + 1] & 255, h[4 * v[q].second + 1] >> 8, v[q].first / 1e6);
+                cudaFree(dj);
+                m.dbg_jobs = nullptr;
+            }
         }
         if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;   // the level's one host sync
         if (!m.finish_radix) {

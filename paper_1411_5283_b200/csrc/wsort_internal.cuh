@@ -278,6 +278,7 @@ struct MsdArgs {
     uint32_t finish_radix;         // 1: small jobs with kw <= 4 by local LSD radix, else odd-even transposition
     uint32_t stream_fin;           // 1: every child is a finishing job of k_msd_fin, which writes the text
     uint32_t *seg_skip;            // [segments of this level] 1: all keys share the digit (not scattered)
+    uint32_t *dbg_jobs;            // (experiments, nullable) per finishing job: n, kw | L << 8, cycles
     uint8_t *words;                // (stream_fin) output text
     uint32_t small_base;           // k_msd_fin: first job of this launch in q_small
     uint32_t big_base;             // k_msd_fin (streaming): first job of this launch in q_tiny (big jobs)
