@@ -194,7 +194,16 @@ uint64_t wsort_launch_count(const wsort_ctx *c);
  *   library); wsort_load_keys(received); wsort_sort; wsort_set_global(global histogram, word_base,
  *   byte_base); wsort_fetch returns this rank's slice of the global output.
  * Global order = (length, key, source rank): the concatenation of the ranks' outputs in rank
- * order equals the one-GPU output. */
+ * order equals the one-GPU output.
+ *
+ * Split variant (the default when every word has <= 66 letters; SURVEY.md §8(f) NEXT-1 with P > 1):
+ * the words of <= 5 letters never travel. wsort_pack_long (instead of wsort_pack) packs only the
+ * words of >= 6 letters and hands out the context's dense count table; the caller sums the tables of
+ * all ranks in place (all-reduce, NCCL) while the long keys go through sample / partition / all-to-all
+ * / wsort_load_keys as above; wsort_dense_range then tells each rank which global dense words it emits
+ * (rank r: [r*Wd/P, (r+1)*Wd/P), Wd = the words of <= 5 letters), and wsort_sort writes that dense
+ * slice followed by the sorted received keys. The global output is then: the ranks' dense slices in
+ * rank order, then their key slices in rank order. */
 
 /* Local length histogram hist[0..255] (state >= TOKENIZED). */
 int wsort_histogram(wsort_ctx *c, uint64_t *hist);
@@ -220,6 +229,23 @@ int wsort_partition(wsort_ctx *c, const uint32_t *splitters, uint32_t nparts, ui
 /* Adopt received keys: dev_recv holds, for src = 0..nparts-1, the ranges [length][keys] whose key
  * counts are counts[src*256 + L] (host). State -> PACKED; wsort_sort then sorts and emits them. */
 int wsort_load_keys(wsort_ctx *c, const uint32_t *dev_recv, const uint64_t *counts, uint32_t nparts);
+
+/* Split variant, instead of wsort_pack (state TOKENIZED -> PACKED; keys only). Moves the staged keys of
+ * the words of >= 6 letters (K3c) into the packed layout wsort_sample / wsort_partition read; from here
+ * on the local histogram and the packed summary count only those words. *dense_table receives the
+ * context's device table of dense counts of the words of <= 5 letters (u32[*dense_entries]: entry
+ * (26^L - 26)/25 + sum_j c_j 26^(L-1-j) counts the word c_0..c_{L-1}, c_j = letter - 'a'; owned by the
+ * context, valid until the next wsort_load_text): the caller may add the other ranks' tables into it
+ * (device memory, stream-ordered after this call) before wsort_sort. STATE if a word of > 66 letters
+ * was not staged (use wsort_pack). */
+int wsort_pack_long(wsort_ctx *c, uint32_t **dense_table, uint64_t *dense_entries);
+
+/* Split variant, after wsort_load_keys: this context's wsort_sort emits the global dense words
+ * [lo, hi) (indices into the words of <= 5 letters in their global order, from the summed tables and
+ * the global histogram ghist[256], host) in front of the sorted received keys; wsort_fetch then returns
+ * n_words = (hi - lo) + received keys and words = dense slice, then key slice. INVALID_ARG if
+ * hi > sum ghist[1..5] or lo > hi; STATE if the context did not run wsort_pack_long + wsort_load_keys. */
+int wsort_dense_range(wsort_ctx *c, const uint64_t *ghist, uint64_t lo, uint64_t hi);
 
 /* Make wsort_fetch report the GLOBAL bucket offsets (from the all-reduced histogram ghist[256]) and
  * this rank's word_base / byte_base. */

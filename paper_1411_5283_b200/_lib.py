@@ -41,6 +41,7 @@ EXPORTS = [
     "wsort_destroy", "wsort_set_profiling", "wsort_kernel_stats", "wsort_reset_kernel_stats",
     "wsort_launch_count", "wsort_histogram", "wsort_pack", "wsort_sample", "wsort_select_splitters",
     "wsort_partition", "wsort_load_keys", "wsort_set_global", "wsort_fetch_async", "wsort_sync",
+    "wsort_pack_long", "wsort_dense_range",
 ]
 
 
@@ -111,6 +112,8 @@ def load():
     L.wsort_partition.argtypes = [P, P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, P, U64, P, P]
     L.wsort_load_keys.argtypes = [P, P, P, ctypes.c_uint32]
     L.wsort_set_global.argtypes = [P, P, U64, U64]
+    L.wsort_pack_long.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(U64)]
+    L.wsort_dense_range.argtypes = [P, P, U64, U64]
     for name in EXPORTS:
         if name not in ("wsort_strerror", "wsort_destroy", "wsort_launch_count"):
             getattr(L, name).restype = I

@@ -172,6 +172,19 @@ class WSort:
     def pack(self):
         self._check(self._lib.wsort_pack(self._h), "wsort_pack")
 
+    def pack_long(self):
+        """Split variant: pack the words of >= 6 letters; returns the context's dense count table as a
+        zero-copy cuda int32 tensor (u32 counts; the caller may all-reduce it in place)."""
+        torch = _torch()
+        p = ctypes.c_void_p()
+        n = ctypes.c_uint64(0)
+        self._check(self._lib.wsort_pack_long(self._h, ctypes.byref(p), ctypes.byref(n)), "wsort_pack_long")
+        return torch.as_tensor(_DeviceArray(p.value, int(n.value)), device=self.torch_device)
+
+    def dense_range(self, ghist: np.ndarray, lo: int, hi: int):
+        g = np.ascontiguousarray(ghist, dtype=np.uint64)
+        self._check(self._lib.wsort_dense_range(self._h, g.ctypes.data, int(lo), int(hi)), "wsort_dense_range")
+
     def sample(self, nsamples: int, rank: int, rec_words: int, out):
         """Write nsamples sample records into `out` (cuda int32/uint32 tensor [nsamples, rec_words])."""
         assert out.is_cuda and out.numel() >= nsamples * rec_words
@@ -225,6 +238,14 @@ def select_splitters(samples: np.ndarray, nparts: int) -> np.ndarray:
         if rc != L.OK:
             raise WSortError(rc, "wsort_select_splitters")
     return out
+
+
+class _DeviceArray:
+    """A library-owned device int32 array, exposed to torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr or 0, False),
+                                         "strides": None, "version": 2}
 
 
 def _as_buffer(text):

@@ -98,6 +98,13 @@ struct wsort_ctx {
     uint64_t goff[kHistBins + 1] = {0};
     uint32_t gmax = 0;
     uint64_t word_base = 0, byte_base = 0;
+    // multi-GPU split of the ingest path (wsort_pack_long / wsort_dense_range): the dense table may be
+    // summed over the ranks; this context emits the global dense words [dense_lo, dense_hi)
+    bool dist_dense = false, dense_range = false;
+    uint64_t dense_lo = 0, dense_hi = 0;
+    uint64_t dslice_off[kDenseMaxLen + 2] = {0};   // global word index of the slice's first word of length L
+    uint64_t dslice_n[kDenseMaxLen + 2] = {0};     // its words of length L
+    uint64_t slice_words = 0, slice_bytes = 0;     // the dense slice in front of the sorted keys
     DevBuf bk, d_counts, d_cursor, d_sbase, d_split, d_lohi, d_tiles, d_ranges;
 
     // profiling
@@ -409,6 +416,8 @@ int wsort_load_text(wsort_ctx *c, const void *bytes, uint64_t n, int mem, uint64
     c->keys_external = false;
     c->has_global = false;
     c->word_base = c->byte_base = 0;
+    c->dist_dense = c->dense_range = false;
+    c->slice_words = c->slice_bytes = 0;
     uint64_t nsteps = (n + kTkStep - 1) / kTkStep;
     size_t need = kTextFrontPad + nsteps * kTkStep + kIgStep + kTkHalo + 64;   // ingest reads up to 16 KiB + halo past a range
     int rc = ensure(c, c->text_alloc, need, "text");
@@ -1171,12 +1180,80 @@ int sort_msd(wsort_ctx *c, bool finish_radix) {
                          });
 }
 
-// AUTO (keys only, every word <= 48 letters): the one-pass ingest already counted the words of L <= 5
+// K3c: the ingest's staged keys (chunks) into their length buckets in buffer A (layout of `db`)
+int chunk_scatter(wsort_ctx *c, const BucketInfo *db, double key_bytes) {
+    int rc;
+    if ((rc = ensure(c, c->d_lcursor, 256 * 4, "length cursors"))) return rc;
+    CK(cudaMemsetAsync(c->d_lcursor.p, 0, 256 * 4, c->stream), "memset length cursors");
+    L0Args la{};
+    la.buckets = db;
+    la.pool = static_cast<const uint32_t *>(c->pool.p);
+    la.chunk_cls = static_cast<const uint32_t *>(c->chunk_cls.p);
+    la.chunk_fill = static_cast<const uint32_t *>(c->chunk_fill.p);
+    la.lcursor = static_cast<uint32_t *>(c->d_lcursor.p);
+    la.dst = static_cast<uint32_t *>(c->keys_a.p);
+    la.cta_chunks = c->cta_chunks;
+    la.used_chunks = std::min(c->h_ig[kIgMaxChunks], c->cta_chunks);
+    return launch(c, "k3c_chunk_scatter", 2 * key_bytes, [&] { return launch_lscatter(la, c->tk.grid, c->stream); });
+}
+
+// The dense buckets (L <= 5) on the second stream, beside the MSD of the long ones: scan + compact the
+// dense table, then emit bucket L's words bk[L].word_off .. + bk[L].n (global dense word indices) at
+// bk[L].byte_off. Records ev_join on the aux stream; the caller joins.
+int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketInfo *d_bk, double out_bytes) {
+    uint32_t dpfx[257], ndt = 0;   // dense emit tiles, bucket by bucket (tile_from_prefix)
+    const uint32_t te = dense_emit_tile_words();
+    for (uint32_t L = 0; L < 256; L++) {
+        dpfx[L] = ndt;
+        if (L >= 1 && L <= kDenseMaxLen) ndt += (bk[L].n + te - 1) / te;
+    }
+    dpfx[256] = ndt;
+    const uint32_t ne = dense_entries(), nblk = dense_scan_blocks(ne);
+    int rc;
+    if ((rc = ensure(c, c->d_blk_sum, (size_t)nblk * 4, "dense block sums"))) return rc;
+    if ((rc = ensure(c, c->d_blk_nnz, (size_t)nblk * 4, "dense block nnz"))) return rc;
+    if ((rc = ensure(c, c->d_ent_idx, (size_t)ne * 4, "dense entries"))) return rc;
+    if ((rc = ensure(c, c->d_ent_end, (size_t)ne * 4, "dense entry ends"))) return rc;
+    if ((rc = ensure(c, c->d_n_ent, 16, "dense entry count"))) return rc;
+    if ((rc = arena_upload(c, c->d_tiles2, dpfx, sizeof dpfx, "dense tile prefix"))) return rc;
+    static const bool no_aux = getenv("WSORT_NO_AUX") != nullptr;   // (experiments: serial dense branch)
+    if (!c->aux) {
+        if (no_aux) c->aux = c->stream;
+        else CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking), "aux stream");
+        CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
+        CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
+    }
+    CK(cudaEventRecord(c->ev_fork, c->stream), "fork");
+    CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0), "fork wait");
+    DenseArgs da{};
+    da.dense = static_cast<const uint32_t *>(c->dense.p);
+    da.n_entries = ne;
+    da.blk_sum = static_cast<uint32_t *>(c->d_blk_sum.p);
+    da.blk_nnz = static_cast<uint32_t *>(c->d_blk_nnz.p);
+    da.ent_idx = static_cast<uint32_t *>(c->d_ent_idx.p);
+    da.ent_end = static_cast<uint32_t *>(c->d_ent_end.p);
+    da.n_ent = static_cast<uint32_t *>(c->d_n_ent.p);
+    rc = launch_on(c, c->aux, "k2d_dense_scan", 2.0 * ne * 4, [&] { return launch_dense_scan(da, c->aux); });
+    if (rc) return rc;
+    DenseEmitArgs ea{};
+    ea.buckets = d_bk;
+    ea.tile_pfx = static_cast<const uint32_t *>(c->d_tiles2.p);
+    ea.ntiles = ndt;
+    ea.ent_idx = da.ent_idx;
+    ea.ent_end = da.ent_end;
+    ea.n_ent = da.n_ent;
+    ea.words = static_cast<uint8_t *>(c->words.p);
+    rc = launch_on(c, c->aux, "k5d_emit_dense", out_bytes, [&] { return launch_emit_dense(ea, c->aux); });
+    if (rc) return rc;
+    CK(cudaEventRecord(c->ev_join, c->aux), "join");
+    return WSORT_OK;
+}
+
+// AUTO (keys only, every word <= 66 letters): the one-pass ingest already counted the words of L <= 5
 // (dense tables) and staged the longer ones as keys in chunks. Dense buckets: scan + compact + emit.
 // Long buckets: K3c moves the staged keys into their length buckets, then MSD_OETS sorts them.
 int sort_dense_msd(wsort_ctx *c) {
     const Summary &s = *c->h_sum;
-    const uint32_t lmax = s.max_len;
     uint32_t max_tw, levels;
     uint64_t key_words;
     std::vector<BucketInfo> bk = msd_buckets(s, kDenseMaxLen + 1, max_tw, levels, key_words);
@@ -1185,73 +1262,50 @@ int sort_dense_msd(wsort_ctx *c) {
     if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
     if ((rc = arena_upload(c, c->plan, bk.data(), bk.size() * sizeof(BucketInfo), "plan"))) return rc;
     const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
-    if (n_dense) {   // dense buckets (scan + compact + emit) on the second stream, beside the MSD
-        uint32_t dpfx[257], ndt = 0;   // dense emit tiles, bucket by bucket (tile_from_prefix)
-        const uint32_t te = dense_emit_tile_words();
-        for (uint32_t L = 0; L < 256; L++) {
-            dpfx[L] = ndt;
-            if (L >= 1 && L <= std::min<uint32_t>(lmax, kDenseMaxLen)) ndt += (bk[L].n + te - 1) / te;
-        }
-        dpfx[256] = ndt;
-        const uint32_t ne = dense_entries(), nblk = dense_scan_blocks(ne);
-        if ((rc = ensure(c, c->d_blk_sum, (size_t)nblk * 4, "dense block sums"))) return rc;
-        if ((rc = ensure(c, c->d_blk_nnz, (size_t)nblk * 4, "dense block nnz"))) return rc;
-        if ((rc = ensure(c, c->d_ent_idx, (size_t)ne * 4, "dense entries"))) return rc;
-        if ((rc = ensure(c, c->d_ent_end, (size_t)ne * 4, "dense entry ends"))) return rc;
-        if ((rc = ensure(c, c->d_n_ent, 16, "dense entry count"))) return rc;
-        if ((rc = arena_upload(c, c->d_tiles2, dpfx, sizeof dpfx, "dense tile prefix"))) return rc;
-        static const bool no_aux = getenv("WSORT_NO_AUX") != nullptr;   // (experiments: serial dense branch)
-        if (!c->aux) {
-            if (no_aux) c->aux = c->stream;
-            else CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking), "aux stream");
-            CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
-            CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
-        }
-        CK(cudaEventRecord(c->ev_fork, c->stream), "fork");
-        CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0), "fork wait");
-        DenseArgs da{};
-        da.dense = static_cast<const uint32_t *>(c->dense.p);
-        da.n_entries = ne;
-        da.blk_sum = static_cast<uint32_t *>(c->d_blk_sum.p);
-        da.blk_nnz = static_cast<uint32_t *>(c->d_blk_nnz.p);
-        da.ent_idx = static_cast<uint32_t *>(c->d_ent_idx.p);
-        da.ent_end = static_cast<uint32_t *>(c->d_ent_end.p);
-        da.n_ent = static_cast<uint32_t *>(c->d_n_ent.p);
-        rc = launch_on(c, c->aux, "k2d_dense_scan", 2.0 * ne * 4, [&] { return launch_dense_scan(da, c->aux); });
-        if (rc) return rc;
-        DenseEmitArgs ea{};
-        ea.buckets = d_bk;
-        ea.tile_pfx = static_cast<const uint32_t *>(c->d_tiles2.p);
-        ea.ntiles = ndt;
-        ea.ent_idx = da.ent_idx;
-        ea.ent_end = da.ent_end;
-        ea.n_ent = da.n_ent;
-        ea.words = static_cast<uint8_t *>(c->words.p);
-        rc = launch_on(c, c->aux, "k5d_emit_dense", (double)s.byte_off[kDenseMaxLen + 1],
-                       [&] { return launch_emit_dense(ea, c->aux); });
-        if (rc) return rc;
-        CK(cudaEventRecord(c->ev_join, c->aux), "join");
-    }
+    if (n_dense && (rc = dense_branch(c, bk, d_bk, (double)s.byte_off[kDenseMaxLen + 1]))) return rc;
     if (W > n_dense) {
-        if ((rc = ensure(c, c->d_lcursor, 256 * 4, "length cursors"))) return rc;
-        CK(cudaMemsetAsync(c->d_lcursor.p, 0, 256 * 4, c->stream), "memset length cursors");
         rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, W - n_dense, false,
                            [&](const BucketInfo *db, double key_bytes) {
-                               L0Args la{};
-                               la.buckets = db;
-                               la.pool = static_cast<const uint32_t *>(c->pool.p);
-                               la.chunk_cls = static_cast<const uint32_t *>(c->chunk_cls.p);
-                               la.chunk_fill = static_cast<const uint32_t *>(c->chunk_fill.p);
-                               la.lcursor = static_cast<uint32_t *>(c->d_lcursor.p);
-                               la.dst = static_cast<uint32_t *>(c->keys_a.p);
-                               la.cta_chunks = c->cta_chunks;
-                               la.used_chunks = std::min(c->h_ig[kIgMaxChunks], c->cta_chunks);
-                               return launch(c, "k3c_chunk_scatter", 2 * key_bytes,
-                                             [&] { return launch_lscatter(la, c->tk.grid, c->stream); });
+                               return chunk_scatter(c, db, key_bytes);
                            },
                            d_bk);
     }
     if (n_dense) {   // join: the sort is complete when both streams are
+        const cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+        if (!rc && e != cudaSuccess) return cuda_err(c, e, "join wait");
+    }
+    return rc;
+}
+
+// Split multi-GPU sort (after wsort_pack_long, the all-reduce of the dense tables, wsort_load_keys and
+// wsort_dense_range): this rank's slice of the global dense words, then the keys it received, sorted.
+int sort_dist_dense(wsort_ctx *c) {
+    const Summary &s = *c->h_sum;   // the received keys (lengths >= 6 only)
+    uint32_t max_tw, levels;
+    uint64_t key_words;
+    std::vector<BucketInfo> bk = msd_buckets(s, kDenseMaxLen + 1, max_tw, levels, key_words);
+    uint64_t dbytes = 0;
+    for (uint32_t L = 1; L <= kDenseMaxLen; L++) {
+        BucketInfo &b = bk[L];
+        b = BucketInfo{};
+        b.word_off = c->dslice_off[L];
+        b.n = (uint32_t)c->dslice_n[L];
+        b.byte_off = dbytes;
+        b.kw = 1;
+        dbytes += c->dslice_n[L] * (L + 1);
+    }
+    for (uint32_t L = kDenseMaxLen + 1; L < 256; L++) bk[L].byte_off += dbytes;
+    int rc;
+    if ((rc = ensure(c, c->words, dbytes + s.byte_off[256] + 64, "words"))) return rc;
+    if ((rc = arena_upload(c, c->plan, bk.data(), bk.size() * sizeof(BucketInfo), "plan"))) return rc;
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
+    const bool dense = c->slice_words != 0;
+    if (dense && (rc = dense_branch(c, bk, d_bk, (double)dbytes))) return rc;
+    if (s.n_words)
+        rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, s.n_words, false,
+                           [&](const BucketInfo *, double) { return (int)WSORT_OK; },   // keys_a: wsort_load_keys
+                           d_bk);
+    if (dense) {
         const cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_join, 0);
         if (!rc && e != cudaSuccess) return cuda_err(c, e, "join wait");
     }
@@ -1280,7 +1334,9 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     // the dense + MSD path reads what K1 ingest left (dense counts, staged keys): a text this context
     // tokenized, keys only, every word staged (<= 48 letters)
     const bool ingest_ok = !want_src && !c->packed_pending && !c->keys_external && c->h_ig[kIgVeryLong] == 0;
-    if (algo == WSORT_ALGO_OETS_MERGE) {
+    if (c->keys_external && c->dense_range) {   // split multi-GPU sort: dense slice + received keys
+        rc = sort_dist_dense(c);
+    } else if (algo == WSORT_ALGO_OETS_MERGE) {
         rc = sort_oets(c, want_src);
     } else if ((algo == WSORT_ALGO_AUTO || algo == WSORT_ALGO_DENSE_MSD) && ingest_ok) {
         rc = sort_dense_msd(c);
@@ -1320,8 +1376,8 @@ int fetch_impl(wsort_ctx *c, wsort_result *r, bool wait) {
     if (r->mem != WSORT_MEM_HOST && r->mem != WSORT_MEM_DEVICE) return set_err(c, WSORT_E_INVALID_ARG, "bad mem");
     cudaSetDevice(c->device);
     const Summary &s = *c->h_sum;
-    r->n_words = s.n_words;
-    r->words_len = s.byte_off[256];
+    r->n_words = s.n_words + c->slice_words;          // (dense slice of a split multi-GPU sort, if any)
+    r->words_len = s.byte_off[256] + c->slice_bytes;
     r->max_len = c->has_global ? c->gmax : s.max_len;
     r->word_base = c->word_base;
     r->byte_base = c->byte_base;
@@ -1484,6 +1540,55 @@ int wsort_pack(wsort_ctx *c) {
     return WSORT_OK;
 }
 
+int wsort_pack_long(wsort_ctx *c, uint32_t **dense_table, uint64_t *dense_entries_out) {
+    if (!c || !dense_table || !dense_entries_out) return WSORT_E_INVALID_ARG;
+    if (c->state != ST_TOKENIZED || c->keys_external || c->packed_pending)
+        return set_err(c, WSORT_E_STATE, "wsort_pack_long needs a freshly tokenized text");
+    if (c->h_ig[kIgVeryLong])
+        return set_err(c, WSORT_E_STATE, "wsort_pack_long: words longer than %d letters were not staged", 6 * kMaxStageKw);
+    cudaSetDevice(c->device);
+    Summary &s = *c->h_sum;
+    std::vector<uint64_t> n(256, 0);
+    for (uint32_t L = kDenseMaxLen + 1; L < 256; L++) n[L] = s.off[L + 1] - s.off[L];
+    summary_from_counts(s, n.data());   // the packed keys: lengths >= 6 only
+    int rc;
+    if ((rc = upload_small(c, c->d_sum, &s, sizeof(Summary), "long summary"))) return rc;
+    std::vector<BucketInfo> bk = bucket_table(s);
+    if ((rc = upload_small(c, c->bk, bk.data(), bk.size() * sizeof(BucketInfo), "bucket table"))) return rc;
+    if ((rc = ensure(c, c->keys_a, s.key_off[256] * 4 + 64, "keys_a"))) return rc;
+    if (s.n_words && (rc = chunk_scatter(c, static_cast<const BucketInfo *>(c->bk.p), (double)s.key_off[256] * 4)))
+        return rc;
+    c->packed_pending = true;
+    c->dist_dense = true;
+    c->state = ST_PACKED;
+    *dense_table = static_cast<uint32_t *>(c->dense.p);
+    *dense_entries_out = dense_entries();
+    return WSORT_OK;
+}
+
+int wsort_dense_range(wsort_ctx *c, const uint64_t *ghist, uint64_t lo, uint64_t hi) {
+    if (!c || !ghist || lo > hi) return WSORT_E_INVALID_ARG;
+    if (!c->dist_dense || !c->keys_external || !c->packed_pending)
+        return set_err(c, WSORT_E_STATE, "wsort_dense_range needs wsort_pack_long, then wsort_load_keys");
+    uint64_t g = 0;   // global word index of the first word of length L
+    for (uint32_t L = 1; L <= kDenseMaxLen; L++) {
+        const uint64_t a = std::max(g, lo), b = std::min(g + ghist[L], hi);
+        c->dslice_off[L] = a;
+        c->dslice_n[L] = b > a ? b - a : 0;
+        g += ghist[L];
+    }
+    if (hi > g) return set_err(c, WSORT_E_INVALID_ARG, "dense range end %llu > %llu dense words",
+                               (unsigned long long)hi, (unsigned long long)g);
+    if (g > 0xffffffffull) return set_err(c, WSORT_E_TOO_LARGE, "more than 2^32 - 1 dense words");
+    c->slice_words = hi - lo;
+    c->slice_bytes = 0;
+    for (uint32_t L = 1; L <= kDenseMaxLen; L++) c->slice_bytes += c->dslice_n[L] * (L + 1);
+    c->dense_lo = lo;
+    c->dense_hi = hi;
+    c->dense_range = true;
+    return WSORT_OK;
+}
+
 int wsort_sample(wsort_ctx *c, uint32_t nsamples, uint32_t rank, uint32_t rec_words, uint32_t *dev_records) {
     if (!c || (nsamples && !dev_records) || rec_words < 3) return WSORT_E_INVALID_ARG;
     if (c->state != ST_PACKED || !c->packed_pending) return set_err(c, WSORT_E_STATE, "wsort_sample needs packed keys");
@@ -1641,6 +1746,8 @@ int wsort_load_keys(wsort_ctx *c, const uint32_t *dev_recv, const uint64_t *coun
     c->n = 0;
     c->packed_pending = true;
     c->keys_external = true;
+    c->dense_range = false;
+    c->slice_words = c->slice_bytes = 0;
     c->has_global = false;
     c->state = ST_PACKED;
     return WSORT_OK;

@@ -19,7 +19,27 @@ import torch.multiprocessing as mp
 
 import gen
 import oracle
-from paper_1411_5283_b200.dist import DistSorter, KW, TorchComm, kw_of, shard_cuts, sort_distributed
+from paper_1411_5283_b200.dist import (DistSorter, KW, RankResult, TorchComm, assemble, dense_byte_pos,
+                                       dense_range, kw_of, shard_cuts, sort_distributed, split_mode)
+
+DENSE_BASE = [0, 0, 26, 702, 18278, 475254, 12356630]   # entries of the dense tables of lengths < L
+
+
+def dense_index(w: bytes) -> int:
+    x = 0
+    for ch in w:
+        x = x * 26 + (ch - 97)
+    return DENSE_BASE[len(w)] + x
+
+
+def dense_word(e: int) -> bytes:
+    L = max(l for l in range(1, 6) if DENSE_BASE[l] <= e)
+    x = e - DENSE_BASE[L]
+    out = []
+    for _ in range(L):
+        out.append(97 + x % 26)
+        x //= 26
+    return bytes(reversed(out))
 
 
 def pack_word(w: bytes) -> list:
@@ -54,10 +74,25 @@ class FakeWS:
         return h
 
     def pack(self):
+        self.dense = None
         self.buckets = {}
         for w in self.words:
             self.buckets.setdefault(len(w), []).append(pack_word(w))
         self.flat = [(L, k) for L in sorted(self.buckets) for k in self.buckets[L]]
+
+    def pack_long(self):
+        """Split variant: dense table (the real indexing) for L <= 5; only longer words are packed."""
+        table = np.zeros(DENSE_BASE[6], np.int32)
+        for w in self.words:
+            if len(w) <= 5:
+                table[dense_index(w)] += 1
+        self.words = [w for w in self.words if len(w) > 5]
+        self.pack()
+        self.dense = torch.from_numpy(table)
+        return self.dense
+
+    def dense_range(self, ghist, lo, hi):
+        self.dlo, self.dhi = lo, hi
 
     def sample(self, n, rank, rec_words, out):
         W = len(self.flat)
@@ -97,6 +132,7 @@ class FakeWS:
         return counts, sw
 
     def load_keys(self, recv, counts):
+        self.dlo = self.dhi = 0
         r = recv.numpy().view(np.uint32)
         pos = 0
         self.recv = {}
@@ -109,11 +145,19 @@ class FakeWS:
 
     def sort(self, algo="auto"):
         self.out = b""
+        if self.dense is not None and self.dhi > self.dlo:   # this rank's share of the summed dense table
+            t = self.dense.numpy()
+            nz = np.nonzero(t)[0]
+            ends = np.cumsum(t[nz].astype(np.int64))
+            for e, end in zip(nz, ends):
+                a, b = max(int(end) - int(t[e]), self.dlo), min(int(end), self.dhi)
+                if b > a:
+                    self.out += (dense_word(int(e)) + b"\n") * (b - a)
         for L in sorted(self.recv):
             for k in sorted(self.recv[L]):
                 w = bytes(((k[j // 6] >> (25 - 5 * (j % 6))) & 31) | 0x60 for j in range(L))
                 self.out += w + b"\n"
-        self.n = sum(len(v) for v in self.recv.values())
+        self.n = sum(len(v) for v in self.recv.values()) + (self.dhi - self.dlo)
 
     def sizes(self):
         class S:
@@ -127,15 +171,15 @@ class FakeWS:
         self.ghist, self.wb, self.bb = ghist, wb, bb
 
 
-def _worker(rank, world, port, text, q):
+def _worker(rank, world, port, text, q, mode):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         cuts = shard_cuts(text, world)
         ws = FakeWS()
         comm = TorchComm("cpu")
-        res = sort_distributed(ws, text[cuts[rank]: cuts[rank + 1]], cuts[rank], comm, nsamples=64)
-        q.put((rank, ws.out, res.word_base, res.byte_base, [int(x) for x in ws.ghist]))
+        res = sort_distributed(ws, text[cuts[rank]: cuts[rank + 1]], cuts[rank], comm, nsamples=64, mode=mode)
+        q.put((rank, ws.out, res, [int(x) for x in ws.ghist]))
     finally:
         dist.destroy_process_group()
 
@@ -148,8 +192,9 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("mode", ["split", "legacy"])
 @pytest.mark.parametrize("src", ["config1", "dups"])
-def test_gloo_world2_matches_oracle(src):
+def test_gloo_world2_matches_oracle(src, mode):
     if src == "config1":
         text = gen.generate(1)[0][:60_000].copy()
     else:   # heavy duplicates: splitters fall inside runs of one word
@@ -157,7 +202,7 @@ def test_gloo_world2_matches_oracle(src):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, text, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, text, q, mode)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=240) for _ in procs)
@@ -165,11 +210,16 @@ def test_gloo_world2_matches_oracle(src):
         p.join(timeout=60)
         assert p.exitcode == 0
     ref = oracle.sort(text, oracle.MERGE)
-    assert b"".join(r[1] for r in res) == ref.words
-    assert res[0][2] == 0 and res[1][2] == ref.words.count(b"\n") - res[1][1].count(b"\n")
-    assert res[1][3] == len(res[0][1])
+    assert assemble([(r[1], r[2]) for r in res]) == ref.words
+    if mode == "legacy":
+        assert b"".join(r[1] for r in res) == ref.words
+        assert res[0][2].word_base == 0 and res[1][2].word_base == ref.words.count(b"\n") - res[1][1].count(b"\n")
+        assert res[1][2].byte_base == len(res[0][1])
+    else:
+        assert all(len(r[2].slices) == 2 for r in res)
+        assert res[0][2].slices[0][2] == 0                      # rank 0's dense slice opens the output
     hist = oracle.histogram(text)[0]
-    assert res[0][4] == [int(x) for x in hist]
+    assert res[0][3] == [int(x) for x in hist]
 
 
 def test_shard_cuts_never_split_a_word():
@@ -203,3 +253,28 @@ def test_select_splitters_host_function():
         order = sorted(range(n), key=lambda i: (rec[i, 0], rec[i, 2], rec[i, 3], rec[i, 1], i))
         for d in range(1, P):
             assert (spl[d - 1] == rec[order[(d * n) // P]]).all()
+
+
+def test_dense_split_host_arithmetic():
+    """dense_range / dense_byte_pos / split_mode against a direct count on a known histogram."""
+    ghist = np.zeros(256, np.uint64)
+    ghist[1], ghist[2], ghist[3], ghist[5], ghist[7] = 3, 4, 5, 2, 6
+    wd = 3 + 4 + 5 + 2
+    layout = b"a\n" * 3 + b"ab\n" * 4 + b"abc\n" * 5 + b"abcde\n" * 2
+    for w in range(wd + 1):
+        assert dense_byte_pos(ghist, w) == len(b"".join(layout.split(b"\n")[i] + b"\n" for i in range(w)))
+    for P in (1, 2, 3, 5, 14, 20):
+        rs = [dense_range(ghist, r, P) for r in range(P)]
+        assert rs[0][0] == 0 and rs[-1][1] == wd
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(P - 1))
+        assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+    assert split_mode(ghist)
+    ghist[67] = 1
+    assert not split_mode(ghist)
+    assert split_mode(np.zeros(256, np.uint64))
+
+
+def test_assemble_places_slices():
+    outs = [(b"aa\nccc\n", RankResult(2, 7, 0, 0, [(0, 3, 0, 1, 0), (3, 4, 6, 1, 2)])),
+            (b"bb\nddd\n", RankResult(2, 7, 1, 3, [(0, 3, 3, 1, 1), (3, 4, 10, 1, 3)]))]
+    assert assemble(outs) == b"aa\nbb\nccc\nddd\n"

@@ -1,8 +1,10 @@
 """Multi-rank pipeline on one GPU (-m gpu): P virtual ranks, each with its own libwsort context,
-run the real kernels (pack, sample, partition, regroup, sort, emit) in lockstep; the collectives are
-done by host-side concatenation (no kernel ever waits on another rank). The concatenation of the
-ranks' outputs must equal the oracle's output byte for byte, every rank must report the global
-bucket offsets, and word_base / byte_base must tile the output."""
+run the real kernels (ingest, pack / pack_long, sample, partition, regroup, sort, emit) in lockstep;
+the collectives (all-reduce of the dense tables, all-gather, all-to-all) are done by host-side
+concatenation / summation (no kernel ever waits on another rank). The output assembled from the
+ranks' slices must equal the oracle's output byte for byte, every rank must report the global bucket
+offsets, and the slices must tile the output. Both modes: split (dense tables all-reduced, only the
+words of >= 6 letters exchanged) and legacy (every word exchanged)."""
 import numpy as np
 import pytest
 
@@ -12,11 +14,11 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def run(text, P, algo="auto", nsamples=256):
+def run(text, P, algo="auto", nsamples=256, mode="auto"):
     from paper_1411_5283_b200 import WSort
     from paper_1411_5283_b200.dist import sort_emulated
 
-    ranks, cuts = sort_emulated(lambda: WSort(0), text, P, algo=algo, nsamples=nsamples)
+    ranks, cuts = sort_emulated(lambda: WSort(0), text, P, algo=algo, nsamples=nsamples, mode=mode)
     outs = []
     for ws, res in ranks:
         words, off = ws.fetch()
@@ -26,45 +28,88 @@ def run(text, P, algo="auto", nsamples=256):
     return outs, cuts
 
 
-@pytest.mark.parametrize("P", [2, 3, 4, 8])
-@pytest.mark.parametrize("cfg", [1, 2])
-def test_emulated_ranks_match_oracle(cfg, P):
-    text, _ = gen.generate(cfg)
-    ref = oracle.sort(text, oracle.MERGE)
-    outs, cuts = run(text, P)
-    assert b"".join(o[0] for o in outs) == ref.words
-    wb = bb = 0
+def check(outs, ref, split):
+    from paper_1411_5283_b200.dist import assemble
+
+    assert assemble([(o[0], o[2]) for o in outs]) == ref.words
+    tiles = []
     for words, off, res in outs:
         assert off == ref.off                       # every rank reports the global offsets
-        assert res.word_base == wb and res.byte_base == bb
-        wb += words.count(b"\n")
-        bb += len(words)
-    assert wb == ref.n_words
+        assert res.n_words == words.count(b"\n") and res.words_len == len(words)
+        assert len(res.slices) == (2 if split else 1)
+        for lo, nb, gb, nw, gw in res.slices:
+            piece = words[lo: lo + nb]
+            assert piece.count(b"\n") == nw
+            assert ref.words[:gb].count(b"\n") == gw   # word base consistent with byte base
+            tiles.append((gb, nb))
+    tiles.sort()
+    pos = 0
+    for gb, nb in tiles:
+        assert gb == pos
+        pos += nb
+    assert pos == len(ref.words)
+    if not split:   # legacy: the concatenation in rank order is the output
+        assert b"".join(o[0] for o in outs) == ref.words
 
 
-def test_emulated_heavy_duplicates_and_long_words():
+@pytest.mark.parametrize("mode", ["split", "legacy"])
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_emulated_ranks_match_oracle(cfg, P, mode):
+    text, _ = gen.generate(cfg)
+    ref = oracle.sort(text, oracle.MERGE)
+    outs, cuts = run(text, P, mode=mode)
+    check(outs, ref, mode == "split")
+
+
+@pytest.mark.parametrize("mode", ["split", "legacy"])
+def test_emulated_heavy_duplicates_and_long_words(mode):
     parts = [b"a " * 40000, b"the " * 30000, b"zz " * 20000,
              b" ".join(bytes([97 + (i * j) % 26 for j in range(13 + i % 40)]) for i in range(4000))]
     text = np.frombuffer(b" ".join(parts), np.uint8).copy()
     ref = oracle.sort(text, oracle.MERGE)
     for P in (2, 4, 8):
-        outs, _ = run(text, P, nsamples=128)
-        assert b"".join(o[0] for o in outs) == ref.words
-        # a hot word is split across ranks (by source rank), not dumped on one
+        outs, _ = run(text, P, nsamples=128, mode=mode)
+        check(outs, ref, mode == "split")
+        # a hot word is split across ranks (by source rank / dense share), not dumped on one
         if P == 8:
             assert max(len(o[0]) for o in outs) < 0.6 * len(ref.words)
 
 
-def test_emulated_config3_four_ranks_oets():
+def test_emulated_split_dense_share_is_balanced():
+    """Split mode: every rank emits Wd/P dense words (+-1) whatever its shard held."""
+    text, _ = gen.generate(2)
+    ref = oracle.sort(text, oracle.MERGE)
+    P = 4
+    outs, _ = run(text, P, mode="split")
+    check(outs, ref, True)
+    wd = sum(ref.off[L + 1] - ref.off[L] for L in range(1, 6))
+    for _, _, res in outs:
+        assert abs(res.slices[0][3] - wd / P) <= 1
+
+
+def test_emulated_auto_falls_back_to_legacy_for_very_long_words():
+    """A word of > 66 letters is not staged by K1: every rank must take the legacy exchange."""
+    text = np.frombuffer(b"alpha beta " * 500 + b"x" * 80 + b" gamma " + b"y" * 70 + b" delta", np.uint8).copy()
+    ref = oracle.sort(text, oracle.MERGE)
+    outs, _ = run(text, 2, nsamples=16)
+    check(outs, ref, False)
+    with pytest.raises(ValueError):
+        run(text, 2, nsamples=16, mode="split")
+
+
+@pytest.mark.parametrize("mode", ["split", "legacy"])
+def test_emulated_config3_four_ranks(mode):
     text, _ = gen.generate(3, n=8 << 20)
     ref = oracle.sort(text, oracle.MERGE)
-    outs, _ = run(text, 4, algo="oets_merge")
-    assert b"".join(o[0] for o in outs) == ref.words
+    outs, _ = run(text, 4, algo="oets_merge", mode=mode)
+    check(outs, ref, mode == "split")
 
 
-def test_emulated_empty_and_tiny():
-    for t in (b"", b"x", b"a b", b"   !!! "):
+@pytest.mark.parametrize("mode", ["split", "legacy"])
+def test_emulated_empty_and_tiny(mode):
+    for t in (b"", b"x", b"a b", b"   !!! ", b"abcdefgh", b"abcdefgh a"):
         text = np.frombuffer(t, np.uint8).copy()
         ref = oracle.sort(text, oracle.MERGE)
-        outs, _ = run(text, 2, nsamples=8)
-        assert b"".join(o[0] for o in outs) == ref.words
+        outs, _ = run(text, 2, nsamples=8, mode=mode)
+        check(outs, ref, mode == "split")
