@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cerrno>
 #include <cstdarg>
 #include <cstdio>
@@ -1620,16 +1621,33 @@ int wsort_select_splitters(const uint32_t *samples, uint64_t nsamples, uint32_t 
                            uint32_t *splitters) {
     if (!samples || !splitters || nparts < 1 || nparts > kMaxRanks || rec_words < 3 || nsamples < nparts)
         return WSORT_E_INVALID_ARG;
-    std::vector<uint64_t> idx(nsamples);
-    for (uint64_t i = 0; i < nsamples; i++) idx[i] = i;
-    std::sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) {
-        const int r = cmp_records(samples + a * rec_words, samples + b * rec_words, rec_words);
-        return r < 0 || (r == 0 && a < b);
-    });
-    for (uint32_t d = 1; d < nparts; d++) {
-        const uint64_t k = (d * nsamples) / nparts;
-        memcpy(splitters + (size_t)(d - 1) * rec_words, samples + idx[k] * rec_words, rec_words * 4);
-    }
+    // (length, first key word) as one u64 decides almost every comparison without touching the records
+    struct Ent {
+        uint64_t head, i;
+    };
+    std::vector<Ent> e(nsamples);
+    for (uint64_t i = 0; i < nsamples; i++)
+        e[i] = Ent{((uint64_t)samples[i * rec_words] << 32) | samples[i * rec_words + 2], i};
+    auto less = [&](const Ent &x, const Ent &y) {
+        if (x.head != y.head) return x.head < y.head;
+        const int r = cmp_records(samples + x.i * rec_words, samples + y.i * rec_words, rec_words);
+        return r < 0 || (r == 0 && x.i < y.i);
+    };
+    // only the nparts-1 order statistics are needed: multi-select (median quantile first, then each
+    // side), O(n log nparts) instead of a full sort
+    std::vector<uint64_t> ks(nparts - 1);
+    for (uint32_t d = 1; d < nparts; d++) ks[d - 1] = (d * nsamples) / nparts;
+    std::function<void(uint64_t, uint64_t, size_t, size_t)> select = [&](uint64_t a, uint64_t b, size_t i, size_t j) {
+        if (i >= j) return;
+        const size_t m = (i + j) / 2;
+        const uint64_t k = ks[m];
+        std::nth_element(e.begin() + a, e.begin() + k, e.begin() + b, less);
+        select(a, k, i, m);
+        select(k + 1, b, m + 1, j);
+    };
+    select(0, nsamples, 0, ks.size());
+    for (uint32_t d = 1; d < nparts; d++)
+        memcpy(splitters + (size_t)(d - 1) * rec_words, samples + e[ks[d - 1]].i * rec_words, rec_words * 4);
     return WSORT_OK;
 }
 
