@@ -1070,12 +1070,9 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
     };
     const uint32_t W = (sg.L + 1 + 16 + 3) & ~3u;
     uint8_t *R = reinterpret_cast<uint8_t *>(slots);
-    if (nd * W + 4 <= kStreamSlots * (sizeof(T) + 4)) {
-        build_run_patterns<KW>(R, W, sg.L, nd, key_of);
-        emit_runs_text(a, b, sg.L, sg.start, n, R, W, pos, nd);
-    } else {
-        emit_job_text<KW>(a, b, sg.L, sg.start, n, R, [&](uint32_t i, uint32_t (&k)[KW]) { key_of(run_of(pos, nd, i), k); });
-    }
+    if (nd * W + 4 > kStreamSlots * (sizeof(T) + 4)) R = a.pat + (size_t)blockIdx.x * kFinPatBytes;   // (global)
+    build_run_patterns<KW>(R, W, sg.L, nd, key_of);
+    emit_runs_text(a, b, sg.L, sg.start, n, R, W, pos, nd);
 }
 
 // Finishing job of KW >= 3-word keys of any size: as fin_stream, but the table key is a 64-bit
@@ -1262,12 +1259,9 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
         for (int u = 0; u < KW; u++) k[u] = rep[id * KW + u];
     };
     const uint32_t W = (sg.L + 1 + 16 + 3) & ~3u;
-    if (nd * W + 4 <= kWideSlots * 16) {
-        build_run_patterns<KW>(smraw, W, sg.L, nd, key_of);
-        emit_runs_text(a, b, sg.L, sg.start, n, smraw, W, pos, nd);
-    } else {
-        emit_job_text<KW>(a, b, sg.L, sg.start, n, smraw, [&](uint32_t i, uint32_t (&k)[KW]) { key_of(run_of(pos, nd, i), k); });
-    }
+    uint8_t *R = nd * W + 4 <= kWideSlots * 16 ? smraw : a.pat + (size_t)blockIdx.x * kFinPatBytes;   // (global)
+    build_run_patterns<KW>(R, W, sg.L, nd, key_of);
+    emit_runs_text(a, b, sg.L, sg.start, n, R, W, pos, nd);
 }
 
 // Persistent: jobs [small_base, ctr[kQSmall]) — the end is read on the device (this level's plan

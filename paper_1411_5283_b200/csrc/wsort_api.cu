@@ -79,7 +79,7 @@ struct wsort_ctx {
 
     // sort
     DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y, splits;
-    DevBuf m_hist, m_cursor, m_ctr, m_big[2], m_tiles[2], m_tiny, m_small, m_copy, m_skip;
+    DevBuf m_hist, m_cursor, m_ctr, m_big[2], m_tiles[2], m_tiny, m_small, m_copy, m_skip, m_pat;
     uint32_t *h_ctr = nullptr;   // pinned mirror of the msd queue counters
     std::vector<uint8_t> hplan;
     uint8_t *h_plan_pinned = nullptr;
@@ -375,7 +375,7 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->tickets, &c->plan, &c->va_x, &c->va_y, &c->splits, &c->bk, &c->d_counts,
                       &c->d_cursor, &c->d_sbase, &c->d_split, &c->d_lohi, &c->d_tiles, &c->d_ranges,
                       &c->m_hist, &c->m_cursor, &c->m_ctr, &c->m_big[0], &c->m_big[1], &c->m_tiles[0],
-                      &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->ghist, &c->dense,
+                      &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->m_pat, &c->ghist, &c->dense,
                       &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
                       &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor};
     for (DevBuf *b : bufs)
@@ -925,6 +925,7 @@ int msd_alloc(wsort_ctx *c, MsdArgs &m, uint64_t W, uint64_t key_words) {
     if ((rc = ensure(c, c->m_copy, (size_t)cap_copy * sizeof(CopyRange), "msd copy"))) return rc;
     if ((rc = ensure(c, c->m_ctr, kQCount * 4, "msd counters"))) return rc;
     if ((rc = ensure(c, c->m_skip, (size_t)cap_big * 4, "msd skip flags"))) return rc;
+    if ((rc = ensure(c, c->m_pat, (size_t)c->sms * 4 * kFinPatBytes, "finish patterns"))) return rc;
     if (!c->h_ctr && cudaMallocHost(&c->h_ctr, kQCount * 4) != cudaSuccess) {
         cudaGetLastError();
         return set_err(c, WSORT_E_NOMEM, "pinned counters");
@@ -941,6 +942,7 @@ int msd_alloc(wsort_ctx *c, MsdArgs &m, uint64_t W, uint64_t key_words) {
     m.keys_a = static_cast<uint32_t *>(c->keys_a.p);
     m.keys_b = static_cast<uint32_t *>(c->keys_b.p);
     m.seg_skip = static_cast<uint32_t *>(c->m_skip.p);
+    m.pat = static_cast<uint8_t *>(c->m_pat.p);
     return WSORT_OK;
 }
 

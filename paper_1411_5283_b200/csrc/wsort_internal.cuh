@@ -280,10 +280,13 @@ struct MsdArgs {
     uint32_t *seg_skip;            // [segments of this level] 1: all keys share the digit (not scattered)
     uint32_t *dbg_jobs;            // (experiments, nullable) per finishing job: n, kw | L << 8, cycles
     uint8_t *words;                // (stream_fin) output text
+    uint8_t *pat;                  // (stream_fin) per finishing CTA kFinPatBytes of run patterns that do not
+                                   // fit its shared memory (global, L1-resident while the job emits)
     uint32_t small_base;           // k_msd_fin: first job of this launch in q_small
     uint32_t big_base;             // k_msd_fin (streaming): first job of this launch in q_tiny (big jobs)
 };
 size_t msd_scatter_smem();
+constexpr uint32_t kFinPatBytes = 1024 * 48;   // >= max distinct keys x pattern width (1024 x 32, 512 x 88)
 cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
 cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s);
 cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
