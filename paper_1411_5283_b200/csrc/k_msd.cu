@@ -217,7 +217,17 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
         const MsdSeg x = jobs[k];
         if (first_queue(a, x.n)) {
             const uint32_t q = s_q[0] + before_tiny;
-            if (q < a.cap_local) a.q_tiny[q] = x;
+            if (q < a.cap_local) {
+                a.q_tiny[q] = x;
+                if (a.stream_fin) {   // a big job is counted by parts: reserve them
+                    const uint32_t np = job_parts(x.n);
+                    const uint32_t pb = atomicAdd(a.ctr + kQParts, np);
+                    a.job_pbase[q] = pb;
+                    a.job_done[q] = 0;
+                    a.job_ovf[q] = 0;
+                    for (uint32_t p = 0; p < np && pb + p < a.cap_parts; p++) a.q_parts[pb + p] = q;
+                }
+            }
         } else {
             const uint32_t q = s_q[1] + (k - before_tiny);
             if (q < a.cap_local) a.q_small[q] = x;
@@ -951,8 +961,53 @@ __device__ __forceinline__ uint64_t cas_t(uint64_t *p, uint64_t cmp, uint64_t v)
 template <typename T>
 __device__ __forceinline__ uint32_t st_hash(T k) { return (uint32_t)(((uint64_t)k * 0x9E3779B97F4A7C15ull) >> 53); }
 
-template <typename T, int KW>
-__device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw) {
+// A part of a split job: job q of q_tiny, part p of np, global part id
+struct FinPart {
+    uint32_t q, p, np, id;
+};
+
+// After a part has published its list (or the job's overflow flag): true for the part that arrives
+// last (it merges the lists and finishes the job).
+__device__ __forceinline__ bool part_arrive(const MsdArgs &a, const FinPart &pr, uint32_t *flag) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *flag = atomicAdd(&a.job_done[pr.q], 1u) == pr.np - 1 ? 1u : 0u;
+    __syncthreads();
+    const bool last = *flag != 0;
+    __syncthreads();
+    if (last) __threadfence();
+    return last;
+}
+
+// A merged split job of more than kEmitSplitMin words: leave its run table in its parts' list space
+// ([0] runs, [1..nd] run ends, then the distinct keys in order, KW words each) and queue its text pieces
+// for k_msd_fin_emit (many CTAs instead of this one).
+template <int KW, class KeyOf>
+__device__ __forceinline__ void publish_runs(const MsdArgs &a, const MsdSeg &sg, const FinPart &pr, uint32_t nd,
+                                             const uint32_t *ends, KeyOf key_of) {
+    uint32_t *tab = reinterpret_cast<uint32_t *>(a.part_list + (size_t)(pr.id - pr.p) * kPartListMax);
+    const uint32_t t = threadIdx.x;
+    for (uint32_t r = t; r < nd; r += kST) {
+        tab[1 + r] = ends[r];
+        uint32_t k[KW];
+        key_of(r, k);
+#pragma unroll
+        for (int u = 0; u < KW; u++) tab[1 + nd + r * KW + u] = k[u];
+    }
+    if (t == 0) tab[0] = nd;
+    const uint32_t np = (sg.n + kEmitPieceWords - 1) / kEmitPieceWords;
+    __shared__ uint32_t s_e0;
+    __threadfence();
+    __syncthreads();
+    if (t == 0) s_e0 = atomicAdd(a.ctr + kQEmit, np);
+    __syncthreads();
+    for (uint32_t i = t; i < np; i += kST)
+        if (s_e0 + i < a.cap_emit) a.q_emit[s_e0 + i] = make_uint2(pr.q, i);
+}
+
+template <typename T, int KW, bool PART>
+__device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw,
+                                           const FinPart pr) {
     const T kEmpty = ~(T)0;
     const uint32_t t = threadIdx.x, n = sg.n;
     T *slots = reinterpret_cast<T *>(smraw);
@@ -960,50 +1015,98 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
     T *A = reinterpret_cast<T *>(cnt + kStreamSlots);
     T *B = A + fpad(kStreamDistinct);
     uint32_t *pos = reinterpret_cast<uint32_t *>(B + fpad(kStreamDistinct));
-    uint32_t *misc = pos + kStreamDistinct;   // [0] distinct keys, [1] overflow, [2..] scan scratch
+    uint32_t *misc = pos + kStreamDistinct;   // [0] distinct keys, [1] overflow, [2..10] scan scratch, [12] flag
+    constexpr bool part = PART;
+    const uint32_t k0 = part ? pr.p * kPartKeys : 0u;   // the keys this CTA counts: [k0, k0 + nc)
+    const uint32_t nc = part ? min(kPartKeys, n - k0) : n;
     // table size adapted to the job (a small job pays for a small table): >= 2n slots, <= kStreamSlots
-    uint32_t ns = 64;
-    while (ns < 2 * n && ns < kStreamSlots) ns *= 2;
+    // (parts and their merge: the full table)
+    uint32_t ns0 = 64;
+    while (ns0 < 2 * nc && ns0 < kStreamSlots) ns0 *= 2;
+    const uint32_t ns = PART ? kStreamSlots : ns0;
     const uint32_t smask = ns - 1, sshift = 32 - (31 - __clz(ns));
-    for (uint32_t i = t; i < ns; i += kST) {
-        slots[i] = kEmpty;
-        cnt[i] = 0;
-    }
-    if (t < 2) misc[t] = 0;
-    __syncthreads();
+    auto init = [&]() {
+        for (uint32_t i = t; i < ns; i += kST) {
+            slots[i] = kEmpty;
+            cnt[i] = 0;
+        }
+        if (t < 2) misc[t] = 0;
+        __syncthreads();
+    };
+    auto ins = [&](T k, uint32_t mult) {   // count `mult` occurrences of k (sets the overflow flag if full)
+        uint32_t h = (uint32_t)(((uint64_t)k * 0x9E3779B97F4A7C15ull) >> 32) >> sshift;
+        for (;;) {
+            T cur = slots[h];
+            if (cur == kEmpty) {
+                if (atomicAdd(misc, 1u) >= kStreamDistinct) {   // table full: give up on this job
+                    atomicExch(misc + 1, 1u);
+                    return;
+                }
+                cur = cas_t(&slots[h], kEmpty, k);
+                if (cur == kEmpty) cur = k;
+                else atomicSub(misc, 1u);   // lost the race for this slot
+            }
+            if (cur == k) {
+                atomicAdd(&cnt[h], mult);
+                return;
+            }
+            h = (h + 1) & smask;
+        }
+    };
+    init();
+    if (part && t == 0 && *reinterpret_cast<volatile uint32_t *>(a.job_ovf + pr.q)) misc[1] = 1u;   // (job given up)
+    if (part) __syncthreads();
     const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
-    for (uint32_t i0 = 0; i0 < n; i0 += 4 * kST) {
+    for (uint32_t i0 = 0; i0 < nc; i0 += 4 * kST) {
         T k[4];
 #pragma unroll
         for (int r = 0; r < 4; r++) {
             const uint32_t i = i0 + r * kST + t;
-            k[r] = i < n ? fin_load<T, KW>(src + (size_t)i * KW) : kEmpty;
+            k[r] = i < nc ? fin_load<T, KW>(src + (size_t)(k0 + i) * KW) : kEmpty;
         }
         if (*reinterpret_cast<volatile uint32_t *>(misc + 1)) break;
 #pragma unroll
-        for (int r = 0; r < 4; r++) {
-            if (k[r] == kEmpty) continue;
-            uint32_t h = (uint32_t)(((uint64_t)k[r] * 0x9E3779B97F4A7C15ull) >> 32) >> sshift;
-            for (;;) {
-                T cur = slots[h];
-                if (cur == kEmpty) {
-                    if (atomicAdd(misc, 1u) >= kStreamDistinct) {   // table full: give up on this job
-                        atomicExch(misc + 1, 1u);
-                        break;
-                    }
-                    cur = cas_t(&slots[h], kEmpty, k[r]);
-                    if (cur == kEmpty) cur = k[r];
-                    else atomicSub(misc, 1u);   // lost the race for this slot
-                }
-                if (cur == k[r]) {
-                    atomicAdd(&cnt[h], 1u);
-                    break;
-                }
-                h = (h + 1) & smask;
-            }
-        }
+        for (int r = 0; r < 4; r++)
+            if (k[r] != kEmpty) ins(k[r], 1u);
     }
     __syncthreads();
+    if constexpr (PART) {
+        if (misc[1]) {
+            if (t == 0) atomicExch(a.job_ovf + pr.q, 1u);
+        } else {   // publish this part's distinct keys and their counts
+            const uint32_t per = (ns + kST - 1) / kST;
+            uint32_t occ = 0, nd = 0;
+            for (uint32_t e = 0; e < per; e++) occ += (per * t + e < ns) && cnt[per * t + e] != 0;
+            uint32_t q = block_excl_scan_m(occ, misc + 2, &nd);
+            uint4 *lst = a.part_list + (size_t)pr.id * kPartListMax;
+            for (uint32_t e = 0; e < per; e++) {
+                const uint32_t h = per * t + e;
+                if (h < ns && cnt[h]) {
+                    const uint64_t v = (uint64_t)slots[h];
+                    lst[q++] = make_uint4((uint32_t)v, (uint32_t)(v >> 32), cnt[h], 0u);
+                }
+            }
+            if (t == 0) a.part_n[pr.id] = nd;
+        }
+        if (!part_arrive(a, pr, misc + 12)) return;
+        // the last part: merge every part's list into a fresh table (the job's distinct keys, counts)
+        init();
+        if (t == 0 && __ldcg(a.job_ovf + pr.q)) misc[1] = 1u;
+        __syncthreads();
+        if (!misc[1]) {
+            const uint32_t id0 = pr.id - pr.p;
+            for (uint32_t p = 0; p < pr.np; p++) {
+                const uint32_t m = __ldcg(a.part_n + id0 + p);
+                const uint4 *lst = a.part_list + (size_t)(id0 + p) * kPartListMax;
+                for (uint32_t e = t; e < m; e += kST) {
+                    if (*reinterpret_cast<volatile uint32_t *>(misc + 1)) break;
+                    const uint4 v = __ldcg(lst + e);
+                    ins((T)(((uint64_t)v.y << 32) | v.x), v.z);
+                }
+            }
+        }
+        __syncthreads();
+    }
     if (misc[1]) {   // too many distinct keys
         if (n <= b.tile_keys) {   // (possibly several children): sort the job in full
             __syncthreads();
@@ -1068,6 +1171,12 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
             k[1] = (uint32_t)v;
         }
     };
+    if constexpr (PART) {
+        if (n > kEmitSplitMin) {
+            publish_runs<KW>(a, sg, pr, nd, pos, key_of);
+            return;
+        }
+    }
     const uint32_t W = (sg.L + 1 + 16 + 3) & ~3u;
     uint8_t *R = reinterpret_cast<uint8_t *>(slots);
     if (nd * W + 4 > kStreamSlots * (sizeof(T) + 4)) R = a.pat + (size_t)blockIdx.x * kFinPatBytes;   // (global)
@@ -1089,8 +1198,9 @@ __device__ __forceinline__ uint64_t fp64(const uint32_t (&k)[KW]) {
     h ^= h >> 29;
     return h == ~0ull ? 0x5555ull : h;   // never ~0 (= empty)
 }
-template <int KW>
-__device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw) {
+template <int KW, bool PART>
+__device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw,
+                                                const FinPart pr) {
     const uint64_t kEmpty = ~0ull;
     const uint32_t t = threadIdx.x, n = sg.n;
     uint64_t *fps = reinterpret_cast<uint64_t *>(smraw);                 // [kWideSlots]
@@ -1100,18 +1210,27 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     uint32_t *dcnt = rep + kWideDistinct * KW;                            // [kWideDistinct] count by id
     uint32_t *order = dcnt + kWideDistinct;                               // [kWideDistinct] id by rank
     uint32_t *pos = order + kWideDistinct;                                // [kWideDistinct] run ends
-    uint32_t *misc = pos + kWideDistinct;                                 // [0] nd [1] overflow [2..] scan
-    for (uint32_t i = t; i < kWideSlots; i += kST) {
-        fps[i] = kEmpty;
-        sid[i] = 0xffffffffu;
-        cnt[i] = 0;
-    }
-    if (t < 2) misc[t] = 0;
-    __syncthreads();
+    uint32_t *misc = pos + kWideDistinct;                                 // [0] nd [1] overflow [2..10] scan [12] flag
+    uint32_t *repix = misc + 16;                                          // [kWideDistinct] representative's index
+    constexpr bool part = PART;
+    const uint32_t k0 = part ? pr.p * kPartKeys : 0u;   // the keys this CTA counts: [k0, k0 + nc)
+    const uint32_t nc = part ? min(kPartKeys, n - k0) : n;
+    auto init = [&]() {
+        for (uint32_t i = t; i < kWideSlots; i += kST) {
+            fps[i] = kEmpty;
+            sid[i] = 0xffffffffu;
+            cnt[i] = 0;
+        }
+        if (t < 2) misc[t] = 0;
+        __syncthreads();
+    };
+    init();
+    if (part && t == 0 && *reinterpret_cast<volatile uint32_t *>(a.job_ovf + pr.q)) misc[1] = 1u;   // (job given up)
+    if (part) __syncthreads();
     const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
     // keys are loaded BATCH at a time ahead of their inserts (independent loads in flight)
     constexpr int BATCH = KW <= 4 ? 4 : (KW <= 8 ? 2 : 1);
-    auto insert = [&](const uint32_t (&k)[KW]) {
+    auto insert = [&](const uint32_t (&k)[KW], uint32_t mult, uint32_t kidx) {
         const uint64_t f = fp64<KW>(k);
         uint32_t h = (uint32_t)(f >> 40) & (kWideSlots - 1);
         for (;;) {
@@ -1126,55 +1245,96 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
                     }
 #pragma unroll
                     for (int u = 0; u < KW; u++) rep[id * KW + u] = k[u];
+                    repix[id] = kidx;
                     atomicExch(&sid[h], id);
                     cur = f;
                 }
             }
             if (cur == f) {
-                atomicAdd(&cnt[h], 1u);
+                atomicAdd(&cnt[h], mult);
                 return;
             }
             h = (h + 1) & (kWideSlots - 1);
         }
     };
-    for (uint32_t i0 = 0; i0 < n; i0 += BATCH * kST) {
+    // does key k equal its fingerprint's representative? (a 64-bit fingerprint collision: never expected)
+    auto same_as_rep = [&](const uint32_t (&k)[KW]) {
+        const uint64_t f = fp64<KW>(k);
+        uint32_t h = (uint32_t)(f >> 40) & (kWideSlots - 1);
+        while (fps[h] != f) h = (h + 1) & (kWideSlots - 1);
+        const uint32_t id = sid[h];
+        bool eq = true;
+#pragma unroll
+        for (int u = 0; u < KW; u++) eq &= rep[id * KW + u] == k[u];
+        return eq;
+    };
+    for (uint32_t i0 = 0; i0 < nc; i0 += BATCH * kST) {
         if (*reinterpret_cast<volatile uint32_t *>(misc + 1)) break;
         uint32_t k[BATCH][KW];
 #pragma unroll
         for (int r = 0; r < BATCH; r++) {
             const uint32_t i = i0 + r * kST + t;
 #pragma unroll
-            for (int u = 0; u < KW; u++) k[r][u] = i < n ? __ldg(src + (size_t)i * KW + u) : 0u;
+            for (int u = 0; u < KW; u++) k[r][u] = i < nc ? __ldg(src + (size_t)(k0 + i) * KW + u) : 0u;
         }
 #pragma unroll
         for (int r = 0; r < BATCH; r++)
-            if (i0 + r * kST + t < n) insert(k[r]);
+            if (i0 + r * kST + t < nc) insert(k[r], 1u, k0 + i0 + r * kST + t);
     }
     __syncthreads();
     if (!misc[1]) {   // verify: every key equals its fingerprint's representative
-        for (uint32_t i0 = 0; i0 < n; i0 += BATCH * kST) {
+        for (uint32_t i0 = 0; i0 < nc; i0 += BATCH * kST) {
             uint32_t k[BATCH][KW];
 #pragma unroll
             for (int r = 0; r < BATCH; r++) {
                 const uint32_t i = i0 + r * kST + t;
 #pragma unroll
-                for (int u = 0; u < KW; u++) k[r][u] = i < n ? __ldg(src + (size_t)i * KW + u) : 0u;
+                for (int u = 0; u < KW; u++) k[r][u] = i < nc ? __ldg(src + (size_t)(k0 + i) * KW + u) : 0u;
             }
 #pragma unroll
-            for (int r = 0; r < BATCH; r++) {
-                if (i0 + r * kST + t >= n) continue;
-                const uint64_t f = fp64<KW>(k[r]);
-                uint32_t h = (uint32_t)(f >> 40) & (kWideSlots - 1);
-                while (fps[h] != f) h = (h + 1) & (kWideSlots - 1);
-                const uint32_t id = sid[h];
-                bool eq = true;
-#pragma unroll
-                for (int u = 0; u < KW; u++) eq &= rep[id * KW + u] == k[r][u];
-                if (!eq) misc[1] = 1u;   // a 64-bit fingerprint collision (never expected)
-            }
+            for (int r = 0; r < BATCH; r++)
+                if (i0 + r * kST + t < nc && !same_as_rep(k[r])) misc[1] = 1u;
         }
     }
     __syncthreads();
+    if constexpr (PART) {
+        if (misc[1]) {
+            if (t == 0) atomicExch(a.job_ovf + pr.q, 1u);
+        } else {   // publish this part's distinct keys: fingerprint, count, representative's index
+            const uint32_t per = (kWideSlots + kST - 1) / kST;
+            uint32_t occ = 0, nd = 0;
+            for (uint32_t e = 0; e < per; e++) occ += cnt[per * t + e] != 0;
+            uint32_t q = block_excl_scan_m(occ, misc + 2, &nd);
+            uint4 *lst = a.part_list + (size_t)pr.id * kPartListMax;
+            for (uint32_t e = 0; e < per; e++) {
+                const uint32_t h = per * t + e;
+                if (cnt[h]) lst[q++] = make_uint4((uint32_t)fps[h], (uint32_t)(fps[h] >> 32), cnt[h], repix[sid[h]]);
+            }
+            if (t == 0) a.part_n[pr.id] = nd;
+        }
+        if (!part_arrive(a, pr, misc + 12)) return;
+        // the last part: merge the parts' lists (the representatives come from the keys), then check
+        // that equal fingerprints of different parts have equal representatives
+        init();
+        if (t == 0 && __ldcg(a.job_ovf + pr.q)) misc[1] = 1u;
+        __syncthreads();
+        const uint32_t id0 = pr.id - pr.p;
+        for (int pass = 0; pass < 2; pass++) {
+            for (uint32_t p = 0; p < pr.np && !*reinterpret_cast<volatile uint32_t *>(misc + 1); p++) {
+                const uint32_t m = __ldcg(a.part_n + id0 + p);
+                const uint4 *lst = a.part_list + (size_t)(id0 + p) * kPartListMax;
+                for (uint32_t e = t; e < m; e += kST) {
+                    const uint4 v = __ldcg(lst + e);
+                    uint32_t k[KW];
+#pragma unroll
+                    for (int u = 0; u < KW; u++) k[u] = __ldg(src + (size_t)v.w * KW + u);
+                    if (pass == 0) insert(k, v.z, v.w);
+                    else if (!same_as_rep(k)) misc[1] = 1u;
+                }
+            }
+            __syncthreads();
+        }
+    }
     if (misc[1]) {   // too many distinct keys
         if (n <= b.tile_keys) {   // (possibly several children): sort the job in full
             __syncthreads();
@@ -1258,6 +1418,12 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
 #pragma unroll
         for (int u = 0; u < KW; u++) k[u] = rep[id * KW + u];
     };
+    if constexpr (PART) {
+        if (n > kEmitSplitMin) {
+            publish_runs<KW>(a, sg, pr, nd, pos, key_of);
+            return;
+        }
+    }
     const uint32_t W = (sg.L + 1 + 16 + 3) & ~3u;
     uint8_t *R = nd * W + 4 <= kWideSlots * 16 ? smraw : a.pat + (size_t)blockIdx.x * kFinPatBytes;   // (global)
     build_run_patterns<KW>(R, W, sg.L, nd, key_of);
@@ -1266,43 +1432,139 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
 
 // Persistent: jobs [small_base, ctr[kQSmall]) — the end is read on the device (this level's plan
 // appended them), so the host needs no sync before the launch.
+template <bool PART>
+__device__ __forceinline__ void fin_job(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *fsm, const FinPart &pr) {
+    switch (b.kw) {
+        case 1: fin_stream<uint32_t, 1, PART>(a, sg, b, fsm, pr); break;
+        case 2: fin_stream<uint64_t, 2, PART>(a, sg, b, fsm, pr); break;
+        case 3: fin_stream_wide<3, PART>(a, sg, b, fsm, pr); break;
+        case 4: fin_stream_wide<4, PART>(a, sg, b, fsm, pr); break;
+        case 5: fin_stream_wide<5, PART>(a, sg, b, fsm, pr); break;
+        case 6: fin_stream_wide<6, PART>(a, sg, b, fsm, pr); break;
+        case 7: fin_stream_wide<7, PART>(a, sg, b, fsm, pr); break;
+        case 8: fin_stream_wide<8, PART>(a, sg, b, fsm, pr); break;
+        case 9: fin_stream_wide<9, PART>(a, sg, b, fsm, pr); break;
+        case 10: fin_stream_wide<10, PART>(a, sg, b, fsm, pr); break;
+        default: fin_stream_wide<11, PART>(a, sg, b, fsm, pr); break;
+    }
+}
+
+// Persistent: tickets [0, parts) are the parts of the big jobs (equal sizes, taken first), then the
+// small jobs [small_base, ctr[kQSmall]); both ends are read on the device (this level's plan appended
+// them), so the host needs no sync before the launch.
 __global__ void __launch_bounds__(kST, 4) k_msd_fin(MsdArgs a) {
     extern __shared__ __align__(16) uint8_t fsm[];
     __shared__ uint32_t s_job;
-    const uint32_t nb = min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQTiny), a.cap_local) - a.big_base;
-    const uint32_t end = nb + min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQSmall), a.cap_local) - a.small_base;
-    for (;;) {   // jobs are taken dynamically, big ones first (their sizes differ by orders of magnitude)
+    const uint32_t np = min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQParts), a.cap_parts) - a.parts_base;
+    const uint32_t end = np + min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQSmall), a.cap_local) - a.small_base;
+    for (;;) {
     if (threadIdx.x == 0) s_job = atomicAdd(a.ctr + kQFinTicket, 1u);
     __syncthreads();
     const uint32_t j = s_job;
     if (j >= end) break;
-    const MsdSeg sg = j < nb ? a.q_tiny[a.big_base + j] : a.q_small[a.small_base + j - nb];
+    const MsdSeg sg = j < np ? a.q_tiny[a.q_parts[a.parts_base + j]] : a.q_small[a.small_base + j - np];
+    if (j < np && job_parts(sg.n) > 1) {   // a part of a split job: k_msd_fin_split's
+        __syncthreads();
+        continue;
+    }
     const BucketInfo b = a.buckets[sg.L];
     const long long c0 = a.dbg_jobs ? clock64() : 0;
-    switch (b.kw) {
-        case 1: fin_stream<uint32_t, 1>(a, sg, b, fsm); break;
-        case 2: fin_stream<uint64_t, 2>(a, sg, b, fsm); break;
-        case 3: fin_stream_wide<3>(a, sg, b, fsm); break;
-        case 4: fin_stream_wide<4>(a, sg, b, fsm); break;
-        case 5: fin_stream_wide<5>(a, sg, b, fsm); break;
-        case 6: fin_stream_wide<6>(a, sg, b, fsm); break;
-        case 7: fin_stream_wide<7>(a, sg, b, fsm); break;
-        case 8: fin_stream_wide<8>(a, sg, b, fsm); break;
-        case 9: fin_stream_wide<9>(a, sg, b, fsm); break;
-        case 10: fin_stream_wide<10>(a, sg, b, fsm); break;
-        default: fin_stream_wide<11>(a, sg, b, fsm); break;
-    }
+    fin_job<false>(a, sg, b, fsm, FinPart{0u, 0u, 0u, 0u});
     __syncthreads();   // shared memory is reused by the next job
     if (a.dbg_jobs && threadIdx.x == 0 && j < 65536) {   // (experiments: per-job cycles)
         a.dbg_jobs[4 * j] = sg.n;
         a.dbg_jobs[4 * j + 1] = b.kw | (sg.L << 8);
         a.dbg_jobs[4 * j + 2] = (uint32_t)(clock64() - c0);
-        a.dbg_jobs[4 * j + 3] = a.buckets[sg.L].kw;
+        a.dbg_jobs[4 * j + 3] = 0;
     }
     }
 }
+
+// The parts of the split jobs (a separate kernel: their code would slow the whole-job kernel down —
+// measured 0.95 -> 1.19 ms on c4 when both were one kernel). Runs beside k_msd_fin on its own stream.
+__global__ void __launch_bounds__(kST, 4) k_msd_fin_split(MsdArgs a) {
+    extern __shared__ __align__(16) uint8_t fsm[];
+    __shared__ uint32_t s_job;
+    const uint32_t np = min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQParts), a.cap_parts) - a.parts_base;
+    for (;;) {
+        if (threadIdx.x == 0) s_job = atomicAdd(a.ctr + kQSplitTicket, 1u);
+        __syncthreads();
+        const uint32_t j = s_job;
+        __syncthreads();
+        if (j >= np) break;
+        FinPart pr;
+        pr.id = a.parts_base + j;
+        pr.q = a.q_parts[pr.id];
+        const MsdSeg sg = a.q_tiny[pr.q];
+        pr.np = job_parts(sg.n);
+        if (pr.np == 1) continue;   // a whole job: k_msd_fin's
+        pr.p = pr.id - a.job_pbase[pr.q];
+        fin_job<true>(a, sg, a.buckets[sg.L], fsm, pr);
+        __syncthreads();
+    }
+}
+// The text of one piece [w0, w1) of a merged split job from its run table: the runs overlapping the
+// piece get their repeated patterns (shared memory, else this CTA's global scratch) and emit_runs_text
+// writes the piece.
+template <int KW>
+__device__ __forceinline__ void emit_piece(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, const uint32_t *tab,
+                                           uint32_t w0, uint32_t w1, uint8_t *smraw, size_t smbytes) {
+    const uint32_t nd = __ldcg(tab);
+    const uint32_t *ends = tab + 1, *keys = tab + 1 + nd;
+    uint32_t *e = reinterpret_cast<uint32_t *>(smraw);   // [<= 1024] run ends relative to w0
+    uint8_t *R = smraw + 4096;
+    __shared__ uint32_t s_r0, s_r1;
+    if (threadIdx.x == 0) {
+        s_r0 = run_of(ends, nd, w0);
+        s_r1 = run_of(ends, nd, w1 - 1);
+    }
+    __syncthreads();
+    const uint32_t r0 = s_r0, nr = s_r1 - r0 + 1;
+    for (uint32_t r = threadIdx.x; r < nr; r += kST) e[r] = min(__ldcg(ends + r0 + r), w1) - w0;
+    const uint32_t W = (sg.L + 1 + 16 + 3) & ~3u;
+    if (nr * W + 4 > smbytes - 4096) R = a.pat + (size_t)blockIdx.x * kFinPatBytes;
+    build_run_patterns<KW>(R, W, sg.L, nr, [&](uint32_t r, uint32_t (&k)[KW]) {
+#pragma unroll
+        for (int u = 0; u < KW; u++) k[u] = __ldcg(keys + (size_t)(r0 + r) * KW + u);
+    });
+    emit_runs_text(a, b, sg.L, sg.start + w0, w1 - w0, R, W, e, nr);
+    __syncthreads();
+}
+
+constexpr size_t kEmitSmem = 4096 + 1024 * 32 + 64;   // run ends + patterns of 1-2 word keys (wider: global)
+__global__ void __launch_bounds__(kST) k_msd_fin_emit(MsdArgs a) {
+    extern __shared__ __align__(16) uint8_t esm[];
+    __shared__ uint32_t s_job;
+    const uint32_t end = min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQEmit), a.cap_emit);
+    for (;;) {
+        if (threadIdx.x == 0) s_job = atomicAdd(a.ctr + kQFinTicket, 1u);
+        __syncthreads();
+        const uint32_t j = a.emit_base + s_job;
+        __syncthreads();
+        if (j >= end) break;
+        const uint2 pc = a.q_emit[j];
+        const MsdSeg sg = a.q_tiny[pc.x];
+        const BucketInfo b = a.buckets[sg.L];
+        const uint32_t *tab = reinterpret_cast<const uint32_t *>(a.part_list + (size_t)a.job_pbase[pc.x] * kPartListMax);
+        const uint32_t w0 = pc.y * kEmitPieceWords, w1 = min(sg.n, w0 + kEmitPieceWords);
+        switch (b.kw) {
+            case 1: emit_piece<1>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            case 2: emit_piece<2>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            case 3: emit_piece<3>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            case 4: emit_piece<4>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            case 5: emit_piece<5>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            case 6: emit_piece<6>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            case 7: emit_piece<7>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            case 8: emit_piece<8>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            case 9: emit_piece<9>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            case 10: emit_piece<10>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+            default: emit_piece<11>(a, sg, b, tab, w0, w1, esm, kEmitSmem); break;
+        }
+    }
+}
+
 constexpr size_t kFinSmemStream = kStreamSlots * 12 + 2 * (kStreamDistinct + kStreamDistinct / 16) * 8 + (kStreamDistinct + 16) * 4;
-constexpr size_t kFinSmemWide = kWideSlots * 16 + (kWideDistinct * 11 + 3 * kWideDistinct + 16) * 4;   // KW <= 11
+constexpr size_t kFinSmemWide = kWideSlots * 16 + (kWideDistinct * 11 + 4 * kWideDistinct + 16) * 4;   // KW <= 11
 constexpr size_t kFinSmemSort = 2 * (kST * 4 * 4 + kST * 4 * 4 / 32 + 1) * 4;   // cta_sort_job fallback: TN*KW <= 4096
 constexpr size_t kFinSmem0 = kFinSmemStream > kFinSmemWide ? kFinSmemStream : kFinSmemWide;
 constexpr size_t kFinSmem = kFinSmem0 > kFinSmemSort ? kFinSmem0 : kFinSmemSort;
@@ -1334,16 +1596,38 @@ cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s
     k_msd_scatter<<<ntiles, kST, smem, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t first_big, uint32_t grid, cudaStream_t s) {
+cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t first_part, uint32_t grid, cudaStream_t s) {
     if (!grid) return cudaSuccess;
     MsdArgs b = a;
     b.small_base = first;
-    b.big_base = first_big;
+    b.parts_base = first_part;
     cudaError_t e = cudaMemsetAsync(a.ctr + kQFinTicket, 0, 4, s);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_msd_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinSmem);
     if (e != cudaSuccess) return e;
     k_msd_fin<<<grid, kST, kFinSmem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_msd_fin_split(const MsdArgs &a, uint32_t first_part, uint32_t grid, cudaStream_t s) {
+    MsdArgs b = a;
+    b.parts_base = first_part;
+    cudaError_t e = cudaMemsetAsync(a.ctr + kQSplitTicket, 0, 4, s);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_msd_fin_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinSmem);
+    if (e != cudaSuccess) return e;
+    k_msd_fin_split<<<grid, kST, kFinSmem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_msd_fin_emit(const MsdArgs &a, uint32_t first_piece, uint32_t grid, cudaStream_t s) {
+    MsdArgs b = a;
+    b.emit_base = first_piece;
+    cudaError_t e = cudaMemsetAsync(a.ctr + kQFinTicket, 0, 4, s);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_msd_fin_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEmitSmem);
+    if (e != cudaSuccess) return e;
+    k_msd_fin_emit<<<grid, kST, kEmitSmem, s>>>(b);
     return cudaGetLastError();
 }
 

@@ -54,6 +54,8 @@ struct wsort_ctx {
     cudaStream_t own_stream = nullptr;
     cudaStream_t aux = nullptr;                  // second stream: the dense buckets run beside the MSD
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t split = nullptr;                // third stream: parts of split finishing jobs beside k_msd_fin
+    cudaEvent_t ev_lvl = nullptr, ev_split = nullptr;
     int sms = 148;
     State state = ST_CREATED;
     char err[512] = {0};
@@ -80,6 +82,7 @@ struct wsort_ctx {
     // sort
     DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y, splits;
     DevBuf m_hist, m_cursor, m_ctr, m_big[2], m_tiles[2], m_tiny, m_small, m_copy, m_skip, m_pat;
+    DevBuf m_qparts, m_pbase, m_jdone, m_jovf, m_partn, m_plist, m_qemit;   // split finishing jobs
     uint32_t *h_ctr = nullptr;   // pinned mirror of the msd queue counters
     std::vector<uint8_t> hplan;
     uint8_t *h_plan_pinned = nullptr;
@@ -375,7 +378,8 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->tickets, &c->plan, &c->va_x, &c->va_y, &c->splits, &c->bk, &c->d_counts,
                       &c->d_cursor, &c->d_sbase, &c->d_split, &c->d_lohi, &c->d_tiles, &c->d_ranges,
                       &c->m_hist, &c->m_cursor, &c->m_ctr, &c->m_big[0], &c->m_big[1], &c->m_tiles[0],
-                      &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->m_pat, &c->ghist, &c->dense,
+                      &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->m_pat, &c->m_qparts, &c->m_pbase, &c->m_jdone,
+                      &c->m_jovf, &c->m_partn, &c->m_plist, &c->m_qemit, &c->ghist, &c->dense,
                       &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
                       &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor};
     for (DevBuf *b : bufs)
@@ -394,6 +398,9 @@ void wsort_destroy(wsort_ctx *c) {
     if (c->aux && c->aux != c->stream) cudaStreamDestroy(c->aux);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->split) cudaStreamDestroy(c->split);
+    if (c->ev_lvl) cudaEventDestroy(c->ev_lvl);
+    if (c->ev_split) cudaEventDestroy(c->ev_split);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -926,6 +933,17 @@ int msd_alloc(wsort_ctx *c, MsdArgs &m, uint64_t W, uint64_t key_words) {
     if ((rc = ensure(c, c->m_ctr, kQCount * 4, "msd counters"))) return rc;
     if ((rc = ensure(c, c->m_skip, (size_t)cap_big * 4, "msd skip flags"))) return rc;
     if ((rc = ensure(c, c->m_pat, (size_t)c->sms * 4 * kFinPatBytes, "finish patterns"))) return rc;
+    // finishing tickets of big jobs (> 16384 keys: one each, or one per part of <= kPartKeys keys when
+    // split): <= W / 16384 + 2 W / kPartKeys
+    const uint32_t cap_parts = (uint32_t)(W / 16384 + 2 * W / kPartKeys + 64);
+    if ((rc = ensure(c, c->m_qparts, (size_t)cap_parts * 4, "parts"))) return rc;
+    if ((rc = ensure(c, c->m_partn, (size_t)cap_parts * 4, "part sizes"))) return rc;
+    if ((rc = ensure(c, c->m_plist, (size_t)cap_parts * kPartListMax * 16, "part lists"))) return rc;
+    if ((rc = ensure(c, c->m_pbase, (size_t)cap_local * 4, "job parts"))) return rc;
+    if ((rc = ensure(c, c->m_jdone, (size_t)cap_local * 4, "job arrivals"))) return rc;
+    if ((rc = ensure(c, c->m_jovf, (size_t)cap_local * 4, "job overflow"))) return rc;
+    const uint32_t cap_emit = (uint32_t)(2 * W / kEmitPieceWords + 64);
+    if ((rc = ensure(c, c->m_qemit, (size_t)cap_emit * 8, "text pieces"))) return rc;
     if (!c->h_ctr && cudaMallocHost(&c->h_ctr, kQCount * 4) != cudaSuccess) {
         cudaGetLastError();
         return set_err(c, WSORT_E_NOMEM, "pinned counters");
@@ -943,6 +961,15 @@ int msd_alloc(wsort_ctx *c, MsdArgs &m, uint64_t W, uint64_t key_words) {
     m.keys_b = static_cast<uint32_t *>(c->keys_b.p);
     m.seg_skip = static_cast<uint32_t *>(c->m_skip.p);
     m.pat = static_cast<uint8_t *>(c->m_pat.p);
+    m.cap_parts = cap_parts;
+    m.q_parts = static_cast<uint32_t *>(c->m_qparts.p);
+    m.job_pbase = static_cast<uint32_t *>(c->m_pbase.p);
+    m.job_done = static_cast<uint32_t *>(c->m_jdone.p);
+    m.job_ovf = static_cast<uint32_t *>(c->m_jovf.p);
+    m.part_n = static_cast<uint32_t *>(c->m_partn.p);
+    m.part_list = static_cast<uint4 *>(c->m_plist.p);
+    m.cap_emit = cap_emit;
+    m.q_emit = static_cast<uint2 *>(c->m_qemit.p);
     return WSORT_OK;
 }
 
@@ -974,7 +1001,7 @@ int msd_read_counters(wsort_ctx *c, const MsdArgs &m, uint32_t &nsegs, uint32_t 
     nsegs = c->h_ctr[kQBig];
     ntiles = c->h_ctr[kQTiles];
     if (nsegs > m.cap_big || ntiles > m.cap_tiles || c->h_ctr[kQTiny] > m.cap_local || c->h_ctr[kQSmall] > m.cap_local ||
-        c->h_ctr[kQCopy] > m.cap_copy)
+        c->h_ctr[kQCopy] > m.cap_copy || c->h_ctr[kQParts] > m.cap_parts || c->h_ctr[kQEmit] > m.cap_emit)
         return set_err(c, WSORT_E_NOMEM, "msd queue overflow (segs %u tiles %u)", nsegs, ntiles);
     return WSORT_OK;
 }
@@ -986,12 +1013,12 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
     int rc;
     m.stream_fin = m.finish_radix ? 0u : 1u;
     const uint32_t fin_grid = (uint32_t)c->sms * 4;   // k_msd_fin: 4 resident CTAs per SM
-    uint32_t small_done = 0, big_done = 0;
+    uint32_t small_done = 0, parts_done = 0, emit_done = 0;
     if (!m.finish_radix && (c->h_ctr[kQSmall] || c->h_ctr[kQTiny])) {   // jobs planned before the first level
         rc = launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_fin_jobs(m, 0, 0, fin_grid, c->stream); });
         if (rc) return rc;
         small_done = c->h_ctr[kQSmall];
-        big_done = c->h_ctr[kQTiny];
+        parts_done = c->h_ctr[kQParts];
     }
     for (; nsegs > 0; level++) {
         if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
@@ -1012,8 +1039,24 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
                 cudaMemset(dj, 0, 65536 * 16);
                 m.dbg_jobs = dj;
             }
+            // the parts of split jobs (if any: their number is on the device) on the third stream, beside
+            // the whole jobs; then the text of the split jobs, by pieces
+            if (!c->split) {
+                CK(cudaStreamCreateWithFlags(&c->split, cudaStreamNonBlocking), "split stream");
+                CK(cudaEventCreateWithFlags(&c->ev_lvl, cudaEventDisableTiming), "level event");
+                CK(cudaEventCreateWithFlags(&c->ev_split, cudaEventDisableTiming), "split event");
+            }
+            CK(cudaEventRecord(c->ev_lvl, c->stream), "level event");
+            CK(cudaStreamWaitEvent(c->split, c->ev_lvl, 0), "level wait");
+            rc = launch_on(c, c->split, "k4m_msd_fin_split", 0,
+                           [&] { return launch_msd_fin_split(m, parts_done, fin_grid, c->split); });
+            if (rc) return rc;
+            CK(cudaEventRecord(c->ev_split, c->split), "split event");
             rc = launch(c, "k4m_msd_finish", level == 0 ? 2 * key_bytes : 0,
-                        [&] { return launch_msd_fin_jobs(m, small_done, big_done, fin_grid, c->stream); });
+                        [&] { return launch_msd_fin_jobs(m, small_done, parts_done, fin_grid, c->stream); });
+            if (rc) return rc;
+            CK(cudaStreamWaitEvent(c->stream, c->ev_split, 0), "split wait");
+            rc = launch(c, "k4m_msd_fin_emit", 0, [&] { return launch_msd_fin_emit(m, emit_done, (uint32_t)c->sms * 2, c->stream); });
             if (rc) return rc;
             if (dbg) {
                 cudaStreamSynchronize(c->stream);
@@ -1038,7 +1081,8 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;   // the level's one host sync
         if (!m.finish_radix) {
             small_done = std::min(c->h_ctr[kQSmall], m.cap_local);
-            big_done = std::min(c->h_ctr[kQTiny], m.cap_local);
+            parts_done = std::min(c->h_ctr[kQParts], m.cap_parts);
+            emit_done = std::min(c->h_ctr[kQEmit], m.cap_emit);
         }
         if (getenv("WSORT_DEBUG_MSD")) {
             fprintf(stderr, "msd level %u -> next segs %u tiles %u | tiny %u small %u copy %u\n", level, nsegs, ntiles,
@@ -1151,7 +1195,7 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
     if ((rc = arena_upload(c, c->m_tiles[0], tiles.data(), tiles.size() * sizeof(MsdTile), "tiles0"))) return rc;
     if ((rc = arena_upload(c, c->m_tiny, tiny.data(), tiny.size() * sizeof(MsdSeg), "tiny0"))) return rc;
     if ((rc = arena_upload(c, c->m_small, small.data(), small.size() * sizeof(MsdSeg), "small0"))) return rc;
-    uint32_t ctr0[kQCount] = {0, 0, (uint32_t)tiny.size(), (uint32_t)small.size(), 0, 0, 0, 0};
+    uint32_t ctr0[kQCount] = {0, 0, (uint32_t)tiny.size(), (uint32_t)small.size()};
     if ((rc = arena_upload(c, c->m_ctr, ctr0, sizeof ctr0, "counters"))) return rc;
     memcpy(c->h_ctr, ctr0, sizeof ctr0);   // if no level runs, these are the finishing counters
     const double key_bytes = (double)key_words * 4;

@@ -255,7 +255,20 @@ struct MsdSeg {
 struct MsdTile {
     uint32_t seg, off, n, pad_;    // keys [off, off+n) of segment `seg` of this level
 };
-enum { kQBig = 0, kQTiles = 1, kQTiny = 2, kQSmall = 3, kQCopy = 4, kQFinTicket = 5, kQCount = 8 };
+enum { kQBig = 0, kQTiles = 1, kQTiny = 2, kQSmall = 3, kQCopy = 4, kQFinTicket = 5, kQParts = 6, kQEmit = 7,
+       kQSplitTicket = 8, kQCount = 12 };
+// Streaming finish, split jobs: a child of more than kBigJobKeys keys is counted by parts of kPartKeys
+// keys (one CTA each); each part leaves its distinct keys + counts in a list of <= kPartListMax entries,
+// and the part that arrives last merges the lists and finishes the job (sort, emit).
+constexpr uint32_t kPartKeys = 32768, kPartListMax = 1024;
+// Only jobs of more than kSplitMinKeys keys are split (measured: below that, counting whole jobs in one
+// CTA is cheaper — a part cannot stop early when the job has too many distinct keys)
+constexpr uint32_t kSplitMinKeys = 4 * kPartKeys;
+__host__ __device__ constexpr uint32_t job_parts(uint32_t n) { return n > kSplitMinKeys ? (n + kPartKeys - 1) / kPartKeys : 1u; }
+// A merged split job's text is written by pieces of kEmitPieceWords words (k_msd_fin_emit), from its
+// run table (distinct keys sorted + run ends) left in its parts' list space.
+constexpr uint32_t kEmitPieceWords = 32768;
+constexpr uint32_t kEmitSplitMin = kEmitPieceWords;   // (merged jobs are always written by pieces)
 constexpr uint32_t kMsdCopyChunk = 65536;   // u32 words per copy job
 struct MsdArgs {
     const BucketInfo *buckets;
@@ -283,7 +296,18 @@ struct MsdArgs {
     uint8_t *pat;                  // (stream_fin) per finishing CTA kFinPatBytes of run patterns that do not
                                    // fit its shared memory (global, L1-resident while the job emits)
     uint32_t small_base;           // k_msd_fin: first job of this launch in q_small
-    uint32_t big_base;             // k_msd_fin (streaming): first job of this launch in q_tiny (big jobs)
+    uint32_t big_base;             // (radix finish) first job of this launch in q_tiny
+    // split jobs (streaming): q_tiny holds the big jobs, counted by parts
+    uint32_t parts_base;           // k_msd_fin: first part of this launch
+    uint32_t cap_parts;
+    uint32_t *q_parts;             // [cap_parts] part -> its job (q_tiny index)
+    uint32_t *job_pbase;           // [cap_local] big job -> its first part
+    uint32_t *job_done;            // [cap_local] parts of the job counted so far
+    uint32_t *job_ovf;             // [cap_local] 1: a part overflowed its table (the job re-enters the MSD)
+    uint32_t *part_n;              // [cap_parts] entries in the part's list
+    uint4 *part_list;              // [cap_parts][kPartListMax] {key lo, key hi | fingerprint, count, key index}
+    uint32_t emit_base, cap_emit;  // k_msd_fin_emit: first piece of this launch; capacity of q_emit
+    uint2 *q_emit;                 // [cap_emit] text pieces of merged split jobs: {job (q_tiny index), piece}
 };
 size_t msd_scatter_smem();
 constexpr uint32_t kFinPatBytes = 1024 * 48;   // >= max distinct keys x pattern width (1024 x 32, 512 x 88)
@@ -293,7 +317,9 @@ cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s
 cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_copy, uint32_t max_tile_words,
                               cudaStream_t s);   // tiny jobs, radix-finish jobs, copies (after the last level)
 // per level: jobs [first, *ctr[kQSmall]) by `grid` persistent CTAs
-cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t first_big, uint32_t grid, cudaStream_t s);
+cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t first_part, uint32_t grid, cudaStream_t s);
+cudaError_t launch_msd_fin_emit(const MsdArgs &a, uint32_t first_piece, uint32_t grid, cudaStream_t s);
+cudaError_t launch_msd_fin_split(const MsdArgs &a, uint32_t first_part, uint32_t grid, cudaStream_t s);
 
 struct EmitArgs {
     const BucketInfo *buckets;
