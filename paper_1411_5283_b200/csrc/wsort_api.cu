@@ -1085,8 +1085,8 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
             emit_done = std::min(c->h_ctr[kQEmit], m.cap_emit);
         }
         if (getenv("WSORT_DEBUG_MSD")) {
-            fprintf(stderr, "msd level %u -> next segs %u tiles %u | tiny %u small %u copy %u\n", level, nsegs, ntiles,
-                    c->h_ctr[kQTiny], c->h_ctr[kQSmall], c->h_ctr[kQCopy]);
+            fprintf(stderr, "msd level %u -> next segs %u tiles %u | tiny %u small %u copy %u parts %u pieces %u\n", level,
+                    nsegs, ntiles, c->h_ctr[kQTiny], c->h_ctr[kQSmall], c->h_ctr[kQCopy], c->h_ctr[kQParts], c->h_ctr[kQEmit]);
             std::vector<MsdSeg> jobs(c->h_ctr[kQSmall]);
             cudaMemcpy(jobs.data(), c->m_small.p, jobs.size() * sizeof(MsdSeg), cudaMemcpyDeviceToHost);
             std::vector<uint32_t> sz;

@@ -135,6 +135,45 @@ def test_edge_cases(ws, name, algo):
     check(ws, EDGE[name], algo)
 
 
+def _split_cases():
+    """MSD children of > 128K keys, which the streaming finish splits into parts of 32K keys (one CTA
+    each) merged by the last part: one word (all-equal runs), few distinct words (merged), too many
+    distinct words in every part or only in their union (the job re-enters the MSD), for 2-word keys
+    (L = 7..9) and wider keys (L = 14, 20)."""
+    rng = np.random.default_rng(1411)
+
+    def words(prefix: bytes, L: int, n_distinct: int, n: int, blocks: bool = False):
+        letters = rng.integers(97, 123, size=(n_distinct, L - len(prefix)), dtype=np.uint8)
+        vocab = [prefix + bytes(r) for r in letters]
+        if blocks:   # consecutive runs of 32K words drawn from disjoint eighths of the vocabulary
+            q = n_distinct // 8
+            idx = np.concatenate([(i % 8) * q + rng.integers(0, q, size=32768) for i in range(n // 32768 + 1)])[:n]
+        else:
+            idx = rng.integers(0, n_distinct, size=n)
+        # a few words of the same length with other first letters: the bucket is split at the first digit
+        # (not skipped), so the prefix's child is one job of n keys
+        decoy = [bytes([97 + i % 26, 97 + (i // 26) % 26]) + b"x" * (L - 2) for i in range(40)]
+        return b" ".join(vocab[i] for i in idx) + b" " + b" ".join(decoy) + b" "
+
+    return {
+        "split_one_word": b"quietly " * 300_000 + b"quintessential " * 200_000 + b"abcdefg nopqrstuvwxyza ",
+        "split_few_distinct": words(b"qu", 9, 600, 300_000),
+        "split_few_distinct_wide": words(b"qu", 20, 400, 300_000),
+        "split_overflow_parts": words(b"qu", 8, 50_000, 200_000),
+        "split_overflow_union": words(b"qu", 8, 8 * 900, 270_000, blocks=True),
+        "split_overflow_wide": words(b"qu", 14, 3000, 200_000),
+    }
+
+
+SPLIT = _split_cases()
+
+
+@pytest.mark.parametrize("algo", ["dense_msd", "msd_oets", "lsd_radix"])
+@pytest.mark.parametrize("name", list(SPLIT))
+def test_split_jobs(ws, name, algo):
+    check(ws, SPLIT[name], algo)
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 def test_word_too_long(ws, algo):
     from paper_1411_5283_b200 import WSortError
