@@ -1537,7 +1537,7 @@ __global__ void __launch_bounds__(kST) k_msd_fin_emit(MsdArgs a) {
     __shared__ uint32_t s_job;
     const uint32_t end = min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQEmit), a.cap_emit);
     for (;;) {
-        if (threadIdx.x == 0) s_job = atomicAdd(a.ctr + kQFinTicket, 1u);
+        if (threadIdx.x == 0) s_job = atomicAdd(a.ctr + kQEmitTicket, 1u);
         __syncthreads();
         const uint32_t j = a.emit_base + s_job;
         __syncthreads();
@@ -1623,7 +1623,7 @@ cudaError_t launch_msd_fin_split(const MsdArgs &a, uint32_t first_part, uint32_t
 cudaError_t launch_msd_fin_emit(const MsdArgs &a, uint32_t first_piece, uint32_t grid, cudaStream_t s) {
     MsdArgs b = a;
     b.emit_base = first_piece;
-    cudaError_t e = cudaMemsetAsync(a.ctr + kQFinTicket, 0, 4, s);
+    cudaError_t e = cudaMemsetAsync(a.ctr + kQEmitTicket, 0, 4, s);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_msd_fin_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEmitSmem);
     if (e != cudaSuccess) return e;

@@ -1051,13 +1051,14 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
             rc = launch_on(c, c->split, "k4m_msd_fin_split", 0,
                            [&] { return launch_msd_fin_split(m, parts_done, fin_grid, c->split); });
             if (rc) return rc;
+            rc = launch_on(c, c->split, "k4m_msd_fin_emit", 0,
+                           [&] { return launch_msd_fin_emit(m, emit_done, (uint32_t)c->sms * 2, c->split); });
+            if (rc) return rc;
             CK(cudaEventRecord(c->ev_split, c->split), "split event");
             rc = launch(c, "k4m_msd_finish", level == 0 ? 2 * key_bytes : 0,
                         [&] { return launch_msd_fin_jobs(m, small_done, parts_done, fin_grid, c->stream); });
             if (rc) return rc;
             CK(cudaStreamWaitEvent(c->stream, c->ev_split, 0), "split wait");
-            rc = launch(c, "k4m_msd_fin_emit", 0, [&] { return launch_msd_fin_emit(m, emit_done, (uint32_t)c->sms * 2, c->stream); });
-            if (rc) return rc;
             if (dbg) {
                 cudaStreamSynchronize(c->stream);
                 std::vector<uint32_t> h(65536 * 4);

@@ -256,7 +256,7 @@ struct MsdTile {
     uint32_t seg, off, n, pad_;    // keys [off, off+n) of segment `seg` of this level
 };
 enum { kQBig = 0, kQTiles = 1, kQTiny = 2, kQSmall = 3, kQCopy = 4, kQFinTicket = 5, kQParts = 6, kQEmit = 7,
-       kQSplitTicket = 8, kQCount = 12 };
+       kQSplitTicket = 8, kQEmitTicket = 9, kQCount = 12 };
 // Streaming finish, split jobs: a child of more than kBigJobKeys keys is counted by parts of kPartKeys
 // keys (one CTA each); each part leaves its distinct keys + counts in a list of <= kPartListMax entries,
 // and the part that arrives last merges the lists and finishes the job (sort, emit).

@@ -18,6 +18,7 @@ CLASS = {
     "k_emit_dense": "k5d_emit_dense", "k_lscatter": "k3c_chunk_scatter", "k_msd_count": "k4m_msd_count",
     "k_msd_plan": "k4m_msd_plan", "k_msd_scatter": "k4m_msd_scatter", "k_msd_fin": "k4m_msd_finish",
     "k_msd_warp_sort": "k4m_msd_finish", "k_msd_copy": "k4m_msd_finish", "k_emit": "k5_emit",
+    "k_msd_fin_split": "k4m_msd_fin_split", "k_msd_fin_emit": "k4m_msd_fin_emit",
 }
 
 
