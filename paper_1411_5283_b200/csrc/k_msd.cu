@@ -954,6 +954,9 @@ __device__ __forceinline__ void build_run_patterns(uint8_t *R, uint32_t W, uint3
 // kStreamDistinct distinct keys: a job of <= 2048 keys is sorted in full; a larger one goes back to
 // the MSD as a segment of the next level.
 constexpr uint32_t kStreamSlots = 2048, kStreamDistinct = 1024;
+// patterns that do not fit shared memory go to global scratch only for runs of >= kPatRunMin words on
+// average (measured on c4: shorter runs are cheaper word by word)
+constexpr uint32_t kPatRunMin = 8;
 __device__ __forceinline__ uint32_t cas_t(uint32_t *p, uint32_t cmp, uint32_t v) { return atomicCAS(p, cmp, v); }
 __device__ __forceinline__ uint64_t cas_t(uint64_t *p, uint64_t cmp, uint64_t v) {
     return atomicCAS(reinterpret_cast<unsigned long long *>(p), (unsigned long long)cmp, (unsigned long long)v);
@@ -1179,7 +1182,13 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
     }
     const uint32_t W = (sg.L + 1 + 16 + 3) & ~3u;
     uint8_t *R = reinterpret_cast<uint8_t *>(slots);
-    if (nd * W + 4 > kStreamSlots * (sizeof(T) + 4)) R = a.pat + (size_t)blockIdx.x * kFinPatBytes;   // (global)
+    if (nd * W + 4 > kStreamSlots * (sizeof(T) + 4)) {   // the patterns do not fit shared memory
+        if (n < kPatRunMin * nd) {   // short runs: word by word through a shared-memory stage
+            emit_job_text<KW>(a, b, sg.L, sg.start, n, R, [&](uint32_t i, uint32_t (&k)[KW]) { key_of(run_of(pos, nd, i), k); });
+            return;
+        }
+        R = a.pat + (size_t)blockIdx.x * kFinPatBytes;   // long runs: patterns in global scratch
+    }
     build_run_patterns<KW>(R, W, sg.L, nd, key_of);
     emit_runs_text(a, b, sg.L, sg.start, n, R, W, pos, nd);
 }
@@ -1190,6 +1199,7 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
 // the job in full / sends it to the next MSD level). At most kWideDistinct distinct keys, ranked by
 // counting the smaller ones.
 constexpr uint32_t kWideSlots = 1024, kWideDistinct = 512;
+constexpr uint32_t kRankMax = 96;   // distinct wide keys ordered by rank counting (nd^2 comparisons) up to here
 template <int KW>
 __device__ __forceinline__ uint64_t fp64(const uint32_t (&k)[KW]) {
     uint64_t h = 0x9E3779B97F4A7C15ull;
@@ -1358,11 +1368,30 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     for (uint32_t i = t; i < kWideSlots; i += kST)
         if (cnt[i]) dcnt[sid[i]] = cnt[i];
     __syncthreads();
-    // sort the distinct keys: 64-bit sort key = the 11 letters from the job's first undecided position
-    // (its keys share the letters before 2*level) and the key's index, by the odd-even transposition +
-    // merge-path block sort; if keys agree on those 11 letters, the indices are sorted again with the
-    // full-key comparison (same block sort)
-    {
+    // sort the distinct keys. Few (<= kRankMax): rank = number of smaller keys (full comparison).
+    // Else: 64-bit sort key = the 11 letters from the job's first undecided position (its keys share
+    // the letters before 2*level) and the key's index, by the odd-even transposition + merge-path block
+    // sort; if keys agree on those 11 letters, the indices are sorted again with the full-key
+    // comparison (same block sort)
+    if (nd <= kRankMax) {
+        for (uint32_t me = t; me < nd; me += kST) {
+            uint32_t rank = 0;
+            for (uint32_t j = 0; j < nd; j++) {
+                bool lt = false, decided = false;
+#pragma unroll
+                for (int u = 0; u < KW; u++) {
+                    const uint32_t x = rep[j * KW + u], y = rep[me * KW + u];
+                    if (!decided && x != y) {
+                        lt = x < y;
+                        decided = true;
+                    }
+                }
+                rank += lt;
+            }
+            order[rank] = me;
+        }
+        __syncthreads();
+    } else {
         uint64_t *SA = reinterpret_cast<uint64_t *>(smraw), *SB = SA + fpad(kWideDistinct);   // (table space: free now)
         const uint32_t p0 = 2u * (sg.buf >> 8);
         for (uint32_t id = t; id < nd; id += kST) {
@@ -1425,7 +1454,14 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
         }
     }
     const uint32_t W = (sg.L + 1 + 16 + 3) & ~3u;
-    uint8_t *R = nd * W + 4 <= kWideSlots * 16 ? smraw : a.pat + (size_t)blockIdx.x * kFinPatBytes;   // (global)
+    uint8_t *R = smraw;
+    if (nd * W + 4 > kWideSlots * 16) {   // the patterns do not fit shared memory
+        if (n < kPatRunMin * nd) {   // short runs: word by word through a shared-memory stage
+            emit_job_text<KW>(a, b, sg.L, sg.start, n, smraw, [&](uint32_t i, uint32_t (&k)[KW]) { key_of(run_of(pos, nd, i), k); });
+            return;
+        }
+        R = a.pat + (size_t)blockIdx.x * kFinPatBytes;   // long runs: patterns in global scratch
+    }
     build_run_patterns<KW>(R, W, sg.L, nd, key_of);
     emit_runs_text(a, b, sg.L, sg.start, n, R, W, pos, nd);
 }
