@@ -1199,7 +1199,7 @@ __device__ __forceinline__ void fin_stream(const MsdArgs &a, const MsdSeg &sg, c
 // the job in full / sends it to the next MSD level). At most kWideDistinct distinct keys, ranked by
 // counting the smaller ones.
 constexpr uint32_t kWideSlots = 1024, kWideDistinct = 512;
-constexpr uint32_t kRankMax = 96;   // distinct wide keys ordered by rank counting (nd^2 comparisons) up to here
+constexpr uint32_t kRankMax = 256;   // distinct wide keys ordered by rank counting (nd^2 comparisons) up to here
 template <int KW>
 __device__ __forceinline__ uint64_t fp64(const uint32_t (&k)[KW]) {
     uint64_t h = 0x9E3779B97F4A7C15ull;
