@@ -1239,7 +1239,7 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
     if (part) __syncthreads();
     const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
     // keys are loaded BATCH at a time ahead of their inserts (independent loads in flight)
-    constexpr int BATCH = KW <= 4 ? 4 : (KW <= 8 ? 2 : 1);
+    constexpr int BATCH = KW <= 2 ? 4 : (KW <= 4 ? 2 : 1);
     auto insert = [&](const uint32_t (&k)[KW], uint32_t mult, uint32_t kidx) {
         const uint64_t f = fp64<KW>(k);
         uint32_t h = (uint32_t)(f >> 40) & (kWideSlots - 1);
