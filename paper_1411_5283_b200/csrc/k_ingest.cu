@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
                 }
             }
             uint32_t *dst = a.pool + (size_t)(id == kTrash16 ? trash : cbase + id) * kChunkWords + pos * k;
-            for (uint32_t q = 0; q < k; q++) dst[q] = pack6(wb32, s + 6u * q, L - 6u * q);
+            pack_key(wb32, s, L, k, dst);
         }
         __syncwarp();   // the warp buffer and list are rewritten by the next sub-step
     }

@@ -49,5 +49,32 @@ __device__ __forceinline__ uint32_t pack6(const uint32_t *buf32, uint32_t boff, 
     return key;
 }
 
+// Letter codes of 6 bytes (bytes 0..3 in lo, 4..5 in the low half of hi) as one key word, as pack6.
+__device__ __forceinline__ uint32_t codes6(uint32_t lo, uint32_t hi) {
+    lo &= 0x1f1f1f1fu;
+    hi &= 0x00001f1fu;
+    const uint32_t r = __byte_perm(lo, 0, 0x0123);                   // letter 0 in the top byte
+    const uint32_t t1 = (r & 0x001f001fu) | ((r & 0x1f001f00u) >> 3);
+    const uint32_t t2 = (t1 & 0x3ffu) | ((t1 >> 16) << 10);           // 4 letters, 20 bits
+    return (t2 << 10) | ((hi & 0x1fu) << 5) | (hi >> 8);
+}
+
+// All k = ceil(L/6) key words of the word of L letters at byte s (pack6 of each 6-letter slice): two key
+// words are 12 bytes = 3 aligned words at one shift, so the window is read once (3 loads per pair);
+// only the last key word is masked.
+__device__ __forceinline__ void pack_key(const uint32_t *buf32, uint32_t s, uint32_t L, uint32_t k, uint32_t *dst) {
+    const uint32_t sh = 8u * (s & 3u), rem = L - 6u * (k - 1u);   // letters in the last key word: 1..6
+    const uint32_t last = rem < 6u ? ~((1u << (5u * (6u - rem))) - 1u) : 0xffffffffu;
+    const uint32_t *p = buf32 + (s >> 2);
+    uint32_t w0 = p[0];
+    for (uint32_t q = 0; q < k; q += 2, p += 3) {
+        const uint32_t w1 = p[1], w2 = p[2], w3 = p[3];
+        const uint32_t b0 = __funnelshift_r(w0, w1, sh), b1 = __funnelshift_r(w1, w2, sh), b2 = __funnelshift_r(w2, w3, sh);
+        dst[q] = codes6(b0, b1) & (q + 1u == k ? last : 0xffffffffu);
+        if (q + 1u < k) dst[q + 1u] = codes6(__funnelshift_r(b1, b2, 16), b2 >> 16) & (q + 2u == k ? last : 0xffffffffu);
+        w0 = w3;
+    }
+}
+
 }  // namespace text
 }  // namespace wsort
