@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(kTkThreads) k_tokenize(TkArgs a) {
                 const uint32_t idx = atomicAdd(&sm.run[L], 1u);
                 const uint32_t kw = (L + 5) / 6;
                 uint32_t *dst = a.keys + sm.key_off[L] + (uint64_t)idx * kw;
-                for (uint32_t q = 0; q < kw; q++) dst[q] = pack6(buf32, kTkPre + start + 6 * q, L - 6 * q);
+                if (L <= 192) pack_key(buf32, kTkPre + start, L, kw, dst);   // (its window reads <= 12 bytes past the word)
+                else for (uint32_t q = 0; q < kw; q++) dst[q] = pack6(buf32, kTkPre + start + 6 * q, L - 6 * q);
             }
             __syncthreads();
         } else {
@@ -198,7 +199,8 @@ __global__ void __launch_bounds__(kTkThreads) k_tokenize(TkArgs a) {
                 const uint32_t kw = (L + 5) / 6;
                 uint32_t *dst = a.keys + sm.key_off[L] + (uint64_t)idx * kw;
                 const uint32_t *buf32 = reinterpret_cast<const uint32_t *>(sm.c.buf);
-                for (uint32_t q = 0; q < kw; q++) dst[q] = pack6(buf32, kTkPre + start + 6 * q, L - 6 * q);
+                if (L <= 192) pack_key(buf32, kTkPre + start, L, kw, dst);   // (its window reads <= 12 bytes past the word)
+                else for (uint32_t q = 0; q < kw; q++) dst[q] = pack6(buf32, kTkPre + start + 6 * q, L - 6 * q);
                 if (a.payload) a.payload[sm.word_off[L] + idx] = (uint32_t)(s0 + start);
             }
             __syncthreads();
