@@ -50,6 +50,9 @@ constexpr uint16_t kNoChunk16 = 0xffffu, kTrash16 = 0xfffeu;
 
 // keys per chunk of class k: the largest power of two <= kChunkWords / k
 __host__ __device__ constexpr uint32_t cls_lg(uint32_t k) { return k == 1 ? 12u : k == 2 ? 11u : k <= 4 ? 10u : k <= 8 ? 9u : 8u; }
+// the same for 1 <= k <= 16 in two instructions: 12 - ceil(log2 k)
+__device__ __forceinline__ uint32_t cls_lg_fast(uint32_t k) { return (uint32_t)__clz(k - 1u) - 20u; }
+static_assert(cls_lg(1) == 12 && cls_lg(3) == 10 && cls_lg(5) == 9 && cls_lg(9) == 8 && cls_lg(11) == 8, "cls_lg");
 
 struct IgSmem {
     uint4 wbuf[kIgWarps][kWBuf / 16 + 1];  // per warp: its sub-step + tail (+16 B: packing reads whole words)
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
                 if (v) atomicAdd(&sm.hist[L], 1u);
                 else atomicAdd(&a.ctr[kIgVeryLong], 1u);   // too long to stage: the host sorts with K3 + LSD
             }
-            const uint32_t k = (L + 5u) / 6u, lg = cls_lg(k);
+            const uint32_t k = (L + 5u) / 6u, lg = cls_lg_fast(k);
             uint32_t r = 0;
             if (v) r = atomicAdd(&sm.cls_fill[k - 1], 1u);
             const uint32_t seq = r >> lg, pos = r & ((1u << lg) - 1u);
