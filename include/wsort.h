@@ -68,7 +68,7 @@ enum wsort_mem { WSORT_MEM_HOST = 0, WSORT_MEM_DEVICE = 1 };
 /* in-bucket sort (phase 3) */
 enum wsort_algo {
     WSORT_ALGO_AUTO = 0,       /* library picks: DENSE_MSD for keys-only sorts of a tokenized text with every
-                                  word <= 48 letters, else MSD_OETS (keys only, L <= 48), else LSD radix
+                                  word <= 66 letters, else MSD_OETS (keys only, L <= 48), else LSD radix
                                   (measured) */
     WSORT_ALGO_OETS_MERGE = 1, /* odd-even transposition tiles (the data-parallel bubble sort,
                                   PAPER.md:23) + merge-path merging (the paper's merge) */

@@ -9,7 +9,7 @@
 //       idx = sum c_j 26^(L-1-j) (c_j = letter code 0..25), so its sub-array sorted alphabetically
 //       is the counting sort of idx. L <= 2 count in shared memory; L = 3..5 go through a small
 //       shared-memory hash cache (hot words) and fall back to global atomics (cold words);
-//     * 6 <= L <= 48: the word is packed into its fixed-width key (kw = ceil(L/6) u32, the paper's
+//     * 6 <= L <= 66: the word is packed into its fixed-width key (kw = ceil(L/6) u32, the paper's
 //       "array char 3D") and appended to a staging chunk of its key-width class.
 //       Chunks (16 KiB) come from the CTA's own region of the pool (bounded: key bytes <= text bytes);
 //       order inside a chunk is arbitrary (keys only: equal keys are identical words).
@@ -43,7 +43,7 @@ __host__ __device__ constexpr uint32_t dense_base(uint32_t L) {
 #endif
 constexpr int kIgMinBlocks = WSORT_IG_MINB;
 constexpr int kSub = 1024;                   // bytes per warp sub-step (32 per lane)
-constexpr int kSubTail = 128;                // staged bytes past it (a staged word: <= 48 letters + slack)
+constexpr int kSubTail = 128;                // staged bytes past it (a staged word: <= 66 letters + slack)
 constexpr int kWBuf = kSub + kSubTail;
 constexpr int kWList = kSub / 2;             // at most one word start per two bytes
 constexpr uint16_t kNoChunk16 = 0xffffu, kTrash16 = 0xfffeu;
@@ -56,7 +56,7 @@ static_assert(cls_lg(1) == 12 && cls_lg(3) == 10 && cls_lg(5) == 9 && cls_lg(9) 
 
 struct IgSmem {
     uint4 wbuf[kIgWarps][kWBuf / 16 + 1];  // per warp: its sub-step + tail (+16 B: packing reads whole words)
-    uint16_t wlist[kIgWarps][kWList];      // per warp: s | (L-3) << 10; L = 3..5 from the front, 6..48 from the back
+    uint16_t wlist[kIgWarps][kWList];      // per warp: s | (L-3) << 10; L = 3..5 from the front, 6..66 from the back
     uint32_t d12[702];                     // dense counts of L = 1, 2
     uint32_t ctag[kCacheSlots];            // hash cache for L = 3..5: tag = L << 24 | idx, 0 = empty
     uint32_t ccnt[kCacheSlots];
@@ -117,7 +117,7 @@ __device__ __forceinline__ uint32_t lead_run(uint32_t M) { return M == 0xfffffff
 // streams its sub-steps with no block barrier: every lane classifies 32 bytes (SWAR letter mask, loaded
 // one sub-step ahead), word starts / ends come from mask shifts, the letter runs crossing lane
 // boundaries from a suffix scan of (l1,f1)+(l2,f2) = (l1 + f1*l2, f1 & f2) (l = letters leading a
-// segment, f = all letters). Words of L <= 2 are counted by their owner lane; L = 3..5 and 6..48 are
+// segment, f = all letters). Words of L <= 2 are counted by their owner lane; L = 3..5 and 6..66 are
 // listed by category (warp scan) and then taken round-robin by the lanes: hash-cache count / key
 // packing into the class's chunk. Chunk (class, seq) is allocated by the lane that receives its
 // first rank; the others read its id from shared memory (written once).
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
                 }
             }
             qh = __shfl_sync(kFull, tl, 0);
-            if (qh == (uint32_t)kSubTail) {   // rare: a run of >= 128 letters; count on (it is > 48 letters anyway)
+            if (qh == (uint32_t)kSubTail) {   // rare: a run of >= 128 letters; count on (it is > 66 letters anyway)
                 const uint8_t *p = a.text + base + kSub;
                 uint32_t i = kSubTail;
                 while (i < 300u && is_letter(p[i])) i++;
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
             const uint32_t s = x & 1023u, L = (x >> 10) + 3u;
             cache_add(sm, a.dense, L, dense_index(wb32, s, L));
         }
-        for (uint32_t i0 = 0; i0 < ((a.debug & 8) ? 0u : nlg); i0 += 32) {   // L = 6..48: key into its class's chunk
+        for (uint32_t i0 = 0; i0 < ((a.debug & 8) ? 0u : nlg); i0 += 32) {   // L = 6..66: key into its class's chunk
             const uint32_t i = i0 + lane;
             const uint32_t x = i < nlg ? wlst[kWList - 1 - i] : 0u;
             const uint32_t s = x & 1023u, L = (x >> 10) + 6u;
