@@ -39,7 +39,7 @@ def env_int(name, default):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)   # >= 10: the paper's 10 trials
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--algo", default="auto")
@@ -107,6 +107,14 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def trials_summary(trial_ms):
+    """The paper's protocol: each configuration "tested 10 times to get the average" (PAPER.md:31, :58;
+    SPEC.md:284-293): every timed step is one trial; mean (the paper's statistic), median and minimum."""
+    return {"n": len(trial_ms), "mean_ms": statistics.mean(trial_ms), "median_ms": statistics.median(trial_ms),
+            "min_ms": min(trial_ms), "max_ms": max(trial_ms),
+            "protocol": "per-step CUDA events on the launching stream; PAPER.md:31 10-trial average"}
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -139,10 +147,44 @@ def cpu_baseline(text, sample_mb: int):
     t0 = time.perf_counter()
     out = oracle.sort(sample, oracle.MERGE)
     dt = time.perf_counter() - t0
-    return {"value": out.n_words / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": out.n_words / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"first {n} bytes ({n / 2**20:.0f} MiB, {out.n_words} words) of the workload; "
                       f"oracle_sort(MERGE): tokenize+bucket+merge sort+emit, {dt:.2f} s",
             "seconds": dt, "input_gbs": n / dt / 1e9}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def cpu_baseline_all_cores(text, sample_mb: int):
+    """The oracle's paper-mpi shape (per length bucket, p chunks sorted on p threads, then
+    the master's k-way merge) on the host's cores, on a bounded prefix of the workload."""
+    import numpy as np
+
+    import oracle
+
+    ncpu = os.cpu_count() or 1
+    p = max(1, min(ncpu, 32))   # (the k-way merge scans all p runs per word: more threads stop paying)
+    n = min(len(text), sample_mb << 20)
+    while 0 < n < len(text) and (int(text[n - 1]) | 0x20) - 97 in range(26) and (int(text[n]) | 0x20) - 97 in range(26):
+        n -= 1
+    sample = np.ascontiguousarray(text[:n])
+    t0 = time.perf_counter()
+    out = oracle.sort_paper_mpi(sample, p, oracle.MERGE)
+    dt = time.perf_counter() - t0
+    return {"value": out.n_words / dt, "unit": UNIT, "cores": p, "host_cpus": ncpu, "cpu_model": cpu_model(),
+            "kind": "oracle paper-mpi (merge chunks + k-way merge)",
+            "sample": f"first {n} bytes ({n / 2**20:.0f} MiB, {out.n_words} words) of the workload, {p} threads, "
+                      f"{dt:.2f} s", "seconds": dt, "input_gbs": n / dt / 1e9}
 
 
 def run_reference(args, rank, world):
@@ -228,14 +270,18 @@ def run_wsort(args, rank, world, local_rank):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(dev) as clk:
         ev0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            evs[i].record(stream)
             ws.tokenize()
             ws.sort(args.algo)
+        evs[args.steps].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize(dev)
     ms = ev0.elapsed_time(ev1) / args.steps
+    trial_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     launches = ws.launch_count() - l0
     stats = ws.kernel_stats()
     ws.set_profiling(False)
@@ -279,6 +325,7 @@ def run_wsort(args, rank, world, local_rank):
                      "alg_min_bytes_per_step": alg_min,
                      "alg_min_frac": alg_min / (ms / 1000) / 1e9 / peak},
         "kernels": kernels,
+        "trials": trials_summary(trial_ms),
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -287,6 +334,7 @@ def run_wsort(args, rank, world, local_rank):
         line["e2e"] = e2e_pipelined(args, ws, host, stream, dev, n_words, words_len, sizes)
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(text, args.cpu_sample_mb)
+        line["cpu_baseline_all_cores"] = cpu_baseline_all_cores(text, 128)
     ws.close()
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -55,6 +55,9 @@ def _load():
         L.oracle_sort_paper_mpi.restype = ctypes.c_int
         L.oracle_sort_paper_mpi.argtypes = [_P, _U64, ctypes.c_uint32, ctypes.c_int, _P, _U64, _P,
                                             ctypes.POINTER(_Result), ctypes.POINTER(_Stats)]
+        L.oracle_sort_lengths.restype = ctypes.c_int
+        L.oracle_sort_lengths.argtypes = [_P, _U64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _P, _U64,
+                                          ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
         L.oracle_partition.restype = None
         L.oracle_partition.argtypes = [_U64, ctypes.c_uint32, _P]
         L.oracle_fingerprint.restype = ctypes.c_int
@@ -153,6 +156,30 @@ def sort_paper_mpi(text, p: int, inner: int = BUBBLE) -> OracleOutput:
         raise OracleError(rc, "oracle_sort_paper_mpi")
     return OracleOutput(words[: res.words_len].tobytes(), [int(x) for x in off[: res.max_len + 2]], None,
                         res.n_words, res.max_len, st.comparisons, st.swaps, st.passes)
+
+
+def sort_lengths(text, lmin: int, lmax: int, p: int = 1, as_array: bool = False):
+    """The sorted sub-arrays of the words of lengths lmin..lmax as "w\\n" bytes, shorter first (PAPER.md:58
+    phases 2-3 for those lengths, paper-mpi shape on p threads). Concatenated over consecutive length
+    ranges it is sort(text).words (length-major)."""
+    t = _buf(text)
+    lib = _load()
+    nw, nb = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    rc = lib.oracle_sort_lengths(_ptr(t), t.size, lmin, lmax, p, None, 0, ctypes.byref(nw), ctypes.byref(nb))
+    if rc < 0:
+        raise OracleError(rc, "oracle_sort_lengths(size)")
+    out = np.empty(max(nb.value, 1), np.uint8)
+    rc = lib.oracle_sort_lengths(_ptr(t), t.size, lmin, lmax, p, out.ctypes.data, out.size, ctypes.byref(nw),
+                                 ctypes.byref(nb))
+    if rc < 0:
+        raise OracleError(rc, "oracle_sort_lengths")
+    out = out[: nb.value]
+    return out if as_array else out.tobytes()
+
+
+def sort_length(text, L: int, p: int = 1) -> bytes:
+    """The sorted sub-array of the words of length L (sort_lengths(text, L, L, p))."""
+    return sort_lengths(text, L, L, p)
 
 
 def partition(n: int, p: int) -> list:

@@ -371,6 +371,100 @@ done:
     return rc;
 }
 
+/* ------------------------------------------------------------------ some sub-arrays (full-size goldens) */
+
+/* Phases 2-3 for the lengths Lmin..Lmax only: the sub-array of the words of each length L (PAPER.md:58
+ * "array of list ... based on the length"; the fixed-width "array char 3D" of PAPER.md:29: word i at
+ * bytes [i*L, i*L+L) of a compact folded array), sorted alphabetically in the paper-mpi shape (p chunks,
+ * each merge-sorted on its own thread, then the k-way merge), emitted as "word\n"
+ * per word, shorter lengths first. Because the output is length-major (reading A5), these outputs for
+ * consecutive length ranges concatenate to oracle_sort's output (pinned in tests/test_oracle.py); it
+ * lets a test-golden script sort texts whose whole token array does not fit in host memory, a few
+ * sub-arrays at a time. words = NULL: *n_words (words of lengths Lmin..Lmax) and *words_len only.
+ * Returns 0 or an error (a run of > 255 letters anywhere: WORD_TOO_LONG). */
+int oracle_sort_lengths(const uint8_t *text, uint64_t n, uint32_t Lmin, uint32_t Lmax, uint32_t p, uint8_t *words,
+                        uint64_t words_cap, uint64_t *n_words, uint64_t *words_len) {
+    if (Lmin < 1 || Lmax > ORACLE_MAX_LEN || Lmin > Lmax || p < 1 || p > 1024 || !n_words || !words_len ||
+        (n && !text))
+        return ORACLE_E_INVALID_ARG;
+    uint64_t cnt[ORACLE_MAX_LEN + 2] = {0}, i = 0;
+    while (i < n) {   /* phase 1: count the words of each length */
+        if (!is_letter(text[i])) { i++; continue; }
+        uint64_t s = i;
+        while (i < n && is_letter(text[i])) i++;
+        if (i - s > ORACLE_MAX_LEN) return ORACLE_E_WORD_TOO_LONG;
+        cnt[i - s]++;
+    }
+    uint64_t nw = 0, nb = 0, sub_bytes = 0, nmax = 0;
+    uint64_t sub_off[ORACLE_MAX_LEN + 2] = {0}, fill[ORACLE_MAX_LEN + 2] = {0};
+    for (uint32_t L = Lmin; L <= Lmax; L++) {
+        sub_off[L] = sub_bytes;
+        sub_bytes += cnt[L] * L;
+        nw += cnt[L];
+        nb += cnt[L] * (L + 1);
+        if (cnt[L] > nmax) nmax = cnt[L];
+    }
+    *n_words = nw;
+    *words_len = nb;
+    if (!words) return 0;
+    if (words_cap < nb) return ORACLE_E_BUFFER_TOO_SMALL;
+    uint8_t *sub = (uint8_t *)malloc(sub_bytes ? sub_bytes : 1);
+    uint64_t *order = (uint64_t *)malloc((nmax ? nmax : 1) * 8), *tmp = (uint64_t *)malloc((nmax ? nmax : 1) * 8);
+    uint64_t *merged = (uint64_t *)malloc((nmax ? nmax : 1) * 8);
+    chunk_job *jobs = (chunk_job *)calloc(p, sizeof(chunk_job));
+    pthread_t *th = (pthread_t *)calloc(p, sizeof(pthread_t));
+    uint64_t *bounds = (uint64_t *)calloc(p + 1, 8), *head = (uint64_t *)calloc(p, 8);
+    int rc = 0;
+    if (!sub || !order || !tmp || !merged || !jobs || !th || !bounds || !head) { rc = ORACLE_E_NOMEM; goto done; }
+    /* phase 2: the folded words of each length L in [Lmin, Lmax], text order */
+    i = 0;
+    while (i < n) {
+        if (!is_letter(text[i])) { i++; continue; }
+        uint64_t s = i;
+        while (i < n && is_letter(text[i])) i++;
+        uint64_t L = i - s;
+        if (L < Lmin || L > Lmax) continue;
+        uint8_t *dst = sub + sub_off[L] + fill[L]++ * L;
+        for (uint64_t j = 0; j < L; j++) dst[j] = fold(text[s + j]);
+    }
+    /* phase 3 per length: p chunks sorted on p threads, then the k-way merge; emit */
+    uint64_t out = 0;
+    for (uint32_t L = Lmin; L <= Lmax; L++) {
+        const uint64_t nL = cnt[L];
+        if (!nL) continue;
+        bucket_ctx b = {sub + sub_off[L], L};
+        for (uint64_t k = 0; k < nL; k++) order[k] = k * L;
+        oracle_partition(nL, p, bounds);
+        for (uint32_t q = 0; q < p; q++) {
+            jobs[q].b = &b;
+            jobs[q].a = order + bounds[q];
+            jobs[q].tmp = tmp + bounds[q];
+            jobs[q].n = bounds[q + 1] - bounds[q];
+            jobs[q].inner = ORACLE_MERGE;
+            if (q) pthread_create(&th[q], NULL, chunk_worker, &jobs[q]);
+        }
+        chunk_worker(&jobs[0]);
+        for (uint32_t q = 1; q < p; q++) pthread_join(th[q], NULL);
+        for (uint32_t q = 0; q < p; q++) head[q] = bounds[q];
+        for (uint64_t m = 0; m < nL; m++) {
+            int best = -1;
+            for (uint32_t q = 0; q < p; q++) {
+                if (head[q] >= bounds[q + 1]) continue;
+                if (best < 0 || cmp_alpha(&b, order[head[q]], order[head[best]]) < 0) best = (int)q;
+            }
+            merged[m] = order[head[best]++];
+        }
+        for (uint64_t m = 0; m < nL; m++) {
+            memcpy(words + out, b.folded + merged[m], L);
+            words[out + L] = '\n';
+            out += L + 1;
+        }
+    }
+done:
+    free(sub); free(order); free(tmp); free(merged); free(jobs); free(th); free(bounds); free(head);
+    return rc;
+}
+
 /* ------------------------------------------------------------------ fingerprint / verify */
 
 /* Order-independent multiset fingerprint of the tokens of `text` (test helper, not part of

@@ -16,7 +16,9 @@ Output files hold one word per line, the library's own output format.
           sequence is fixed by its multiset, so (a) + byte equality <=> (b)). Names the first bad line.
   bench   mean wall time of load+tokenize+sort+fetch per trial, one row per algorithm.
 
-Exit codes: 0 ok, 1 usage error, 2 I/O error, 3 verification failure. Diagnostics go to
+Exit codes: 0 ok, 1 usage error, 2 I/O error or an input the library refuses (e.g. a
+run of more than 255 letters, WSORT_E_WORD_TOO_LONG; reading A7) or a library failure, 3 verification
+failure. Diagnostics go to
 stderr, data to stdout or --output.
 """
 from __future__ import annotations
@@ -241,6 +243,13 @@ def main(argv=None) -> int:
         return EXIT_USAGE
     except OSError as e:
         print(f"wsort: I/O error: {e}", file=sys.stderr)
+        return EXIT_IO
+    except Exception as e:   # the library refused the input or failed (WSortError: status + message)
+        from .api import WSortError
+
+        if not isinstance(e, WSortError):
+            raise
+        print(f"wsort: cannot process input: {e}", file=sys.stderr)
         return EXIT_IO
 
 

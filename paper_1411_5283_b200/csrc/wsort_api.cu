@@ -521,7 +521,7 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     CK(copy_small(c->h_sum, c->d_sum.p, sizeof(Summary), c->stream), "copy summary");
     CK(cudaStreamSynchronize(c->stream), "tokenize");
     c->cta_bases_ready = c->cta_counts_ready = false;
-    if (c->h_ig[kIgVeryLong]) {   // words of 49..255 letters were not staged: histogram them the K3 way
+    if (c->h_ig[kIgVeryLong]) {   // words of 67..255 letters were not staged: histogram them the K3 way
         CK(cudaMemsetAsync(c->ghist.p, 0, kHistBins * 4, c->stream), "memset ghist");
         rc = launch(c, "k1b_count_lengths", (double)c->n,
                     [&] { return launch_count_lengths(a, ia.ghist, c->stream); });
@@ -1380,7 +1380,7 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     int rc = arena_begin(c);
     if (rc) return rc;
     // the dense + MSD path reads what K1 ingest left (dense counts, staged keys): a text this context
-    // tokenized, keys only, every word staged (<= 48 letters)
+    // tokenized, keys only, every word staged (<= 66 letters)
     const bool ingest_ok = !want_src && !c->packed_pending && !c->keys_external && c->h_ig[kIgVeryLong] == 0;
     if (c->keys_external && c->dense_range) {   // split multi-GPU sort: dense slice + received keys
         rc = sort_dist_dense(c);

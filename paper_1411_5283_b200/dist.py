@@ -189,8 +189,15 @@ class DistSorter:
         else:
             self.ws.pack()
         rec = self.torch.zeros((self.nsamples, self.rec_words), dtype=self.torch.int32, device=self.device)
+        self._torch_before_ws()
         self.ws.sample(self.nsamples, self.rank, self.rec_words, rec)
+        self.ws.sync()   # the collectives (torch's stream) read rec and the dense table
         return rec
+
+    def _torch_before_ws(self):
+        """Order the library's stream after torch's current stream (buffers torch wrote or received)."""
+        if self.torch.cuda.is_available():
+            self.torch.cuda.current_stream(self.device).synchronize()
 
     def stage_partition(self, all_samples: np.ndarray):
         from .api import select_splitters
@@ -198,7 +205,9 @@ class DistSorter:
         spl = select_splitters(all_samples.view(np.uint32), self.nparts)
         local_words = int((self.ws.histogram() * KW).sum())
         send = self.torch.empty(max(local_words, 1), dtype=self.torch.int32, device=self.device)
+        self._torch_before_ws()
         counts, send_words = self.ws.partition(spl, self.nparts, self.rec_words, self.rank, send)
+        self.ws.sync()   # all_to_all (torch's stream) reads send
         return counts, send, send_words
 
     @staticmethod
@@ -207,6 +216,7 @@ class DistSorter:
 
     def stage_sort(self, recv, recv_counts: np.ndarray, algo: str = "auto"):
         """Regroup the received keys and sort; returns this rank's (key words, key bytes)."""
+        self._torch_before_ws()   # recv (all_to_all) and the summed dense table (all_reduce)
         self.ws.load_keys(recv, recv_counts)
         self.dlo = self.dhi = 0
         if self.split:

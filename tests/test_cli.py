@@ -131,3 +131,14 @@ def test_bench_csv(built, tmp_path):
     assert rows[0] == "algo,mean_time_s,words_per_s,bytes,trials"
     assert [r.split(",")[0] for r in rows[1:]] == ["auto", "lsd_radix"]
     assert all(float(r.split(",")[2]) > 0 for r in rows[1:])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cmd", ["sort", "clean"])
+def test_word_too_long_exit_2(tmp_path, cmd, capsys):
+    """A run of > 255 letters (reading A7, WSORT_E_WORD_TOO_LONG): a one-line diagnostic and exit 2,
+    not a traceback."""
+    p = tmp_path / "blob.txt"
+    p.write_bytes(b"hello " + b"Q" * 300 + b" world\n")
+    assert cli.main([cmd, str(p), "-o", str(tmp_path / "out.txt")]) == cli.EXIT_IO
+    assert "cannot process input" in capsys.readouterr().err

@@ -60,6 +60,9 @@ class FakeWS:
 
     torch_device = "cpu"
 
+    def sync(self):
+        pass
+
     def load_text(self, text, global_base=0):
         self.text = bytes(np.asarray(text, dtype=np.uint8))
 

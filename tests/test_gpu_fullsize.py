@@ -1,0 +1,115 @@
+"""Full-size parity (-m gpu): the CUDA path's whole output at BASELINE.json's full sizes, byte for byte.
+
+The expected values are the ORACLE's: tests/golden/full_size_sha256.json holds the SHA-256 of the
+oracle's sorted output and its bucket offsets for config 4 (1 GiB, the bench workload), a 1 GiB slice
+of config 5, and config 5 in full (8 GiB), written by tools/golden_full_size.py (gen/ + oracle/ only).
+A test hashes the GPU output (SHA-256 over every byte) and compares offsets exactly, so any differing
+byte fails. Config 4 runs in bench.py's launch configuration (one context, AUTO) and with the two other
+in-bucket sorts; config 5 in full runs as 8 ranks (one libwsort context each, on one GPU: the split-mode
+sample sort with its collectives done host-side, no kernel waiting on another rank), the output
+assembled in global order from the ranks' slices. On a mismatch the test re-runs the oracle on the
+buckets that differ and reports the first differing word.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from conftest import GOLDEN
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+GOLD = json.load(open(os.path.join(GOLDEN, "full_size_sha256.json")))
+
+
+def first_difference(text, words: np.ndarray, off: list):
+    """Locate the first differing word against the oracle (diagnostics only, slow)."""
+    pos = 0
+    for L in range(1, len(off) - 1):
+        n = off[L + 1] - off[L]
+        ref = oracle.sort_length(text, L, os.cpu_count() or 1)
+        got = words[pos: pos + n * (L + 1)].tobytes()
+        if got != ref:
+            a, b = got.split(b"\n"), ref.split(b"\n")
+            i = next(i for i in range(min(len(a), len(b))) if a[i] != b[i])
+            return f"bucket L={L}: word #{off[L] + i} gpu={a[i]!r} oracle={b[i]!r}"
+        pos += n * (L + 1)
+    return "no per-bucket difference found"
+
+
+def check_single(ws, name, algo, text=None):
+    g = GOLD[name]
+    if text is None:
+        text, _ = gen.generate(g["config"], n=g["n"])
+    ws.load_text(text)
+    n = ws.tokenize()
+    ws.sort(algo)
+    words, off = ws.fetch()
+    assert n == g["n_words"]
+    assert off == g["off"]
+    assert words.size == g["words_len"]
+    if hashlib.sha256(memoryview(words)).hexdigest() != g["sha256"]:
+        pytest.fail(f"{name}/{algo}: output differs from the oracle: " + first_difference(text, words, off))
+    return text
+
+
+@pytest.fixture(scope="module")
+def ws():
+    import build_native
+
+    build_native.build_wsort()
+    from paper_1411_5283_b200 import WSort
+
+    w = WSort(0)
+    yield w
+    w.close()
+
+
+@pytest.fixture(scope="module")
+def c4_text():
+    return gen.generate(4)[0]
+
+
+@pytest.mark.parametrize("algo", ["auto", "lsd_radix", "oets_merge", "msd_oets"])
+def test_config4_full_output_equals_oracle(ws, c4_text, algo):
+    check_single(ws, "c4", algo, c4_text)
+
+
+def test_config5_slice_full_output_equals_oracle(ws):
+    check_single(ws, "c5_slice", "auto")
+
+
+def test_config5_full_8_ranks_equals_oracle():
+    """BASELINE.json configs[4] in full (8 GiB, skewed: 70 % of the tokens of length 5, a 12-letter prefix
+    family, heavy duplicates) on 8 ranks; the received-words balance is reported (max/mean
+    <= 1.05)."""
+    from paper_1411_5283_b200 import WSort
+    from paper_1411_5283_b200.dist import sort_emulated
+
+    g = GOLD["c5_full"]
+    text, _ = gen.generate(5)
+    assert len(text) == g["n"]
+    ranks, _ = sort_emulated(lambda: WSort(0), text, 8)
+    pieces, per_rank = [], []
+    for ws, res in ranks:
+        words, off = ws.fetch()
+        assert off == g["off"]                      # every rank reports the global offsets
+        per_rank.append(res.n_words)
+        for lo, nb, gb, _, _ in res.slices:
+            pieces.append((gb, words[lo: lo + nb]))
+        ws.close()
+    pieces.sort(key=lambda x: x[0])
+    sha, pos = hashlib.sha256(), 0
+    for gb, piece in pieces:
+        assert gb == pos, "slices do not tile the output"
+        sha.update(memoryview(np.ascontiguousarray(piece)))
+        pos += piece.size
+    assert pos == g["words_len"] and sum(per_rank) == g["n_words"]
+    balance = max(per_rank) / (sum(per_rank) / len(per_rank))
+    print(f"c5 8 ranks: words per rank {per_rank}, max/mean {balance:.4f}")
+    assert sha.hexdigest() == g["sha256"], "assembled 8-rank output differs from the oracle"
+    assert balance <= 1.05

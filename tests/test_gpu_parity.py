@@ -2,9 +2,8 @@
 
 Bar: bit-exact words, bucket offsets and src_off (all integer/byte work).
 Sizes: hand-written edge cases, random texts spanning many 8 KiB tokenizer steps / CTA chunks /
-radix tiles with ragged tails, BASELINE configs 1-3 in full, and config 4 (the bench workload,
-same launch configuration) plus a 1 GiB slice of config 5 via exact per-bucket checks and
-whole-output properties (offsets exact, sorted, multiset fingerprint equal).
+radix tiles with ragged tails, BASELINE configs 1-3 in full. The full-size workloads (config 4, the
+bench workload in its launch configuration, and config 5) are in tests/test_gpu_fullsize.py.
 """
 import glob
 import json
@@ -251,64 +250,6 @@ def test_keys_only_path(ws, algo):
     ref = oracle.sort(text, oracle.MERGE)
     words, off, _ = gpu_sort(ws, text, algo, src=False)
     assert words == ref.words and off == ref.off
-
-
-# ---------------------------------------------------------------- full-size (bench launch config)
-def _bucket_rows(words: np.ndarray, off: list, L: int) -> np.ndarray:
-    """Bucket L of the output as an array of fixed-width byte strings (numpy 'S<L>')."""
-    start = sum((off[l + 1] - off[l]) * (l + 1) for l in range(1, L))
-    n = off[L + 1] - off[L]
-    rows = words[start: start + n * (L + 1)].reshape(n, L + 1)
-    assert (rows[:, L] == 10).all()
-    return np.ascontiguousarray(rows[:, :L]).view(f"S{L}").ravel()
-
-
-def _full_size_check(ws, text: np.ndarray, exact_from: int, algo: str = "auto"):
-    hist, ref_off, lmax = oracle.histogram(text)
-    ref_off = [int(x) for x in ref_off[: lmax + 2]]
-    ws.load_text(text)
-    n = ws.tokenize()
-    ws.sort(algo)
-    words, off = ws.fetch()
-    assert n == ref_off[-1]
-    assert off == ref_off                                                   # exact offsets
-    assert len(words) == sum(L * int(hist[L]) for L in range(256)) + n     # C + W bytes
-    assert oracle.fingerprint(text) == oracle.fingerprint_words(words)      # same multiset
-    for L in range(1, lmax + 1):                                            # sorted in every bucket
-        r = _bucket_rows(words, off, L)
-        if r.size > 1:
-            assert (r[1:] >= r[:-1]).all(), f"bucket {L} not sorted"
-    # exact comparison of the long buckets (L >= exact_from) against the oracle
-    pos, ln = oracle.tokenize(text)
-    sel = ln >= exact_from
-    sub = b" ".join(text[p: p + l].tobytes() for p, l in zip(pos[sel].tolist(), ln[sel].tolist()))
-    ref = oracle.sort(sub, oracle.MERGE)
-    start = sum((off[l + 1] - off[l]) * (l + 1) for l in range(1, exact_from))
-    assert words[start:].tobytes() == ref.words
-
-
-@pytest.mark.slow
-def test_config4_full_size(ws):
-    text, _ = gen.generate(4)
-    _full_size_check(ws, text, exact_from=11)
-
-
-@pytest.mark.slow
-def test_config4_full_size_lsd(ws):
-    text, _ = gen.generate(4)
-    _full_size_check(ws, text, exact_from=13, algo="lsd_radix")
-
-
-@pytest.mark.slow
-def test_config4_full_size_oets_merge(ws):
-    text, _ = gen.generate(4)
-    _full_size_check(ws, text, exact_from=13, algo="oets_merge")
-
-
-@pytest.mark.slow
-def test_config5_slice_full_size(ws):
-    text, _ = gen.generate(5, n=1 << 30)
-    _full_size_check(ws, text, exact_from=13)
 
 
 # ---------------------------------------------------------------- ABI behaviour

@@ -252,3 +252,41 @@ def test_fingerprint_is_order_independent():
     assert a == oracle.fingerprint(b"A, C; a b")
     assert a == oracle.fingerprint_words(b"a\na\nb\nc\n")
     assert a != oracle.fingerprint(b"a a b d")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_sort_length_vs_library_routine(seed):
+    """oracle_sort_length (one sub-array, paper-mpi shape) against regex + sorted() per length, and its
+    concatenation over the lengths against the whole-text oracle (the full-size golden script relies on
+    this: tools/golden_full_size.py)."""
+    rng = np.random.default_rng(seed)
+    alpha = [b"abcde ", b"aAbB \n.,", b"the quick brown fox jumps over a lazy dog ", bytes(range(256))][seed % 4]
+    text = np.frombuffer(alpha, np.uint8)[rng.integers(0, len(alpha), 1 + seed * 9973)].tobytes()
+    ref_words, ref_off, _ = py_reference(text)
+    toks = [m.group().lower() for m in re.finditer(rb"[A-Za-z]+", text)]
+    lmax = max((len(w) for w in toks), default=0)
+    p = [1, 2, 3, 8][seed % 4]
+    parts = []
+    for L in range(1, lmax + 2):
+        got = oracle.sort_length(text, L, p)
+        assert got == b"".join(w + b"\n" for w in sorted(w for w in toks if len(w) == L))
+        parts.append(got)
+    assert b"".join(parts) == ref_words
+
+
+def test_sort_length_concat_equals_sort_config2():
+    import gen
+
+    text, _ = gen.generate(2)
+    ref = oracle.sort(text, oracle.MERGE)
+    assert b"".join(oracle.sort_length(text, L, 4) for L in range(1, ref.max_len + 1)) == ref.words
+    with pytest.raises(oracle.OracleError):
+        oracle.sort_length(b"ok " + b"z" * 256, 2)
+
+
+@pytest.mark.parametrize("ranges", [[(1, 3), (4, 4), (5, 255)], [(1, 255)], [(1, 1), (2, 9), (10, 40), (41, 255)]])
+def test_sort_lengths_ranges_concat(ranges):
+    text = np.frombuffer(b" ".join(bytes([97 + (i * j * 7 + j) % 26 for j in range(1 + i % 45)]) * (1 + i % 3)
+                                   for i in range(3000)), np.uint8)
+    ref_words, _, _ = py_reference(text.tobytes())
+    assert b"".join(oracle.sort_lengths(text, a, b, 3) for a, b in ranges) == ref_words

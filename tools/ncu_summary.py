@@ -12,7 +12,8 @@ KEYS = [
     ("time_ms", "gpu__time_duration.sum", 1e-6),
     ("dram_read_B", "dram__bytes_read.sum", 1),
     ("dram_write_B", "dram__bytes_write.sum", 1),
-    ("dram_pct", "dram__throughput.avg.pct_of_peak_sustained_elapsed", 1),
+    ("dram_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),   # (B200 --set full name)
+    ("dram_pct_alt", "dram__throughput.avg.pct_of_peak_sustained_elapsed", 1),
     ("sm_pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed", 1),
     ("warps_active_pct", "sm__warps_active.avg.pct_of_peak_sustained_active", 1),
     ("regs", "launch__registers_per_thread", 1),
@@ -34,7 +35,7 @@ def load(rep):
     res = []
     for r in rows[2:]:
         d = {"kernel": r[hdr.index("Kernel Name")]}
-        for k, m, scale in KEYS:
+        for k, m, scale in KEYS:   # (a metric absent from the report is skipped, not read as 0)
             if m in hdr:
                 v = r[hdr.index(m)].replace(",", "")
                 try:
@@ -51,6 +52,8 @@ def load(rep):
                 elif u.lower().startswith("kbyte"):
                     x *= 1e3
                 d[k] = x
+        if "dram_pct" not in d and "dram_pct_alt" in d:
+            d["dram_pct"] = d["dram_pct_alt"]
         res.append(d)
     return res
 
@@ -62,7 +65,7 @@ def main():
         dram = d.get("dram_read_B", 0) + d.get("dram_write_B", 0)
         gbs = dram / (d["time_ms"] / 1e3) / 1e9 if d.get("time_ms") else 0
         print(f"{d['kernel'][:60]:60s} {d.get('time_ms', 0):8.3f} ms  dram {dram / 1e6:9.1f} MB  {gbs:7.0f} GB/s "
-              f"dram% {d.get('dram_pct', 0):5.1f} sm% {d.get('sm_pct', 0):5.1f} warps% {d.get('warps_active_pct', 0):5.1f} "
+              f"dram% {d['dram_pct'] if 'dram_pct' in d else float('nan'):5.1f} sm% {d.get('sm_pct', 0):5.1f} warps% {d.get('warps_active_pct', 0):5.1f} "
               f"lsu% {d.get('lsu_pct', 0):5.1f} alu% {d.get('alu_pct', 0):5.1f} adu% {d.get('adu_pct', 0):5.1f} "
               f"regs {d.get('regs', 0):.0f} conflicts {d.get('smem_conflicts', 0):.3g}")
     if "--json" in sys.argv:
