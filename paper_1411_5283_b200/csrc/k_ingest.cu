@@ -53,9 +53,12 @@ __host__ __device__ constexpr uint32_t cls_lg(uint32_t k) { return k == 1 ? 12u 
 // the same for 1 <= k <= 16 in two instructions: 12 - ceil(log2 k)
 __device__ __forceinline__ uint32_t cls_lg_fast(uint32_t k) { return (uint32_t)__clz(k - 1u) - 20u; }
 static_assert(cls_lg(1) == 12 && cls_lg(3) == 10 && cls_lg(5) == 9 && cls_lg(9) == 8 && cls_lg(11) == 8, "cls_lg");
+// cls_lg_fast == cls_lg only for 1 <= k <= 16: the staged key widths must stay in that range
+static_assert(kMaxStageKw <= 16, "cls_lg_fast covers key widths 1..16 only");
 
 struct IgSmem {
-    uint4 wbuf[kIgWarps][kWBuf / 16 + 1];  // per warp: its sub-step + tail (+16 B: packing reads whole words)
+    uint4 wbuf[kIgWarps][2][kWBuf / 16 + 1];   // per warp, two slots: a sub-step + tail (+16 B: packing reads
+                                               // whole words)
     uint16_t wlist[kIgWarps][kWList];      // per warp: s | (L-3) << 10; L = 3..5 from the front, 6..66 from the back
     uint32_t d12[702];                     // dense counts of L = 1, 2
     uint32_t ctag[kCacheSlots];            // hash cache for L = 3..5: tag = L << 24 | idx, 0 = empty
@@ -142,79 +145,68 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
 
     const uint32_t nsub = b0 < b1 ? (uint32_t)((b1 - b0) / kSub) : 0u;
     const uint32_t w0 = (uint32_t)((uint64_t)nsub * warp / kIgWarps), w1 = (uint32_t)((uint64_t)nsub * (warp + 1) / kIgWarps);
-    uint8_t *wb = reinterpret_cast<uint8_t *>(sm.wbuf[warp]);
-    const uint32_t *wb32 = reinterpret_cast<const uint32_t *>(sm.wbuf[warp]);
     uint16_t *wlst = sm.wlist[warp];
-    uint4 va, vb, ta, tb;
-    uint32_t prev_last = 0;
+    // Two shared-memory slots per warp: the sub-step being processed (+ the next one's first 128 bytes: the
+    // tail a word crossing the sub-step continues into) and the next sub-step, written one iteration ahead
+    // from the registers that prefetched it. Each sub-step's letter mask is computed once, one iteration
+    // ahead, so the tail needs neither its own loads nor its own mask.
+    uint4 va = make_uint4(0, 0, 0, 0), vb = va;
+    uint32_t prev_last = 0, M = 0;
     if (w0 < w1) {
         const uint8_t *p = a.text + b0 + (uint64_t)w0 * kSub;
-        va = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane);
-        vb = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1);
-        if (lane < kSubTail / 32) {
-            ta = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane);
-            tb = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane + 1);
-        }
+        const uint4 ca = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane);
+        const uint4 cb = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1);
+        va = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane);   // (the text buffer is padded:
+        vb = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane + 1);   //  reads past a range are safe)
+        uint4 *s0 = reinterpret_cast<uint4 *>(sm.wbuf[warp][w0 & 1]);
+        s0[2 * lane] = ca;
+        s0[2 * lane + 1] = cb;
+        M = letter_mask32(ca, cb);
         prev_last = is_letter(p[-1]);
     }
     for (uint32_t sub = w0; sub < w1; sub++) {
+        uint8_t *wb = reinterpret_cast<uint8_t *>(sm.wbuf[warp][sub & 1]);
+        const uint32_t *wb32 = reinterpret_cast<const uint32_t *>(wb);
         const uint64_t base = b0 + (uint64_t)sub * kSub;
-        reinterpret_cast<uint4 *>(wb)[2 * lane] = va;
-        reinterpret_cast<uint4 *>(wb)[2 * lane + 1] = vb;
-        const uint32_t M = letter_mask32(va, vb);
-        uint32_t Mt = 0;
-        if (lane < kSubTail / 32) {
-            reinterpret_cast<uint4 *>(wb + kSub)[2 * lane] = ta;
-            reinterpret_cast<uint4 *>(wb + kSub)[2 * lane + 1] = tb;
-            Mt = letter_mask32(ta, tb);
-        }
-        if (sub + 1 < w1) {   // prefetch the next sub-step
-            const uint8_t *p = a.text + base + kSub;
-            va = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane);
-            vb = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1);
+        // the next sub-step (prefetched last iteration): its mask, its slot, and the current slot's tail
+        const uint32_t Mn = letter_mask32(va, vb);
+        {
+            uint4 *sn = reinterpret_cast<uint4 *>(sm.wbuf[warp][(sub + 1) & 1]);
+            sn[2 * lane] = va;
+            sn[2 * lane + 1] = vb;
             if (lane < kSubTail / 32) {
-                ta = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane);
-                tb = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane + 1);
+                reinterpret_cast<uint4 *>(wb + kSub)[2 * lane] = va;
+                reinterpret_cast<uint4 *>(wb + kSub)[2 * lane + 1] = vb;
             }
         }
+        {   // prefetch the sub-step after the next
+            const uint8_t *p = a.text + base + 2 * kSub;
+            va = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane);
+            vb = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1);
+        }
+        __syncwarp();
         const uint32_t pm = __shfl_up_sync(kFull, M, 1), nm = __shfl_down_sync(kFull, M, 1);
         const uint32_t pl = lane ? (pm >> 31) : prev_last;
-        const uint32_t mt0 = __shfl_sync(kFull, Mt, 0);   // (every lane shuffles: full-mask shuffles must not diverge)
+        const uint32_t mt0 = __shfl_sync(kFull, Mn, 0);
         const uint32_t nx = lane < 31 ? (nm & 1u) : (mt0 & 1u);
         prev_last = __shfl_sync(kFull, M, 31) >> 31;
         const uint32_t starts = M & ~((M << 1) | pl);
         const uint32_t ends = M & ~((M >> 1) | (nx << 31));
-        // letters at the head of the tail (the run a word crossing the sub-step continues with)
-        uint32_t qh;
+        // letters continuing past this lane's last byte: the all-letter lanes after it (32 each), then the
+        // leading letters of the first lane that is not all letters; past lane 31, the next sub-step's
+        // leading letters qh (>= 1024: a run longer than any staged / legal word)
+        uint32_t carry;
         {
-            uint32_t tl = lane < kSubTail / 32 ? lead_run(Mt) : 0u, tf = lane < kSubTail / 32 ? (uint32_t)(Mt == 0xffffffffu) : 0u;
-#pragma unroll
-            for (int o = 1; o < kSubTail / 32; o <<= 1) {
-                const uint32_t l2 = __shfl_down_sync(kFull, tl, o), f2 = __shfl_down_sync(kFull, tf, o);
-                if (lane + o < kSubTail / 32 && tf) {
-                    tl += l2;
-                    tf = f2;
-                }
-            }
-            qh = __shfl_sync(kFull, tl, 0);
-            if (qh == (uint32_t)kSubTail) {   // rare: a run of >= 128 letters; count on (it is > 66 letters anyway)
-                const uint8_t *p = a.text + base + kSub;
-                uint32_t i = kSubTail;
-                while (i < 300u && is_letter(p[i])) i++;
-                qh = i;
-            }
+            const uint32_t fullN = __ballot_sync(kFull, Mn == 0xffffffffu);
+            const uint32_t kN = fullN == 0xffffffffu ? 0u : (uint32_t)(__ffs(~fullN) - 1);
+            const uint32_t leadN = __shfl_sync(kFull, lead_run(Mn), kN);
+            const uint32_t qh = fullN == 0xffffffffu ? 1024u : 32u * kN + leadN;
+            const uint32_t fullM = __ballot_sync(kFull, M == 0xffffffffu);
+            const uint32_t nf = lane < 31 ? ~fullM & (0xfffffffeu << lane) : 0u;
+            const uint32_t k = nf ? (uint32_t)(__ffs(nf) - 1) : 0u;
+            const uint32_t lk = __shfl_sync(kFull, lead_run(M), k);
+            carry = nf ? 32u * (k - lane - 1u) + lk : 32u * (31u - lane) + qh;
         }
-        uint32_t l = lead_run(M), f = M == 0xffffffffu;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t l2 = __shfl_down_sync(kFull, l, o), f2 = __shfl_down_sync(kFull, f, o);
-            if (lane + o < 32 && f) {
-                l += l2;
-                f = f2;
-            }
-        }
-        const uint32_t l1 = __shfl_down_sync(kFull, l, 1), f1 = __shfl_down_sync(kFull, f, 1);
-        const uint32_t carry = lane < 31 ? l1 + (f1 ? qh : 0u) : qh;
         const uint32_t seg0 = 32u * lane;
         // categories from the masks: a word starting at bit i has L >= j iff bytes i..i+j-1 are letters
         // (X = this lane's letters followed by the next lane's / the tail's); one branch-free loop each
@@ -291,7 +283,8 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
             uint32_t *dst = a.pool + (size_t)(id == kTrash16 ? trash : cbase + id) * kChunkWords + pos * k;
             pack_key(wb32, s, L, k, dst);
         }
-        __syncwarp();   // the warp buffer and list are rewritten by the next sub-step
+        __syncwarp();   // the slot and list are rewritten by the next sub-steps
+        M = Mn;
     }
     __syncthreads();
     if (t == 0) atomicMax(&a.ctr[kIgMaxChunks], sm.nchunk);
@@ -472,94 +465,149 @@ __global__ void __launch_bounds__(256) k_dense_compact(DenseArgs a) {
     }
 }
 
-// ------------------------------------------------------------------ K5d: emit the dense buckets
-constexpr uint32_t kDenseTile = 2048;                 // words per emit tile
-constexpr uint32_t kDenseStage = kDenseTile * 6 + 32; // <= 6 bytes per word (L <= 5)
-
-// first i in [0, n) with arr[i] > x (n if none): k-ary search, 256 probes per round
-__device__ __forceinline__ uint32_t block_first_greater(const uint32_t *arr, uint32_t n, uint32_t x) {
-    uint32_t lo = 0, hi = n;
+// The entries holding the first and the last word of every emit tile (k_emit_dense): one thread per tile,
+// binary search over the compacted entries' word ends.
+__device__ __forceinline__ uint32_t first_end_above(const uint32_t *ends, uint32_t n, uint32_t w) {
+    uint32_t lo = 0, hi = n;   // first e with ends[e] > w
     while (lo < hi) {
-        const uint32_t stride = (hi - lo + 255u) / 256u;
-        const uint32_t p = lo + threadIdx.x * stride;
-        const bool le = p < hi && __ldg(arr + p) <= x;
-        const uint32_t m = (uint32_t)__syncthreads_count(le);
-        if (m == 0) return lo;
-        const uint32_t nlo = lo + (m - 1u) * stride + 1u, nhi = min(hi, lo + m * stride);
-        lo = nlo;
-        hi = nhi;
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(ends + mid) > w) hi = mid;
+        else lo = mid + 1;
     }
     return lo;
 }
+__global__ void __launch_bounds__(256) k_dense_tiles(DenseArgs a, uint32_t ntiles) {
+    const uint32_t tile = blockIdx.x * 256 + threadIdx.x;
+    if (tile >= ntiles) return;
+    const TileDesc td = tile_from_prefix(a.tile_pfx, tile);
+    const BucketInfo b = a.buckets[td.L];
+    const uint32_t te = dense_tile_words(td.L), k0 = td.tile * te, nk = min(te, b.n - k0);
+    const uint32_t w0 = (uint32_t)b.word_off + k0, E = a.n_ent[0];
+    a.tile_e0[tile] = first_end_above(a.ent_end, E, w0);
+    a.tile_e1[tile] = first_end_above(a.ent_end, E, w0 + nk - 1u);
+}
 
+// ------------------------------------------------------------------ K5d: emit the dense buckets
+constexpr uint32_t kDenseTileEnt = 2048;   // entries one emit tile can hold (<= its words for L >= 3)
+
+// 16 bytes of the periodic sequence W0|W1|W2 (the pattern repeated) from byte r (0 <= r < 8)
+__device__ __forceinline__ uint64_t fshr64(uint64_t lo, uint64_t hi, uint32_t s) {
+    return s ? (lo >> s) | (hi << (64 - s)) : lo;
+}
+// the P-byte pattern (P <= 6) repeated over 8 bytes, starting at its byte ph
+__device__ __forceinline__ uint64_t rep64(uint64_t pat, uint32_t P, uint32_t ph) {
+    const uint64_t m = (1ull << (8 * P)) - 1ull;
+    uint64_t x = ph ? ((pat >> (8 * ph)) | (pat << (8 * (P - ph)))) & m : pat;
+    for (uint32_t s = 8 * P; s < 64; s *= 2) x |= x << s;
+    return x;
+}
+
+// Output-parallel: a tile's output bytes [ob, end) are cut into 16-byte aligned chunks and every thread
+// assembles a run of consecutive chunks in registers and writes each with one 16-byte store. A chunk
+// inside one entry's run is the entry's "word\n" pattern repeated from some phase (three words of the
+// periodic sequence, rebuilt only when the entry changes); a chunk crossing entries is assembled word by
+// word; only the chunks shared with the neighbouring tiles (head, tail) are written byte by byte. The
+// tile's entries [tile_e0, tile_e1] come from k_dense_compact (no search).
 __global__ void __launch_bounds__(256) k_emit_dense(DenseEmitArgs a) {
-    __shared__ __align__(16) uint8_t stage[kDenseStage];
-    __shared__ uint32_t s_end[kDenseTile], s_idx[kDenseTile];
+    extern __shared__ __align__(16) uint8_t dsm[];
+    uint64_t *s_pat = reinterpret_cast<uint64_t *>(dsm);                 // entry j's word + '\n' (LE bytes)
+    uint32_t *s_end = reinterpret_cast<uint32_t *>(dsm + 8 * kDenseTileEnt);   // inclusive end, tile-relative
     const uint32_t t = threadIdx.x;
     const TileDesc td = tile_from_prefix(a.tile_pfx, blockIdx.x);
-    const uint32_t L = td.L;
+    const uint32_t L = td.L, P = L + 1u, magic = 65536u / P + 1u;   // (n * magic) >> 16 == n / P for n <= 21
     const BucketInfo b = a.buckets[L];
-    const uint32_t k0 = td.tile * kDenseTile;
-    const uint32_t nk = min(kDenseTile, b.n - k0);
-    const uint32_t w0 = (uint32_t)b.word_off + k0, w1 = w0 + nk;
-    const uint32_t E = a.n_ent[0];
-    const uint32_t e0 = block_first_greater(a.ent_end, E, w0);
-    const uint32_t e1 = block_first_greater(a.ent_end, E, w1 - 1u);
-    const uint32_t ne = e1 - e0 + 1u;   // <= nk: every entry holds >= 1 word
+    const uint32_t te = dense_tile_words(L);
+    const uint32_t k0 = td.tile * te;
+    const uint32_t nk = min(te, b.n - k0);
+    const uint32_t w0 = (uint32_t)b.word_off + k0;
+    const uint32_t e0 = a.tile_e0[blockIdx.x], ne = a.tile_e1[blockIdx.x] - e0 + 1u;   // <= min(nk, 676) for L <= 2
     for (uint32_t j = t; j < ne; j += 256) {
-        s_end[j] = __ldg(a.ent_end + e0 + j);
-        s_idx[j] = __ldg(a.ent_idx + e0 + j) - dense_base(L);
-    }
-    const uint64_t ob = b.byte_off + (uint64_t)k0 * (L + 1);
-    const uint32_t head = (uint32_t)(ob & 15u);
-    __syncthreads();
-    constexpr uint32_t G = kDenseTile / 256;   // consecutive words per thread
-    const uint32_t i0 = G * t;
-    if (i0 < nk) {
-        const uint32_t wfirst = w0 + i0;
-        uint32_t lo = 0, hi = ne - 1;   // first j with s_end[j] > wfirst
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (s_end[mid] > wfirst) hi = mid;
-            else lo = mid + 1;
+        s_end[j] = min(__ldg(a.ent_end + e0 + j) - w0, nk);
+        uint32_t x = __ldg(a.ent_idx + e0 + j) - dense_base(L);
+        uint64_t pat = (uint64_t)'\n' << (8 * L);
+        for (int q = (int)L - 1; q >= 0; q--) {
+            const uint32_t y = x / 26u;
+            pat |= (uint64_t)('a' + (x - y * 26u)) << (8 * q);
+            x = y;
         }
-        uint32_t j = lo, dec_j = 0xffffffffu;
-        uint8_t ch[5];
-        for (uint32_t i = i0; i < min(i0 + G, nk); i++) {
-            const uint32_t w = w0 + i;
-            while (s_end[j] <= w) j++;
-            if (j != dec_j) {
-                uint32_t x = s_idx[j];
-#pragma unroll
-                for (int q = 4; q >= 0; q--) {
-                    if ((uint32_t)q < L) {
-                        const uint32_t y = x / 26u;
-                        ch[q] = (uint8_t)('a' + (x - y * 26u));
-                        x = y;
-                    }
-                }
-                dec_j = j;
+        s_pat[j] = pat;
+    }
+    __syncthreads();
+    // tile-relative byte offsets (u32): the tile's bytes are [ob, ob + nb); chunk i covers [16 i - h, 16 i - h + 16)
+    const uint64_t ob = b.byte_off + (uint64_t)k0 * P;
+    const uint32_t h = (uint32_t)(ob & 15u), nb = nk * P;
+    const uint32_t nch = (h + nb + 15) >> 4;
+    const uint32_t G = (nch + 255) / 256;
+    const uint32_t i0 = t * G;
+    if (i0 >= nch) return;
+    uint4 *dst4 = reinterpret_cast<uint4 *>(a.words + (ob - h));
+    uint8_t *dst1 = a.words + (ob - h);
+    int32_t x = (int32_t)(16 * i0) - (int32_t)h;   // tile-relative start of chunk i0 (may be < 0 for i0 = 0)
+    uint32_t lo = x > 0 ? (uint32_t)x : 0u;
+    uint32_t q = lo / P, r = lo - q * P;   // tile-relative word, byte inside it
+    uint32_t j = 0;
+    {   // first entry with s_end > q
+        uint32_t hi = ne - 1;
+        while (j < hi) {
+            const uint32_t mid = (j + hi) >> 1;
+            if (s_end[mid] > q) hi = mid;
+            else j = mid + 1;
+        }
+    }
+    uint32_t wj = 0xffffffffu;   // entry whose periodic window is in W0..W2
+    uint64_t W0 = 0, W1 = 0, W2 = 0;
+    const uint32_t iend = min(i0 + G, nch);
+    for (uint32_t i = i0; i < iend; i++, x += 16) {
+        const uint32_t hb = min((uint32_t)(x + 16), nb);   // this tile's bytes of the chunk: [lo, hb)
+        const bool full = (int32_t)lo == x && hb == (uint32_t)(x + 16);
+        uint64_t acc0 = 0, acc1 = 0;
+        if (full && (s_end[j] - q) * P - r >= 16u) {   // inside entry j's run
+            if (j != wj) {
+                const uint64_t pat = s_pat[j];
+                W0 = rep64(pat, P, 0);
+                W1 = rep64(pat, P, 8u % P);
+                W2 = rep64(pat, P, 16u % P);
+                wj = j;
             }
-            uint8_t *o = stage + head + i * (L + 1);
-#pragma unroll
-            for (int q = 0; q < 5; q++)
-                if ((uint32_t)q < L) o[q] = ch[q];
-            o[L] = '\n';
+            acc0 = fshr64(W0, W1, 8 * r);
+            acc1 = fshr64(W1, W2, 8 * r);
+            const uint32_t n = r + 16u, d = (n * magic) >> 16;
+            q += d;
+            r = n - d * P;
+            if (q >= s_end[j] && j + 1 < ne) j++;
+        } else {
+            uint32_t o = lo - (uint32_t)x;
+            while (o < hb - (uint32_t)x) {
+                const uint64_t pat = s_pat[j] >> (8 * r);
+                if (o < 8) {
+                    acc0 |= pat << (8 * o);
+                    if (o) acc1 |= pat >> (64 - 8 * o);
+                } else {
+                    acc1 |= pat << (8 * (o - 8));
+                }
+                o += P - r;
+                r = 0;
+                if (++q >= s_end[j] && j + 1 < ne) j++;
+            }
+            // the word that crossed into the next chunk resumes at byte (o - 16) of itself
+            if (o > 16) {
+                q--;
+                if (j > 0 && q < s_end[j - 1]) j--;
+                r = P - (o - 16);
+            }
         }
+        if (full) {
+            dst4[i] = make_uint4((uint32_t)acc0, (uint32_t)(acc0 >> 32), (uint32_t)acc1, (uint32_t)(acc1 >> 32));
+        } else {   // a chunk shared with the neighbouring tile: only this tile's bytes
+            for (uint32_t y = lo; y < hb; y++) {
+                const uint32_t k = y - (uint32_t)x;
+                dst1[16 * i + k] = (uint8_t)((k < 8 ? acc0 >> (8 * k) : acc1 >> (8 * (k - 8))) & 0xffu);
+            }
+        }
+        lo = (uint32_t)(x + 16);
     }
-    __syncthreads();
-    const uint64_t end = ob + (uint64_t)nk * (L + 1);
-    const uint64_t a0 = (ob + 15) & ~15ull, a1 = end & ~15ull;
-    if (a0 >= a1) {
-        for (uint64_t x = ob + t; x < end; x += 256) a.words[x] = stage[head + (x - ob)];
-        return;
-    }
-    for (uint64_t x = ob + t; x < a0; x += 256) a.words[x] = stage[head + (x - ob)];
-    for (uint64_t x = a1 + t; x < end; x += 256) a.words[x] = stage[head + (x - ob)];
-    const uint64_t base16 = ob & ~15ull;
-    uint4 *dst = reinterpret_cast<uint4 *>(a.words);
-    for (uint64_t x = a0 + 16ull * t; x < a1; x += 16ull * 256) dst[x >> 4] = *reinterpret_cast<const uint4 *>(stage + (x - base16));
 }
+constexpr size_t kEmitDenseSmem = 12 * kDenseTileEnt;
 
 // ------------------------------------------------------------------ K3c: chunks -> length buckets
 // Each staged key's length is recovered from its trailing zero 5-bit codes (letters are codes 1..26,
@@ -704,6 +752,7 @@ cudaError_t launch_dense_scan(const DenseArgs &a, cudaStream_t s) {
     k_dense_reduce<<<nblk, 256, 0, s>>>(a);
     k_dense_scan<<<1, 1024, 0, s>>>(a, nblk);
     k_dense_compact<<<nblk, 256, 0, s>>>(a);
+    if (a.tile_e0 && a.ntiles) k_dense_tiles<<<(a.ntiles + 255) / 256, 256, 0, s>>>(a, a.ntiles);
     return cudaGetLastError();
 }
 uint32_t dense_scan_blocks(uint32_t n_entries) { return (n_entries + kDenseBlk - 1) / kDenseBlk; }
@@ -712,10 +761,11 @@ cudaError_t launch_dense_lensum(const uint32_t *dense, uint32_t *ghist, cudaStre
     return cudaGetLastError();
 }
 
-uint32_t dense_emit_tile_words() { return kDenseTile; }
 cudaError_t launch_emit_dense(const DenseEmitArgs &a, cudaStream_t s) {
     if (a.ntiles == 0) return cudaSuccess;
-    k_emit_dense<<<a.ntiles, 256, 0, s>>>(a);
+    cudaError_t e = cudaFuncSetAttribute(k_emit_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEmitDenseSmem);
+    if (e != cudaSuccess) return e;
+    k_emit_dense<<<a.ntiles, 256, kEmitDenseSmem, s>>>(a);
     return cudaGetLastError();
 }
 

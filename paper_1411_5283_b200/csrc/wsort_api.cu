@@ -77,7 +77,7 @@ struct wsort_ctx {
     DevBuf ghist, dense, pool, chunk_cls, chunk_fill, ig_ctr;
     uint32_t *h_ig = nullptr;   // pinned mirror of ig_ctr
     uint32_t cta_chunks = 0, n_chunks = 0;
-    DevBuf d_blk_sum, d_blk_nnz, d_ent_idx, d_ent_end, d_n_ent, d_tiles2, d_lcursor;
+    DevBuf d_blk_sum, d_blk_nnz, d_ent_idx, d_ent_end, d_n_ent, d_tiles2, d_lcursor, d_tile_e;
 
     // sort
     DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y, splits;
@@ -381,7 +381,7 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->m_pat, &c->m_qparts, &c->m_pbase, &c->m_jdone,
                       &c->m_jovf, &c->m_partn, &c->m_plist, &c->m_qemit, &c->ghist, &c->dense,
                       &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
-                      &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor};
+                      &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor, &c->d_tile_e};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_sum) cudaFreeHost(c->h_sum);
@@ -1250,10 +1250,9 @@ int chunk_scatter(wsort_ctx *c, const BucketInfo *db, double key_bytes) {
 // bk[L].byte_off. Records ev_join on the aux stream; the caller joins.
 int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketInfo *d_bk, double out_bytes) {
     uint32_t dpfx[257], ndt = 0;   // dense emit tiles, bucket by bucket (tile_from_prefix)
-    const uint32_t te = dense_emit_tile_words();
     for (uint32_t L = 0; L < 256; L++) {
         dpfx[L] = ndt;
-        if (L >= 1 && L <= kDenseMaxLen) ndt += (bk[L].n + te - 1) / te;
+        if (L >= 1 && L <= kDenseMaxLen) ndt += (bk[L].n + dense_tile_words(L) - 1) / dense_tile_words(L);
     }
     dpfx[256] = ndt;
     const uint32_t ne = dense_entries(), nblk = dense_scan_blocks(ne);
@@ -1263,6 +1262,7 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
     if ((rc = ensure(c, c->d_ent_idx, (size_t)ne * 4, "dense entries"))) return rc;
     if ((rc = ensure(c, c->d_ent_end, (size_t)ne * 4, "dense entry ends"))) return rc;
     if ((rc = ensure(c, c->d_n_ent, 16, "dense entry count"))) return rc;
+    if ((rc = ensure(c, c->d_tile_e, (size_t)2 * (ndt + 1) * 4, "dense tile entries"))) return rc;
     if ((rc = arena_upload(c, c->d_tiles2, dpfx, sizeof dpfx, "dense tile prefix"))) return rc;
     static const bool no_aux = getenv("WSORT_NO_AUX") != nullptr;   // (experiments: serial dense branch)
     if (!c->aux) {
@@ -1281,6 +1281,11 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
     da.ent_idx = static_cast<uint32_t *>(c->d_ent_idx.p);
     da.ent_end = static_cast<uint32_t *>(c->d_ent_end.p);
     da.n_ent = static_cast<uint32_t *>(c->d_n_ent.p);
+    da.buckets = d_bk;
+    da.tile_pfx = static_cast<const uint32_t *>(c->d_tiles2.p);
+    da.tile_e0 = static_cast<uint32_t *>(c->d_tile_e.p);
+    da.tile_e1 = da.tile_e0 + ndt + 1;
+    da.ntiles = ndt;
     rc = launch_on(c, c->aux, "k2d_dense_scan", 2.0 * ne * 4, [&] { return launch_dense_scan(da, c->aux); });
     if (rc) return rc;
     DenseEmitArgs ea{};
@@ -1290,6 +1295,8 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
     ea.ent_idx = da.ent_idx;
     ea.ent_end = da.ent_end;
     ea.n_ent = da.n_ent;
+    ea.tile_e0 = da.tile_e0;
+    ea.tile_e1 = da.tile_e1;
     ea.words = static_cast<uint8_t *>(c->words.p);
     rc = launch_on(c, c->aux, "k5d_emit_dense", out_bytes, [&] { return launch_emit_dense(ea, c->aux); });
     if (rc) return rc;

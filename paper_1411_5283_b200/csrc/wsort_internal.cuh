@@ -124,12 +124,19 @@ uint32_t dense_entries();
 uint32_t dense_table_base(uint32_t L);
 cudaError_t launch_ingest(const IngestArgs &a, cudaStream_t s);
 
+// words per k_emit_dense tile of dense bucket L: L <= 2 has <= 676 entries in all, longer buckets <= one
+// entry per word (the tile's entries must fit its shared memory, kDenseTileEnt)
+__host__ __device__ constexpr uint32_t dense_tile_words(uint32_t L) { return L <= 2 ? 32768u : 2048u; }
 struct DenseArgs {
     const uint32_t *dense;
     uint32_t n_entries;
     uint32_t *blk_sum, *blk_nnz;            // [dense_scan_blocks()]
     uint32_t *ent_idx, *ent_end;            // compacted non-zero entries: table index, inclusive word end
     uint32_t *n_ent;                        // [2]: entries, words
+    const BucketInfo *buckets;              // (emit tiles) the dense buckets' word ranges
+    const uint32_t *tile_pfx;               // [257] first emit tile of each dense bucket
+    uint32_t *tile_e0, *tile_e1;            // [emit tiles] entry of the tile's first / last word (nullable)
+    uint32_t ntiles;                        // emit tiles
 };
 uint32_t dense_scan_blocks(uint32_t n_entries);
 cudaError_t launch_dense_lensum(const uint32_t *dense, uint32_t *ghist, cudaStream_t s);   // ghist[1..5] += table sums
@@ -140,9 +147,9 @@ struct DenseEmitArgs {
     const uint32_t *tile_pfx;      // [257] first tile of each dense bucket (tile_from_prefix)
     uint32_t ntiles;
     const uint32_t *ent_idx, *ent_end, *n_ent;
+    const uint32_t *tile_e0, *tile_e1;   // from k_dense_compact
     uint8_t *words;
 };
-uint32_t dense_emit_tile_words();
 cudaError_t launch_emit_dense(const DenseEmitArgs &a, cudaStream_t s);
 
 struct L0Args {
