@@ -181,6 +181,18 @@ int wsort_set_profiling(wsort_ctx *c, int on);
 /* Synchronises; fills up to cap entries and *n with the number of kernel classes seen. */
 int wsort_kernel_stats(wsort_ctx *c, wsort_kernel_stat *out, int cap, int *n);
 int wsort_reset_kernel_stats(wsort_ctx *c);
+/* How the last wsort_tokenize counted the words of >= 6 letters (diagnostics): */
+typedef struct {
+    int32_t mode;              /* 1: counted into the table of distinct words (k_hash.cuh); 0: staged as keys */
+    uint32_t overflow;         /* nonzero: the table overflowed (reason code) and the text was staged instead */
+    uint64_t distinct_narrow;  /* distinct words of 6..12 letters seen by the table */
+    uint64_t distinct_wide;    /* distinct words of 13..66 letters seen by the table */
+    uint64_t narrow_slots, wide_slots;
+    uint32_t grow;             /* table size factor the context has reached (x4 per overflow) */
+    uint32_t reserved;
+} wsort_ingest_info;
+int wsort_get_ingest_info(const wsort_ctx *c, wsort_ingest_info *out);
+
 /* Number of kernel launches enqueued by this context since creation. */
 uint64_t wsort_launch_count(const wsort_ctx *c);
 

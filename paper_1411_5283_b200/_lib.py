@@ -41,7 +41,7 @@ EXPORTS = [
     "wsort_destroy", "wsort_set_profiling", "wsort_kernel_stats", "wsort_reset_kernel_stats",
     "wsort_launch_count", "wsort_histogram", "wsort_pack", "wsort_sample", "wsort_select_splitters",
     "wsort_partition", "wsort_load_keys", "wsort_set_global", "wsort_fetch_async", "wsort_sync",
-    "wsort_pack_long", "wsort_dense_range",
+    "wsort_pack_long", "wsort_dense_range", "wsort_get_ingest_info",
 ]
 
 
@@ -59,6 +59,19 @@ class Result(ctypes.Structure):
         ("n_words", ctypes.c_uint64),
         ("word_base", ctypes.c_uint64),
         ("byte_base", ctypes.c_uint64),
+    ]
+
+
+class IngestInfo(ctypes.Structure):
+    _fields_ = [
+        ("mode", ctypes.c_int32),
+        ("overflow", ctypes.c_uint32),
+        ("distinct_narrow", ctypes.c_uint64),
+        ("distinct_wide", ctypes.c_uint64),
+        ("narrow_slots", ctypes.c_uint64),
+        ("wide_slots", ctypes.c_uint64),
+        ("grow", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
     ]
 
 
@@ -106,6 +119,7 @@ def load():
     L.wsort_launch_count.argtypes = [P]
     L.wsort_launch_count.restype = U64
     L.wsort_histogram.argtypes = [P, P]
+    L.wsort_get_ingest_info.argtypes = [P, P]
     L.wsort_pack.argtypes = [P]
     L.wsort_sample.argtypes = [P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, P]
     L.wsort_select_splitters.argtypes = [P, U64, ctypes.c_uint32, ctypes.c_uint32, P]

@@ -223,6 +223,12 @@ class WSort:
     def reset_kernel_stats(self):
         self._check(self._lib.wsort_reset_kernel_stats(self._h), "wsort_reset_kernel_stats")
 
+    def ingest_info(self) -> dict:
+        """How the last tokenize counted the words of >= 6 letters (wsort_get_ingest_info)."""
+        info = L.IngestInfo()
+        self._check(self._lib.wsort_get_ingest_info(self._h, ctypes.byref(info)), "wsort_get_ingest_info")
+        return {k: int(getattr(info, k)) for k, _ in L.IngestInfo._fields_}
+
     def launch_count(self) -> int:
         return int(self._lib.wsort_launch_count(self._h))
 

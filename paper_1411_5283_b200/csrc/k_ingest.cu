@@ -21,6 +21,7 @@
 //   the entry whose count range holds w; written as "word\n" (reading A12).
 #include <algorithm>
 
+#include "k_hash.cuh"
 #include "k_text.cuh"
 #include "k_tma.cuh"
 #include "wsort_internal.cuh"
@@ -116,6 +117,40 @@ __device__ __forceinline__ uint32_t inclusive_scan_warp(uint32_t v, int lane) {
 // letters leading a 32-bit letter mask, and whether all 32 are letters
 __device__ __forceinline__ uint32_t lead_run(uint32_t M) { return M == 0xffffffffu ? 32u : (uint32_t)(__ffs(~M) - 1); }
 
+// ---- hash mode: long words counted into the global table of distinct words (k_hash.cuh)
+// Words [0, i1) of a warp's long list (from the back), one per lane: histogram, then the word's slot
+// (found or inserted) gets one more occurrence. Words of > 66 letters are not counted (the host takes
+// the K3 path for such texts).
+__device__ __forceinline__ void hash_long(const IngestArgs &a, IgSmem &sm, const uint16_t *lst, uint32_t i1,
+                                          const uint32_t *wb32, int lane) {
+    for (uint32_t b = 0; b < i1; b += 32) {
+        const uint32_t i = b + lane;
+        if (i >= i1) break;
+        const uint32_t x = lst[kWList - 1 - i];
+        const uint32_t s = x & 1023u, L = (x >> 10) + 6u;
+        if (L > 6u * kMaxStageKw) {
+            atomicAdd(&a.ctr[kIgVeryLong], 1u);
+            continue;
+        }
+        atomicAdd(&sm.hist[L], 1u);
+        if (a.debug & 2) continue;
+        if (L <= 24u) {
+            const uint32_t w0 = pack6(wb32, s, 6u);
+            const uint32_t w1 = L > 6u ? pack6(wb32, s + 6u, L - 6u) : 0u;
+            const uint32_t w2 = L > 12u ? pack6(wb32, s + 12u, L - 12u) : 0u;
+            const uint32_t w3 = L > 18u ? pack6(wb32, s + 18u, L - 18u) : 0u;
+            const uint32_t slot = hashtab::find_narrow(a.tab, hashtab::narrow_key(w0, w1, w2, w3), L, true);
+            if (slot != hashtab::kUnset) atomicAdd(a.tab.ncnt + slot, 1u);   // (else overflow: staging fallback)
+        } else {   // key word q = letters 6q .. 6q+5, recomputed from the text when needed
+            const uint32_t k = (L + 5u) / 6u;
+            auto get = [&](uint32_t q) { return pack6(wb32, s + 6u * q, L - 6u * q); };
+            const uint64_t fp = hashtab::fingerprint(L, k, get);
+            const uint32_t slot = hashtab::find(a.tab, L, k, fp, get, true);
+            if (slot != hashtab::kUnset) atomicAdd(a.tab.cnt + slot, 1u);
+        }
+    }
+}
+
 // K1. The CTA's byte range is split into 16 contiguous warp ranges of 1 KiB sub-steps; each warp
 // streams its sub-steps with no block barrier: every lane classifies 32 bytes (SWAR letter mask, loaded
 // one sub-step ahead), word starts / ends come from mask shifts, the letter runs crossing lane
@@ -124,6 +159,7 @@ __device__ __forceinline__ uint32_t lead_run(uint32_t M) { return M == 0xfffffff
 // listed by category (warp scan) and then taken round-robin by the lanes: hash-cache count / key
 // packing into the class's chunk. Chunk (class, seq) is allocated by the lane that receives its
 // first rank; the others read its id from shared memory (written once).
+template <bool HASH>
 __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs a) {
     extern __shared__ __align__(16) uint8_t ig_smem[];
     IgSmem &sm = *reinterpret_cast<IgSmem *>(ig_smem);
@@ -246,6 +282,12 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
             const uint32_t s = x & 1023u, L = (x >> 10) + 3u;
             cache_add(sm, a.dense, L, dense_index(wb32, s, L));
         }
+        if (HASH) {   // L = 6..66: counted into the global table
+            if (!(a.debug & 8)) hash_long(a, sm, wlst, nlg, wb32, lane);
+            __syncwarp();
+            M = Mn;
+            continue;
+        }
         for (uint32_t i0 = 0; i0 < ((a.debug & 8) ? 0u : nlg); i0 += 32) {   // L = 6..66: key into its class's chunk
             const uint32_t i = i0 + lane;
             const uint32_t x = i < nlg ? wlst[kWList - 1 - i] : 0u;
@@ -288,7 +330,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
     }
     __syncthreads();
     if (t == 0) atomicMax(&a.ctr[kIgMaxChunks], sm.nchunk);
-    if (t < (int)kMaxStageKw) {
+    if (!HASH && t < (int)kMaxStageKw) {
         const uint32_t fill = sm.cls_fill[t], lg = cls_lg(t + 1), cap = 1u << lg;
         const uint32_t nseq = (fill + cap - 1) >> lg;
         for (uint32_t q = 0; q < nseq && q < a.cta_chunks; q++) {
@@ -741,9 +783,15 @@ uint32_t dense_table_base(uint32_t L) { return dense_base(L); }
 cudaError_t launch_ingest(const IngestArgs &a, cudaStream_t s) {
     if (a.grid == 0) return cudaSuccess;
     const size_t smem = ingest_smem(a.cta_chunks);
-    cudaError_t e = cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (a.hash) {
+        cudaError_t e = cudaFuncSetAttribute(k_ingest<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_ingest<true><<<a.grid, kIgThreads, smem, s>>>(a);
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaFuncSetAttribute(k_ingest<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_ingest<<<a.grid, kIgThreads, smem, s>>>(a);
+    k_ingest<false><<<a.grid, kIgThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

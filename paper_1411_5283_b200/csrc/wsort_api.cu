@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "k_hash.cuh"
 #include "wsort.h"
 #include "wsort_internal.cuh"
 
@@ -78,6 +79,14 @@ struct wsort_ctx {
     uint32_t *h_ig = nullptr;   // pinned mirror of ig_ctr
     uint32_t cta_chunks = 0, n_chunks = 0;
     DevBuf d_blk_sum, d_blk_nnz, d_ent_idx, d_ent_end, d_n_ent, d_tiles2, d_lcursor, d_tile_e;
+    // K1 hash mode: the table of distinct long words (k_hash.cuh) and the run emission after the sort
+    bool hashed = false;                         // the last tokenize counted the long words into the table
+    int ingest_mode = 0;                         // 0 = auto (hash, staging if the table overflows), 1 = staging
+    uint64_t hash_grow = 1;                      // table size factor (x4 after an overflow, up to 64)
+    DevBuf t_nkey, t_ncnt, t_fp, t_meta, t_cnt, t_keys, t_top, t_dcount, t_runend, t_scan, t_tilee, t_kplan, t_dpfx, t_rpfx;
+    HashTab tab{};
+    uint32_t *h_tab = nullptr;                   // pinned: top[4] + dcount[256]
+    wsort_ingest_info ig_info{};                 // what the last tokenize did (wsort_get_ingest_info)
 
     // sort
     DevBuf keys_a, keys_b, pay_a, pay_b, words, src_off, dh, status0, status1, tickets, plan, va_x, va_y, splits;
@@ -381,7 +390,9 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->m_pat, &c->m_qparts, &c->m_pbase, &c->m_jdone,
                       &c->m_jovf, &c->m_partn, &c->m_plist, &c->m_qemit, &c->ghist, &c->dense,
                       &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
-                      &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor, &c->d_tile_e};
+                      &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor, &c->d_tile_e,
+                      &c->t_nkey, &c->t_ncnt, &c->t_fp, &c->t_meta, &c->t_cnt, &c->t_keys, &c->t_top, &c->t_dcount, &c->t_runend,
+                      &c->t_scan, &c->t_tilee, &c->t_kplan, &c->t_dpfx, &c->t_rpfx};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_sum) cudaFreeHost(c->h_sum);
@@ -390,6 +401,7 @@ void wsort_destroy(wsort_ctx *c) {
     if (c->arena_done) cudaEventDestroy(c->arena_done);
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->h_ig) cudaFreeHost(c->h_ig);
+    if (c->h_tab) cudaFreeHost(c->h_tab);
     for (auto &pe : c->pending) {
         cudaEventDestroy(pe.a);
         cudaEventDestroy(pe.b);
@@ -465,10 +477,90 @@ int wsort_load_file(wsort_ctx *c, const char *path) {
     return WSORT_OK;
 }
 
+}  // extern "C"
+namespace {
+int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash);
+}
+extern "C" {
 int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     if (!c) return WSORT_E_INVALID_ARG;
     if (c->state < ST_LOADED) return set_err(c, WSORT_E_STATE, "wsort_tokenize before wsort_load_text");
     cudaSetDevice(c->device);
+    static const bool env_stage = getenv("WSORT_INGEST_STAGE") != nullptr;   // (experiments)
+    int rc = tokenize_impl(c, n_words, c->ingest_mode == 0 && !env_stage);
+    while (rc == WSORT_OK && c->hashed && c->h_tab[hashtab::kTopOverflow] && c->hash_grow < 64) {
+        // more distinct long words than the table holds: count again with 4x the slots (kept for later texts)
+        c->hash_grow *= 4;
+        rc = tokenize_impl(c, n_words, true);
+    }
+    if (rc == WSORT_OK && c->hashed && c->h_tab[hashtab::kTopOverflow]) {
+        // still overflowing (e.g. random letters: nearly every long word distinct): stage the keys instead
+        // (one more text pass; the result does not depend on the mode)
+        rc = tokenize_impl(c, n_words, false);
+    }
+    c->ig_info = wsort_ingest_info{};
+    c->ig_info.mode = c->hashed ? 1 : 0;
+    if (c->hashed) {
+        c->ig_info.overflow = c->h_tab[hashtab::kTopOverflow];
+        c->ig_info.grow = (uint32_t)c->hash_grow;
+        c->ig_info.distinct_narrow = c->h_tab[hashtab::kTopNarrow];
+        c->ig_info.distinct_wide = c->h_tab[hashtab::kTopDistinct];
+        c->ig_info.narrow_slots = (uint64_t)c->tab.nmask + 1;
+        c->ig_info.wide_slots = (uint64_t)c->tab.mask + 1;
+    }
+    return rc;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Hash-mode table sizing: 2^k slots ~ one per 512 (narrow: 6..24 letters) / 4096 (wide: 25..66 letters)
+// text bytes, times the context's growth factor (x4 after each overflow, kept for later texts), each
+// table at most 70 % filled; key store for 8 words per distinct wide word. c4 (1 GiB): ~1 M distinct
+// words of 6..24 letters in 2 M slots.
+int hash_alloc(wsort_ctx *c) {
+    uint32_t nslots = 4096, slots = 4096;
+    while (nslots < (1u << 24) && ((uint64_t)nslots * 512 < c->n * c->hash_grow || nslots < 4096 * c->hash_grow)) nslots <<= 1;
+    while (slots < (1u << 24) && ((uint64_t)slots * 4096 < c->n * c->hash_grow || slots < 4096 * c->hash_grow)) slots <<= 1;
+    const uint32_t maxd = (uint32_t)((uint64_t)slots * 7 / 10), key_cap = maxd * 8 + 1024;
+    int rc;
+    if ((rc = ensure(c, c->t_nkey, (size_t)nslots * 16, "hash narrow keys"))) return rc;
+    if ((rc = ensure(c, c->t_ncnt, (size_t)nslots * 4, "hash narrow counts"))) return rc;
+    CK(cudaMemsetAsync(c->t_nkey.p, 0, (size_t)nslots * 16, c->stream), "memset hash narrow keys");
+    CK(cudaMemsetAsync(c->t_ncnt.p, 0, (size_t)nslots * 4, c->stream), "memset hash narrow counts");
+    if ((rc = ensure(c, c->t_fp, (size_t)slots * 8, "hash fingerprints"))) return rc;
+    if ((rc = ensure(c, c->t_meta, (size_t)slots * 4, "hash meta"))) return rc;
+    if ((rc = ensure(c, c->t_cnt, (size_t)slots * 4, "hash counts"))) return rc;
+    if ((rc = ensure(c, c->t_keys, (size_t)key_cap * 4, "hash keys"))) return rc;
+    if ((rc = ensure(c, c->t_top, 16, "hash top"))) return rc;
+    if ((rc = ensure(c, c->t_dcount, 256 * 4, "hash distinct counts"))) return rc;
+    if (!c->h_tab && cudaMallocHost(&c->h_tab, (4 + 256) * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(c, WSORT_E_NOMEM, "pinned hash info");
+    }
+    CK(cudaMemsetAsync(c->t_fp.p, 0, (size_t)slots * 8, c->stream), "memset hash fp");
+    CK(cudaMemsetAsync(c->t_meta.p, 0xff, (size_t)slots * 4, c->stream), "memset hash meta");
+    CK(cudaMemsetAsync(c->t_cnt.p, 0, (size_t)slots * 4, c->stream), "memset hash counts");
+    CK(cudaMemsetAsync(c->t_top.p, 0, 16, c->stream), "memset hash top");
+    CK(cudaMemsetAsync(c->t_dcount.p, 0, 256 * 4, c->stream), "memset hash distinct");
+    HashTab &t = c->tab;
+    t.nkey = static_cast<unsigned long long *>(c->t_nkey.p);
+    t.ncnt = static_cast<uint32_t *>(c->t_ncnt.p);
+    t.nmask = nslots - 1;
+    t.fp = static_cast<unsigned long long *>(c->t_fp.p);
+    t.meta = static_cast<uint32_t *>(c->t_meta.p);
+    t.cnt = static_cast<uint32_t *>(c->t_cnt.p);
+    t.keys = static_cast<uint32_t *>(c->t_keys.p);
+    t.top = static_cast<uint32_t *>(c->t_top.p);
+    t.dcount = static_cast<uint32_t *>(c->t_dcount.p);
+    t.mask = slots - 1;
+    t.key_cap = key_cap;
+    t.max_distinct = maxd;
+    return WSORT_OK;
+}
+
+int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     TkArgs &a = c->tk;
     int rc;
     const uint32_t G = std::max<uint32_t>(a.grid, 1);
@@ -480,8 +572,10 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     if ((rc = ensure(c, c->ig_ctr, kIgCtrs * 4, "ingest counters"))) return rc;
     // staging chunks: each CTA owns a region of the pool; a staged word of kw key words has >= 6kw-4
     // letters plus a separator, so its key bytes <= its text bytes
-    c->cta_chunks = ingest_cta_chunks((uint64_t)a.steps_per_cta * kTkStep);
+    c->cta_chunks = hash ? 0u : ingest_cta_chunks((uint64_t)a.steps_per_cta * kTkStep);
     c->n_chunks = G * c->cta_chunks;
+    c->hashed = hash;
+    if (hash && (rc = hash_alloc(c))) return rc;
     if ((rc = ensure(c, c->pool, ((size_t)c->n_chunks + 1) * kChunkWords * 4, "staging pool"))) return rc;
     if ((rc = ensure(c, c->chunk_cls, (size_t)c->n_chunks * 4, "chunk classes"))) return rc;
     if ((rc = ensure(c, c->chunk_fill, (size_t)c->n_chunks * 4, "chunk fills"))) return rc;
@@ -508,6 +602,8 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     ia.chunk_fill = static_cast<uint32_t *>(c->chunk_fill.p);
     ia.cta_chunks = c->cta_chunks;
     ia.ctr = static_cast<uint32_t *>(c->ig_ctr.p);
+    ia.hash = hash ? 1u : 0u;
+    ia.tab = c->tab;
     if (const char *dbg = getenv("WSORT_INGEST_DEBUG")) ia.debug = (uint32_t)atoi(dbg);
     rc = launch(c, "k1_ingest", (double)c->n, [&] { return launch_ingest(ia, c->stream); });
     if (rc) return rc;
@@ -519,7 +615,20 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     if (rc) return rc;
     CK(copy_small(c->h_ig, c->ig_ctr.p, kIgCtrs * 4, c->stream), "copy ingest counters");
     CK(copy_small(c->h_sum, c->d_sum.p, sizeof(Summary), c->stream), "copy summary");
+    if (hash) {
+        CK(copy_small(c->h_tab, c->t_top.p, 16, c->stream), "copy hash top");
+        CK(copy_small(c->h_tab + 4, c->t_dcount.p, 256 * 4, c->stream), "copy hash distinct counts");
+    }
     CK(cudaStreamSynchronize(c->stream), "tokenize");
+    if (hash) {   // fill of the tables (distinct words per length counted by K1) against their capacity
+        uint64_t dn = 0, dw = 0;
+        for (uint32_t L = kDenseMaxLen + 1; L < 256; L++) (L <= 24 ? dn : dw) += c->h_tab[4 + L];
+        c->h_tab[hashtab::kTopNarrow] = (uint32_t)dn;
+        c->h_tab[hashtab::kTopDistinct] = (uint32_t)dw;
+        if (dn * 10 > (uint64_t)(c->tab.nmask + 1) * 7 || dw * 10 > (uint64_t)(c->tab.mask + 1) * 7)
+            c->h_tab[hashtab::kTopOverflow] |= 8u;
+        if (c->h_tab[hashtab::kTopOverflow]) return WSORT_OK;   // (the caller re-tokenizes: bigger table / staging)
+    }
     c->cta_bases_ready = c->cta_counts_ready = false;
     if (c->h_ig[kIgVeryLong]) {   // words of 67..255 letters were not staged: histogram them the K3 way
         CK(cudaMemsetAsync(c->ghist.p, 0, kHistBins * 4, c->stream), "memset ghist");
@@ -534,7 +643,7 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
         CK(cudaStreamSynchronize(c->stream), "tokenize (long words)");
     }
     const Summary &s = *c->h_sum;
-    if (c->prof && !c->h_ig[kIgVeryLong]) {   // K1's algorithmic bytes: the text + the staged keys it wrote
+    if (c->prof && !c->h_ig[kIgVeryLong] && !hash) {   // K1's algorithmic bytes: the text + the staged keys it wrote
         double staged = 0;
         for (uint32_t L = kDenseMaxLen + 1; L <= s.max_len && L <= 6 * kMaxStageKw; L++)
             staged += 4.0 * kw_of((int)L) * (double)(s.off[L + 1] - s.off[L]);
@@ -557,7 +666,8 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     return WSORT_OK;
 }
 
-}  // extern "C"
+}  // namespace
+
 
 namespace {
 
@@ -1166,9 +1276,10 @@ std::vector<BucketInfo> msd_buckets(const Summary &s, uint32_t lkey, uint32_t &m
 // buckets of at most one CTA tile go straight to the finishing jobs. Ends with the keys emitted.
 template <class Pack>
 int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint32_t max_tw, uint32_t levels,
-                  uint64_t key_words, uint64_t W, bool finish_radix, Pack pack, const BucketInfo *d_bk_pre = nullptr) {
+                  uint64_t key_words, uint64_t W, bool finish_radix, Pack pack, const BucketInfo *d_bk_pre = nullptr,
+                  bool emit = true, uint32_t lmax_keys = 0) {
     const Summary &s = *c->h_sum;
-    const uint32_t lmax = s.max_len;
+    const uint32_t lmax = lmax_keys ? lmax_keys : s.max_len;
     int rc;
     if ((rc = ensure(c, c->keys_a, key_words * 4 + 64, "keys_a"))) return rc;
     if ((rc = ensure(c, c->keys_b, key_words * 4 + 64, "keys_b"))) return rc;
@@ -1206,7 +1317,7 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
     m.words = static_cast<uint8_t *>(c->words.p);
     if ((rc = msd_levels_and_finish(c, m, 0, (uint32_t)segs.size(), (uint32_t)tiles.size(), levels, key_bytes, max_tw)))
         return rc;
-    if (!finish_radix) return WSORT_OK;   // the streaming finish wrote the text (K5 fused)
+    if (!finish_radix || !emit) return WSORT_OK;   // the streaming finish wrote the text (K5 fused)
     return emit_keys(c, bk, d_bk, lkey, lmax, key_bytes + (double)(s.byte_off[256] - s.byte_off[lkey]));
 }
 
@@ -1332,6 +1443,89 @@ int sort_dense_msd(wsort_ctx *c) {
     return rc;
 }
 
+// AUTO after a hash-mode tokenize (every word <= 66 letters): dense buckets as in sort_dense_msd; the long
+// words from the table of distinct words: gather the D distinct keys into their length buckets, sort them
+// (MSD, radix finish: keys end in buffer B), look up each one's count, scan, and write the runs.
+int sort_dense_hash(wsort_ctx *c) {
+    const Summary &s = *c->h_sum;
+    uint32_t max_tw, levels;
+    uint64_t key_words;
+    std::vector<BucketInfo> bk = msd_buckets(s, kDenseMaxLen + 1, max_tw, levels, key_words);
+    const uint64_t n_dense = s.off[kDenseMaxLen + 1];
+    int rc;
+    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    if ((rc = arena_upload(c, c->plan, bk.data(), bk.size() * sizeof(BucketInfo), "plan"))) return rc;
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
+    if (n_dense && (rc = dense_branch(c, bk, d_bk, (double)s.byte_off[kDenseMaxLen + 1]))) return rc;
+    // the distinct keys' buckets (kb[L].n = distinct words of length L), laid out as msd_buckets does
+    const uint32_t *dcount = c->h_tab + 4;
+    Summary ks = s;
+    std::vector<uint64_t> nd(256, 0);
+    uint32_t dpfx[257], rpfx[257], D = 0, ntiles = 0, lmax_d = 0;
+    for (uint32_t L = 0; L < 256; L++) {
+        dpfx[L] = D;
+        rpfx[L] = ntiles;
+        if (L > kDenseMaxLen && dcount[L]) {
+            nd[L] = dcount[L];
+            D += dcount[L];
+            lmax_d = L;
+            ntiles += (bk[L].n + run_tile_words(L) - 1) / run_tile_words(L);
+        }
+    }
+    dpfx[256] = D;
+    rpfx[256] = ntiles;
+    if (D) {
+        for (uint32_t L = 0; L < 256; L++) ks.off[L + 1] = ks.off[L] + nd[L];   // (only the sizes are used)
+        uint32_t kmax_tw, klevels;
+        uint64_t kkey_words;
+        std::vector<BucketInfo> kb = msd_buckets(ks, kDenseMaxLen + 1, kmax_tw, klevels, kkey_words);
+        if ((rc = ensure(c, c->t_runend, (size_t)D * 4, "run ends"))) return rc;
+        if ((rc = ensure(c, c->t_scan, (size_t)hash_scan_blocks(D) * 4, "run scan"))) return rc;
+        if ((rc = ensure(c, c->t_tilee, (size_t)2 * (ntiles + 1) * 4, "run tiles"))) return rc;
+        if ((rc = ensure(c, c->d_lcursor, 256 * 4, "length cursors"))) return rc;
+        if ((rc = arena_upload(c, c->t_kplan, kb.data(), kb.size() * sizeof(BucketInfo), "key plan"))) return rc;
+        if ((rc = arena_upload(c, c->t_dpfx, dpfx, sizeof dpfx, "distinct prefix"))) return rc;
+        if ((rc = arena_upload(c, c->t_rpfx, rpfx, sizeof rpfx, "run tile prefix"))) return rc;
+        const BucketInfo *d_kb = reinterpret_cast<const BucketInfo *>(c->t_kplan.p);
+        rc = sort_msd_core(c, kb, kDenseMaxLen + 1, kmax_tw, klevels, kkey_words, D, true,
+                           [&](const BucketInfo *db, double kbytes) {
+                               CK(cudaMemsetAsync(c->d_lcursor.p, 0, 256 * 4, c->stream), "memset length cursors");
+                               HashGatherArgs ga{};
+                               ga.tab = c->tab;
+                               ga.buckets = db;
+                               ga.lcursor = static_cast<uint32_t *>(c->d_lcursor.p);
+                               ga.keys_a = static_cast<uint32_t *>(c->keys_a.p);
+                               return launch(c, "kh1_hash_gather", kbytes, [&] { return launch_hash_gather(ga, c->stream); });
+                           },
+                           d_kb, false, lmax_d);
+        if (rc) return rc;
+        HashRunArgs ra{};
+        ra.tab = c->tab;
+        ra.buckets = d_bk;
+        ra.kbuckets = d_kb;
+        ra.dist_pfx = static_cast<const uint32_t *>(c->t_dpfx.p);
+        ra.D = D;
+        ra.keys = static_cast<const uint32_t *>(c->keys_b.p);
+        ra.run_end = static_cast<uint32_t *>(c->t_runend.p);
+        ra.long_base = s.off[kDenseMaxLen + 1];
+        ra.tile_pfx = static_cast<const uint32_t *>(c->t_rpfx.p);
+        ra.ntiles = ntiles;
+        ra.tile_e0 = static_cast<uint32_t *>(c->t_tilee.p);
+        ra.tile_e1 = ra.tile_e0 + ntiles + 1;
+        ra.words = static_cast<uint8_t *>(c->words.p);
+        rc = launch(c, "kh2_hash_runs", (double)D * 8, [&] { return launch_hash_runs(ra, static_cast<uint32_t *>(c->t_scan.p), c->stream); });
+        if (rc) return rc;
+        rc = launch(c, "kh5_emit_runs", (double)(s.byte_off[256] - s.byte_off[kDenseMaxLen + 1]),
+                    [&] { return launch_emit_runs(ra, c->stream); });
+        if (rc) return rc;
+    }
+    if (n_dense) {   // join: the sort is complete when both streams are
+        const cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+        if (!rc && e != cudaSuccess) return cuda_err(c, e, "join wait");
+    }
+    return rc;
+}
+
 // Split multi-GPU sort (after wsort_pack_long, the all-reduce of the dense tables, wsort_load_keys and
 // wsort_dense_range): this rank's slice of the global dense words, then the keys it received, sorted.
 int sort_dist_dense(wsort_ctx *c) {
@@ -1393,7 +1587,13 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
         rc = sort_dist_dense(c);
     } else if (algo == WSORT_ALGO_OETS_MERGE) {
         rc = sort_oets(c, want_src);
+    } else if (algo == WSORT_ALGO_AUTO && ingest_ok && c->hashed && kw_of((int)c->h_sum->max_len) <= (int)kRadixRegMaxKw) {
+        rc = sort_dense_hash(c);   // (the distinct keys' MSD radix finish holds keys of <= 8 words: L <= 48)
     } else if ((algo == WSORT_ALGO_AUTO || algo == WSORT_ALGO_DENSE_MSD) && ingest_ok) {
+        if (c->hashed) {   // DENSE_MSD reads the staged keys: tokenize again, staging
+            rc = tokenize_impl(c, nullptr, false);
+            if (rc) return rc;
+        }
         rc = sort_dense_msd(c);
     } else if ((algo == WSORT_ALGO_MSD_RADIX || algo == WSORT_ALGO_MSD_OETS || algo == WSORT_ALGO_AUTO ||
                 algo == WSORT_ALGO_DENSE_MSD) && !want_src &&
@@ -1511,6 +1711,13 @@ int wsort_reset_kernel_stats(wsort_ctx *c) {
 
 uint64_t wsort_launch_count(const wsort_ctx *c) { return c ? c->launches : 0; }
 
+int wsort_get_ingest_info(const wsort_ctx *c, wsort_ingest_info *out) {
+    if (!c || !out) return WSORT_E_INVALID_ARG;
+    *out = c->ig_info;
+    if (c->ig_info.overflow) out->mode = 0;
+    return WSORT_OK;
+}
+
 }  // extern "C"
 
 // ====================================================================================
@@ -1602,6 +1809,10 @@ int wsort_pack_long(wsort_ctx *c, uint32_t **dense_table, uint64_t *dense_entrie
     if (c->h_ig[kIgVeryLong])
         return set_err(c, WSORT_E_STATE, "wsort_pack_long: words longer than %d letters were not staged", 6 * kMaxStageKw);
     cudaSetDevice(c->device);
+    if (c->hashed) {   // the split exchange reads the staged keys: tokenize again, staging
+        int rc0 = tokenize_impl(c, nullptr, false);
+        if (rc0) return rc0;
+    }
     Summary &s = *c->h_sum;
     std::vector<uint64_t> n(256, 0);
     for (uint32_t L = kDenseMaxLen + 1; L < 256; L++) n[L] = s.off[L + 1] - s.off[L];

@@ -104,6 +104,48 @@ enum { kIgMaxChunks = 0, kIgOverflow = 1, kIgVeryLong = 2, kIgCtrs = 4 };
 __host__ __device__ constexpr uint32_t ingest_cta_chunks(uint64_t range_bytes) {
     return (uint32_t)((range_bytes + 256) / 9000 + 2 * kMaxStageKw + 10);
 }
+// The table of distinct long words (k_hash.cuh): K1 counts every word of 6..66 letters into it.
+struct HashTab {
+    // narrow words (6..24 letters: 1-4 key words): the 128-bit key itself is the slot's tag (exact)
+    unsigned long long *nkey;               // [2 (nmask + 1)] (0, 0) = empty, else the key (k_hash.cuh)
+    uint32_t *ncnt;                         // [nmask + 1] occurrences
+    uint32_t nmask;
+    // wide words (25..66 letters): fingerprint-tagged slots, keys in a side store, verified word by word
+    unsigned long long *fp;                 // [mask + 1] 0 = empty, else fingerprint | 1
+    uint32_t *meta;                         // [mask + 1] key offset | L << 25 (kUnset / kDead)
+    uint32_t *cnt;                          // [mask + 1] occurrences
+    uint32_t *keys;                         // [key_cap] key words of the distinct wide words
+    uint32_t *top;                          // [4] key words used, distinct words, overflow flag
+    uint32_t *dcount;                       // [256] distinct words per length
+    uint32_t mask, key_cap, max_distinct;
+};
+struct HashGatherArgs {
+    HashTab tab;
+    const BucketInfo *buckets;              // distinct-key buckets (key_off, kw)
+    uint32_t *lcursor;                      // [256] zeroed by the host
+    uint32_t *keys_a;
+};
+// words per k_emit_runs tile (its runs are handled in segments that fit shared memory)
+__host__ __device__ constexpr uint32_t run_tile_words(uint32_t L) { return L ? 8192u : 8192u; }
+struct HashRunArgs {
+    HashTab tab;
+    const BucketInfo *buckets;              // output buckets: word_off (global word index), byte_off, n words
+    const BucketInfo *kbuckets;             // distinct-key buckets: key_off into `keys`, n distinct keys
+    const uint32_t *dist_pfx;               // [257] first distinct key of bucket L (tile_from_prefix layout)
+    uint32_t D;                             // distinct keys
+    const uint32_t *keys;                   // the sorted distinct keys (buffer B)
+    uint32_t *run_end;                      // [D] inclusive run ends, long-word index (words of >= 6 letters)
+    uint64_t long_base;                     // global word index of the first long word (off[6])
+    const uint32_t *tile_pfx;               // [257] first emit tile of bucket L
+    uint32_t ntiles;
+    uint32_t *tile_e0, *tile_e1;            // [ntiles] runs of the tile's first / last word
+    uint8_t *words;
+};
+cudaError_t launch_hash_gather(const HashGatherArgs &a, cudaStream_t s);
+cudaError_t launch_hash_runs(const HashRunArgs &a, uint32_t *scan_blk, cudaStream_t s);   // runs, scan, tiles
+uint32_t hash_scan_blocks(uint32_t D);
+cudaError_t launch_emit_runs(const HashRunArgs &a, cudaStream_t s);
+
 struct IngestArgs {
     const uint8_t *text;
     uint64_t n;
@@ -117,6 +159,8 @@ struct IngestArgs {
     uint32_t *ctr;                          // [kIgCtrs] (zeroed by the host)
     uint32_t debug;                         // timing experiments only (WSORT_INGEST_DEBUG): 1 = skip dense
                                             // counting, 2 = skip key packing, 4 = direct L3-5 counts
+    uint32_t hash;                          // 1: count the long words into `tab` instead of staging them
+    HashTab tab;
 };
 size_t ingest_smem(uint32_t cta_chunks);
 uint32_t ingest_ctas_per_sm();   // resident K1 CTAs per SM (the tokenizer grid is one wave of them)
