@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(kHT) k_hash_gather(HashGatherArgs a) {
             const uint32_t m = __ldcg(a.tab.meta + i);
             if (m < hashtab::kDead) info[r] = m;
         }
-        if (info[r] != hashtab::kUnset) rank[r] = atomicAdd(&cnt[narrow ? info[r] : info[r] >> 25], 1u);
+        if (info[r] != hashtab::kUnset) rank[r] = atomicAdd(&cnt[narrow ? info[r] : info[r] >> 24], 1u);
     }
     __syncthreads();
     if (cnt[t]) base[t] = atomicAdd(a.lcursor + t, cnt[t]);
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kHT) k_hash_gather(HashGatherArgs a) {
 #pragma unroll
     for (int r = 0; r < (int)(kGatherSlots / kHT); r++) {
         if (info[r] == hashtab::kUnset) continue;
-        const uint32_t L = narrow ? info[r] : info[r] >> 25, kw = (L + 5u) / 6u;
+        const uint32_t L = narrow ? info[r] : info[r] >> 24, kw = (L + 5u) / 6u;
         uint32_t *dst = a.keys_a + a.buckets[L].key_off + (uint64_t)(base[L] + rank[r]) * kw;
         if (narrow) {
             const uint32_t kk[4] = {(uint32_t)(nk[r].lo >> 32), (uint32_t)nk[r].lo, (uint32_t)(nk[r].hi >> 32), (uint32_t)nk[r].hi};
@@ -61,9 +61,32 @@ __global__ void __launch_bounds__(kHT) k_hash_gather(HashGatherArgs a) {
             for (uint32_t q = 0; q < 4; q++)
                 if (q < kw) dst[q] = kk[q];
         } else {
-            const uint32_t *src = a.tab.keys + (info[r] & 0x1ffffffu);
+            const uint32_t *src = a.tab.keys + (info[r] & 0xffffffu);
             for (uint32_t q = 0; q < kw; q++) dst[q] = __ldcg(src + q);
         }
+    }
+}
+
+// ---------------------------------------------------------------- KH1b: distinct keys of > 48 letters
+// The MSD finish holds keys of <= 8 words (48 letters); longer distinct words are rare (a text's few very
+// long words): one CTA per such bucket ranks its keys (rank = how many keys of the bucket are smaller;
+// distinct keys, so ranks are a permutation) and writes each to buffer B at its rank. The host takes this
+// path only while a bucket's keys fit shared memory (kWideSortWords).
+__global__ void __launch_bounds__(kHT) k_sort_wide(const BucketInfo *kb, const uint32_t *lens, const uint32_t *keys_a,
+                                                   uint32_t *keys_b) {
+    __shared__ uint32_t sk[kWideSortWords];
+    const uint32_t L = lens[blockIdx.x], kw = (L + 5u) / 6u;
+    const BucketInfo b = kb[L];
+    for (uint32_t i = threadIdx.x; i < b.n * kw; i += kHT) sk[i] = keys_a[b.key_off + i];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < b.n; i += kHT) {
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < b.n; j++) {
+            uint32_t q = 0;
+            while (q < kw && sk[j * kw + q] == sk[i * kw + q]) q++;
+            rank += q < kw && sk[j * kw + q] < sk[i * kw + q];
+        }
+        for (uint32_t q = 0; q < kw; q++) keys_b[b.key_off + (uint64_t)rank * kw + q] = sk[i * kw + q];
     }
 }
 
@@ -305,6 +328,13 @@ __global__ void __launch_bounds__(kHT) k_emit_runs(HashRunArgs a) {
 cudaError_t launch_hash_gather(const HashGatherArgs &a, cudaStream_t s) {
     const uint32_t nb = (a.tab.nmask + kGatherSlots) / kGatherSlots, wb = (a.tab.mask + kGatherSlots) / kGatherSlots;
     k_hash_gather<<<nb + wb, kHT, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sort_wide(const BucketInfo *kb, const uint32_t *lens, uint32_t nlens, const uint32_t *keys_a,
+                             uint32_t *keys_b, cudaStream_t s) {
+    if (!nlens) return cudaSuccess;
+    k_sort_wide<<<nlens, kHT, 0, s>>>(kb, lens, keys_a, keys_b);
     return cudaGetLastError();
 }
 

@@ -8,8 +8,8 @@
 //
 // Open addressing, linear probing, lock-free:
 //   fp[i]   u64: 0 = empty, else the key's 64-bit fingerprint | 1 (set once by atomicCAS);
-//   meta[i] u32: kHashUnset until the inserting thread has stored the key words, then
-//           key offset (u32 words into keys[]) | L << 25; kHashDead if the insert hit a capacity limit;
+//   meta[i] u32: kUnset until the inserting thread has stored the key words, then
+//           key offset (u32 words into keys[], < 2^24) | L << 24; kDead if the key store was exhausted;
 //   cnt[i]  u32: occurrences (atomics);
 //   keys[]  the key words of every distinct word (bump-allocated by top[0]).
 // A lookup verifies the key word by word against the stored one (exact; the fingerprint only filters),
@@ -77,7 +77,7 @@ __device__ __forceinline__ uint32_t find(const HashTab &h, uint32_t L, uint32_t 
                 }
                 for (uint32_t q = 0; q < k; q++) h.keys[off + q] = get(q);
                 atomicAdd(h.dcount + L, 1u);
-                st_release(h.meta + i, off | (L << 25));
+                st_release(h.meta + i, off | (L << 24));
                 return i;
             }
         }
@@ -89,14 +89,16 @@ __device__ __forceinline__ uint32_t find(const HashTab &h, uint32_t L, uint32_t 
                 return kUnset;
             }
         }
-        if (m == kDead || (m >> 25) != L) continue;
-        const uint32_t *kk = h.keys + (m & 0x1ffffffu);
-        uint32_t st[kMaxStageKw];   // all the stored words in flight at once, then compared
-#pragma unroll
-        for (uint32_t q = 0; q < kMaxStageKw; q++) st[q] = q < k ? __ldcg(kk + q) : 0u;
+        if (m == kDead || (m >> 24) != L) continue;
+        const uint32_t *kk = h.keys + (m & 0xffffffu);
         bool eq = true;
+        for (uint32_t q0 = 0; q0 < k && eq; q0 += 11u) {   // 11 stored words in flight at once, then compared
+            uint32_t st[11];
 #pragma unroll
-        for (uint32_t q = 0; q < kMaxStageKw; q++) eq &= q >= k || st[q] == get(q);
+            for (uint32_t q = 0; q < 11u; q++) st[q] = q0 + q < k ? __ldcg(kk + q0 + q) : 0u;
+#pragma unroll
+            for (uint32_t q = 0; q < 11u; q++) eq &= q0 + q >= k || st[q] == get(q0 + q);
+        }
         if (eq) return i;
     }
     if (insert) atomicExch(h.top + kTopOverflow, 3u);

@@ -118,18 +118,36 @@ __device__ __forceinline__ uint32_t inclusive_scan_warp(uint32_t v, int lane) {
 __device__ __forceinline__ uint32_t lead_run(uint32_t M) { return M == 0xffffffffu ? 32u : (uint32_t)(__ffs(~M) - 1); }
 
 // ---- hash mode: long words counted into the global table of distinct words (k_hash.cuh)
+// key word of letters [0, n) (n <= 6) of the word at global byte p (words of > 66 letters: not all in the
+// shared-memory window)
+__device__ __forceinline__ uint32_t pack6_global(const uint8_t *p, uint32_t n) {
+    uint32_t key = 0;
+    for (uint32_t j = 0; j < 6u && j < n; j++) key |= (uint32_t)(__ldg(p + j) & 31u) << (25u - 5u * j);
+    return key;
+}
+
 // Words [0, i1) of a warp's long list (from the back), one per lane: histogram, then the word's slot
-// (found or inserted) gets one more occurrence. Words of > 66 letters are not counted (the host takes
-// the K3 path for such texts).
+// (found or inserted) gets one more occurrence. Every length 6..255 is counted (words of > 66 letters,
+// listed as 67, are re-measured and packed from the text in global memory).
 __device__ __forceinline__ void hash_long(const IngestArgs &a, IgSmem &sm, const uint16_t *lst, uint32_t i1,
-                                          const uint32_t *wb32, int lane) {
+                                          const uint32_t *wb32, const uint8_t *gtext, int lane) {
     for (uint32_t b = 0; b < i1; b += 32) {
         const uint32_t i = b + lane;
         if (i >= i1) break;
         const uint32_t x = lst[kWList - 1 - i];
-        const uint32_t s = x & 1023u, L = (x >> 10) + 6u;
-        if (L > 6u * kMaxStageKw) {
-            atomicAdd(&a.ctr[kIgVeryLong], 1u);
+        const uint32_t s = x & 1023u;
+        uint32_t L = (x >> 10) + 6u;
+        if (L > 6u * kMaxStageKw) {   // (listed as 67: >= 67 letters) the exact length from the text
+            L = 6u * kMaxStageKw;
+            while (L <= (uint32_t)kMaxLen && is_letter(__ldg(gtext + s + L))) L++;
+            if (L > (uint32_t)kMaxLen) continue;   // (> 255: flagged as too long by the list loop)
+            atomicAdd(&sm.hist[L], 1u);
+            if (a.debug & 2) continue;
+            const uint32_t k = (L + 5u) / 6u;
+            auto get = [&](uint32_t q) { return pack6_global(gtext + s + 6u * q, L - 6u * q); };
+            const uint64_t fp = hashtab::fingerprint(L, k, get);
+            const uint32_t slot = hashtab::find(a.tab, L, k, fp, get, true);
+            if (slot != hashtab::kUnset) atomicAdd(a.tab.cnt + slot, 1u);
             continue;
         }
         atomicAdd(&sm.hist[L], 1u);
@@ -283,7 +301,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
             cache_add(sm, a.dense, L, dense_index(wb32, s, L));
         }
         if (HASH) {   // L = 6..66: counted into the global table
-            if (!(a.debug & 8)) hash_long(a, sm, wlst, nlg, wb32, lane);
+            if (!(a.debug & 8)) hash_long(a, sm, wlst, nlg, wb32, a.text + base, lane);
             __syncwarp();
             M = Mn;
             continue;

@@ -83,7 +83,7 @@ struct wsort_ctx {
     bool hashed = false;                         // the last tokenize counted the long words into the table
     int ingest_mode = 0;                         // 0 = auto (hash, staging if the table overflows), 1 = staging
     uint64_t hash_grow = 1;                      // table size factor (x4 after an overflow, up to 64)
-    DevBuf t_nkey, t_ncnt, t_fp, t_meta, t_cnt, t_keys, t_top, t_dcount, t_runend, t_scan, t_tilee, t_kplan, t_dpfx, t_rpfx;
+    DevBuf t_wlens, t_nkey, t_ncnt, t_fp, t_meta, t_cnt, t_keys, t_top, t_dcount, t_runend, t_scan, t_tilee, t_kplan, t_dpfx, t_rpfx;
     HashTab tab{};
     uint32_t *h_tab = nullptr;                   // pinned: top[4] + dcount[256]
     wsort_ingest_info ig_info{};                 // what the last tokenize did (wsort_get_ingest_info)
@@ -391,7 +391,7 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->m_jovf, &c->m_partn, &c->m_plist, &c->m_qemit, &c->ghist, &c->dense,
                       &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
                       &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor, &c->d_tile_e,
-                      &c->t_nkey, &c->t_ncnt, &c->t_fp, &c->t_meta, &c->t_cnt, &c->t_keys, &c->t_top, &c->t_dcount, &c->t_runend,
+                      &c->t_wlens, &c->t_nkey, &c->t_ncnt, &c->t_fp, &c->t_meta, &c->t_cnt, &c->t_keys, &c->t_top, &c->t_dcount, &c->t_runend,
                       &c->t_scan, &c->t_tilee, &c->t_kplan, &c->t_dpfx, &c->t_rpfx};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
@@ -523,7 +523,8 @@ int hash_alloc(wsort_ctx *c) {
     uint32_t nslots = 4096, slots = 4096;
     while (nslots < (1u << 24) && ((uint64_t)nslots * 512 < c->n * c->hash_grow || nslots < 4096 * c->hash_grow)) nslots <<= 1;
     while (slots < (1u << 24) && ((uint64_t)slots * 4096 < c->n * c->hash_grow || slots < 4096 * c->hash_grow)) slots <<= 1;
-    const uint32_t maxd = (uint32_t)((uint64_t)slots * 7 / 10), key_cap = maxd * 8 + 1024;
+    const uint32_t maxd = (uint32_t)((uint64_t)slots * 7 / 10);
+    const uint32_t key_cap = std::min<uint32_t>(maxd * 8 + 1024, (1u << 24) - 64);   // (meta: 24-bit offsets)
     int rc;
     if ((rc = ensure(c, c->t_nkey, (size_t)nslots * 16, "hash narrow keys"))) return rc;
     if ((rc = ensure(c, c->t_ncnt, (size_t)nslots * 4, "hash narrow counts"))) return rc;
@@ -1443,7 +1444,14 @@ int sort_dense_msd(wsort_ctx *c) {
     return rc;
 }
 
-// AUTO after a hash-mode tokenize (every word <= 66 letters): dense buckets as in sort_dense_msd; the long
+// The distinct keys of > 48 letters are ranked in shared memory (k_sort_wide): every such bucket must fit.
+bool hash_sortable(const wsort_ctx *c) {
+    for (uint32_t L = kMsdMaxLen + 1; L <= c->h_sum->max_len; L++)
+        if ((uint64_t)c->h_tab[4 + L] * kw_of((int)L) > kWideSortWords) return false;
+    return true;
+}
+
+// AUTO after a hash-mode tokenize (every word <= 255 letters): dense buckets as in sort_dense_msd; the long
 // words from the table of distinct words: gather the D distinct keys into their length buckets, sort them
 // (MSD, radix finish: keys end in buffer B), look up each one's count, scan, and write the runs.
 int sort_dense_hash(wsort_ctx *c) {
@@ -1487,6 +1495,10 @@ int sort_dense_hash(wsort_ctx *c) {
         if ((rc = arena_upload(c, c->t_dpfx, dpfx, sizeof dpfx, "distinct prefix"))) return rc;
         if ((rc = arena_upload(c, c->t_rpfx, rpfx, sizeof rpfx, "run tile prefix"))) return rc;
         const BucketInfo *d_kb = reinterpret_cast<const BucketInfo *>(c->t_kplan.p);
+        std::vector<uint32_t> wide_lens;   // buckets of > 48 letters: k_sort_wide (hash_sortable checked the sizes)
+        for (uint32_t L = kMsdMaxLen + 1; L <= lmax_d; L++)
+            if (kb[L].n) wide_lens.push_back(L);
+        if ((rc = arena_upload(c, c->t_wlens, wide_lens.data(), wide_lens.size() * 4, "wide lengths"))) return rc;
         rc = sort_msd_core(c, kb, kDenseMaxLen + 1, kmax_tw, klevels, kkey_words, D, true,
                            [&](const BucketInfo *db, double kbytes) {
                                CK(cudaMemsetAsync(c->d_lcursor.p, 0, 256 * 4, c->stream), "memset length cursors");
@@ -1497,7 +1509,12 @@ int sort_dense_hash(wsort_ctx *c) {
                                ga.keys_a = static_cast<uint32_t *>(c->keys_a.p);
                                return launch(c, "kh1_hash_gather", kbytes, [&] { return launch_hash_gather(ga, c->stream); });
                            },
-                           d_kb, false, lmax_d);
+                           d_kb, false, std::min<uint32_t>(lmax_d, kMsdMaxLen));
+        if (rc) return rc;
+        rc = launch(c, "kh1b_sort_wide", 0, [&] {
+            return launch_sort_wide(d_kb, static_cast<const uint32_t *>(c->t_wlens.p), (uint32_t)wide_lens.size(),
+                                    static_cast<const uint32_t *>(c->keys_a.p), static_cast<uint32_t *>(c->keys_b.p), c->stream);
+        });
         if (rc) return rc;
         HashRunArgs ra{};
         ra.tab = c->tab;
@@ -1587,14 +1604,16 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
         rc = sort_dist_dense(c);
     } else if (algo == WSORT_ALGO_OETS_MERGE) {
         rc = sort_oets(c, want_src);
-    } else if (algo == WSORT_ALGO_AUTO && ingest_ok && c->hashed && kw_of((int)c->h_sum->max_len) <= (int)kRadixRegMaxKw) {
-        rc = sort_dense_hash(c);   // (the distinct keys' MSD radix finish holds keys of <= 8 words: L <= 48)
+    } else if (algo == WSORT_ALGO_AUTO && ingest_ok && c->hashed && hash_sortable(c)) {
+        rc = sort_dense_hash(c);
     } else if ((algo == WSORT_ALGO_AUTO || algo == WSORT_ALGO_DENSE_MSD) && ingest_ok) {
         if (c->hashed) {   // DENSE_MSD reads the staged keys: tokenize again, staging
             rc = tokenize_impl(c, nullptr, false);
             if (rc) return rc;
         }
-        rc = sort_dense_msd(c);
+        if (!c->h_ig[kIgVeryLong]) rc = sort_dense_msd(c);
+        else if (kw_of((int)c->h_sum->max_len) <= (int)kRadixRegMaxKw) rc = sort_msd(c, false);
+        else rc = sort_radix(c, false);   // (a word of > 66 letters: not staged)
     } else if ((algo == WSORT_ALGO_MSD_RADIX || algo == WSORT_ALGO_MSD_OETS || algo == WSORT_ALGO_AUTO ||
                 algo == WSORT_ALGO_DENSE_MSD) && !want_src &&
                kw_of((int)c->h_sum->max_len) <= (int)kRadixRegMaxKw) {

@@ -110,9 +110,9 @@ struct HashTab {
     unsigned long long *nkey;               // [2 (nmask + 1)] (0, 0) = empty, else the key (k_hash.cuh)
     uint32_t *ncnt;                         // [nmask + 1] occurrences
     uint32_t nmask;
-    // wide words (25..66 letters): fingerprint-tagged slots, keys in a side store, verified word by word
+    // wide words (25..255 letters): fingerprint-tagged slots, keys in a side store, verified word by word
     unsigned long long *fp;                 // [mask + 1] 0 = empty, else fingerprint | 1
-    uint32_t *meta;                         // [mask + 1] key offset | L << 25 (kUnset / kDead)
+    uint32_t *meta;                         // [mask + 1] key offset | L << 24 (kUnset / kDead)
     uint32_t *cnt;                          // [mask + 1] occurrences
     uint32_t *keys;                         // [key_cap] key words of the distinct wide words
     uint32_t *top;                          // [4] key words used, distinct words, overflow flag
@@ -142,6 +142,10 @@ struct HashRunArgs {
     uint8_t *words;
 };
 cudaError_t launch_hash_gather(const HashGatherArgs &a, cudaStream_t s);
+constexpr uint32_t kWideSortWords = 8192;   // k_sort_wide: a bucket's distinct keys (> 48 letters) in shared memory
+constexpr uint32_t kMsdMaxLen = 48;         // the MSD radix finish holds keys of <= 8 words
+cudaError_t launch_sort_wide(const BucketInfo *kb, const uint32_t *lens, uint32_t nlens, const uint32_t *keys_a,
+                             uint32_t *keys_b, cudaStream_t s);
 cudaError_t launch_hash_runs(const HashRunArgs &a, uint32_t *scan_blk, cudaStream_t s);   // runs, scan, tiles
 uint32_t hash_scan_blocks(uint32_t D);
 cudaError_t launch_emit_runs(const HashRunArgs &a, cudaStream_t s);

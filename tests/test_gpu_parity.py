@@ -339,3 +339,34 @@ def test_fetch_async_pipeline(ws):
     finally:
         for c in ctxs:
             c.close()
+
+
+# ---------------------------------------------------------------- no cliff for words of 67..255 letters
+def test_very_long_words_stay_on_the_counting_path(ws):
+    """Config 3 (8 MiB prefix) plus a few words of 67..255 letters: the hash-mode ingest counts them like any
+    long word (no second text pass, no fallback to K3 + LSD), and the output is the oracle's."""
+    base, _ = gen.generate(3, n=8 << 20)
+    extra = b" " + b" ".join([b"Q" * 200, b"abc" * 40, b"z" * 67, b"Q" * 200, b"y" * 255]) + b" "
+    text = np.concatenate([base, np.frombuffer(extra, np.uint8)])
+    ref = oracle.sort(text, oracle.MERGE)
+    ws.load_text(text)
+    ws.tokenize()
+    info = ws.ingest_info()
+    ws.sort("auto")
+    w, off = ws.fetch()
+    assert off == ref.off and w.tobytes() == ref.words
+    assert info["mode"] == 1 and info["overflow"] == 0
+
+
+def test_many_distinct_very_long_words_fall_back(ws):
+    """More distinct words of > 48 letters in one bucket than the wide-key rank sort holds: the library takes
+    the staged / K3 path instead; the output is still the oracle's."""
+    rng = np.random.default_rng(7)
+    words = [bytes(rng.integers(97, 123, 200, dtype=np.uint8)) for _ in range(300)]
+    text = b" ".join(words * 2 + [b"the", b"cat", b"sat", b"on", b"a", b"mat"] * 100)
+    ref = oracle.sort(text, oracle.MERGE)
+    ws.load_text(text)
+    ws.tokenize()
+    ws.sort("auto")
+    w, off = ws.fetch()
+    assert off == ref.off and w.tobytes() == ref.words
