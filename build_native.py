@@ -61,7 +61,7 @@ def build_wsort(force: bool = False, verbose_ptxas: bool = False) -> str:
         return out
     cu = [s for s in srcs if s.endswith(".cu")]
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
-           "-I", os.path.join(ROOT, "include"), "-cudart", "static", "-o", out, *cu]
+           "-I", os.path.join(ROOT, "include"), "-cudart", "static", "-ldl", "-o", out, *cu]
     if verbose_ptxas:
         cmd.insert(1, "-Xptxas=-v")
     _run(cmd)

@@ -52,7 +52,7 @@ extern "C" {
 #define WSORT_E_STATE (-2)             /* call out of order (see the state machine below) */
 #define WSORT_E_NOMEM (-3)             /* device or pinned-host allocation failed */
 #define WSORT_E_CUDA (-4)              /* a CUDA runtime error; message in wsort_last_error */
-#define WSORT_E_NCCL (-5)              /* reserved (the exchange runs in torch.distributed/NCCL) */
+#define WSORT_E_NCCL (-5)              /* an NCCL failure, or (multi-GPU) another rank failed */
 #define WSORT_E_TOO_LARGE (-6)         /* a shard of more than WSORT_MAX_SHARD_BYTES bytes */
 #define WSORT_E_WORD_TOO_LONG (-7)     /* some word has more than WSORT_MAX_WORD_LEN letters (A7) */
 #define WSORT_E_BUFFER_TOO_SMALL (-8)  /* wsort_fetch: a cap is short; sizes are still filled in */
@@ -262,6 +262,55 @@ int wsort_dense_range(wsort_ctx *c, const uint64_t *ghist, uint64_t lo, uint64_t
 /* Make wsort_fetch report the GLOBAL bucket offsets (from the all-reduced histogram ghist[256]) and
  * this rank's word_base / byte_base. */
 int wsort_set_global(wsort_ctx *c, const uint64_t *ghist, uint64_t word_base, uint64_t byte_base);
+
+/* ---- multi-GPU: the context as one rank of P, the library owning the communicator ----
+ * SURVEY.md §8(b), §8(e); the paper's MPI master/slave exchange (§4) replaced by a symmetric
+ * one. Attach once (collective), then per text: wsort_load_text(this rank's shard, global_base = its byte
+ * offset; reading A13: the caller cuts the text where no word straddles a cut) -> wsort_tokenize ->
+ * wsort_sort -> wsort_fetch / wsort_get_slices. While attached, wsort_tokenize and wsort_sort are
+ * COLLECTIVE: every rank calls them, and every rank returns the same status (an error flag is all-reduced
+ * before any exchange: a word of > 255 letters on any rank makes every rank return WSORT_E_WORD_TOO_LONG;
+ * a failure on another rank returns WSORT_E_NCCL). wsort_sort takes WSORT_ALGO_AUTO only, keys only.
+ *   wsort_tokenize: K1 (counting ingest) on the shard; all-reduce of the length histogram, the distinct-word
+ *     counts and the error flags; *n_words = the GLOBAL number of words.
+ *   wsort_sort: the dense tables (words of <= 5 letters) summed over the ranks (all-reduce) and this rank
+ *     emits an equal share of the global dense words; the distinct long words of every rank, with their
+ *     counts, go to the rank owning their (length, word) range (sample splitters, weighted by count;
+ *     records stored straight into the owner's receive window over NVLink, offsets from a device-side scan
+ *     of the all-gathered counts), where equal words add their counts; each rank then sorts and writes its
+ *     range. This rank's output = its dense slice, then its long slice; wsort_fetch returns it with the
+ *     GLOBAL bucket offsets, word_base / byte_base of the first slice; wsort_get_slices gives both places.
+ * The concatenation of all ranks' dense slices in rank order, then their long slices in rank order, is
+ * the one-GPU output (tests/test_gpu_dist.py). */
+#define WSORT_UNIQUE_ID_BYTES 128
+
+/* NCCL unique id for wsort_attach_comm (rank 0 calls it; the caller broadcasts the bytes, e.g. with
+ * torch.distributed). NCCL (libnccl.so.2) is loaded at run time. Errors: NCCL. */
+int wsort_get_unique_id(uint8_t id[WSORT_UNIQUE_ID_BYTES]);
+
+/* Make the context rank `rank` of `nranks` (one process per GPU): ncclCommInitRank on the context's device
+ * (collective; blocks until every rank has called it). Errors: INVALID_ARG, NCCL, NOMEM. */
+int wsort_attach_comm(wsort_ctx *c, int rank, int nranks, const uint8_t id[WSORT_UNIQUE_ID_BYTES]);
+
+/* In-process ranks: a group of nranks contexts driven by nranks threads of one process (any device each;
+ * the tests put every rank on one GPU: the collectives are host barriers + device copies, so no kernel
+ * waits on another rank's). wsort_attach_group is collective over the group's threads. */
+typedef struct wsort_group wsort_group;
+int wsort_group_create(wsort_group **out, int nranks);
+void wsort_group_destroy(wsort_group *g);   /* after every member detached */
+int wsort_attach_group(wsort_ctx *c, wsort_group *g, int rank);
+
+/* Back to a single-GPU context (not collective). */
+int wsort_detach_comm(wsort_ctx *c);
+
+/* This rank's pieces of the global output after a multi-GPU wsort_sort (single GPU: one slice). */
+typedef struct {
+    uint64_t local_byte;   /* where the slice starts in this context's words (wsort_fetch) */
+    uint64_t bytes, words;
+    uint64_t global_byte;  /* its place in the global output */
+    uint64_t global_word;
+} wsort_slice;
+int wsort_get_slices(const wsort_ctx *c, wsort_slice *out, int cap, int *n);
 
 #ifdef __cplusplus
 }

@@ -41,8 +41,10 @@ EXPORTS = [
     "wsort_destroy", "wsort_set_profiling", "wsort_kernel_stats", "wsort_reset_kernel_stats",
     "wsort_launch_count", "wsort_histogram", "wsort_pack", "wsort_sample", "wsort_select_splitters",
     "wsort_partition", "wsort_load_keys", "wsort_set_global", "wsort_fetch_async", "wsort_sync",
-    "wsort_pack_long", "wsort_dense_range", "wsort_get_ingest_info",
+    "wsort_pack_long", "wsort_dense_range", "wsort_get_ingest_info", "wsort_get_unique_id", "wsort_attach_comm",
+    "wsort_group_create", "wsort_group_destroy", "wsort_attach_group", "wsort_detach_comm", "wsort_get_slices",
 ]
+UNIQUE_ID_BYTES = 128
 
 
 class Result(ctypes.Structure):
@@ -72,6 +74,16 @@ class IngestInfo(ctypes.Structure):
         ("wide_slots", ctypes.c_uint64),
         ("grow", ctypes.c_uint32),
         ("reserved", ctypes.c_uint32),
+    ]
+
+
+class Slice(ctypes.Structure):
+    _fields_ = [
+        ("local_byte", ctypes.c_uint64),
+        ("bytes", ctypes.c_uint64),
+        ("words", ctypes.c_uint64),
+        ("global_byte", ctypes.c_uint64),
+        ("global_word", ctypes.c_uint64),
     ]
 
 
@@ -120,6 +132,14 @@ def load():
     L.wsort_launch_count.restype = U64
     L.wsort_histogram.argtypes = [P, P]
     L.wsort_get_ingest_info.argtypes = [P, P]
+    L.wsort_get_unique_id.argtypes = [P]
+    L.wsort_attach_comm.argtypes = [P, I, I, P]
+    L.wsort_group_create.argtypes = [ctypes.POINTER(P), I]
+    L.wsort_group_destroy.argtypes = [P]
+    L.wsort_group_destroy.restype = None
+    L.wsort_attach_group.argtypes = [P, P, I]
+    L.wsort_detach_comm.argtypes = [P]
+    L.wsort_get_slices.argtypes = [P, ctypes.POINTER(Slice), I, ctypes.POINTER(I)]
     L.wsort_pack.argtypes = [P]
     L.wsort_sample.argtypes = [P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, P]
     L.wsort_select_splitters.argtypes = [P, U64, ctypes.c_uint32, ctypes.c_uint32, P]
@@ -129,7 +149,7 @@ def load():
     L.wsort_pack_long.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(U64)]
     L.wsort_dense_range.argtypes = [P, P, U64, U64]
     for name in EXPORTS:
-        if name not in ("wsort_strerror", "wsort_destroy", "wsort_launch_count"):
+        if name not in ("wsort_strerror", "wsort_destroy", "wsort_launch_count", "wsort_group_destroy"):
             getattr(L, name).restype = I
     _lib = L
     return L

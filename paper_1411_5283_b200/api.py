@@ -229,8 +229,56 @@ class WSort:
         self._check(self._lib.wsort_get_ingest_info(self._h, ctypes.byref(info)), "wsort_get_ingest_info")
         return {k: int(getattr(info, k)) for k, _ in L.IngestInfo._fields_}
 
+    # ---- multi-GPU with the library-owned communicator (include/wsort.h) ----
+    def attach_comm(self, rank: int, nranks: int, unique_id: bytes):
+        """Rank `rank` of `nranks` (one process per GPU, NCCL); collective over the ranks."""
+        buf = (ctypes.c_uint8 * L.UNIQUE_ID_BYTES).from_buffer_copy(bytes(unique_id))
+        self._check(self._lib.wsort_attach_comm(self._h, rank, nranks, buf), "wsort_attach_comm")
+
+    def attach_group(self, group: "Group", rank: int):
+        """Rank `rank` of an in-process group (one thread per rank); collective over the group's threads."""
+        self._check(self._lib.wsort_attach_group(self._h, group._h, rank), "wsort_attach_group")
+
+    def detach(self):
+        self._check(self._lib.wsort_detach_comm(self._h), "wsort_detach_comm")
+
+    def slices(self) -> list:
+        """[(local byte, bytes, words, global byte, global word)] of this context's output."""
+        out = (L.Slice * 4)()
+        n = ctypes.c_int(0)
+        self._check(self._lib.wsort_get_slices(self._h, out, 4, ctypes.byref(n)), "wsort_get_slices")
+        return [(int(x.local_byte), int(x.bytes), int(x.words), int(x.global_byte), int(x.global_word))
+                for x in out[: n.value]]
+
     def launch_count(self) -> int:
         return int(self._lib.wsort_launch_count(self._h))
+
+
+def get_unique_id() -> bytes:
+    """NCCL unique id for attach_comm (rank 0; broadcast it to the other ranks)."""
+    lib = L.load()
+    buf = (ctypes.c_uint8 * L.UNIQUE_ID_BYTES)()
+    rc = lib.wsort_get_unique_id(buf)
+    if rc:
+        raise WSortError(rc, "wsort_get_unique_id")
+    return bytes(buf)
+
+
+class Group:
+    """In-process ranks (include/wsort.h wsort_group): one WSort per rank, each driven by its own thread."""
+
+    def __init__(self, nranks: int):
+        self._lib = L.load()
+        h = ctypes.c_void_p()
+        rc = self._lib.wsort_group_create(ctypes.byref(h), nranks)
+        if rc:
+            raise WSortError(rc, "wsort_group_create")
+        self._h, self.nranks = h, nranks
+
+    def close(self):
+        if self._h:
+            self._lib.wsort_group_destroy(self._h)
+            self._h = None
 
 
 def select_splitters(samples: np.ndarray, nparts: int) -> np.ndarray:

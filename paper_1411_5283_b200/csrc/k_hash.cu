@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(kHT) k_hash_gather(HashGatherArgs a) {
     }
 }
 
-// ---------------------------------------------------------------- KH1b: distinct keys of > 48 letters
-// The MSD finish holds keys of <= 8 words (48 letters); longer distinct words are rare (a text's few very
+// ---------------------------------------------------------------- KH1b: distinct keys of > 66 letters
+// The MSD finish holds keys of <= 11 words (66 letters); longer distinct words are rare (a text's few very
 // long words): one CTA per such bucket ranks its keys (rank = how many keys of the bucket are smaller;
 // distinct keys, so ranks are a permutation) and writes each to buffer B at its rank. The host takes this
 // path only while a bucket's keys fit shared memory (kWideSortWords).
@@ -349,6 +349,19 @@ cudaError_t launch_hash_runs(const HashRunArgs &a, uint32_t *scan_blk, cudaStrea
     return cudaGetLastError();
 }
 uint32_t hash_scan_blocks(uint32_t D) { return (D + kScanBlk - 1) / kScanBlk; }
+
+cudaError_t launch_hash_counts(const HashRunArgs &a, cudaStream_t s) {
+    if (a.D) k_hash_runs<<<(a.D + kHT - 1) / kHT, kHT, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_scan_u32(uint32_t *v, uint32_t n, uint32_t *scan_blk, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    const uint32_t nblk = (n + kScanBlk - 1) / kScanBlk;
+    k_scan_reduce<<<nblk, kHT, 0, s>>>(v, n, scan_blk);
+    k_scan_blocks<<<1, 1024, 0, s>>>(scan_blk, nblk);
+    k_scan_apply<<<nblk, kHT, 0, s>>>(v, n, scan_blk);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_emit_runs(const HashRunArgs &a, cudaStream_t s) {
     if (!a.ntiles) return cudaSuccess;

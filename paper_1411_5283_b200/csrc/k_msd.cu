@@ -385,7 +385,10 @@ __global__ void __launch_bounds__(kST) k_msd_warp_sort(MsdArgs a) {
         case 5: warp_oets<5>(a, sg, b); break;
         case 6: warp_oets<6>(a, sg, b); break;
         case 7: warp_oets<7>(a, sg, b); break;
-        default: warp_oets<8>(a, sg, b); break;
+        case 8: warp_oets<8>(a, sg, b); break;
+        case 9: warp_oets<9>(a, sg, b); break;
+        case 10: warp_oets<10>(a, sg, b); break;
+        default: warp_oets<11>(a, sg, b); break;
     }
 }
 
@@ -638,7 +641,10 @@ __global__ void __launch_bounds__(kST) k_msd_cta_sort(MsdArgs a) {
         case 5: cta_sort_job<5>(a, sg, b, sm); break;
         case 6: cta_sort_job<6>(a, sg, b, sm); break;
         case 7: cta_sort_job<7>(a, sg, b, sm); break;
-        default: cta_sort_job<8>(a, sg, b, sm); break;
+        case 8: cta_sort_job<8>(a, sg, b, sm); break;
+        case 9: cta_sort_job<9, 1>(a, sg, b, sm); break;    // (tile_keys 256 for > 8 key words)
+        case 10: cta_sort_job<10, 1>(a, sg, b, sm); break;
+        default: cta_sort_job<11, 1>(a, sg, b, sm); break;
     }
 }
 

@@ -21,6 +21,7 @@
 
 #include "k_hash.cuh"
 #include "wsort.h"
+#include "wsort_comm.cuh"
 #include "wsort_internal.cuh"
 
 using namespace wsort;
@@ -114,6 +115,14 @@ struct wsort_ctx {
     // multi-GPU split of the ingest path (wsort_pack_long / wsort_dense_range): the dense table may be
     // summed over the ranks; this context emits the global dense words [dense_lo, dense_hi)
     bool dist_dense = false, dense_range = false;
+    // multi-GPU with a library-owned communicator (wsort_attach_comm / wsort_attach_group)
+    Comm *comm = nullptr;
+    uint64_t g_hist[257] = {0};        // global length histogram (all ranks), [256] = words > 255 letters
+    uint64_t g_dcount[256] = {0};      // sum over the ranks of the distinct long words per length
+    uint32_t g_lmax = 0;
+    std::vector<wsort_slice> slices;   // this rank's places in the global output (wsort_get_slices)
+    DevBuf x_vec, x_counts, x_prefix, x_samples, x_all, x_order, x_split, x_dest, x_send, x_matrix, x_cursor,
+        x_recvn, x_win, x_peers, x_flag, x_lwords, x_lwords_all;
     uint64_t dense_lo = 0, dense_hi = 0;
     uint64_t dslice_off[kDenseMaxLen + 2] = {0};   // global word index of the slice's first word of length L
     uint64_t dslice_n[kDenseMaxLen + 2] = {0};     // its words of length L
@@ -381,6 +390,7 @@ int wsort_set_stream(wsort_ctx *c, uintptr_t cuda_stream) {
 void wsort_destroy(wsort_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    delete c->comm;
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->text_alloc, &c->cta_hist, &c->cta_base, &c->d_sum, &c->keys_a, &c->keys_b,
                       &c->pay_a, &c->pay_b, &c->words, &c->src_off, &c->dh, &c->status0, &c->status1,
@@ -392,7 +402,10 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
                       &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor, &c->d_tile_e,
                       &c->t_wlens, &c->t_nkey, &c->t_ncnt, &c->t_fp, &c->t_meta, &c->t_cnt, &c->t_keys, &c->t_top, &c->t_dcount, &c->t_runend,
-                      &c->t_scan, &c->t_tilee, &c->t_kplan, &c->t_dpfx, &c->t_rpfx};
+                      &c->t_scan, &c->t_tilee, &c->t_kplan, &c->t_dpfx, &c->t_rpfx, &c->x_vec, &c->x_counts,
+                      &c->x_prefix, &c->x_samples, &c->x_all, &c->x_order, &c->x_split, &c->x_dest, &c->x_send,
+                      &c->x_matrix, &c->x_cursor, &c->x_recvn, &c->x_win, &c->x_peers, &c->x_flag, &c->x_lwords,
+                      &c->x_lwords_all};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_sum) cudaFreeHost(c->h_sum);
@@ -438,6 +451,7 @@ int wsort_load_text(wsort_ctx *c, const void *bytes, uint64_t n, int mem, uint64
     c->word_base = c->byte_base = 0;
     c->dist_dense = c->dense_range = false;
     c->slice_words = c->slice_bytes = 0;
+    c->slices.clear();
     uint64_t nsteps = (n + kTkStep - 1) / kTkStep;
     size_t need = kTextFrontPad + nsteps * kTkStep + kIgStep + kTkHalo + 64;   // ingest reads up to 16 KiB + halo past a range
     int rc = ensure(c, c->text_alloc, need, "text");
@@ -480,12 +494,15 @@ int wsort_load_file(wsort_ctx *c, const char *path) {
 }  // extern "C"
 namespace {
 int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash);
+int tokenize_dist(wsort_ctx *c, uint64_t *n_words);
+int sort_dist(wsort_ctx *c);
 }
 extern "C" {
 int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     if (!c) return WSORT_E_INVALID_ARG;
     if (c->state < ST_LOADED) return set_err(c, WSORT_E_STATE, "wsort_tokenize before wsort_load_text");
     cudaSetDevice(c->device);
+    if (c->comm) return tokenize_dist(c, n_words);
     static const bool env_stage = getenv("WSORT_INGEST_STAGE") != nullptr;   // (experiments)
     int rc = tokenize_impl(c, n_words, c->ingest_mode == 0 && !env_stage);
     while (rc == WSORT_OK && c->hashed && c->h_tab[hashtab::kTopOverflow] && c->hash_grow < 64) {
@@ -519,12 +536,14 @@ namespace {
 // text bytes, times the context's growth factor (x4 after each overflow, kept for later texts), each
 // table at most 70 % filled; key store for 8 words per distinct wide word. c4 (1 GiB): ~1 M distinct
 // words of 6..24 letters in 2 M slots.
-int hash_alloc(wsort_ctx *c) {
+int hash_alloc(wsort_ctx *c, uint64_t narrow_need = 0, uint64_t wide_need = 0) {
     uint32_t nslots = 4096, slots = 4096;
+    while (nslots < (1u << 24) && (uint64_t)nslots * 7 < narrow_need * 10) nslots <<= 1;
+    while (slots < (1u << 24) && (uint64_t)slots * 7 < wide_need * 10) slots <<= 1;
     while (nslots < (1u << 24) && ((uint64_t)nslots * 512 < c->n * c->hash_grow || nslots < 4096 * c->hash_grow)) nslots <<= 1;
     while (slots < (1u << 24) && ((uint64_t)slots * 4096 < c->n * c->hash_grow || slots < 4096 * c->hash_grow)) slots <<= 1;
     const uint32_t maxd = (uint32_t)((uint64_t)slots * 7 / 10);
-    const uint32_t key_cap = std::min<uint32_t>(maxd * 8 + 1024, (1u << 24) - 64);   // (meta: 24-bit offsets)
+    const uint32_t key_cap = std::min<uint32_t>(maxd * 12 + 1024, (1u << 24) - 64);   // (meta: 24-bit offsets)
     int rc;
     if ((rc = ensure(c, c->t_nkey, (size_t)nslots * 16, "hash narrow keys"))) return rc;
     if ((rc = ensure(c, c->t_ncnt, (size_t)nslots * 4, "hash narrow counts"))) return rc;
@@ -1444,7 +1463,7 @@ int sort_dense_msd(wsort_ctx *c) {
     return rc;
 }
 
-// The distinct keys of > 48 letters are ranked in shared memory (k_sort_wide): every such bucket must fit.
+// The distinct keys of > 66 letters are ranked in shared memory (k_sort_wide): every such bucket must fit.
 bool hash_sortable(const wsort_ctx *c) {
     for (uint32_t L = kMsdMaxLen + 1; L <= c->h_sum->max_len; L++)
         if ((uint64_t)c->h_tab[4 + L] * kw_of((int)L) > kWideSortWords) return false;
@@ -1454,20 +1473,16 @@ bool hash_sortable(const wsort_ctx *c) {
 // AUTO after a hash-mode tokenize (every word <= 255 letters): dense buckets as in sort_dense_msd; the long
 // words from the table of distinct words: gather the D distinct keys into their length buckets, sort them
 // (MSD, radix finish: keys end in buffer B), look up each one's count, scan, and write the runs.
-int sort_dense_hash(wsort_ctx *c) {
-    const Summary &s = *c->h_sum;
-    uint32_t max_tw, levels;
-    uint64_t key_words;
-    std::vector<BucketInfo> bk = msd_buckets(s, kDenseMaxLen + 1, max_tw, levels, key_words);
-    const uint64_t n_dense = s.off[kDenseMaxLen + 1];
-    int rc;
-    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
-    if ((rc = arena_upload(c, c->plan, bk.data(), bk.size() * sizeof(BucketInfo), "plan"))) return rc;
-    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
-    if (n_dense && (rc = dense_branch(c, bk, d_bk, (double)s.byte_off[kDenseMaxLen + 1]))) return rc;
-    // the distinct keys' buckets (kb[L].n = distinct words of length L), laid out as msd_buckets does
+void summary_from_counts(Summary &s, const uint64_t *n_per_len);
+
+// The long words (>= 6 letters) of the table of distinct words (c->tab, its distinct counts per length in
+// c->h_tab + 4) into the output buckets bk / d_bk (bk[L].n words at bk[L].byte_off; the run index of
+// bk[L]'s first word is bk[L].word_off - long_base): gather the D distinct keys into their length buckets,
+// sort them (MSD, radix finish, keys end in buffer B; > 66 letters: k_sort_wide), look up each one's count,
+// scan, and write the runs.
+int long_from_table(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketInfo *d_bk, uint64_t long_base) {
     const uint32_t *dcount = c->h_tab + 4;
-    Summary ks = s;
+    Summary ks = *c->h_sum;
     std::vector<uint64_t> nd(256, 0);
     uint32_t dpfx[257], rpfx[257], D = 0, ntiles = 0, lmax_d = 0;
     for (uint32_t L = 0; L < 256; L++) {
@@ -1482,65 +1497,352 @@ int sort_dense_hash(wsort_ctx *c) {
     }
     dpfx[256] = D;
     rpfx[256] = ntiles;
-    if (D) {
-        for (uint32_t L = 0; L < 256; L++) ks.off[L + 1] = ks.off[L] + nd[L];   // (only the sizes are used)
-        uint32_t kmax_tw, klevels;
-        uint64_t kkey_words;
-        std::vector<BucketInfo> kb = msd_buckets(ks, kDenseMaxLen + 1, kmax_tw, klevels, kkey_words);
-        if ((rc = ensure(c, c->t_runend, (size_t)D * 4, "run ends"))) return rc;
-        if ((rc = ensure(c, c->t_scan, (size_t)hash_scan_blocks(D) * 4, "run scan"))) return rc;
-        if ((rc = ensure(c, c->t_tilee, (size_t)2 * (ntiles + 1) * 4, "run tiles"))) return rc;
-        if ((rc = ensure(c, c->d_lcursor, 256 * 4, "length cursors"))) return rc;
-        if ((rc = arena_upload(c, c->t_kplan, kb.data(), kb.size() * sizeof(BucketInfo), "key plan"))) return rc;
-        if ((rc = arena_upload(c, c->t_dpfx, dpfx, sizeof dpfx, "distinct prefix"))) return rc;
-        if ((rc = arena_upload(c, c->t_rpfx, rpfx, sizeof rpfx, "run tile prefix"))) return rc;
-        const BucketInfo *d_kb = reinterpret_cast<const BucketInfo *>(c->t_kplan.p);
-        std::vector<uint32_t> wide_lens;   // buckets of > 48 letters: k_sort_wide (hash_sortable checked the sizes)
-        for (uint32_t L = kMsdMaxLen + 1; L <= lmax_d; L++)
-            if (kb[L].n) wide_lens.push_back(L);
-        if ((rc = arena_upload(c, c->t_wlens, wide_lens.data(), wide_lens.size() * 4, "wide lengths"))) return rc;
-        rc = sort_msd_core(c, kb, kDenseMaxLen + 1, kmax_tw, klevels, kkey_words, D, true,
-                           [&](const BucketInfo *db, double kbytes) {
-                               CK(cudaMemsetAsync(c->d_lcursor.p, 0, 256 * 4, c->stream), "memset length cursors");
-                               HashGatherArgs ga{};
-                               ga.tab = c->tab;
-                               ga.buckets = db;
-                               ga.lcursor = static_cast<uint32_t *>(c->d_lcursor.p);
-                               ga.keys_a = static_cast<uint32_t *>(c->keys_a.p);
-                               return launch(c, "kh1_hash_gather", kbytes, [&] { return launch_hash_gather(ga, c->stream); });
-                           },
-                           d_kb, false, std::min<uint32_t>(lmax_d, kMsdMaxLen));
-        if (rc) return rc;
-        rc = launch(c, "kh1b_sort_wide", 0, [&] {
-            return launch_sort_wide(d_kb, static_cast<const uint32_t *>(c->t_wlens.p), (uint32_t)wide_lens.size(),
-                                    static_cast<const uint32_t *>(c->keys_a.p), static_cast<uint32_t *>(c->keys_b.p), c->stream);
-        });
-        if (rc) return rc;
-        HashRunArgs ra{};
-        ra.tab = c->tab;
-        ra.buckets = d_bk;
-        ra.kbuckets = d_kb;
-        ra.dist_pfx = static_cast<const uint32_t *>(c->t_dpfx.p);
-        ra.D = D;
-        ra.keys = static_cast<const uint32_t *>(c->keys_b.p);
-        ra.run_end = static_cast<uint32_t *>(c->t_runend.p);
-        ra.long_base = s.off[kDenseMaxLen + 1];
-        ra.tile_pfx = static_cast<const uint32_t *>(c->t_rpfx.p);
-        ra.ntiles = ntiles;
-        ra.tile_e0 = static_cast<uint32_t *>(c->t_tilee.p);
-        ra.tile_e1 = ra.tile_e0 + ntiles + 1;
-        ra.words = static_cast<uint8_t *>(c->words.p);
-        rc = launch(c, "kh2_hash_runs", (double)D * 8, [&] { return launch_hash_runs(ra, static_cast<uint32_t *>(c->t_scan.p), c->stream); });
-        if (rc) return rc;
-        rc = launch(c, "kh5_emit_runs", (double)(s.byte_off[256] - s.byte_off[kDenseMaxLen + 1]),
-                    [&] { return launch_emit_runs(ra, c->stream); });
-        if (rc) return rc;
-    }
+    if (!D) return WSORT_OK;
+    int rc;
+    summary_from_counts(ks, nd.data());   // (only the distinct keys' sizes are used)
+    uint32_t kmax_tw, klevels;
+    uint64_t kkey_words;
+    std::vector<BucketInfo> kb = msd_buckets(ks, kDenseMaxLen + 1, kmax_tw, klevels, kkey_words);
+    if ((rc = ensure(c, c->t_runend, (size_t)D * 4, "run ends"))) return rc;
+    if ((rc = ensure(c, c->t_scan, (size_t)hash_scan_blocks(D) * 4, "run scan"))) return rc;
+    if ((rc = ensure(c, c->t_tilee, (size_t)2 * (ntiles + 1) * 4, "run tiles"))) return rc;
+    if ((rc = ensure(c, c->d_lcursor, 256 * 4, "length cursors"))) return rc;
+    if ((rc = arena_upload(c, c->t_kplan, kb.data(), kb.size() * sizeof(BucketInfo), "key plan"))) return rc;
+    if ((rc = arena_upload(c, c->t_dpfx, dpfx, sizeof dpfx, "distinct prefix"))) return rc;
+    if ((rc = arena_upload(c, c->t_rpfx, rpfx, sizeof rpfx, "run tile prefix"))) return rc;
+    const BucketInfo *d_kb = reinterpret_cast<const BucketInfo *>(c->t_kplan.p);
+    std::vector<uint32_t> wide_lens;   // buckets of > 66 letters: k_sort_wide (hash_sortable checked the sizes)
+    for (uint32_t L = kMsdMaxLen + 1; L <= lmax_d; L++)
+        if (kb[L].n) wide_lens.push_back(L);
+    if ((rc = arena_upload(c, c->t_wlens, wide_lens.data(), wide_lens.size() * 4, "wide lengths"))) return rc;
+    rc = sort_msd_core(c, kb, kDenseMaxLen + 1, kmax_tw, klevels, kkey_words, D, true,
+                       [&](const BucketInfo *db, double kbytes) {
+                           CK(cudaMemsetAsync(c->d_lcursor.p, 0, 256 * 4, c->stream), "memset length cursors");
+                           HashGatherArgs ga{};
+                           ga.tab = c->tab;
+                           ga.buckets = db;
+                           ga.lcursor = static_cast<uint32_t *>(c->d_lcursor.p);
+                           ga.keys_a = static_cast<uint32_t *>(c->keys_a.p);
+                           return launch(c, "kh1_hash_gather", kbytes, [&] { return launch_hash_gather(ga, c->stream); });
+                       },
+                       d_kb, false, std::min<uint32_t>(lmax_d, kMsdMaxLen));
+    if (rc) return rc;
+    rc = launch(c, "kh1b_sort_wide", 0, [&] {
+        return launch_sort_wide(d_kb, static_cast<const uint32_t *>(c->t_wlens.p), (uint32_t)wide_lens.size(),
+                                static_cast<const uint32_t *>(c->keys_a.p), static_cast<uint32_t *>(c->keys_b.p), c->stream);
+    });
+    if (rc) return rc;
+    HashRunArgs ra{};
+    ra.tab = c->tab;
+    ra.buckets = d_bk;
+    ra.kbuckets = d_kb;
+    ra.dist_pfx = static_cast<const uint32_t *>(c->t_dpfx.p);
+    ra.D = D;
+    ra.keys = static_cast<const uint32_t *>(c->keys_b.p);
+    ra.run_end = static_cast<uint32_t *>(c->t_runend.p);
+    ra.long_base = long_base;
+    ra.tile_pfx = static_cast<const uint32_t *>(c->t_rpfx.p);
+    ra.ntiles = ntiles;
+    ra.tile_e0 = static_cast<uint32_t *>(c->t_tilee.p);
+    ra.tile_e1 = ra.tile_e0 + ntiles + 1;
+    ra.words = static_cast<uint8_t *>(c->words.p);
+    rc = launch(c, "kh2_hash_runs", (double)D * 8, [&] { return launch_hash_runs(ra, static_cast<uint32_t *>(c->t_scan.p), c->stream); });
+    if (rc) return rc;
+    double out_bytes = 0;
+    for (uint32_t L = kDenseMaxLen + 1; L < 256; L++) out_bytes += (double)bk[L].n * (L + 1);
+    return launch(c, "kh5_emit_runs", out_bytes, [&] { return launch_emit_runs(ra, c->stream); });
+}
+
+// AUTO after a hash-mode tokenize: dense buckets as in sort_dense_msd, the long words from the table.
+int sort_dense_hash(wsort_ctx *c) {
+    const Summary &s = *c->h_sum;
+    uint32_t max_tw, levels;
+    uint64_t key_words;
+    std::vector<BucketInfo> bk = msd_buckets(s, kDenseMaxLen + 1, max_tw, levels, key_words);
+    const uint64_t n_dense = s.off[kDenseMaxLen + 1];
+    int rc;
+    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    if ((rc = arena_upload(c, c->plan, bk.data(), bk.size() * sizeof(BucketInfo), "plan"))) return rc;
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
+    if (n_dense && (rc = dense_branch(c, bk, d_bk, (double)s.byte_off[kDenseMaxLen + 1]))) return rc;
+    rc = long_from_table(c, bk, d_bk, s.off[kDenseMaxLen + 1]);
     if (n_dense) {   // join: the sort is complete when both streams are
         const cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_join, 0);
         if (!rc && e != cudaSuccess) return cuda_err(c, e, "join wait");
     }
     return rc;
+}
+
+// ------------------------------------------------------------------ multi-GPU with an attached communicator
+// The host logic between the collectives; the kernels are in k_xchg.cu. Every rank runs the same sequence
+// of collectives, errors included (a failing rank still takes part in the error all-reduce).
+
+// wsort_tokenize while attached: K1 on the shard (counting ingest), then one all-reduce of
+// [histogram 0..256 | table overflow | error | distinct words per length]; overflow on any rank -> every
+// rank counts again with a bigger table.
+int tokenize_dist(wsort_ctx *c, uint64_t *n_words) {
+    Comm &m = *c->comm;
+    constexpr int kV = 257 + 2 + 256;
+    int rc;
+    if ((rc = ensure(c, c->x_vec, kV * 8, "dist vector"))) return rc;
+    std::vector<uint64_t> v(kV);
+    for (;;) {
+        const int lrc = tokenize_impl(c, nullptr, true);
+        std::fill(v.begin(), v.end(), 0ull);
+        if (lrc == WSORT_OK || lrc == WSORT_E_WORD_TOO_LONG) {
+            const Summary &s = *c->h_sum;
+            for (uint32_t L = 0; L < 256; L++) v[L] = s.off[L + 1] - s.off[L];
+            v[256] = s.too_long;
+            v[257] = c->hashed ? c->h_tab[hashtab::kTopOverflow] != 0 : 1u;
+            for (uint32_t L = 0; L < 256 && c->hashed; L++) v[259 + L] = c->h_tab[4 + L];
+        } else {
+            v[258] = 1;
+        }
+        CK(cudaMemcpyAsync(c->x_vec.p, v.data(), kV * 8, cudaMemcpyHostToDevice, c->stream), "dist vector");
+        if ((rc = m.allreduce_u64(static_cast<uint64_t *>(c->x_vec.p), kV, c->stream)))
+            return set_err(c, rc, "tokenize all-reduce: %s", m.err.c_str());
+        CK(cudaMemcpyAsync(v.data(), c->x_vec.p, kV * 8, cudaMemcpyDeviceToHost, c->stream), "dist vector");
+        CK(cudaStreamSynchronize(c->stream), "dist tokenize");
+        if (v[258]) return lrc ? lrc : set_err(c, WSORT_E_NCCL, "tokenize failed on another rank");
+        if (v[256]) {
+            c->state = ST_LOADED;
+            return set_err(c, WSORT_E_WORD_TOO_LONG, "%llu word(s) longer than %d letters (all ranks)",
+                           (unsigned long long)v[256], kMaxLen);
+        }
+        if (!v[257]) break;
+        if (c->hash_grow >= 64)
+            return set_err(c, WSORT_E_NOMEM, "table of distinct words overflowed on some rank (multi-GPU needs it)");
+        c->hash_grow *= 4;
+    }
+    uint64_t W = 0;
+    c->g_lmax = 0;
+    for (uint32_t L = 0; L < 256; L++) {
+        c->g_hist[L] = v[L];
+        c->g_dcount[L] = v[259 + L];
+        W += v[L];
+        if (v[L]) c->g_lmax = L;
+    }
+    c->g_hist[256] = 0;
+    for (uint32_t L = kMsdMaxLen + 1; L <= c->g_lmax; L++)
+        if (c->g_dcount[L] * kw_of((int)L) > kWideSortWords)
+            return set_err(c, WSORT_E_NOMEM, "multi-GPU: %llu distinct words of %u letters exceed the wide-key sort",
+                           (unsigned long long)c->g_dcount[L], L);
+    if (n_words) *n_words = W;
+    c->state = ST_TOKENIZED;
+    return WSORT_OK;
+}
+
+// wsort_sort while attached (AUTO): see include/wsort.h.
+int sort_dist(wsort_ctx *c) {
+    Comm &m = *c->comm;
+    const uint32_t P = (uint32_t)m.size, me = (uint32_t)m.rank;
+    int rc;
+    auto comm_fail = [&](int code, const char *what) { return set_err(c, code, "%s: %s", what, m.err.c_str()); };
+    // (1) dense: the summed tables; this rank's share of the global dense words
+    if ((rc = m.allreduce_u32(static_cast<uint32_t *>(c->dense.p), dense_entries(), c->stream)))
+        return comm_fail(rc, "dense all-reduce");
+    uint64_t Wd = 0;
+    for (uint32_t L = 1; L <= kDenseMaxLen; L++) Wd += c->g_hist[L];
+    const uint64_t dlo = me * Wd / P, dhi = (me + 1) * Wd / P;
+    uint64_t dslice_off[kDenseMaxLen + 1] = {0}, dslice_n[kDenseMaxLen + 1] = {0}, g = 0, dbytes = 0, gdbytes = 0,
+             dbyte_base = 0;
+    for (uint32_t L = 1; L <= kDenseMaxLen; L++) {
+        const uint64_t a = std::max(g, dlo), b = std::min(g + c->g_hist[L], dhi);
+        dslice_off[L] = a;
+        dslice_n[L] = b > a ? b - a : 0;
+        if (dlo > g) dbyte_base += (std::min(dlo, g + c->g_hist[L]) - g) * (L + 1);
+        g += c->g_hist[L];
+        dbytes += dslice_n[L] * (L + 1);
+        gdbytes += c->g_hist[L] * (L + 1);
+    }
+    // (2) this rank's distinct long words: gathered (keys_a), counted, prefix of the counts
+    const uint32_t *dcount = c->h_tab + 4;
+    Summary ks = *c->h_sum;
+    std::vector<uint64_t> nd(256, 0);
+    uint32_t dpfx[257], D = 0;
+    for (uint32_t L = 0; L < 256; L++) {
+        dpfx[L] = D;
+        if (L > kDenseMaxLen) {
+            nd[L] = dcount[L];
+            D += dcount[L];
+        }
+    }
+    dpfx[256] = D;
+    summary_from_counts(ks, nd.data());
+    uint32_t kmax_tw, klevels;
+    uint64_t kkey_words;
+    std::vector<BucketInfo> kb = msd_buckets(ks, kDenseMaxLen + 1, kmax_tw, klevels, kkey_words);
+    uint64_t gD = 0;
+    for (uint32_t L = 0; L < 256; L++) gD += c->g_dcount[L];
+    const uint32_t kwx = kw_of((int)std::max<uint32_t>(c->g_lmax, 1)), rec = 3 + kwx;
+    const uint32_t ns = std::max<uint32_t>(1, std::min<uint32_t>(1024, 16384 / P)), nall = ns * P;
+    if ((rc = ensure(c, c->keys_a, kkey_words * 4 + 64, "keys_a"))) return rc;
+    if ((rc = ensure(c, c->d_lcursor, 256 * 4, "length cursors"))) return rc;
+    if ((rc = ensure(c, c->x_counts, (size_t)D * 4 + 16, "xchg counts"))) return rc;
+    if ((rc = ensure(c, c->x_prefix, (size_t)D * 4 + 16, "xchg prefix"))) return rc;
+    if ((rc = ensure(c, c->t_scan, (size_t)hash_scan_blocks(D + 1) * 4, "scan"))) return rc;
+    if ((rc = ensure(c, c->x_samples, (size_t)ns * rec * 4, "xchg samples"))) return rc;
+    if ((rc = ensure(c, c->x_all, (size_t)nall * rec * 4, "xchg all samples"))) return rc;
+    if ((rc = ensure(c, c->x_order, (size_t)nall * 4, "xchg order"))) return rc;
+    if ((rc = ensure(c, c->x_split, (size_t)P * rec * 4, "xchg splitters"))) return rc;
+    if ((rc = ensure(c, c->x_dest, (size_t)D + 16, "xchg destinations"))) return rc;
+    if ((rc = ensure(c, c->x_send, kMaxRanks * 4, "xchg send counts"))) return rc;
+    if ((rc = ensure(c, c->x_matrix, (size_t)P * kMaxRanks * 4, "xchg matrix"))) return rc;
+    if ((rc = ensure(c, c->x_cursor, kMaxRanks * 4, "xchg cursors"))) return rc;
+    if ((rc = ensure(c, c->x_recvn, 16, "xchg received"))) return rc;
+    if ((rc = ensure(c, c->x_win, (size_t)(gD + 1) * rec * 4, "xchg window"))) return rc;
+    if ((rc = ensure(c, c->x_peers, kMaxRanks * sizeof(void *), "xchg peers"))) return rc;
+    if ((rc = ensure(c, c->x_flag, 16, "xchg flag"))) return rc;
+    if ((rc = ensure(c, c->x_lwords, 256 * 8, "xchg length words"))) return rc;
+    if ((rc = ensure(c, c->x_lwords_all, (size_t)P * 256 * 8, "xchg all length words"))) return rc;
+    if ((rc = arena_upload(c, c->t_kplan, kb.data(), kb.size() * sizeof(BucketInfo), "key plan"))) return rc;
+    if ((rc = arena_upload(c, c->t_dpfx, dpfx, sizeof dpfx, "distinct prefix"))) return rc;
+    const BucketInfo *d_kb = reinterpret_cast<const BucketInfo *>(c->t_kplan.p);
+    CK(cudaMemsetAsync(c->d_lcursor.p, 0, 256 * 4, c->stream), "memset length cursors");
+    HashGatherArgs ga{};
+    ga.tab = c->tab;
+    ga.buckets = d_kb;
+    ga.lcursor = static_cast<uint32_t *>(c->d_lcursor.p);
+    ga.keys_a = static_cast<uint32_t *>(c->keys_a.p);
+    if ((rc = launch(c, "kh1_hash_gather", (double)kkey_words * 4, [&] { return launch_hash_gather(ga, c->stream); })))
+        return rc;
+    HashRunArgs ra{};
+    ra.tab = c->tab;
+    ra.kbuckets = d_kb;
+    ra.dist_pfx = static_cast<const uint32_t *>(c->t_dpfx.p);
+    ra.D = D;
+    ra.keys = static_cast<const uint32_t *>(c->keys_a.p);
+    ra.run_end = static_cast<uint32_t *>(c->x_counts.p);
+    if ((rc = launch(c, "kx0_counts", (double)D * 4, [&] { return launch_hash_counts(ra, c->stream); }))) return rc;
+    if (D) CK(cudaMemcpyAsync(c->x_prefix.p, c->x_counts.p, (size_t)D * 4, cudaMemcpyDeviceToDevice, c->stream), "prefix");
+    if ((rc = launch(c, "kx0_prefix", (double)D * 8, [&] {
+             return launch_scan_u32(static_cast<uint32_t *>(c->x_prefix.p), D, static_cast<uint32_t *>(c->t_scan.p), c->stream);
+         })))
+        return rc;
+    // (3) samples -> all-gather -> identical splitters on every rank
+    XchgArgs xa{};
+    xa.kbuckets = d_kb;
+    xa.dist_pfx = static_cast<const uint32_t *>(c->t_dpfx.p);
+    xa.keys = static_cast<const uint32_t *>(c->keys_a.p);
+    xa.D = D;
+    xa.counts = static_cast<const uint32_t *>(c->x_counts.p);
+    xa.prefix = static_cast<const uint32_t *>(c->x_prefix.p);
+    xa.rank = me;
+    xa.nparts = P;
+    xa.rec_words = rec;
+    xa.nsamples = ns;
+    xa.nall = nall;
+    xa.samples = static_cast<uint32_t *>(c->x_samples.p);
+    xa.all_samples = static_cast<const uint32_t *>(c->x_all.p);
+    xa.order = static_cast<uint32_t *>(c->x_order.p);
+    xa.splitters = static_cast<uint32_t *>(c->x_split.p);
+    xa.dest = static_cast<uint8_t *>(c->x_dest.p);
+    xa.send_counts = static_cast<uint32_t *>(c->x_send.p);
+    xa.matrix = static_cast<const uint32_t *>(c->x_matrix.p);
+    xa.cursor = static_cast<uint32_t *>(c->x_cursor.p);
+    xa.recv_n = static_cast<uint32_t *>(c->x_recvn.p);
+    xa.win = static_cast<uint32_t *>(c->x_win.p);
+    xa.win_cap = gD + 1;
+    xa.flag = static_cast<uint32_t *>(c->x_flag.p);
+    xa.lwords = static_cast<unsigned long long *>(c->x_lwords.p);
+    if ((rc = launch(c, "kx1_sample", 0, [&] { return launch_xchg_sample(xa, c->stream); }))) return rc;
+    if ((rc = m.allgather(c->x_samples.p, c->x_all.p, (size_t)ns * rec * 4, c->stream))) return comm_fail(rc, "sample all-gather");
+    CK(cudaMemsetAsync(c->x_split.p, 0, (size_t)P * rec * 4, c->stream), "memset splitters");
+    if ((rc = launch(c, "kx2_splitters", 0, [&] { return launch_xchg_split(xa, c->stream); }))) return rc;
+    // (4) destinations and the count matrix; the receive windows of every rank
+    CK(cudaMemsetAsync(c->x_send.p, 0, kMaxRanks * 4, c->stream), "memset send counts");
+    CK(cudaMemsetAsync(c->x_flag.p, 0, 16, c->stream), "memset flag");
+    if ((rc = launch(c, "kx4_count", 0, [&] { return launch_xchg_count(xa, c->stream); }))) return rc;
+    if ((rc = m.allgather(c->x_send.p, c->x_matrix.p, (size_t)P * 4, c->stream))) return comm_fail(rc, "count all-gather");
+    std::vector<void *> peers;
+    if ((rc = m.peer_windows(c->x_win.p, c->x_win.cap, peers, c->stream))) return comm_fail(rc, "peer windows");
+    CK(cudaMemcpyAsync(c->x_peers.p, peers.data(), P * sizeof(void *), cudaMemcpyHostToDevice, c->stream), "peers");
+    CK(cudaStreamSynchronize(c->stream), "peers");   // (the host vector is local)
+    xa.peer_win = static_cast<uint32_t *const *>(c->x_peers.p);
+    // (5) every record stored into its owner's window (P2P), then a barrier
+    if ((rc = launch(c, "kx5_write", (double)D * rec * 4, [&] { return launch_xchg_write(xa, c->stream); }))) return rc;
+    if ((rc = m.barrier(c->stream))) return comm_fail(rc, "exchange barrier");
+    // (6) the received records counted into this rank's table (cleared, sized for every rank's words)
+    uint64_t need_n = 0, need_w = 0;
+    for (uint32_t L = kDenseMaxLen + 1; L < 256; L++) (L <= 24 ? need_n : need_w) += c->g_dcount[L];
+    if ((rc = hash_alloc(c, need_n, need_w))) return rc;
+    xa.tab = c->tab;
+    CK(cudaMemsetAsync(c->x_lwords.p, 0, 256 * 8, c->stream), "memset length words");
+    if ((rc = launch(c, "kx6_absorb", 0, [&] { return launch_xchg_absorb(xa, (uint32_t)c->sms * 4, c->stream); })))
+        return rc;
+    if ((rc = m.allgather(c->x_lwords.p, c->x_lwords_all.p, 256 * 8, c->stream))) return comm_fail(rc, "length all-gather");
+    std::vector<uint64_t> lw((size_t)P * 256);
+    uint32_t xflag = 0;
+    CK(copy_small(c->h_tab, c->t_top.p, 16, c->stream), "copy hash top");
+    CK(copy_small(c->h_tab + 4, c->t_dcount.p, 256 * 4, c->stream), "copy hash distinct counts");
+    CK(cudaMemcpyAsync(lw.data(), c->x_lwords_all.p, lw.size() * 8, cudaMemcpyDeviceToHost, c->stream), "length words");
+    CK(cudaMemcpyAsync(&xflag, c->x_flag.p, 4, cudaMemcpyDeviceToHost, c->stream), "flag");
+    CK(cudaStreamSynchronize(c->stream), "dist sort");
+    if (xflag || c->h_tab[hashtab::kTopOverflow])   // (never expected: the windows and table hold every word)
+        return set_err(c, WSORT_E_NOMEM, "multi-GPU exchange overflow (window %u, table %u)", xflag, c->h_tab[hashtab::kTopOverflow]);
+    // (7) this rank's output: its dense slice, then its long slice (its (length, word) range)
+    std::vector<uint64_t> nl(256, 0);
+    uint64_t lbytes_before = 0, lwords_before = 0;
+    for (uint32_t r = 0; r < P; r++)
+        for (uint32_t L = kDenseMaxLen + 1; L < 256; L++) {
+            const uint64_t x = lw[(size_t)r * 256 + L];
+            if (r == me) nl[L] = x;
+            if (r < me) {
+                lbytes_before += x * (L + 1);
+                lwords_before += x;
+            }
+        }
+    std::vector<BucketInfo> bk(256, BucketInfo{});
+    uint64_t lo = 0, bo = dbytes;
+    for (uint32_t L = 1; L < 256; L++) {
+        BucketInfo &b = bk[L];
+        b.kw = kw_of((int)L);
+        if (L <= kDenseMaxLen) {
+            b.word_off = dslice_off[L];
+            b.n = (uint32_t)dslice_n[L];
+        } else {
+            b.word_off = lo;
+            b.n = (uint32_t)nl[L];
+            lo += nl[L];
+        }
+        b.byte_off = L <= kDenseMaxLen ? 0 : bo;
+        if (L > kDenseMaxLen) bo += nl[L] * (L + 1);
+    }
+    uint64_t db = 0;   // dense byte offsets inside the dense slice
+    for (uint32_t L = 1; L <= kDenseMaxLen; L++) {
+        bk[L].byte_off = db;
+        db += dslice_n[L] * (L + 1);
+    }
+    if ((rc = ensure(c, c->words, bo + 64, "words"))) return rc;
+    if ((rc = arena_upload(c, c->plan, bk.data(), bk.size() * sizeof(BucketInfo), "plan"))) return rc;
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
+    const bool dense = dhi > dlo;
+    if (dense && (rc = dense_branch(c, bk, d_bk, (double)dbytes))) return rc;
+    summary_from_counts(*c->h_sum, nl.data());   // (long_from_table and wsort_fetch: this rank's long slice)
+    rc = long_from_table(c, bk, d_bk, 0);
+    if (dense) {
+        const cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+        if (!rc && e != cudaSuccess) return cuda_err(c, e, "join wait");
+    }
+    if (rc) return rc;
+    // wsort_fetch: this rank's words = dense slice + long slice; the global bucket offsets
+    c->slice_words = dhi - dlo;
+    c->slice_bytes = dbytes;
+    c->has_global = true;
+    uint64_t o = 0;
+    c->gmax = c->g_lmax;
+    for (int L = 0; L < 256; L++) {
+        c->goff[L] = o;
+        o += L ? c->g_hist[L] : 0;
+    }
+    c->goff[256] = o;
+    c->goff[c->gmax + 1] = o;
+    c->word_base = dlo;
+    c->byte_base = dbyte_base;
+    c->slices.clear();
+    c->slices.push_back(wsort_slice{0, dbytes, dhi - dlo, dbyte_base, dlo});
+    c->slices.push_back(wsort_slice{dbytes, bo - dbytes, lo, gdbytes + lbytes_before, Wd + lwords_before});
+    return WSORT_OK;
 }
 
 // Split multi-GPU sort (after wsort_pack_long, the all-reduce of the dense tables, wsort_load_keys and
@@ -1597,6 +1899,20 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     const bool want_src = (flags & WSORT_FLAG_SRC_OFF) != 0;
     int rc = arena_begin(c);
     if (rc) return rc;
+    if (c->comm) {   // collective (include/wsort.h: multi-GPU)
+        if (algo != WSORT_ALGO_AUTO || want_src)
+            return set_err(c, WSORT_E_INVALID_ARG, "multi-GPU wsort_sort: AUTO, keys only");
+        rc = sort_dist(c);
+        if (!rc) rc = arena_end(c);
+        if (rc) {
+            c->state = ST_TOKENIZED;
+            return rc;
+        }
+        c->sorted_with_src = false;
+        c->last_algo = algo;
+        c->state = ST_SORTED;
+        return WSORT_OK;
+    }
     // the dense + MSD path reads what K1 ingest left (dense counts, staged keys): a text this context
     // tokenized, keys only, every word staged (<= 66 letters)
     const bool ingest_ok = !want_src && !c->packed_pending && !c->keys_external && c->h_ig[kIgVeryLong] == 0;
@@ -1729,6 +2045,67 @@ int wsort_reset_kernel_stats(wsort_ctx *c) {
 }
 
 uint64_t wsort_launch_count(const wsort_ctx *c) { return c ? c->launches : 0; }
+
+int wsort_get_unique_id(uint8_t id[WSORT_UNIQUE_ID_BYTES]) {
+    if (!id) return WSORT_E_INVALID_ARG;
+    std::string err;
+    return nccl_unique_id(id, err);
+}
+
+int wsort_attach_comm(wsort_ctx *c, int rank, int nranks, const uint8_t id[WSORT_UNIQUE_ID_BYTES]) {
+    if (!c || !id || nranks < 1 || nranks > (int)kMaxRanks || rank < 0 || rank >= nranks)
+        return c ? set_err(c, WSORT_E_INVALID_ARG, "bad rank %d / nranks %d", rank, nranks) : WSORT_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    delete c->comm;
+    c->comm = nullptr;
+    std::string err;
+    const int rc = comm_create_nccl(&c->comm, id, rank, nranks, c->device, c->stream, err);
+    if (rc) return set_err(c, rc, "wsort_attach_comm: %s", err.c_str());
+    c->state = ST_CREATED;
+    return WSORT_OK;
+}
+
+int wsort_group_create(wsort_group **out, int nranks) {
+    if (!out || nranks < 1 || nranks > (int)kMaxRanks) return WSORT_E_INVALID_ARG;
+    *out = reinterpret_cast<wsort_group *>(group_create(nranks));
+    return WSORT_OK;
+}
+void wsort_group_destroy(wsort_group *g) { group_destroy(reinterpret_cast<Group *>(g)); }
+
+int wsort_attach_group(wsort_ctx *c, wsort_group *g, int rank) {
+    if (!c || !g || rank < 0 || rank >= group_size(reinterpret_cast<Group *>(g))) return WSORT_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    delete c->comm;
+    c->comm = nullptr;
+    const int rc = comm_create_group(&c->comm, reinterpret_cast<Group *>(g), rank, c->device);
+    if (rc) return set_err(c, rc, "wsort_attach_group failed");
+    c->state = ST_CREATED;
+    return WSORT_OK;
+}
+
+int wsort_detach_comm(wsort_ctx *c) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    delete c->comm;
+    c->comm = nullptr;
+    c->has_global = false;
+    c->slice_words = c->slice_bytes = 0;
+    c->word_base = c->byte_base = 0;
+    c->state = ST_CREATED;
+    return WSORT_OK;
+}
+
+int wsort_get_slices(const wsort_ctx *c, wsort_slice *out, int cap, int *n) {
+    if (!c || !n || (cap > 0 && !out)) return WSORT_E_INVALID_ARG;
+    if (c->state != ST_SORTED) return WSORT_E_STATE;
+    std::vector<wsort_slice> sl = c->slices;
+    if (!c->comm) sl.assign(1, wsort_slice{0, c->h_sum->byte_off[256] + c->slice_bytes, c->h_sum->n_words + c->slice_words,
+                                           c->byte_base, c->word_base});
+    *n = (int)sl.size();
+    for (int i = 0; i < cap && i < (int)sl.size(); i++) out[i] = sl[i];
+    return WSORT_OK;
+}
 
 int wsort_get_ingest_info(const wsort_ctx *c, wsort_ingest_info *out) {
     if (!c || !out) return WSORT_E_INVALID_ARG;

@@ -142,13 +142,46 @@ struct HashRunArgs {
     uint8_t *words;
 };
 cudaError_t launch_hash_gather(const HashGatherArgs &a, cudaStream_t s);
-constexpr uint32_t kWideSortWords = 8192;   // k_sort_wide: a bucket's distinct keys (> 48 letters) in shared memory
-constexpr uint32_t kMsdMaxLen = 48;         // the MSD radix finish holds keys of <= 8 words
+constexpr uint32_t kWideSortWords = 8192;   // k_sort_wide: a bucket's distinct keys (> 66 letters) in shared memory
+constexpr uint32_t kMsdMaxLen = 66;         // the MSD radix finish holds keys of <= 11 words
 cudaError_t launch_sort_wide(const BucketInfo *kb, const uint32_t *lens, uint32_t nlens, const uint32_t *keys_a,
                              uint32_t *keys_b, cudaStream_t s);
 cudaError_t launch_hash_runs(const HashRunArgs &a, uint32_t *scan_blk, cudaStream_t s);   // runs, scan, tiles
 uint32_t hash_scan_blocks(uint32_t D);
 cudaError_t launch_emit_runs(const HashRunArgs &a, cudaStream_t s);
+cudaError_t launch_hash_counts(const HashRunArgs &a, cudaStream_t s);   // run_end[j] = count of key j (no scan)
+cudaError_t launch_scan_u32(uint32_t *v, uint32_t n, uint32_t *scan_blk, cudaStream_t s);   // inclusive, in place
+
+// ---------------- multi-GPU exchange of (distinct word, count) records (k_xchg.cu) ----------------
+struct XchgArgs {
+    HashTab tab;                            // (absorb) this rank's table, cleared
+    const BucketInfo *kbuckets;             // the gathered distinct keys' buckets (keys_a layout)
+    const uint32_t *dist_pfx;               // [257] first distinct key of bucket L
+    const uint32_t *keys;                   // the gathered distinct keys
+    uint32_t D;                             // distinct keys of this rank
+    const uint32_t *counts;                 // [D] occurrences of each
+    const uint32_t *prefix;                 // [D] inclusive prefix of the counts
+    uint32_t rank, nparts, rec_words, nsamples, nall;
+    uint32_t *samples;                      // [nsamples][rec_words] this rank's sample records
+    const uint32_t *all_samples;            // [nall][rec_words] every rank's (all-gathered)
+    uint32_t *order;                        // [nall] samples in (length, word, index) order
+    uint32_t *splitters;                    // [nparts - 1][rec_words - 2]: L, key words
+    uint8_t *dest;                          // [D] destination rank of each distinct key
+    uint32_t *send_counts;                  // [nparts] records to each rank (zeroed)
+    const uint32_t *matrix;                 // [nparts][nparts] every rank's send_counts (all-gathered)
+    uint32_t *cursor;                       // [nparts]
+    uint32_t *recv_n;                       // [1] records this rank receives
+    uint32_t *const *peer_win;              // [nparts] every rank's receive window (device pointers)
+    uint32_t *win;                          // this rank's receive window
+    uint64_t win_cap;                       // records a window holds
+    uint32_t *flag;                         // set on a window overflow (never expected)
+    unsigned long long *lwords;             // [256] received words per length (zeroed)
+};
+cudaError_t launch_xchg_sample(const XchgArgs &a, cudaStream_t s);
+cudaError_t launch_xchg_split(const XchgArgs &a, cudaStream_t s);
+cudaError_t launch_xchg_count(const XchgArgs &a, cudaStream_t s);
+cudaError_t launch_xchg_write(const XchgArgs &a, cudaStream_t s);
+cudaError_t launch_xchg_absorb(const XchgArgs &a, uint32_t grid, cudaStream_t s);
 
 struct IngestArgs {
     const uint8_t *text;

@@ -292,3 +292,51 @@ def sort_emulated(make_ws, text: np.ndarray, nparts: int, algo: str = "auto", ns
         sizes.append(s.stage_sort(recv, recv_counts, algo))
     all_sizes = np.stack(sizes).astype(np.uint64)
     return [(s.ws, s.stage_finish(all_sizes)) for s in sorters], cuts
+
+
+# ---------------------------------------------------------------------------------------- C-owned comm
+def sort_group(text: np.ndarray, nparts: int, device: int = 0, make_ws=None):
+    """P ranks as threads of this process (include/wsort.h wsort_group): each rank's context attaches to one
+    in-process group, loads its byte-range shard (reading A13) and runs the collective wsort_tokenize /
+    wsort_sort; the exchange (splitters, count matrix, records stored into the owners' windows, dense
+    all-reduce) happens inside libwsort. Returns ([(words bytes, slices, global offsets, status)], cuts)."""
+    import threading
+
+    from .api import Group, WSort, WSortError
+
+    cuts = shard_cuts(text, nparts)
+    group = Group(nparts)
+    ctxs = [make_ws() if make_ws else WSort(device) for _ in range(nparts)]
+    out = [None] * nparts
+
+    def run(r):
+        ws = ctxs[r]
+        try:
+            ws.attach_group(group, r)
+            ws.load_text(np.ascontiguousarray(text[cuts[r]: cuts[r + 1]]), cuts[r])
+            ws.tokenize()
+            ws.sort("auto")
+            words, off = ws.fetch()
+            out[r] = (words.tobytes(), ws.slices(), off, 0)
+        except WSortError as e:
+            out[r] = (None, None, None, e.status)
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(nparts)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for ws in ctxs:
+        ws.close()
+    group.close()
+    return out, cuts
+
+
+def assemble_slices(outs) -> bytes:
+    """The global output from every rank's (words, slices) (tests / tools)."""
+    pieces = []
+    for words, slices, _, _ in outs:
+        for lo, nb, _, gb, _ in slices:
+            pieces.append((gb, words[lo: lo + nb]))
+    pieces.sort(key=lambda p: p[0])
+    return b"".join(p for _, p in pieces)
