@@ -392,14 +392,18 @@ def e2e_pipelined(args, ws, host, stream, dev, n_words, words_len, sizes):
 
 
 def run_wsort_dist(args, rank, world, local_rank):
-    """N > 1: the config text sharded by byte range over the ranks (strong scaling: the total text is
-    fixed), one sample-sort exchange per step over NCCL (paper_1411_5283_b200/dist.py)."""
+    """N > 1: the config text sharded by byte range over the ranks (strong scaling: the total text is fixed).
+    libwsort owns the NCCL communicator (wsort_attach_comm; the unique id is broadcast with torch.distributed):
+    wsort_tokenize / wsort_sort are collective, the exchange (dense all-reduce, count-weighted splitters,
+    (word, count) records stored into the owners' windows over NVLink) runs inside the library."""
     import numpy as np
     import torch
+    import torch.distributed as dist
 
     import gen
     from paper_1411_5283_b200 import WSort
-    from paper_1411_5283_b200.dist import TorchComm, shard_cuts, sort_distributed
+    from paper_1411_5283_b200.api import get_unique_id
+    from paper_1411_5283_b200.dist import shard_cuts
 
     dev = local_rank
     stream = torch.cuda.current_stream(dev)
@@ -411,70 +415,80 @@ def run_wsort_dist(args, rank, world, local_rank):
     host.numpy()[:] = text[a:b]
     shard = host.to(f"cuda:{dev}")
     del text
-    comm = TorchComm(f"cuda:{dev}")
+    obj = [get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
     ws = WSort(dev, stream=stream.cuda_stream)
-    res = sort_distributed(ws, shard, a, comm, args.algo)
+    ws.attach_comm(rank, world, obj[0])
+    ws.load_text(shard, a)
+    n_words = ws.tokenize()
+    ws.sort(args.algo)
     for _ in range(args.warmup):
-        res = sort_distributed(ws, shard, a, comm, args.algo)
+        ws.tokenize()
+        ws.sort(args.algo)
     torch.cuda.synchronize(dev)
-    comm.barrier()
+    dist.barrier()
     ws.reset_kernel_stats()
     ws.set_profiling(True)
     l0 = ws.launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(dev) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            res = sort_distributed(ws, shard, a, comm, args.algo)
-        e1.record(stream)
+        evs[0].record(stream)
+        for i in range(args.steps):
+            ws.tokenize()
+            ws.sort(args.algo)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1) / args.steps
+    trial_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    ms = sum(trial_ms) / args.steps
     launches = ws.launch_count() - l0
     stats = ws.kernel_stats()
     ws.set_profiling(False)
-    t = torch.tensor([ms], device=comm.wire)
-    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    t = torch.tensor([ms], device=f"cuda:{dev}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    tot = torch.tensor([res.n_words, res.words_len], dtype=torch.int64, device=comm.wire)
-    torch.distributed.all_reduce(tot)
-    W, out_bytes = int(tot[0]), int(tot[1])
+    sizes = ws.sizes()
+    tot = torch.tensor([int(sizes.words_len)], dtype=torch.int64, device=f"cuda:{dev}")
+    dist.all_reduce(tot)
+    out_bytes = int(tot[0])
     peak, peak_src = measured_peaks()
-    dom = max(stats.items(), key=lambda kv: kv[1]["ms"])
-    dname, d = dom
+    dname, d = max(stats.items(), key=lambda kv: kv[1]["ms"])
     achieved = d["bytes"] / d["launches"] / (d["ms"] / d["launches"] / 1000) / 1e9
     line = {
-        "metric": METRIC, "value": W / (ms / 1000), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": n_words / (ms / 1000), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": cfg.name, "n_bytes": cfg.n, "seed": cfg.seed, "words": W, "output_bytes": out_bytes,
-                   "algo": args.algo, "parallelism": f"byte-range shards x{world}, sample sort + NCCL all-to-all",
+        "config": {"workload": cfg.name, "n_bytes": cfg.n, "seed": cfg.seed, "words": n_words, "output_bytes": out_bytes,
+                   "algo": args.algo, "parallelism": f"byte-range shards x{world}; library-owned NCCL communicator: "
+                   "dense all-reduce + (word, count) records into the owners' windows",
                    "l2": "inputs larger than L2; no extra flush"},
         "input_gbs": cfg.n / (ms / 1000) / 1e9,
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(dname), "peak_source": peak_src,
-                     "rank": 0},
+                     "frac": achieved / peak, "traffic": ncu_traffic(dname), "peak_source": peak_src, "rank": rank},
         "kernels": {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
                     for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])},
+        "trials": trials_summary(trial_ms),
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     if not args.no_e2e:
-        out = torch.empty(max(res.words_len, 1) + 64, dtype=torch.uint8, pin_memory=True).numpy()
-        comm.barrier()
+        out = torch.empty(int(sizes.words_len) + 64, dtype=torch.uint8, pin_memory=True).numpy()
+        dist.barrier()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.e2e_steps):
-            r = sort_distributed(ws, host, a, comm, args.algo)
+            ws.load_text(host, a)
+            ws.tokenize()
+            ws.sort(args.algo)
             ws.fetch(out=out)
         f1.record(stream)
         torch.cuda.synchronize(dev)
-        ems = torch.tensor([f0.elapsed_time(f1) / args.e2e_steps], device=comm.wire)
-        torch.distributed.all_reduce(ems, op=torch.distributed.ReduceOp.MAX)
-        line["e2e"] = {"value": W / (float(ems.item()) / 1000), "unit": UNIT, "h2d_bytes_per_step": cfg.n,
+        ems = torch.tensor([f0.elapsed_time(f1) / args.e2e_steps], device=f"cuda:{dev}")
+        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        line["e2e"] = {"value": n_words / (float(ems.item()) / 1000), "unit": UNIT, "h2d_bytes_per_step": cfg.n,
                        "d2h_bytes_per_step": out_bytes, "ms_per_step": float(ems.item()),
-                       "path": "per rank: pinned host shard -> sort_distributed -> wsort_fetch(pinned host)"}
+                       "path": "per rank: pinned host shard -> wsort_load_text -> collective tokenize + sort -> "
+                               "wsort_fetch(pinned host)"}
     ws.close()
     if rank == 0:
         print(json.dumps(line), flush=True)

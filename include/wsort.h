@@ -181,6 +181,18 @@ int wsort_set_profiling(wsort_ctx *c, int on);
 /* Synchronises; fills up to cap entries and *n with the number of kernel classes seen. */
 int wsort_kernel_stats(wsort_ctx *c, wsort_kernel_stat *out, int cap, int *n);
 int wsort_reset_kernel_stats(wsort_ctx *c);
+/* How wsort_tokenize (K1) treats the words of >= 6 letters (PAPER.md:58 phases 2-3 start there):
+ *   STAGE  their fixed-width keys are staged in chunks (the paper's "array char 3D") and AUTO
+ *          sorts them by MSD radix with an exact multiset finish (k_msd.cu); words of > 66 letters are not
+ *          staged (the sort then packs every word from the text again, K3, and uses LSD radix);
+ *   COUNT  every distinct word is counted into a table (k_hash.cuh) and AUTO sorts only the distinct words,
+ *          writing each as often as it occurred (k_hash.cu); any length up to 255;
+ *   AUTO   (default) STAGE, or COUNT for a text with a word of > 66 letters.
+ * Multi-GPU (attached) always counts: the exchange sends (word, count) records. The output never depends
+ * on the mode. */
+enum wsort_ingest { WSORT_INGEST_AUTO = 0, WSORT_INGEST_STAGE = 1, WSORT_INGEST_COUNT = 2 };
+int wsort_set_ingest(wsort_ctx *c, int mode);
+
 /* How the last wsort_tokenize counted the words of >= 6 letters (diagnostics): */
 typedef struct {
     int32_t mode;              /* 1: counted into the table of distinct words (k_hash.cuh); 0: staged as keys */

@@ -223,6 +223,10 @@ class WSort:
     def reset_kernel_stats(self):
         self._check(self._lib.wsort_reset_kernel_stats(self._h), "wsort_reset_kernel_stats")
 
+    def set_ingest(self, mode: str):
+        """"auto" (default), "stage" or "count" (include/wsort.h wsort_set_ingest)."""
+        self._check(self._lib.wsort_set_ingest(self._h, L.INGEST[mode]), "wsort_set_ingest")
+
     def ingest_info(self) -> dict:
         """How the last tokenize counted the words of >= 6 letters (wsort_get_ingest_info)."""
         info = L.IngestInfo()

@@ -82,7 +82,7 @@ struct wsort_ctx {
     DevBuf d_blk_sum, d_blk_nnz, d_ent_idx, d_ent_end, d_n_ent, d_tiles2, d_lcursor, d_tile_e;
     // K1 hash mode: the table of distinct long words (k_hash.cuh) and the run emission after the sort
     bool hashed = false;                         // the last tokenize counted the long words into the table
-    int ingest_mode = 0;                         // 0 = auto (hash, staging if the table overflows), 1 = staging
+    int ingest_mode = WSORT_INGEST_AUTO;         // wsort_set_ingest
     uint64_t hash_grow = 1;                      // table size factor (x4 after an overflow, up to 64)
     DevBuf t_wlens, t_nkey, t_ncnt, t_fp, t_meta, t_cnt, t_keys, t_top, t_dcount, t_runend, t_scan, t_tilee, t_kplan, t_dpfx, t_rpfx;
     HashTab tab{};
@@ -503,8 +503,13 @@ int wsort_tokenize(wsort_ctx *c, uint64_t *n_words) {
     if (c->state < ST_LOADED) return set_err(c, WSORT_E_STATE, "wsort_tokenize before wsort_load_text");
     cudaSetDevice(c->device);
     if (c->comm) return tokenize_dist(c, n_words);
-    static const bool env_stage = getenv("WSORT_INGEST_STAGE") != nullptr;   // (experiments)
-    int rc = tokenize_impl(c, n_words, c->ingest_mode == 0 && !env_stage);
+    // WSORT_INGEST_AUTO: stage the long words' keys (the MSD path); a text with a word of > 66 letters (not
+    // staged) is counted into the table of distinct words instead (no fallback to K3 + LSD). COUNT: always
+    // the table (it grows x4 per overflow; still overflowing -> staged). STAGE: always staged.
+    const bool count_first = c->ingest_mode == WSORT_INGEST_COUNT;
+    int rc = tokenize_impl(c, n_words, count_first);
+    if (rc == WSORT_OK && !c->hashed && c->ingest_mode == WSORT_INGEST_AUTO && c->h_ig[kIgVeryLong])
+        rc = tokenize_impl(c, n_words, true);
     while (rc == WSORT_OK && c->hashed && c->h_tab[hashtab::kTopOverflow] && c->hash_grow < 64) {
         // more distinct long words than the table holds: count again with 4x the slots (kept for later texts)
         c->hash_grow *= 4;
@@ -2104,6 +2109,14 @@ int wsort_get_slices(const wsort_ctx *c, wsort_slice *out, int cap, int *n) {
                                            c->byte_base, c->word_base});
     *n = (int)sl.size();
     for (int i = 0; i < cap && i < (int)sl.size(); i++) out[i] = sl[i];
+    return WSORT_OK;
+}
+
+int wsort_set_ingest(wsort_ctx *c, int mode) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    if (mode != WSORT_INGEST_AUTO && mode != WSORT_INGEST_STAGE && mode != WSORT_INGEST_COUNT)
+        return set_err(c, WSORT_E_INVALID_ARG, "bad ingest mode %d", mode);
+    c->ingest_mode = mode;
     return WSORT_OK;
 }
 

@@ -45,9 +45,11 @@ def check_single(ws, name, algo, text=None):
     g = GOLD[name]
     if text is None:
         text, _ = gen.generate(g["config"], n=g["n"])
+    ws.set_ingest("count" if algo == "auto_count" else "auto")
     ws.load_text(text)
     n = ws.tokenize()
-    ws.sort(algo)
+    ws.sort("auto" if algo == "auto_count" else algo)
+    ws.set_ingest("auto")
     words, off = ws.fetch()
     assert n == g["n_words"]
     assert off == g["off"]
@@ -74,13 +76,14 @@ def c4_text():
     return gen.generate(4)[0]
 
 
-@pytest.mark.parametrize("algo", ["auto", "lsd_radix", "oets_merge", "msd_oets"])
+@pytest.mark.parametrize("algo", ["auto", "auto_count", "lsd_radix", "oets_merge", "msd_oets"])
 def test_config4_full_output_equals_oracle(ws, c4_text, algo):
     check_single(ws, "c4", algo, c4_text)
 
 
-def test_config5_slice_full_output_equals_oracle(ws):
-    check_single(ws, "c5_slice", "auto")
+@pytest.mark.parametrize("algo", ["auto", "auto_count"])
+def test_config5_slice_full_output_equals_oracle(ws, algo):
+    check_single(ws, "c5_slice", algo)
 
 
 def _group_full(name, P):

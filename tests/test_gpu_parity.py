@@ -19,9 +19,10 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["lsd_radix", "oets_merge", "msd_radix", "msd_oets", "dense_msd"]
+ALGOS = ["lsd_radix", "oets_merge", "msd_radix", "msd_oets", "dense_msd", "auto_count"]
 # keys-only algorithms: without src_off (with it they fall back to the stable LSD path)
-KEYS_ONLY = {"msd_radix", "msd_oets", "dense_msd"}
+KEYS_ONLY = {"msd_radix", "msd_oets", "dense_msd", "auto_count"}
+# "auto_count": AUTO after a counting ingest (wsort_set_ingest COUNT: the table of distinct long words)
 
 
 @pytest.fixture(scope="module")
@@ -37,9 +38,11 @@ def ws():
 
 
 def gpu_sort(ws, text, algo="lsd_radix", src=True):
+    ws.set_ingest("count" if algo == "auto_count" else "auto")
     ws.load_text(text)
     ws.tokenize()
-    ws.sort(algo, src_off=src)
+    ws.sort("auto" if algo == "auto_count" else algo, src_off=src)
+    ws.set_ingest("auto")
     if src:
         w, off, so = ws.fetch(src_off=True)
         return w.tobytes(), off, so

@@ -3,7 +3,7 @@
 TAG=$1; K=$2
 python build_native.py || exit 1
 python -m pytest tests -q -x -m gpu --deselect tests/test_gpu_fullsize.py > gpurun_out/${TAG}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${TAG}_tests.log
-python -m pytest tests/test_gpu_fullsize.py -q -x -k "auto or slice" > gpurun_out/${TAG}_full.log 2>&1; echo "full rc=$?" >> gpurun_out/${TAG}_full.log
+python -m pytest tests/test_gpu_fullsize.py -q -x -k "auto or slice or count" > gpurun_out/${TAG}_full.log 2>&1; echo "full rc=$?" >> gpurun_out/${TAG}_full.log
 WSORT_DEBUG_TIMELINE=1 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_timeline.json 2> gpurun_out/${TAG}_timeline.err
 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 if [ -n "$K" ]; then
