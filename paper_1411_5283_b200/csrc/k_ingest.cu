@@ -96,13 +96,15 @@ __device__ __forceinline__ bool cache_try(IgSmem &sm, uint32_t h, uint32_t tag) 
 }
 
 // two-choice hash cache (hot words stay in shared memory); a word whose slots are both taken by other
-// words is counted in the global table directly
-__device__ __forceinline__ void cache_add(IgSmem &sm, uint32_t *dense, uint32_t L, uint32_t idx) {
+// words is counted in the global table directly (its block of the table marked as touched)
+__device__ __forceinline__ void cache_add(IgSmem &sm, uint32_t *dense, uint8_t *touched, uint32_t L, uint32_t idx) {
     const uint32_t tag = (L << 24) | idx;
     const uint32_t hh = tag * 0x9E3779B1u;
     if (cache_try(sm, hh >> 21, tag)) return;
     if (cache_try(sm, (hh >> 10) & (kCacheSlots - 1), tag)) return;
-    atomicAdd(&dense[dense_base(L) + idx], 1u);
+    const uint32_t e = dense_base(L) + idx;
+    atomicAdd(&dense[e], 1u);
+    touched[e / kDenseBlkEntries] = 1;
 }
 
 __device__ __forceinline__ uint32_t inclusive_scan_warp(uint32_t v, int lane) {
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
         for (uint32_t i = lane; i < ((a.debug & 17) ? 0u : n3); i += 32) {   // L = 3..5: hash cache
             const uint32_t x = wlst[i];
             const uint32_t s = x & 1023u, L = (x >> 10) + 3u;
-            cache_add(sm, a.dense, L, dense_index(wb32, s, L));
+            cache_add(sm, a.dense, a.touched, L, dense_index(wb32, s, L));
         }
         if (HASH) {   // L = 6..66: counted into the global table
             if (!(a.debug & 8)) hash_long(a, sm, wlst, nlg, wb32, a.text + base, lane);
@@ -357,15 +359,31 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
         }
     }
     for (int i = t; i < 702; i += kIgThreads)
-        if (sm.d12[i]) atomicAdd(&a.dense[i], sm.d12[i]);
+        if (sm.d12[i]) {
+            atomicAdd(&a.dense[i], sm.d12[i]);
+            a.touched[0] = 1;   // (702 < one block)
+        }
     for (int i = t; i < kCacheSlots; i += kIgThreads) {
         const uint32_t tag = sm.ctag[i];
-        if (tag) atomicAdd(&a.dense[dense_base(tag >> 24) + (tag & 0xffffffu)], sm.ccnt[i]);
+        if (tag) {
+            const uint32_t e = dense_base(tag >> 24) + (tag & 0xffffffu);
+            atomicAdd(&a.dense[e], sm.ccnt[i]);
+            a.touched[e / kDenseBlkEntries] = 1;
+        }
     }
     for (int i = t; i < kHistBins; i += kIgThreads) {   // lengths >= 6 (the dense ones come from the tables)
         const uint32_t h = sm.hist[i];
         if (h) atomicAdd(&a.ghist[i], h);
     }
+}
+
+// Before K1: the blocks the previous text touched are zeroed (instead of the whole 49 MB table)
+__global__ void __launch_bounds__(256) k_dense_clear(uint32_t *dense, uint8_t *touched, uint32_t n_entries) {
+    const uint32_t b = blockIdx.x;
+    if (!touched[b]) return;
+    for (uint32_t e = b * kDenseBlkEntries + threadIdx.x; e < min(n_entries, (b + 1) * kDenseBlkEntries); e += 256) dense[e] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) touched[b] = 0;
 }
 
 // ------------------------------------------------------------------ block scan helper (256 threads)
@@ -398,11 +416,16 @@ __device__ __forceinline__ uint32_t excl_scan256(uint32_t v, uint32_t *wsum, uin
 }
 
 // ------------------------------------------------------------------ K2d: dense scan + compaction
-constexpr uint32_t kDenseBlk = 4096;   // entries per block (16 per thread)
+constexpr uint32_t kDenseBlk = kDenseBlkEntries;   // entries per block (16 per thread)
 
+// The table's blocks of kDenseBlk entries that no word touched are all zero: skipped (a block-uniform exit)
 __global__ void __launch_bounds__(256) k_dense_reduce(DenseArgs a) {
     __shared__ uint32_t wsum[9];
     const uint32_t b = blockIdx.x, t = threadIdx.x;
+    if (!a.touched[b]) {
+        if (t == 0) a.blk_sum[b] = a.blk_nnz[b] = 0;
+        return;
+    }
     uint32_t sum = 0, nnz = 0;
     const uint32_t e0 = b * kDenseBlk + 16u * t;
 #pragma unroll
@@ -422,8 +445,9 @@ __global__ void __launch_bounds__(256) k_dense_reduce(DenseArgs a) {
 }
 
 // words of each length L <= 5 = the sum of its dense table (the length histogram of the dense buckets)
-__global__ void __launch_bounds__(256) k_dense_lensum(const uint32_t *dense, uint32_t *ghist) {
+__global__ void __launch_bounds__(256) k_dense_lensum(const uint32_t *dense, const uint8_t *touched, uint32_t *ghist) {
     __shared__ uint32_t h[kDenseMaxLen + 1];
+    if (!touched[blockIdx.x]) return;
     const uint32_t t = threadIdx.x, e0 = blockIdx.x * kDenseBlk + 16u * t, ne = dense_base(kDenseMaxLen + 1);
     if (t <= kDenseMaxLen) h[t] = 0;
     __syncthreads();
@@ -503,6 +527,7 @@ __global__ void __launch_bounds__(1024) k_dense_scan(DenseArgs a, uint32_t nblk)
 __global__ void __launch_bounds__(256) k_dense_compact(DenseArgs a) {
     __shared__ uint32_t wsum[9];
     const uint32_t b = blockIdx.x, t = threadIdx.x;
+    if (!a.touched[b]) return;
     const uint32_t e0 = b * kDenseBlk + 16u * t;
     uint32_t v[16], sum = 0, nnz = 0;
 #pragma unroll
@@ -822,8 +847,12 @@ cudaError_t launch_dense_scan(const DenseArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 uint32_t dense_scan_blocks(uint32_t n_entries) { return (n_entries + kDenseBlk - 1) / kDenseBlk; }
-cudaError_t launch_dense_lensum(const uint32_t *dense, uint32_t *ghist, cudaStream_t s) {
-    k_dense_lensum<<<dense_scan_blocks(dense_base(kDenseMaxLen + 1)), 256, 0, s>>>(dense, ghist);
+cudaError_t launch_dense_lensum(const uint32_t *dense, const uint8_t *touched, uint32_t *ghist, cudaStream_t s) {
+    k_dense_lensum<<<dense_scan_blocks(dense_base(kDenseMaxLen + 1)), 256, 0, s>>>(dense, touched, ghist);
+    return cudaGetLastError();
+}
+cudaError_t launch_dense_clear(uint32_t *dense, uint8_t *touched, cudaStream_t s) {
+    k_dense_clear<<<dense_scan_blocks(dense_base(kDenseMaxLen + 1)), 256, 0, s>>>(dense, touched, dense_base(kDenseMaxLen + 1));
     return cudaGetLastError();
 }
 

@@ -76,7 +76,8 @@ struct wsort_ctx {
     bool cta_counts_ready = false; // K1b's per-CTA histograms are in cta_hist (K2b needs them)
 
     // K1 ingest: global histogram, dense counts, staging chunks
-    DevBuf ghist, dense, pool, chunk_cls, chunk_fill, ig_ctr;
+    DevBuf ghist, dense, pool, chunk_cls, chunk_fill, ig_ctr, d_touched;
+    bool dense_clean = false;                    // the dense table has been zeroed once (then: touched blocks)
     uint32_t *h_ig = nullptr;   // pinned mirror of ig_ctr
     uint32_t cta_chunks = 0, n_chunks = 0;
     DevBuf d_blk_sum, d_blk_nnz, d_ent_idx, d_ent_end, d_n_ent, d_tiles2, d_lcursor, d_tile_e;
@@ -400,7 +401,7 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->m_pat, &c->m_qparts, &c->m_pbase, &c->m_jdone,
                       &c->m_jovf, &c->m_partn, &c->m_plist, &c->m_qemit, &c->ghist, &c->dense,
                       &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
-                      &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_tiles2, &c->d_lcursor, &c->d_tile_e,
+                      &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_touched, &c->d_tiles2, &c->d_lcursor, &c->d_tile_e,
                       &c->t_wlens, &c->t_nkey, &c->t_ncnt, &c->t_fp, &c->t_meta, &c->t_cnt, &c->t_keys, &c->t_top, &c->t_dcount, &c->t_runend,
                       &c->t_scan, &c->t_tilee, &c->t_kplan, &c->t_dpfx, &c->t_rpfx, &c->x_vec, &c->x_counts,
                       &c->x_prefix, &c->x_samples, &c->x_all, &c->x_order, &c->x_split, &c->x_dest, &c->x_send,
@@ -611,7 +612,17 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     a.cta_hist = static_cast<uint32_t *>(c->cta_hist.p);
     a.cta_base = static_cast<uint32_t *>(c->cta_base.p);
     CK(cudaMemsetAsync(c->ghist.p, 0, kHistBins * 4, c->stream), "memset ghist");
-    CK(cudaMemsetAsync(c->dense.p, 0, (size_t)dense_entries() * 4, c->stream), "memset dense");
+    if ((rc = ensure(c, c->d_touched, dense_scan_blocks(dense_entries()), "dense touched flags", true))) return rc;
+    if (!c->dense_clean) {   // (first use of the table: zero it all; later only the touched blocks)
+        CK(cudaMemsetAsync(c->dense.p, 0, (size_t)dense_entries() * 4, c->stream), "memset dense");
+        CK(cudaMemsetAsync(c->d_touched.p, 0, dense_scan_blocks(dense_entries()), c->stream), "memset touched");
+        c->dense_clean = true;
+    } else {
+        rc = launch(c, "k0_dense_clear", 0, [&] {
+            return launch_dense_clear(static_cast<uint32_t *>(c->dense.p), static_cast<uint8_t *>(c->d_touched.p), c->stream);
+        });
+        if (rc) return rc;
+    }
     CK(cudaMemsetAsync(c->ig_ctr.p, 0, kIgCtrs * 4, c->stream), "memset ingest counters");
     CK(cudaMemsetAsync(c->chunk_fill.p, 0, (size_t)c->n_chunks * 4, c->stream), "memset chunk fills");
     IngestArgs ia{};
@@ -622,6 +633,7 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     ia.grid = a.grid;
     ia.ghist = static_cast<uint32_t *>(c->ghist.p);
     ia.dense = static_cast<uint32_t *>(c->dense.p);
+    ia.touched = static_cast<uint8_t *>(c->d_touched.p);
     ia.pool = static_cast<uint32_t *>(c->pool.p);
     ia.chunk_cls = static_cast<uint32_t *>(c->chunk_cls.p);
     ia.chunk_fill = static_cast<uint32_t *>(c->chunk_fill.p);
@@ -633,7 +645,7 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     rc = launch(c, "k1_ingest", (double)c->n, [&] { return launch_ingest(ia, c->stream); });
     if (rc) return rc;
     rc = launch(c, "k2_dense_lensum", (double)dense_entries() * 4,
-                [&] { return launch_dense_lensum(ia.dense, ia.ghist, c->stream); });
+                [&] { return launch_dense_lensum(ia.dense, ia.touched, ia.ghist, c->stream); });
     if (rc) return rc;
     rc = launch(c, "k2_bucket_offsets", (double)kHistBins * 4,
                 [&] { return launch_bucket_offsets(ia.ghist, static_cast<Summary *>(c->d_sum.p), c->stream); });
@@ -1417,6 +1429,7 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
     da.ent_idx = static_cast<uint32_t *>(c->d_ent_idx.p);
     da.ent_end = static_cast<uint32_t *>(c->d_ent_end.p);
     da.n_ent = static_cast<uint32_t *>(c->d_n_ent.p);
+    da.touched = static_cast<const uint8_t *>(c->d_touched.p);
     da.buckets = d_bk;
     da.tile_pfx = static_cast<const uint32_t *>(c->d_tiles2.p);
     da.tile_e0 = static_cast<uint32_t *>(c->d_tile_e.p);
@@ -1646,6 +1659,8 @@ int sort_dist(wsort_ctx *c) {
     // (1) dense: the summed tables; this rank's share of the global dense words
     if ((rc = m.allreduce_u32(static_cast<uint32_t *>(c->dense.p), dense_entries(), c->stream)))
         return comm_fail(rc, "dense all-reduce");
+    // (other ranks' words: every block may be non-zero now)
+    CK(cudaMemsetAsync(c->d_touched.p, 1, dense_scan_blocks(dense_entries()), c->stream), "touched");
     uint64_t Wd = 0;
     for (uint32_t L = 1; L <= kDenseMaxLen; L++) Wd += c->g_hist[L];
     const uint64_t dlo = me * Wd / P, dhi = (me + 1) * Wd / P;
@@ -2236,6 +2251,8 @@ int wsort_pack_long(wsort_ctx *c, uint32_t **dense_table, uint64_t *dense_entrie
     c->packed_pending = true;
     c->dist_dense = true;
     c->state = ST_PACKED;
+    // the caller adds the other ranks' tables: every block may be non-zero
+    CK(cudaMemsetAsync(c->d_touched.p, 1, dense_scan_blocks(dense_entries()), c->stream), "touched");
     *dense_table = static_cast<uint32_t *>(c->dense.p);
     *dense_entries_out = dense_entries();
     return WSORT_OK;

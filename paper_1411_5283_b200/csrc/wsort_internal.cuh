@@ -96,6 +96,7 @@ constexpr int kIgThreads = 512;
 constexpr int kIgStep = 16384;                       // bytes per ingest step = 32 per thread
 constexpr int kIgBuf = kTkPre + kIgStep + kTkHalo;   // 16656 bytes
 constexpr uint32_t kDenseMaxLen = 5;                 // words of L <= 5 are counted, not sorted
+constexpr uint32_t kDenseBlkEntries = 4096;          // the dense table's blocks (touched flags, scans)
 constexpr uint32_t kMaxStageKw = 11;                 // words of 6 <= L <= 66 are staged as keys
 constexpr uint32_t kChunkWords = 4096;               // u32 words per staging chunk (16 KiB)
 enum { kIgMaxChunks = 0, kIgOverflow = 1, kIgVeryLong = 2, kIgCtrs = 4 };
@@ -189,6 +190,7 @@ struct IngestArgs {
     uint32_t nsteps, steps_per_cta, grid;   // the K3 geometry (8 KiB steps): same CTA byte ranges
     uint32_t *ghist;                        // [257] histogram of lengths >= 6 and of > 255 (zeroed by the host)
     uint32_t *dense;                        // [dense_entries()] counts (zeroed by the host)
+    uint8_t *touched;                       // [dense_scan_blocks()] 1: a word was counted in this block
     uint32_t *pool;                         // [grid * cta_chunks + 1][kChunkWords]; the last is a trash chunk
     uint32_t *chunk_cls, *chunk_fill;       // [grid * cta_chunks] key width (1..8) and keys of each chunk
                                             // (fills zeroed by the host: unused chunks stay empty)
@@ -214,13 +216,15 @@ struct DenseArgs {
     uint32_t *blk_sum, *blk_nnz;            // [dense_scan_blocks()]
     uint32_t *ent_idx, *ent_end;            // compacted non-zero entries: table index, inclusive word end
     uint32_t *n_ent;                        // [2]: entries, words
+    const uint8_t *touched;                 // [dense_scan_blocks()] blocks with a non-zero entry (others skipped)
     const BucketInfo *buckets;              // (emit tiles) the dense buckets' word ranges
     const uint32_t *tile_pfx;               // [257] first emit tile of each dense bucket
     uint32_t *tile_e0, *tile_e1;            // [emit tiles] entry of the tile's first / last word (nullable)
     uint32_t ntiles;                        // emit tiles
 };
 uint32_t dense_scan_blocks(uint32_t n_entries);
-cudaError_t launch_dense_lensum(const uint32_t *dense, uint32_t *ghist, cudaStream_t s);   // ghist[1..5] += table sums
+cudaError_t launch_dense_lensum(const uint32_t *dense, const uint8_t *touched, uint32_t *ghist, cudaStream_t s);   // ghist[1..5] += table sums
+cudaError_t launch_dense_clear(uint32_t *dense, uint8_t *touched, cudaStream_t s);   // zero the touched blocks
 cudaError_t launch_dense_scan(const DenseArgs &a, cudaStream_t s);
 
 struct DenseEmitArgs {
