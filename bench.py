@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--cpu-sample-mb", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-streamed", dest="e2e_streamed", action="store_true",
+                    help="e2e: wsort_ingest_host (H2D streamed under K1) instead of load_text two steps ahead "
+                         "(measured slower in the 3-context pipeline: the ingest call returns only after K2)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 path with several ranks on one GPU (tests)")
     return ap.parse_args()
@@ -376,13 +379,18 @@ def e2e_pipelined(args, ws, host, stream, dev, n_words, words_len, sizes):
     e0.record(streams[0])
     for s in streams[1:]:
         s.wait_event(e0)
-    for j in range(min(D - 1, K)):
-        ctx[j].load_text(host)
+    streamed = getattr(args, "e2e_streamed", False)
+    if not streamed:
+        for j in range(min(D - 1, K)):
+            ctx[j].load_text(host)
     for i in range(K):
         cur = ctx[i % D]
-        cur.tokenize()
-        if i + D - 1 < K:
-            ctx[(i + D - 1) % D].load_text(host)   # two steps ahead
+        if streamed:   # wsort_ingest_host: this text's H2D copy in stages under K1, while earlier texts sort / copy out
+            cur.ingest_host(host)
+        else:
+            cur.tokenize()
+            if i + D - 1 < K:
+                ctx[(i + D - 1) % D].load_text(host)   # two steps ahead
         cur.sort(args.algo)
         cur.fetch_async(outs[i % D])
     for s in streams[1:]:
@@ -396,8 +404,11 @@ def e2e_pipelined(args, ws, host, stream, dev, n_words, words_len, sizes):
         c.close()
     return {"value": n_words / (ems / 1000), "unit": UNIT, "h2d_bytes_per_step": int(host.numel()),
             "d2h_bytes_per_step": words_len + 8 * (sizes.max_len + 2), "ms_per_step": ems, "steps": K,
-            "path": "wsort_load_text(pinned host) + wsort_tokenize + wsort_sort + wsort_fetch_async(pinned host); "
-                    "3 contexts round-robin, texts loaded 2 steps ahead: copies in, copies out and sorts overlap"}
+            "path": ("wsort_ingest_host(pinned host: H2D streamed in 8 stages under K1) + wsort_sort + "
+                     "wsort_fetch_async(pinned host); 3 contexts round-robin: a text's copy in overlaps its K1 and the "
+                     "earlier texts' sorts and copies out" if streamed else
+                     "wsort_load_text(pinned host) + wsort_tokenize + wsort_sort + wsort_fetch_async(pinned host); "
+                     "3 contexts round-robin, texts loaded 2 steps ahead: copies in, copies out and sorts overlap")}
 
 
 def run_wsort_dist(args, rank, world, local_rank):

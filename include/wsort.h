@@ -104,6 +104,12 @@ int wsort_set_stream(wsort_ctx *c, uintptr_t cuda_stream);
  * (host source memory must stay valid until the next synchronising call, e.g. wsort_tokenize). */
 int wsort_load_text(wsort_ctx *c, const void *bytes, uint64_t n, int mem, uint64_t global_base);
 
+/* wsort_load_text + wsort_tokenize for a text in HOST memory (pinned for the overlap), with the copy
+ * streamed: the text is copied to the device in stages on a second stream and K1 runs on each stage as soon
+ * as it has arrived, so the host->device copy overlaps phase 1 (SURVEY.md §8(f) NEXT-4 streaming ingest).
+ * Same state, results and errors as the two calls. Not while attached to a communicator (STATE). */
+int wsort_ingest_host(wsort_ctx *c, const void *bytes, uint64_t n, uint64_t global_base, uint64_t *n_words);
+
 /* Helper: read a whole file and wsort_load_text it (global_base 0). NOFILE if it does not exist,
  * IO if it cannot be read. */
 int wsort_load_file(wsort_ctx *c, const char *path);

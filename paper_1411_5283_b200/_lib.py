@@ -42,7 +42,7 @@ EXPORTS = [
     "wsort_launch_count", "wsort_histogram", "wsort_pack", "wsort_sample", "wsort_select_splitters",
     "wsort_partition", "wsort_load_keys", "wsort_set_global", "wsort_fetch_async", "wsort_sync",
     "wsort_pack_long", "wsort_dense_range", "wsort_get_ingest_info", "wsort_get_unique_id", "wsort_attach_comm",
-    "wsort_group_create", "wsort_group_destroy", "wsort_attach_group", "wsort_detach_comm", "wsort_get_slices", "wsort_set_ingest",
+    "wsort_group_create", "wsort_group_destroy", "wsort_attach_group", "wsort_detach_comm", "wsort_get_slices", "wsort_set_ingest", "wsort_ingest_host",
 ]
 INGEST = {"auto": 0, "stage": 1, "count": 2}
 UNIQUE_ID_BYTES = 128
@@ -134,6 +134,7 @@ def load():
     L.wsort_histogram.argtypes = [P, P]
     L.wsort_get_ingest_info.argtypes = [P, P]
     L.wsort_set_ingest.argtypes = [P, I]
+    L.wsort_ingest_host.argtypes = [P, P, U64, U64, ctypes.POINTER(U64)]
     L.wsort_get_unique_id.argtypes = [P]
     L.wsort_attach_comm.argtypes = [P, I, I, P]
     L.wsort_group_create.argtypes = [ctypes.POINTER(P), I]

@@ -223,6 +223,15 @@ class WSort:
     def reset_kernel_stats(self):
         self._check(self._lib.wsort_reset_kernel_stats(self._h), "wsort_reset_kernel_stats")
 
+    def ingest_host(self, text, global_base: int = 0) -> int:
+        """load_text + tokenize of a HOST text with the copy streamed under K1 (wsort_ingest_host)."""
+        mem, ptr, n, keep = _as_buffer(text)
+        if mem != L.MEM_HOST:
+            raise ValueError("ingest_host takes host memory")
+        nw = ctypes.c_uint64(0)
+        self._check(self._lib.wsort_ingest_host(self._h, ptr, n, int(global_base), ctypes.byref(nw)), "wsort_ingest_host")
+        return int(nw.value)
+
     def set_ingest(self, mode: str):
         """"auto" (default), "stage" or "count" (include/wsort.h wsort_set_ingest)."""
         self._check(self._lib.wsort_set_ingest(self._h, L.INGEST[mode]), "wsort_set_ingest")

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
     IgSmem &sm = *reinterpret_cast<IgSmem *>(ig_smem);
     uint16_t *chunk_of = reinterpret_cast<uint16_t *>(ig_smem + sizeof(IgSmem));
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint32_t c = blockIdx.x;
+    const uint32_t c = blockIdx.x + a.cta_first;
     const uint64_t b0 = (uint64_t)c * a.steps_per_cta * kTkStep;
     const uint64_t b1 = min((uint64_t)(c + 1) * a.steps_per_cta, (uint64_t)a.nsteps) * kTkStep;
     const uint32_t cbase = c * a.cta_chunks;
@@ -823,18 +823,21 @@ size_t ingest_smem(uint32_t cta_chunks) { return sizeof(IgSmem) + kMaxStageKw * 
 uint32_t dense_entries() { return dense_base(kDenseMaxLen + 1); }
 uint32_t dense_table_base(uint32_t L) { return dense_base(L); }
 
-cudaError_t launch_ingest(const IngestArgs &a, cudaStream_t s) {
-    if (a.grid == 0) return cudaSuccess;
+cudaError_t launch_ingest(const IngestArgs &a, cudaStream_t s) { return launch_ingest_range(a, 0, a.grid, s); }
+
+cudaError_t launch_ingest_range(IngestArgs a, uint32_t first, uint32_t count, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    a.cta_first = first;
     const size_t smem = ingest_smem(a.cta_chunks);
     if (a.hash) {
         cudaError_t e = cudaFuncSetAttribute(k_ingest<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        k_ingest<true><<<a.grid, kIgThreads, smem, s>>>(a);
+        k_ingest<true><<<count, kIgThreads, smem, s>>>(a);
         return cudaGetLastError();
     }
     cudaError_t e = cudaFuncSetAttribute(k_ingest<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_ingest<false><<<a.grid, kIgThreads, smem, s>>>(a);
+    k_ingest<false><<<count, kIgThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

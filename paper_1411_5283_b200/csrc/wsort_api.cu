@@ -116,6 +116,11 @@ struct wsort_ctx {
     // multi-GPU split of the ingest path (wsort_pack_long / wsort_dense_range): the dense table may be
     // summed over the ranks; this context emits the global dense words [dense_lo, dense_hi)
     bool dist_dense = false, dense_range = false;
+    // streamed ingest (wsort_ingest_host): the host text copied stage by stage under K1
+    const uint8_t *stream_src = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> copy_ev;
+    cudaEvent_t ev_ingest = nullptr;
     // multi-GPU with a library-owned communicator (wsort_attach_comm / wsort_attach_group)
     Comm *comm = nullptr;
     uint64_t g_hist[257] = {0};        // global length histogram (all ranks), [256] = words > 255 letters
@@ -427,6 +432,9 @@ void wsort_destroy(wsort_ctx *c) {
     if (c->split) cudaStreamDestroy(c->split);
     if (c->ev_lvl) cudaEventDestroy(c->ev_lvl);
     if (c->ev_split) cudaEventDestroy(c->ev_split);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (auto e : c->copy_ev) cudaEventDestroy(e);
+    if (c->ev_ingest) cudaEventDestroy(c->ev_ingest);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -435,6 +443,30 @@ int wsort_last_error(const wsort_ctx *c, char *msg, size_t cap) {
     if (!c || !msg || cap == 0) return WSORT_E_INVALID_ARG;
     snprintf(msg, cap, "%s", c->err);
     return WSORT_OK;
+}
+
+int wsort_ingest_host(wsort_ctx *c, const void *bytes, uint64_t n, uint64_t global_base, uint64_t *n_words) {
+    if (!c) return WSORT_E_INVALID_ARG;
+    if (c->comm) return set_err(c, WSORT_E_STATE, "wsort_ingest_host: not while attached (use load_text + tokenize)");
+    int rc = wsort_load_text(c, nullptr, n ? 0 : 0, WSORT_MEM_HOST, global_base);   // (prepares an empty text)
+    if (rc) return rc;
+    if (n && !bytes) return set_err(c, WSORT_E_INVALID_ARG, "bytes is NULL with n=%llu", (unsigned long long)n);
+    if (n > WSORT_MAX_SHARD_BYTES) return set_err(c, WSORT_E_TOO_LARGE, "shard of %llu bytes", (unsigned long long)n);
+    // the buffer for n bytes: zero pads around it, the text itself arrives stage by stage in tokenize
+    uint64_t nsteps = (n + kTkStep - 1) / kTkStep;
+    size_t need = kTextFrontPad + nsteps * kTkStep + kIgStep + kTkHalo + 64;
+    if ((rc = ensure(c, c->text_alloc, need, "text"))) return rc;
+    uint8_t *base = static_cast<uint8_t *>(c->text_alloc.p);
+    CK(cudaMemsetAsync(base, 0, kTextFrontPad, c->stream), "memset text head");
+    CK(cudaMemsetAsync(base + kTextFrontPad + n, 0, need - kTextFrontPad - n, c->stream), "memset text tail");
+    c->d_text = base + kTextFrontPad;
+    c->n = n;
+    plan_tokenizer(c);
+    c->state = ST_LOADED;
+    c->stream_src = static_cast<const uint8_t *>(bytes);
+    rc = wsort_tokenize(c, n_words);
+    c->stream_src = nullptr;
+    return rc;
 }
 
 int wsort_load_text(wsort_ctx *c, const void *bytes, uint64_t n, int mem, uint64_t global_base) {
@@ -642,8 +674,40 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     ia.hash = hash ? 1u : 0u;
     ia.tab = c->tab;
     if (const char *dbg = getenv("WSORT_INGEST_DEBUG")) ia.debug = (uint32_t)atoi(dbg);
-    rc = launch(c, "k1_ingest", (double)c->n, [&] { return launch_ingest(ia, c->stream); });
-    if (rc) return rc;
+    if (c->stream_src) {
+        // streamed ingest: S stages of K1 CTAs; stage s's bytes (+32 KiB: the warps' prefetch and words that
+        // cross the range end) are copied on the copy stream, and its K1 launch waits for that copy only, so
+        // the host->device copy of the later stages overlaps K1 on the earlier ones
+        const uint8_t *src = c->stream_src;
+        c->stream_src = nullptr;   // (a second pass over the same text reads the device copy)
+        if (!c->copy_stream) {
+            CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "copy stream");
+            CK(cudaEventCreateWithFlags(&c->ev_ingest, cudaEventDisableTiming), "ingest event");
+        }
+        const uint32_t S = std::min<uint32_t>(8, std::max<uint32_t>(a.grid, 1));
+        while (c->copy_ev.size() < S) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "copy event");
+            c->copy_ev.push_back(e);
+        }
+        CK(cudaEventRecord(c->ev_ingest, c->stream), "ingest event");   // (earlier work on the old text is done)
+        CK(cudaStreamWaitEvent(c->copy_stream, c->ev_ingest, 0), "ingest wait");
+        uint8_t *dst = const_cast<uint8_t *>(c->d_text);
+        const uint64_t per_cta = (uint64_t)a.steps_per_cta * kTkStep;
+        for (uint32_t st = 0; st < S; st++) {
+            const uint32_t g0 = (uint32_t)((uint64_t)a.grid * st / S), g1 = (uint32_t)((uint64_t)a.grid * (st + 1) / S);
+            const uint64_t b0 = std::min<uint64_t>(c->n, g0 * per_cta), b1 = std::min<uint64_t>(c->n, g1 * per_cta + 32768);
+            if (b1 > b0) CK(cudaMemcpyAsync(dst + b0, src + b0, b1 - b0, cudaMemcpyHostToDevice, c->copy_stream), "copy text stage");
+            CK(cudaEventRecord(c->copy_ev[st], c->copy_stream), "copy event");
+            CK(cudaStreamWaitEvent(c->stream, c->copy_ev[st], 0), "copy wait");
+            rc = launch(c, "k1_ingest", (double)(std::min<uint64_t>(c->n, g1 * per_cta) - b0),
+                        [&] { return launch_ingest_range(ia, g0, g1 - g0, c->stream); });
+            if (rc) return rc;
+        }
+    } else {
+        rc = launch(c, "k1_ingest", (double)c->n, [&] { return launch_ingest(ia, c->stream); });
+        if (rc) return rc;
+    }
     rc = launch(c, "k2_dense_lensum", (double)dense_entries() * 4,
                 [&] { return launch_dense_lensum(ia.dense, ia.touched, ia.ghist, c->stream); });
     if (rc) return rc;

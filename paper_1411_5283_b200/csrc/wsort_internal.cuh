@@ -200,12 +200,14 @@ struct IngestArgs {
                                             // counting, 2 = skip key packing, 4 = direct L3-5 counts
     uint32_t hash;                          // 1: count the long words into `tab` instead of staging them
     HashTab tab;
+    uint32_t cta_first;                     // this launch's first CTA (streamed ingest launches K1 by CTA ranges)
 };
 size_t ingest_smem(uint32_t cta_chunks);
 uint32_t ingest_ctas_per_sm();   // resident K1 CTAs per SM (the tokenizer grid is one wave of them)
 uint32_t dense_entries();
 uint32_t dense_table_base(uint32_t L);
-cudaError_t launch_ingest(const IngestArgs &a, cudaStream_t s);
+cudaError_t launch_ingest(const IngestArgs &a, cudaStream_t s);   // CTAs [a.cta_first, a.cta_first + count)
+cudaError_t launch_ingest_range(IngestArgs a, uint32_t first, uint32_t count, cudaStream_t s);
 
 // words per k_emit_dense tile of dense bucket L: L <= 2 has <= 676 entries in all, longer buckets <= one
 // entry per word (the tile's entries must fit its shared memory, kDenseTileEnt)

@@ -373,3 +373,21 @@ def test_many_distinct_very_long_words_fall_back(ws):
     ws.sort("auto")
     w, off = ws.fetch()
     assert off == ref.off and w.tobytes() == ref.words
+
+
+# ---------------------------------------------------------------- streamed ingest (NEXT-4)
+@pytest.mark.parametrize("case", ["c1", "c2", "c3", "cross_every_step", "ends_mid_word", "empty", "long_words_65_255"])
+def test_ingest_host_streamed_equals_oracle(ws, case):
+    """wsort_ingest_host: the text copied to the device in stages under K1 (8 stages of K1 CTAs) gives the
+    oracle's output (stage boundaries fall inside words: each stage copies 32 KiB beyond its range)."""
+    import torch
+
+    text = {"c1": lambda: gen.generate(1)[0], "c2": lambda: gen.generate(2)[0],
+            "c3": lambda: gen.generate(3, n=24 << 20)[0]}.get(case, lambda: np.frombuffer(EDGE[case], np.uint8))()
+    host = torch.from_numpy(np.ascontiguousarray(text)).pin_memory()
+    ref = oracle.sort(text, oracle.MERGE)
+    n = ws.ingest_host(host)
+    assert n == ref.n_words
+    ws.sort("auto")
+    w, off = ws.fetch()
+    assert off == ref.off and w.tobytes() == ref.words
