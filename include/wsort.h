@@ -77,10 +77,14 @@ enum wsort_algo {
                                   a CTA-local LSD radix in shared memory (keys only, L <= 48; else LSD) */
     WSORT_ALGO_MSD_OETS = 4,   /* as MSD_RADIX, but the small sub-buckets are finished by CTA-local
                                   odd-even transposition (data-parallel bubble sort) + merge paths */
-    WSORT_ALGO_DENSE_MSD = 5   /* words of L <= 5 counted in dense tables during wsort_tokenize (the sorted
+    WSORT_ALGO_DENSE_MSD = 5,  /* words of L <= 5 counted in dense tables during wsort_tokenize (the sorted
                                   sub-array is the counting sort of the word's base-26 value); longer words
                                   staged as keys by the same text pass and sorted by MSD_OETS from there.
                                   Keys only; falls back like AUTO when it does not apply */
+    WSORT_ALGO_RAGGED = 6      /* the paper's other data structure, "vectors of strings": every
+                                  sub-array element is a reference (text offset) to its word, compared through
+                                  the text; bitonic tiles + merge-path merges (stable; src_off). Measured
+                                  against the fixed-width keys ("array char 3D") of the others */
 };
 
 /* wsort_sort flags */

@@ -28,8 +28,10 @@ ALGO_LSD_RADIX = 2
 ALGO_MSD_RADIX = 3
 ALGO_MSD_OETS = 4
 ALGO_DENSE_MSD = 5
+ALGO_RAGGED = 6
 ALGOS = {"auto": ALGO_AUTO, "oets_merge": ALGO_OETS_MERGE, "lsd_radix": ALGO_LSD_RADIX,
-         "msd_radix": ALGO_MSD_RADIX, "msd_oets": ALGO_MSD_OETS, "dense_msd": ALGO_DENSE_MSD}
+         "msd_radix": ALGO_MSD_RADIX, "msd_oets": ALGO_MSD_OETS, "dense_msd": ALGO_DENSE_MSD,
+         "ragged": ALGO_RAGGED}
 
 FLAG_SRC_OFF = 0x1
 MAX_WORD_LEN = 255

@@ -1556,6 +1556,7 @@ bool hash_sortable(const wsort_ctx *c) {
 // words from the table of distinct words: gather the D distinct keys into their length buckets, sort them
 // (MSD, radix finish: keys end in buffer B), look up each one's count, scan, and write the runs.
 void summary_from_counts(Summary &s, const uint64_t *n_per_len);
+std::vector<BucketInfo> bucket_table(const Summary &s);
 
 // The long words (>= 6 letters) of the table of distinct words (c->tab, its distinct counts per length in
 // c->h_tab + 4) into the output buckets bk / d_bk (bk[L].n words at bk[L].byte_off; the run index of
@@ -1929,6 +1930,57 @@ int sort_dist(wsort_ctx *c) {
     return WSORT_OK;
 }
 
+// WSORT_ALGO_RAGGED: K3 writes each word's text offset into its bucket (stable), the references are sorted
+// through the text (k_ragged.cu), and the words are copied out of the text.
+int sort_ragged(wsort_ctx *c, bool want_src) {
+    const Summary &s = *c->h_sum;
+    const uint64_t W = s.n_words;
+    int rc;
+    std::vector<BucketInfo> bk = bucket_table(s);
+    if ((rc = ensure(c, c->keys_a, s.key_off[256] * 4 + 64, "keys_a"))) return rc;
+    if ((rc = ensure(c, c->pay_a, W * 4 + 64, "pay_a"))) return rc;
+    if ((rc = ensure(c, c->pay_b, W * 4 + 64, "pay_b"))) return rc;
+    if ((rc = ensure(c, c->words, s.byte_off[256] + 64, "words"))) return rc;
+    if (want_src && (rc = ensure(c, c->src_off, W * 8 + 64, "src_off"))) return rc;
+    uint32_t pfx[257], nt = 0, nmax = 0;
+    const uint32_t T = ragged_tile();
+    for (uint32_t L = 0; L < 256; L++) {
+        pfx[L] = nt;
+        if (L >= 1 && bk[L].n) nt += (bk[L].n + T - 1) / T;
+        nmax = std::max(nmax, bk[L].n);
+    }
+    pfx[256] = nt;
+    if ((rc = arena_upload(c, c->plan, bk.data(), bk.size() * sizeof(BucketInfo), "plan"))) return rc;
+    if ((rc = arena_upload(c, c->d_tiles, pfx, sizeof pfx, "ragged tiles"))) return rc;
+    const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
+    TkArgs &tk = c->tk;
+    tk.buckets = d_bk;
+    tk.keys = static_cast<uint32_t *>(c->keys_a.p);
+    tk.payload = static_cast<uint32_t *>(c->pay_a.p);
+    if ((rc = launch(c, "k3_pack_scatter", (double)c->n + 4.0 * W, [&] { return pack_scatter(c); }))) return rc;
+    RaggedArgs ra{};
+    ra.text = c->d_text;
+    ra.buckets = d_bk;
+    ra.tile_pfx = static_cast<const uint32_t *>(c->d_tiles.p);
+    ra.ntiles = nt;
+    ra.in = static_cast<const uint32_t *>(c->pay_a.p);
+    ra.out = static_cast<uint32_t *>(c->pay_b.p);
+    ra.words = static_cast<uint8_t *>(c->words.p);
+    ra.src_off = want_src ? static_cast<uint64_t *>(c->src_off.p) : nullptr;
+    ra.global_base = c->global_base;
+    if ((rc = launch(c, "kr1_ragged_tiles", 8.0 * W, [&] { return launch_ragged_tiles(ra, c->stream); }))) return rc;
+    uint32_t *x = static_cast<uint32_t *>(c->pay_b.p), *y = static_cast<uint32_t *>(c->pay_a.p);   // sorted runs in x
+    for (uint32_t run = T; run < nmax; run *= 2) {
+        ra.in = x;
+        ra.out = y;
+        ra.run = run;
+        if ((rc = launch(c, "kr2_ragged_merge", 8.0 * W, [&] { return launch_ragged_merge(ra, c->stream); }))) return rc;
+        std::swap(x, y);
+    }
+    ra.in = x;
+    return launch(c, "kr3_ragged_emit", (double)s.byte_off[256] + 4.0 * W, [&] { return launch_ragged_emit(ra, c->stream); });
+}
+
 // Split multi-GPU sort (after wsort_pack_long, the all-reduce of the dense tables, wsort_load_keys and
 // wsort_dense_range): this rank's slice of the global dense words, then the keys it received, sorted.
 int sort_dist_dense(wsort_ctx *c) {
@@ -1972,7 +2024,8 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
     if (!c) return WSORT_E_INVALID_ARG;
     if (c->state < ST_TOKENIZED) return set_err(c, WSORT_E_STATE, "wsort_sort before wsort_tokenize");
     if (algo != WSORT_ALGO_AUTO && algo != WSORT_ALGO_LSD_RADIX && algo != WSORT_ALGO_OETS_MERGE &&
-        algo != WSORT_ALGO_MSD_RADIX && algo != WSORT_ALGO_MSD_OETS && algo != WSORT_ALGO_DENSE_MSD)
+        algo != WSORT_ALGO_MSD_RADIX && algo != WSORT_ALGO_MSD_OETS && algo != WSORT_ALGO_DENSE_MSD &&
+        algo != WSORT_ALGO_RAGGED)
         return set_err(c, WSORT_E_INVALID_ARG, "bad algo %d", algo);
     if (flags & ~WSORT_FLAG_SRC_OFF) return set_err(c, WSORT_E_INVALID_ARG, "bad flags 0x%x", flags);
     if (c->keys_external && !c->packed_pending)
@@ -2004,6 +2057,8 @@ int wsort_sort(wsort_ctx *c, int algo, unsigned flags) {
         rc = sort_dist_dense(c);
     } else if (algo == WSORT_ALGO_OETS_MERGE) {
         rc = sort_oets(c, want_src);
+    } else if (algo == WSORT_ALGO_RAGGED && !c->packed_pending) {
+        rc = sort_ragged(c, want_src);
     } else if (algo == WSORT_ALGO_AUTO && ingest_ok && c->hashed && hash_sortable(c)) {
         rc = sort_dense_hash(c);
     } else if ((algo == WSORT_ALGO_AUTO || algo == WSORT_ALGO_DENSE_MSD) && ingest_ok) {

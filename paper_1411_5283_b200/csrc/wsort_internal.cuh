@@ -153,6 +153,24 @@ cudaError_t launch_emit_runs(const HashRunArgs &a, cudaStream_t s);
 cudaError_t launch_hash_counts(const HashRunArgs &a, cudaStream_t s);   // run_end[j] = count of key j (no scan)
 cudaError_t launch_scan_u32(uint32_t *v, uint32_t n, uint32_t *scan_blk, cudaStream_t s);   // inclusive, in place
 
+// ---------------- ragged backing: references into the text (k_ragged.cu) ----------------
+struct RaggedArgs {
+    const uint8_t *text;                    // the device text (padded)
+    const BucketInfo *buckets;              // word_off (index into in / out), byte_off, n
+    const uint32_t *tile_pfx;               // [257] first 1024-reference tile of bucket L
+    uint32_t ntiles;
+    const uint32_t *in;                     // references (text byte offsets), bucket order
+    uint32_t *out;
+    uint32_t run;                           // merge pass: sorted run length
+    uint8_t *words;
+    uint64_t *src_off;                      // nullable
+    uint64_t global_base;
+};
+uint32_t ragged_tile();
+cudaError_t launch_ragged_tiles(const RaggedArgs &a, cudaStream_t s);
+cudaError_t launch_ragged_merge(const RaggedArgs &a, cudaStream_t s);
+cudaError_t launch_ragged_emit(const RaggedArgs &a, cudaStream_t s);
+
 // ---------------- multi-GPU exchange of (distinct word, count) records (k_xchg.cu) ----------------
 struct XchgArgs {
     HashTab tab;                            // (absorb) this rank's table, cleared

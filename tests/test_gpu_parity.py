@@ -19,7 +19,7 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["lsd_radix", "oets_merge", "msd_radix", "msd_oets", "dense_msd", "auto_count"]
+ALGOS = ["lsd_radix", "oets_merge", "msd_radix", "msd_oets", "dense_msd", "auto_count", "ragged"]
 # keys-only algorithms: without src_off (with it they fall back to the stable LSD path)
 KEYS_ONLY = {"msd_radix", "msd_oets", "dense_msd", "auto_count"}
 # "auto_count": AUTO after a counting ingest (wsort_set_ingest COUNT: the table of distinct long words)
