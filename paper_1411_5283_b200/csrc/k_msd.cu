@@ -16,6 +16,7 @@
 // finished runs that ended in buffer A into buffer B. Every key ends in buffer B at its final index.
 #include <type_traits>
 
+#include "k_tma.cuh"
 #include "wsort_internal.cuh"
 
 namespace wsort {
@@ -248,14 +249,15 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
 // ---------------------------------------------------------------- scatter
 template <int KW>
 __device__ __forceinline__ void scatter_tile(const MsdArgs &a, const MsdTile &td, const MsdSeg &sg, const BucketInfo &b,
-                                             uint32_t *sm) {
+                                             uint32_t *sm, const uint32_t *tile_keys = nullptr) {
     constexpr int KPT = 32 / KW;   // keys per thread (striped)
     const int t = threadIdx.x;
     uint32_t *hist = sm, *toff = sm + kRadixBins, *gbase = sm + 2 * kRadixBins, *kout = sm + 3 * kRadixBins;
     uint32_t *wsum = kout + 8192 + 8192 / 32 + 8;
     for (int i = t; i < kRadixBins; i += kST) hist[i] = 0;
     __syncthreads();
-    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)(sg.start + td.off) * KW;
+    // the tile's keys: in global memory, or already in shared memory (tile_keys: the persistent kernel's TMA copy)
+    const uint32_t *src = tile_keys ? tile_keys : ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)(sg.start + td.off) * KW;
     uint32_t key[KPT][KW], slot[(KPT + 1) / 2];
 #pragma unroll
     for (int r = 0; r < (KPT + 1) / 2; r++) slot[r] = 0;
@@ -264,7 +266,7 @@ __device__ __forceinline__ void scatter_tile(const MsdArgs &a, const MsdTile &td
     for (int r = 0; r < KPT; r++) {
         const uint32_t i = t + r * kST;
 #pragma unroll
-        for (int u = 0; u < KW; u++) key[r][u] = i < td.n ? __ldg(src + (uint64_t)i * KW + u) : 0u;
+        for (int u = 0; u < KW; u++) key[r][u] = i < td.n ? src[(uint64_t)i * KW + u] : 0u;
     }
 #pragma unroll
     for (int r = 0; r < KPT; r++) {
@@ -331,6 +333,65 @@ __global__ void __launch_bounds__(kST, 2) k_msd_scatter(MsdArgs a) {
         case 10: scatter_tile<10>(a, td, sg, b, sm); break;
         case 11: scatter_tile<11>(a, td, sg, b, sm); break;
         default: break;   // kw > 11 never reaches the scatter: the host sorts such buckets with LSD
+    }
+}
+
+// Persistent scatter: CTA b takes tiles b, b + grid, ... (skipping those of skipped segments); the next
+// tile's keys are fetched by a TMA bulk copy into the other shared-memory buffer while this one is
+// scattered, so the tile's loads no longer stall the scatter (the per-tile kernel waits on them).
+constexpr uint32_t kScatBuf = 8192 + 8;   // key words of a tile (<= 8192) + the 16-byte alignment slack
+__global__ void __launch_bounds__(kST, 2) k_msd_scatter_p(MsdArgs a, uint32_t ntiles) {
+    extern __shared__ __align__(128) uint32_t smp[];
+    uint32_t *inb = smp;                                                    // [2][kScatBuf]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smp + 2 * kScatBuf);      // [2]
+    uint32_t *sj = reinterpret_cast<uint32_t *>(bar + 2);                   // [0..1] tile, [2..3] word offset
+    uint32_t *sm = sj + 8;
+    auto fetch = [&](uint32_t j, uint32_t b) {   // thread 0
+        while (j < ntiles && a.seg_skip[a.tiles[j].seg]) j += gridDim.x;
+        sj[b] = j;
+        if (j >= ntiles) return;
+        const MsdTile td = a.tiles[j];
+        const MsdSeg sg = a.segs[td.seg];
+        const BucketInfo bk = a.buckets[sg.L];
+        const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + bk.key_off + (uint64_t)(sg.start + td.off) * bk.kw;
+        const uintptr_t s0 = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+        const uintptr_t s1 = (reinterpret_cast<uintptr_t>(src + (size_t)td.n * bk.kw) + 15) & ~(uintptr_t)15;
+        sj[2 + b] = (uint32_t)((reinterpret_cast<uintptr_t>(src) - s0) / 4);
+        tma::mbar_expect_tx(&bar[b], (uint32_t)(s1 - s0));
+        tma::bulk_g2s(inb + b * kScatBuf, reinterpret_cast<const void *>(s0), (uint32_t)(s1 - s0), &bar[b]);
+    };
+    if (threadIdx.x == 0) {
+        tma::mbar_init(&bar[0], 1);
+        tma::mbar_init(&bar[1], 1);
+        tma::fence_mbar_init();
+        fetch(blockIdx.x, 0);
+    }
+    __syncthreads();
+    for (uint32_t it = 0;; it++) {
+        const uint32_t cur = it & 1;
+        const uint32_t j = sj[cur];
+        if (j >= ntiles) break;
+        const uint32_t off = sj[2 + cur];
+        if (threadIdx.x == 0) fetch(j + gridDim.x, cur ^ 1);   // (buffer cur^1 was released at the last barrier)
+        tma::mbar_wait(&bar[cur], (it >> 1) & 1);
+        const MsdTile td = a.tiles[j];
+        const MsdSeg sg = a.segs[td.seg];
+        const BucketInfo b = a.buckets[sg.L];
+        const uint32_t *kin = inb + cur * kScatBuf + off;
+        switch (b.kw) {
+            case 1: scatter_tile<1>(a, td, sg, b, sm, kin); break;
+            case 2: scatter_tile<2>(a, td, sg, b, sm, kin); break;
+            case 3: scatter_tile<3>(a, td, sg, b, sm, kin); break;
+            case 4: scatter_tile<4>(a, td, sg, b, sm, kin); break;
+            case 5: scatter_tile<5>(a, td, sg, b, sm, kin); break;
+            case 6: scatter_tile<6>(a, td, sg, b, sm, kin); break;
+            case 7: scatter_tile<7>(a, td, sg, b, sm, kin); break;
+            case 8: scatter_tile<8>(a, td, sg, b, sm, kin); break;
+            case 9: scatter_tile<9>(a, td, sg, b, sm, kin); break;
+            case 10: scatter_tile<10>(a, td, sg, b, sm, kin); break;
+            default: scatter_tile<11>(a, td, sg, b, sm, kin); break;
+        }
+        __syncthreads();
     }
 }
 
@@ -1632,6 +1693,17 @@ cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s) {
 }
 cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s) {
     if (!ntiles) return cudaSuccess;
+    static const bool persistent = getenv("WSORT_SCATTER_TILES") == nullptr;   // (experiments: the per-tile kernel)
+    if (persistent) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const size_t smem = 2 * kScatBuf * 4 + 16 + 32 + msd_scatter_smem();
+        cudaError_t e = cudaFuncSetAttribute(k_msd_scatter_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_msd_scatter_p<<<std::min<uint32_t>(ntiles, (uint32_t)sms * 2), kST, smem, s>>>(a, ntiles);
+        return cudaGetLastError();
+    }
     const size_t smem = msd_scatter_smem();
     cudaError_t e = cudaFuncSetAttribute(k_msd_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
