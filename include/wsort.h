@@ -186,7 +186,9 @@ typedef struct {
     double bytes;           /* sum of ALGORITHMIC bytes (DESIGN.md per-kernel model) */
 } wsort_kernel_stat;
 
-/* on != 0: bracket every kernel launch with CUDA events on the context's stream. */
+/* on != 0: bracket every kernel launch with CUDA events on the stream it is launched on. on == 2 also runs
+ * every kernel on the context's stream (no concurrent side streams), so each kernel's events measure it
+ * alone and the per-kernel times add up to the serialised step (the bench's kernel table). */
 int wsort_set_profiling(wsort_ctx *c, int on);
 /* Synchronises; fills up to cap entries and *n with the number of kernel classes seen. */
 int wsort_kernel_stats(wsort_ctx *c, wsort_kernel_stat *out, int cap, int *n);

@@ -210,8 +210,9 @@ class WSort:
         self._check(self._lib.wsort_set_global(self._h, g.ctypes.data, int(word_base), int(byte_base)), "wsort_set_global")
 
     # ------------------------------------------------------------------ measurement
-    def set_profiling(self, on: bool):
-        self._check(self._lib.wsort_set_profiling(self._h, 1 if on else 0), "wsort_set_profiling")
+    def set_profiling(self, on):
+        """False / True (per-kernel CUDA events) / 2 (also every kernel on the context's stream)."""
+        self._check(self._lib.wsort_set_profiling(self._h, 2 if on == 2 else (1 if on else 0)), "wsort_set_profiling")
 
     def kernel_stats(self) -> dict:
         arr = (L.KernelStat * 64)()

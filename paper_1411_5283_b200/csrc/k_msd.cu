@@ -1,19 +1,28 @@
-// k_msd.cu — phase 3, variant B+ ("msd_radix"): most-significant-digit
-// radix partitioning of every length bucket ("sort each vector ... in the alphabetic
-// order"), finished by CTA-local odd-even transposition sorts (the data-parallel bubble sort of
-// PAPER.md:23) of the small sub-buckets.
+// k_msd.cu — phase 3 for the staged long words: most-significant-digit radix partitioning of every length
+// bucket ("sort each vector ... in the alphabetic order"), finished per
+// sub-bucket on one CTA.
 //
-// Keys only: equal keys are identical words, so no pass has to be stable. A level-l pass splits
-// every "big" segment by its l-th 2-letter digit:
-//   k_msd_count    per tile: digit histogram in shared memory -> per-segment histogram (atomics)
-//   k_msd_plan     per segment: exclusive scan of its histogram -> child bases / scatter cursors;
-//                  every child is queued as final (its digits are exhausted), tiny (<= 32 keys:
-//                  one warp sorts it), small (<= one CTA tile: one CTA sorts it) or big (next level)
-//   k_msd_scatter  per tile: a shared-memory atomic gives each key its slot inside its digit, one
-//                  global atomic per (tile, digit) reserves the range, keys are reordered in shared
-//                  memory and written out coalesced
-// then k_msd_warp_sort / k_msd_cta_sort finish the tiny / small children and k_msd_copy moves
-// finished runs that ended in buffer A into buffer B. Every key ends in buffer B at its final index.
+// Keys only: equal keys are identical words, so no pass has to be stable. A level-l pass splits every
+// "big" segment by its l-th 2-letter digit:
+//   k_msd_count      per tile: digit histogram in shared memory -> per-segment histogram (atomics)
+//   k_msd_plan       per segment: exclusive scan of its histogram -> children's bases / scatter cursors;
+//                    every child is queued as a finishing job, or as a segment of the next level
+//   k_msd_scatter_p  persistent, TMA double-buffered tiles: a shared-memory atomic gives each key its slot
+//                    inside its digit, one global atomic per (tile, digit) reserves the range, keys are
+//                    reordered in shared memory and written out coalesced (k_msd_scatter: per-tile form)
+// Finishing (AUTO, the streaming finish, stream_fin = 1):
+//   k_msd_fin        persistent (job tickets, biggest first): a job (a child of any size, or several small
+//                    children) is counted as an exact multiset in a shared-memory table (1-2-word keys: the
+//                    key itself; wider keys: a 64-bit fingerprint verified word by word against a
+//                    representative), its distinct keys sorted (odd-even transposition = the data-parallel
+//                    bubble sort of PAPER.md:23, + merge paths, or rank counting), and each written as text
+//                    as often as it occurs (16-byte windows of the repeated "word\n" pattern); a job with
+//                    too many distinct keys goes one MSD level deeper
+//   k_msd_fin_split  parts of jobs > 128 K keys (32 K keys each, their own CTA, a third stream); the last
+//                    part merges the parts' lists; k_msd_fin_emit writes such a job's text by pieces
+// Radix finish (msd_radix, and the distinct keys of the COUNT ingest, finish_radix = 1): k_msd_warp_sort
+// (<= 32 keys, one warp), k_msd_radix_job / k_msd_cta_sort (one CTA tile), k_msd_copy (finished runs that
+// ended in buffer A); every key ends in buffer B at its final index.
 #include <type_traits>
 
 #include "k_tma.cuh"

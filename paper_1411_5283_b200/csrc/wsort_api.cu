@@ -137,6 +137,7 @@ struct wsort_ctx {
 
     // profiling
     bool prof = false;
+    bool prof_serial = false;   // wsort_set_profiling(2): every kernel on the context's stream (exact shares)
     std::vector<KernelClass> classes;
     std::vector<PendingEv> pending;
     std::vector<cudaEvent_t> ev_pool;
@@ -1258,14 +1259,15 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
                 CK(cudaEventCreateWithFlags(&c->ev_split, cudaEventDisableTiming), "split event");
             }
             CK(cudaEventRecord(c->ev_lvl, c->stream), "level event");
-            CK(cudaStreamWaitEvent(c->split, c->ev_lvl, 0), "level wait");
-            rc = launch_on(c, c->split, "k4m_msd_fin_split", 0,
-                           [&] { return launch_msd_fin_split(m, parts_done, fin_grid, c->split); });
+            cudaStream_t sp = c->prof_serial ? c->stream : c->split;   // (serial profiling: one stream)
+            CK(cudaStreamWaitEvent(sp, c->ev_lvl, 0), "level wait");
+            rc = launch_on(c, sp, "k4m_msd_fin_split", 0,
+                           [&] { return launch_msd_fin_split(m, parts_done, fin_grid, sp); });
             if (rc) return rc;
-            rc = launch_on(c, c->split, "k4m_msd_fin_emit", 0,
-                           [&] { return launch_msd_fin_emit(m, emit_done, (uint32_t)c->sms * 2, c->split); });
+            rc = launch_on(c, sp, "k4m_msd_fin_emit", 0,
+                           [&] { return launch_msd_fin_emit(m, emit_done, (uint32_t)c->sms * 2, sp); });
             if (rc) return rc;
-            CK(cudaEventRecord(c->ev_split, c->split), "split event");
+            CK(cudaEventRecord(c->ev_split, sp), "split event");
             rc = launch(c, "k4m_msd_finish", level == 0 ? 2 * key_bytes : 0,
                         [&] { return launch_msd_fin_jobs(m, small_done, parts_done, fin_grid, c->stream); });
             if (rc) return rc;
@@ -1484,7 +1486,8 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
     }
     CK(cudaEventRecord(c->ev_fork, c->stream), "fork");
-    CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0), "fork wait");
+    cudaStream_t aux = c->prof_serial ? c->stream : c->aux;   // (serial profiling: one stream)
+    CK(cudaStreamWaitEvent(aux, c->ev_fork, 0), "fork wait");
     DenseArgs da{};
     da.dense = static_cast<const uint32_t *>(c->dense.p);
     da.n_entries = ne;
@@ -1499,7 +1502,7 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
     da.tile_e0 = static_cast<uint32_t *>(c->d_tile_e.p);
     da.tile_e1 = da.tile_e0 + ndt + 1;
     da.ntiles = ndt;
-    rc = launch_on(c, c->aux, "k2d_dense_scan", 2.0 * ne * 4, [&] { return launch_dense_scan(da, c->aux); });
+    rc = launch_on(c, aux, "k2d_dense_scan", 2.0 * ne * 4, [&] { return launch_dense_scan(da, aux); });
     if (rc) return rc;
     DenseEmitArgs ea{};
     ea.buckets = d_bk;
@@ -1511,9 +1514,9 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
     ea.tile_e0 = da.tile_e0;
     ea.tile_e1 = da.tile_e1;
     ea.words = static_cast<uint8_t *>(c->words.p);
-    rc = launch_on(c, c->aux, "k5d_emit_dense", out_bytes, [&] { return launch_emit_dense(ea, c->aux); });
+    rc = launch_on(c, aux, "k5d_emit_dense", out_bytes, [&] { return launch_emit_dense(ea, aux); });
     if (rc) return rc;
-    CK(cudaEventRecord(c->ev_join, c->aux), "join");
+    CK(cudaEventRecord(c->ev_join, aux), "join");
     return WSORT_OK;
 }
 
@@ -2150,6 +2153,7 @@ int wsort_device_results(wsort_ctx *c, const uint8_t **words, const uint64_t **b
 int wsort_set_profiling(wsort_ctx *c, int on) {
     if (!c) return WSORT_E_INVALID_ARG;
     c->prof = on != 0;
+    c->prof_serial = on == 2;
     return WSORT_OK;
 }
 
