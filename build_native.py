@@ -60,11 +60,24 @@ def build_wsort(force: bool = False, verbose_ptxas: bool = False) -> str:
     if not (force or _stale(out, srcs)):
         return out
     cu = [s for s in srcs if s.endswith(".cu")]
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
-           "-I", os.path.join(ROOT, "include"), "-cudart", "static", "-ldl", "-o", out, *cu]
+    # one object per translation unit, compiled in parallel (no device symbol crosses files), then linked
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include")]
     if verbose_ptxas:
-        cmd.insert(1, "-Xptxas=-v")
-    _run(cmd)
+        flags.insert(0, "-Xptxas=-v")
+    headers = [s for s in srcs if not s.endswith(".cu")]
+    objs, jobs = [], []
+    for s in cu:
+        o = os.path.join(objdir, os.path.basename(s)[:-3] + ".o")
+        objs.append(o)
+        if force or _stale(o, [s, *headers]):
+            jobs.append([NVCC, *flags, "-c", "-o", o, s])
+    if jobs:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            list(ex.map(_run, jobs))
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-ldl", "-o", out, *objs])
     return out
 
 

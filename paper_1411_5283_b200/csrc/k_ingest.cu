@@ -10,13 +10,17 @@
 //       is the counting sort of idx. L <= 2 count in shared memory; L = 3..5 go through a small
 //       shared-memory hash cache (hot words) and fall back to global atomics (cold words);
 //     * 6 <= L <= 66: the word is packed into its fixed-width key (kw = ceil(L/6) u32, the paper's
-//       "array char 3D") and appended to a staging chunk of its key-width class.
-//       Chunks (16 KiB) come from the CTA's own region of the pool (bounded: key bytes <= text bytes);
-//       order inside a chunk is arbitrary (keys only: equal keys are identical words).
+//       "array char 3D") and appended to a staging chunk of its key-width class K = kw
+//       (lengths 6K-5 .. 6K). Chunks (16 KiB) come from the CTA's own region of the pool (bounded: key
+//       bytes <= text bytes) and are word-major (word q of key i at q * cap + i, cap = the chunk's key
+//       capacity); order inside a chunk is arbitrary (keys only: equal keys are identical words). Every
+//       chunk is listed under its class; the MSD's first level reads the chunks in place, class by class
+//       (k_msd.cu: k_msd_count0 / k_msd_scatter0). (One chunk stream per length was measured slower: a
+//       warp's keys then go to ~15 chunks, and the stores of the keys cost 0.26 ms more on c4.)
 // K2d k_dense_reduce / k_dense_scan / k_dense_compact: exclusive scan of the dense counts (which is
 //   the global word index, since buckets 1..5 come first) and compaction of the non-zero entries.
-// K3c k_lscatter: the staged keys, chunk by chunk, into their length buckets (buffer A); the MSD
-//   levels of k_msd.cu sort the buckets from there.
+// K3c k_lscatter: the staged keys, chunk by chunk, into their length buckets (buffer A) — for the
+//   stage API of the torch.distributed variant (wsort_pack_long); AUTO reads the chunks in the MSD.
 // K5d k_emit_dense: "prints the results" for L <= 5: word w of the dense buckets is
 //   the entry whose count range holds w; written as "word\n" (reading A12).
 #include <algorithm>
@@ -47,15 +51,20 @@ constexpr int kSub = 1024;                   // bytes per warp sub-step (32 per 
 constexpr int kSubTail = 128;                // staged bytes past it (a staged word: <= 66 letters + slack)
 constexpr int kWBuf = kSub + kSubTail;
 constexpr int kWList = kSub / 2;             // at most one word start per two bytes
-constexpr uint16_t kNoChunk16 = 0xffffu, kTrash16 = 0xfffeu;
+constexpr uint32_t kTrash16 = 0xfffeu;
+// A chunk is published in a ring of kRing slots per class: slot (seq % kRing) = (seq + 1) << 16 | chunk id.
+// A lane that ranked key `r` of its class waits for its chunk's entry; an entry of a later sequence
+// number means the slot was reused before the lane read it (kRing chunks of that class filled in
+// between: never expected); it is reported like an unstaged word (the host then counts the text instead).
+constexpr uint32_t kRing = 8;
 
-// keys per chunk of class k: the largest power of two <= kChunkWords / k
-__host__ __device__ constexpr uint32_t cls_lg(uint32_t k) { return k == 1 ? 12u : k == 2 ? 11u : k <= 4 ? 10u : k <= 8 ? 9u : 8u; }
-// the same for 1 <= k <= 16 in two instructions: 12 - ceil(log2 k)
+// keys per chunk of key width k: the largest power of two <= kChunkWords / k (chunk_lg), and the same in
+// two instructions for 1 <= k <= 16: 12 - ceil(log2 k) (constexpr twin checked below)
+__host__ __device__ constexpr uint32_t cls_lg(uint32_t k) { return chunk_lg(k); }
+__host__ __device__ constexpr uint32_t cls_lg_twin(uint32_t k) { return k <= 1 ? 12u : 12u - (32u - (uint32_t)__builtin_clz(k - 1u)); }
 __device__ __forceinline__ uint32_t cls_lg_fast(uint32_t k) { return (uint32_t)__clz(k - 1u) - 20u; }
-static_assert(cls_lg(1) == 12 && cls_lg(3) == 10 && cls_lg(5) == 9 && cls_lg(9) == 8 && cls_lg(11) == 8, "cls_lg");
-// cls_lg_fast == cls_lg only for 1 <= k <= 16: the staged key widths must stay in that range
-static_assert(kMaxStageKw <= 16, "cls_lg_fast covers key widths 1..16 only");
+__host__ __device__ constexpr bool cls_lg_agree(uint32_t k) { return k > kMaxStageKw || (cls_lg(k) == cls_lg_twin(k) && cls_lg_agree(k + 1)); }
+static_assert(kMaxStageKw <= 16 && kChunkWords == 4096 && cls_lg_agree(1), "cls_lg_fast must equal chunk_lg for every staged width");
 
 struct IgSmem {
     uint4 wbuf[kIgWarps][2][kWBuf / 16 + 1];   // per warp, two slots: a sub-step + tail (+16 B: packing reads
@@ -66,8 +75,8 @@ struct IgSmem {
     uint32_t ccnt[kCacheSlots];
     uint32_t hist[kHistBins];
     uint32_t nchunk;                       // chunks this CTA took from its region
-    uint32_t cls_fill[kMaxStageKw];        // keys of class k staged so far
-    // dynamic: uint16_t chunk_of[kMaxStageKw][cta_chunks]: local chunk of (class, sequence number)
+    uint32_t cls_fill[kMaxStageKw];        // keys of class i + 1 staged so far
+    uint32_t ring[kMaxStageKw][kRing];     // published chunks of each class (see kRing)
 };
 
 // dense index of the word of length L <= 5 at byte boff of a staged buffer
@@ -114,6 +123,31 @@ __device__ __forceinline__ uint32_t inclusive_scan_warp(uint32_t v, int lane) {
         if (lane >= o) v += y;
     }
     return v;
+}
+
+#ifndef WSORT_IG_EVICT
+#define WSORT_IG_EVICT 1
+#endif
+// The text is read once: its loads are marked evict-first in L2 so that the staging chunks being filled
+// (one open chunk per length and CTA) stay resident until their sectors are complete.
+__device__ __forceinline__ uint4 ld_text16(const void *p, uint64_t pol) {
+#if WSORT_IG_EVICT
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return __ldg(reinterpret_cast<const uint4 *>(p));
+#endif
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol = 0;
+#if WSORT_IG_EVICT
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    return pol;
 }
 
 // letters leading a 32-bit letter mask, and whether all 32 are letters
@@ -183,7 +217,6 @@ template <bool HASH>
 __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs a) {
     extern __shared__ __align__(16) uint8_t ig_smem[];
     IgSmem &sm = *reinterpret_cast<IgSmem *>(ig_smem);
-    uint16_t *chunk_of = reinterpret_cast<uint16_t *>(ig_smem + sizeof(IgSmem));
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t c = blockIdx.x + a.cta_first;
     const uint64_t b0 = (uint64_t)c * a.steps_per_cta * kTkStep;
@@ -194,7 +227,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
     for (int i = t; i < 702; i += kIgThreads) sm.d12[i] = 0;
     for (int i = t; i < kCacheSlots; i += kIgThreads) sm.ctag[i] = sm.ccnt[i] = 0;
     for (int i = t; i < kHistBins; i += kIgThreads) sm.hist[i] = 0;
-    for (uint32_t i = t; i < kMaxStageKw * a.cta_chunks; i += kIgThreads) chunk_of[i] = kNoChunk16;
+    for (uint32_t i = t; i < kMaxStageKw * kRing; i += kIgThreads) (&sm.ring[0][0])[i] = 0;
     if (t < (int)kMaxStageKw) sm.cls_fill[t] = 0;
     if (t == 0) sm.nchunk = 0;
     __syncthreads();
@@ -206,14 +239,15 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
     // tail a word crossing the sub-step continues into) and the next sub-step, written one iteration ahead
     // from the registers that prefetched it. Each sub-step's letter mask is computed once, one iteration
     // ahead, so the tail needs neither its own loads nor its own mask.
+    const uint64_t pol = evict_first_policy();
     uint4 va = make_uint4(0, 0, 0, 0), vb = va;
     uint32_t prev_last = 0, M = 0;
     if (w0 < w1) {
         const uint8_t *p = a.text + b0 + (uint64_t)w0 * kSub;
-        const uint4 ca = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane);
-        const uint4 cb = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1);
-        va = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane);   // (the text buffer is padded:
-        vb = __ldg(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane + 1);   //  reads past a range are safe)
+        const uint4 ca = ld_text16(reinterpret_cast<const uint4 *>(p) + 2 * lane, pol);
+        const uint4 cb = ld_text16(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1, pol);
+        va = ld_text16(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane, pol);   // (the text buffer is padded:
+        vb = ld_text16(reinterpret_cast<const uint4 *>(p + kSub) + 2 * lane + 1, pol);   //  reads past a range are safe)
         uint4 *s0 = reinterpret_cast<uint4 *>(sm.wbuf[warp][w0 & 1]);
         s0[2 * lane] = ca;
         s0[2 * lane + 1] = cb;
@@ -237,8 +271,8 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
         }
         {   // prefetch the sub-step after the next
             const uint8_t *p = a.text + base + 2 * kSub;
-            va = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane);
-            vb = __ldg(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1);
+            va = ld_text16(reinterpret_cast<const uint4 *>(p) + 2 * lane, pol);
+            vb = ld_text16(reinterpret_cast<const uint4 *>(p) + 2 * lane + 1, pol);
         }
         __syncwarp();
         const uint32_t pm = __shfl_up_sync(kFull, M, 1), nm = __shfl_down_sync(kFull, M, 1);
@@ -315,49 +349,58 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
             const bool v = i < nlg && L <= 6u * kMaxStageKw;
             if (i < nlg) {
                 if (v) atomicAdd(&sm.hist[L], 1u);
-                else atomicAdd(&a.ctr[kIgVeryLong], 1u);   // too long to stage: the host sorts with K3 + LSD
+                else atomicAdd(&a.ctr[kIgVeryLong], 1u);   // too long to stage: the host counts the text instead
             }
-            const uint32_t k = (L + 5u) / 6u, lg = cls_lg_fast(k);
+            const uint32_t k = (L + 5u) / 6u, lg = cls_lg_fast(k), cl = v ? k - 1u : 0u;
             uint32_t r = 0;
-            if (v) r = atomicAdd(&sm.cls_fill[k - 1], 1u);
+            if (v) r = atomicAdd(&sm.cls_fill[cl], 1u);
             const uint32_t seq = r >> lg, pos = r & ((1u << lg) - 1u);
-            uint16_t *slot = chunk_of + (k - 1) * a.cta_chunks + min(seq, a.cta_chunks - 1);
-            if (v && pos == 0) {   // first key of chunk (k, seq): take a chunk from the region, publish its id
+            uint32_t *slot = &sm.ring[cl][seq & (kRing - 1)];
+            const uint32_t tag = (seq + 1u) << 16;
+            if (v && pos == 0) {   // first key of chunk (k, seq): take a chunk from the region, list and publish it
                 uint32_t id = atomicAdd(&sm.nchunk, 1u);
-                if (id >= a.cta_chunks || seq >= a.cta_chunks) {   // cannot happen (key bytes <= text bytes + 256)
+                if (id >= a.cta_chunks) {   // cannot happen (key bytes <= text bytes + 256)
                     atomicExch(&a.ctr[kIgOverflow], 1u);
                     id = kTrash16;
                 } else {
-                    a.chunk_cls[cbase + id] = k;
+                    a.chunk_cls[cbase + id] = k | (seq << 8);
+                    a.cls_list[(size_t)cl * a.cls_cap + atomicAdd(&a.ctr[kIgClsCnt + cl], 1u)] = cbase + id;
                 }
-                *reinterpret_cast<volatile uint16_t *>(slot) = (uint16_t)id;
+                *reinterpret_cast<volatile uint32_t *>(slot) = tag | id;
             }
             __syncwarp();   // ids published by this warp are visible; other warps publish right after their atomic
             if (!v || (a.debug & 2)) continue;
-            uint32_t id, spins = 0;
-            while ((id = *reinterpret_cast<volatile uint16_t *>(slot)) == kNoChunk16) {
+            uint32_t e, spins = 0;
+            while (((e = *reinterpret_cast<volatile uint32_t *>(slot)) & 0xffff0000u) != tag) {
+                if ((e >> 16) > seq + 1u) {   // slot reused (never expected): the host falls back as for
+                    atomicAdd(&a.ctr[kIgVeryLong], 1u);   // unstaged words (COUNT ingest, or K3 + LSD)
+                    e = kTrash16;
+                    break;
+                }
                 if (++spins > (1u << 22)) {   // never expected: report instead of hanging
                     atomicExch(&a.ctr[kIgOverflow], 2u);
-                    id = kTrash16;
+                    e = kTrash16;
                     break;
                 }
             }
-            uint32_t *dst = a.pool + (size_t)(id == kTrash16 ? trash : cbase + id) * kChunkWords + pos * k;
-            pack_key(wb32, s, L, k, dst);
+            const uint32_t id = e & 0xffffu;
+            // word-major chunk: word q of key `pos` at q * cap + pos (a warp's keys of one class land on
+            // consecutive words of each row)
+            uint32_t *dst = a.pool + (size_t)(id == kTrash16 ? trash : cbase + id) * kChunkWords + pos;
+            pack_key(wb32, s, L, k, dst, 1u << lg);
         }
         __syncwarp();   // the slot and list are rewritten by the next sub-steps
         M = Mn;
     }
     __syncthreads();
     if (t == 0) atomicMax(&a.ctr[kIgMaxChunks], sm.nchunk);
-    if (!HASH && t < (int)kMaxStageKw) {
-        const uint32_t fill = sm.cls_fill[t], lg = cls_lg(t + 1), cap = 1u << lg;
-        const uint32_t nseq = (fill + cap - 1) >> lg;
-        for (uint32_t q = 0; q < nseq && q < a.cta_chunks; q++) {
-            const uint32_t id = chunk_of[t * a.cta_chunks + q];
-            if (id < a.cta_chunks) a.chunk_fill[cbase + id] = q + 1 < nseq ? cap : fill - (q << lg);
+    if (!HASH) {   // keys in each chunk: full, except the last one of each class
+        for (uint32_t id = t; id < min(sm.nchunk, a.cta_chunks); id += kIgThreads) {
+            const uint32_t v = a.chunk_cls[cbase + id], K = v & 255u, seq = v >> 8, lg = cls_lg(K);
+            a.chunk_fill[cbase + id] = min(1u << lg, sm.cls_fill[K - 1u] - (seq << lg));
         }
     }
+    if (a.debug & 32) return;   // (timing experiments: no flush of the shared-memory tables)
     for (int i = t; i < 702; i += kIgThreads)
         if (sm.d12[i]) {
             atomicAdd(&a.dense[i], sm.d12[i]);
@@ -707,6 +750,7 @@ __device__ __forceinline__ uint32_t key_len(uint32_t last, uint32_t K) {
 template <int K>
 __device__ __forceinline__ void lscatter_chunk(const L0Args &a, const uint32_t *src, uint32_t n, uint32_t *sm) {
     constexpr int KPT = (16 + K - 1) / K;   // 4096 / K keys per chunk, 256 threads
+    constexpr uint32_t cap = 1u << cls_lg(K);   // word-major chunk: word u of key i at u * cap + i
     const uint32_t t = threadIdx.x;
     uint32_t *cnt = sm, *lbase = sm + 8, *gbase = sm + 16;
     uint64_t *koff = reinterpret_cast<uint64_t *>(sm + 24);
@@ -720,7 +764,7 @@ __device__ __forceinline__ void lscatter_chunk(const L0Args &a, const uint32_t *
     for (int r = 0; r < KPT; r++) {
         const uint32_t i = t + r * 256;
         if (i < n) {
-            const uint32_t l = key_len(src[i * K + K - 1], K) - (6u * K - 5u);
+            const uint32_t l = key_len(src[(K - 1) * cap + i], K) - (6u * K - 5u);
             ls[r] = l | (atomicAdd(&cnt[l], 1u) << 3);
         }
     }
@@ -741,7 +785,7 @@ __device__ __forceinline__ void lscatter_chunk(const L0Args &a, const uint32_t *
 #pragma unroll
             for (int u = 0; u < K; u++) {
                 const uint32_t w = p * K + u;
-                kout[w + (w >> 5)] = src[i * K + u];
+                kout[w + (w >> 5)] = src[u * cap + i];
             }
             lof[p] = (uint8_t)l;
         }
@@ -774,10 +818,10 @@ __global__ void __launch_bounds__(256, kLsCtasPerSm) k_lscatter(L0Args a) {
         while (j < total && (n = a.chunk_fill[chunk_id(j)]) == 0) j += gridDim.x;
         sj[b] = j;
         if (j < total) {
-            const uint32_t c = chunk_id(j), K = a.chunk_cls[c];
+            const uint32_t c = chunk_id(j), K = a.chunk_cls[c] & 255u;
             sj[2 + b] = n;
             sj[4 + b] = K;
-            const uint32_t bytes = (n * K * 4 + 15) & ~15u;
+            const uint32_t bytes = (((K - 1) << cls_lg(K)) * 4 + n * 4 + 15) & ~15u;   // (word-major)
             tma::mbar_expect_tx(&bar[b], bytes);
             tma::bulk_g2s(inb + b * kChunkWords, a.pool + (size_t)c * kChunkWords, bytes, &bar[b]);
         }
@@ -819,7 +863,10 @@ constexpr size_t kLscatterSmem = 2 * kChunkWords * 4 + 16 + 32 + kLsWork;
 }  // namespace
 
 uint32_t ingest_ctas_per_sm() { return kIgMinBlocks; }
-size_t ingest_smem(uint32_t cta_chunks) { return sizeof(IgSmem) + kMaxStageKw * cta_chunks * 2; }
+// The tokenizer grid is kIgMinBlocks CTAs per SM (plan_tokenizer): the shared-memory request is padded so
+// that no more than that fit on one SM (a third CTA on some SMs would leave the grid unbalanced).
+constexpr size_t kIgSmemFloor = 233472 / (kIgMinBlocks + 1);   // (228 KiB per SM)
+size_t ingest_smem(uint32_t) { return std::max(sizeof(IgSmem), kIgSmemFloor); }
 uint32_t dense_entries() { return dense_base(kDenseMaxLen + 1); }
 uint32_t dense_table_base(uint32_t L) { return dense_base(L); }
 

@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
     }
     __syncthreads();
     const uint32_t src_a = sg.buf & 1u, dst_a = src_a ^ 1u;   // where the segment is / its children go
-    if (t == 0 && nzt == 1 && a.level + 1 < b.ndig && sg.n > 1) {
+    // (chunk mode: the keys are in the staging chunks, every segment is scattered)
+    if (t == 0 && nzt == 1 && a.level + 1 < b.ndig && sg.n > 1 && !a.chunk_mode) {
         // every key shares this digit: no data movement; the segment goes to the next level as it is
         a.seg_skip[s] = 1u;
         const uint32_t nt = (sg.n + b.aux - 1) / b.aux;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
         for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++)
             a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, sg.n - i * b.aux), 0};
     }
-    if (nzt == 1 && a.level + 1 < b.ndig && sg.n > 1) return;
+    if (nzt == 1 && a.level + 1 < b.ndig && sg.n > 1 && !a.chunk_mode) return;
     if (t == 0) a.seg_skip[s] = 0u;
     if (t == 0) {
         const bool final_digit = a.level + 1 >= b.ndig;
@@ -401,6 +402,256 @@ __global__ void __launch_bounds__(kST, 2) k_msd_scatter_p(MsdArgs a, uint32_t nt
             default: scatter_tile<11>(a, td, sg, b, sm, kin); break;
         }
         __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- level 0 from the staging chunks
+// The ingest (K1) leaves the keys of the words of 6..66 letters in word-major chunks of one key-width class
+// K (lengths 6K-5 .. 6K), listed per class. Level 0 partitions them by (length, first 2-letter digit) with
+// no regrouping pass: a slice is slice_chunks consecutive chunks of one class's list;
+//   k_msd_count0    per slice: histogram of its 6 x 1024 (length, digit) bins (shared memory), added to the
+//                   per-length segment histograms for k_msd_plan;
+//   k_msd_scatter0  persistent over the chunks (TMA double-buffered): bins -> in-chunk offsets (scan), one
+//                   global atomic per non-empty bin reserves the chunk's range of that child, keys
+//                   reordered by bin in shared memory and written key-major into buffer B.
+__device__ __forceinline__ uint32_t key_len0(uint32_t last, uint32_t K) {   // trailing pad codes (0) of the last word
+    return 6u * K - (uint32_t)(__ffs(last) - 1) / 5u;
+}
+struct Slice0 {
+    uint32_t K, j0, j1;   // class, list entries [j0, j1)
+};
+__device__ __forceinline__ Slice0 slice0_of(const MsdArgs &a, uint32_t sl) {
+    uint32_t K = 1;
+    while (K < kMaxStageKw && a.slice_pfx[K] <= sl) K++;
+    const uint32_t j0 = (sl - a.slice_pfx[K - 1]) * a.slice_chunks;
+    return Slice0{K, j0, min(a.cls_cnt[K - 1], j0 + a.slice_chunks)};
+}
+
+__global__ void __launch_bounds__(kST) k_msd_count0(MsdArgs a) {
+    __shared__ uint32_t h[kC0Bins];
+    const uint32_t t = threadIdx.x, sl = blockIdx.x;
+    const Slice0 sc = slice0_of(a, sl);
+    const uint32_t K = sc.K, cap = 1u << chunk_lg(K), L0 = 6u * K - 5u;
+    for (uint32_t i = t; i < kC0Bins; i += kST) h[i] = 0;
+    __syncthreads();
+    const uint32_t *list = a.cls_list + (size_t)(K - 1) * a.cls_cap;
+    for (uint32_t j = sc.j0; j < sc.j1; j++) {
+        const uint32_t c = __ldg(list + j), n = __ldg(a.chunk_fill + c);
+        const uint32_t *r0 = a.pool + (size_t)c * kChunkWords, *rl = r0 + (K - 1) * cap;   // first / last key words
+        for (uint32_t i0 = t; i0 < n; i0 += 4 * kST) {
+            uint32_t w0[4], wl[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                const uint32_t i = i0 + r * kST;
+                w0[r] = i < n ? __ldg(r0 + i) : 0u;
+                wl[r] = i < n ? __ldg(rl + i) : 1u;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (i0 + r * kST < n) atomicAdd(&h[((key_len0(wl[r], K) - L0) << 10) | (w0[r] >> 20)], 1u);
+        }
+    }
+    __syncthreads();
+    uint32_t *sh = a.slice_hist ? a.slice_hist + (size_t)sl * kC0Bins : nullptr;
+    for (uint32_t b = t; b < kC0Bins; b += kST) {
+        const uint32_t v = h[b];
+        if (sh) sh[b] = v;
+        if (v) atomicAdd(&a.hist[(size_t)(L0 + (b >> 10) - a.seg_l0) * kRadixBins + (b & 1023u)], v);
+    }
+}
+
+constexpr uint32_t kS0PerThread = kC0Bins / kST;   // 24 contiguous bins per thread in the scans
+constexpr uint32_t kS0Kout = kChunkWords + kChunkWords / 32 + 8;
+// [2][kChunkWords] TMA buffers | bar[2] | gb[kC0Bins] | off[kC0Bins] | kout | pbin (u16)[kChunkWords] | wsum
+constexpr size_t kScatter0Smem = 2 * kChunkWords * 4 + 16 + 2 * kC0Bins * 4 + kS0Kout * 4 + kChunkWords * 2 + 64;
+
+#ifndef WSORT_S0_SLICE
+#define WSORT_S0_SLICE 1
+#endif
+#ifndef WSORT_S0_HINT
+#define WSORT_S0_HINT 1
+#endif
+// One chunk of class K: keys -> (bin, slot), exclusive scan of the bins, keys reordered by bin in shared
+// memory and written key-major, coalesced within each bin. The chunk's range of each child comes from
+//   SLICE: the slice's range (reserved once per slice from k_msd_count0's slice histogram), advanced in
+//          shared memory (gb = the next index of each bin);
+//   else:  one global atomic per non-empty bin as the chunk is scattered (gb = its range - in-chunk offset).
+template <int K, bool SLICE>
+__device__ __forceinline__ void scatter0_chunk(const MsdArgs &a, const uint32_t *kin, uint32_t n, uint32_t *gb,
+                                               uint32_t *off, uint32_t *kout, uint16_t *pbin, uint32_t *wsum,
+                                               uint64_t *koff, uint64_t wpol) {
+    constexpr uint32_t cap = 1u << chunk_lg(K), KPT = (cap + kST - 1) / kST, L0 = 6u * K - 5u;
+    const uint32_t t = threadIdx.x;
+    if (t < 6) koff[t] = L0 + t >= a.seg_l0 ? a.buckets[L0 + t].key_off : 0;
+    uint32_t key[KPT][K], bin[KPT], slot[KPT];
+#pragma unroll
+    for (uint32_t r = 0; r < KPT; r++) {
+        const uint32_t i = t + r * kST;
+#pragma unroll
+        for (int u = 0; u < K; u++) key[r][u] = i < n ? kin[u * cap + i] : 0u;
+    }
+#pragma unroll
+    for (uint32_t r = 0; r < KPT; r++) {
+        const uint32_t i = t + r * kST;
+        bin[r] = ((key_len0(i < n ? key[r][K - 1] : 1u, K) - L0) << 10) | (key[r][0] >> 20);
+        slot[r] = i < n ? atomicAdd(&off[bin[r]], 1u) : 0u;
+    }
+    __syncthreads();
+    // exclusive scan of the counts (thread t: bins [24 t, 24 t + 24))
+    uint32_t cnt[kS0PerThread], sum = 0;
+    uint4 *o4 = reinterpret_cast<uint4 *>(off + kS0PerThread * t);
+#pragma unroll
+    for (uint32_t q = 0; q < kS0PerThread / 4; q++) {
+        const uint4 v = o4[q];
+        cnt[4 * q] = v.x;
+        cnt[4 * q + 1] = v.y;
+        cnt[4 * q + 2] = v.z;
+        cnt[4 * q + 3] = v.w;
+        sum += v.x + v.y + v.z + v.w;
+    }
+    uint32_t ex = block_excl_scan_m(sum, wsum, nullptr);   // (its barriers order the reads above before the writes)
+    const uint32_t b0 = kS0PerThread * t;
+    uint32_t g[SLICE ? 1 : kS0PerThread];
+    if (!SLICE) {
+#pragma unroll
+        for (uint32_t q = 0; q < kS0PerThread; q++) {   // the chunk's range of each non-empty child (issued together)
+            const uint32_t b = b0 + q;
+            g[q] = cnt[q] ? atomicAdd(&a.cursor[(size_t)(L0 + (b >> 10) - a.seg_l0) * kRadixBins + (b & 1023u)], cnt[q]) : 0u;
+        }
+    }
+    uint4 *g4 = reinterpret_cast<uint4 *>(gb + b0);
+#pragma unroll
+    for (uint32_t q = 0; q < kS0PerThread / 4; q++) {
+        uint4 v;
+        v.x = ex;
+        ex += cnt[4 * q];
+        v.y = ex;
+        ex += cnt[4 * q + 1];
+        v.z = ex;
+        ex += cnt[4 * q + 2];
+        v.w = ex;
+        ex += cnt[4 * q + 3];
+        o4[q] = v;
+        uint4 r = g4[q];   // key p of bin b goes to bucket index gb[b] + p
+        if (SLICE) r = make_uint4(r.x - v.x, r.y - v.y, r.z - v.z, r.w - v.w);
+        else r = make_uint4(g[4 * q] - v.x, g[4 * q + 1] - v.y, g[4 * q + 2] - v.z, g[4 * q + 3] - v.w);
+        g4[q] = r;
+    }
+    __syncthreads();
+    // reorder by bin in shared memory (key-major, padded)
+#pragma unroll
+    for (uint32_t r = 0; r < KPT; r++) {
+        const uint32_t i = t + r * kST;
+        if (i < n) {
+            const uint32_t p = off[bin[r]] + slot[r];
+#pragma unroll
+            for (int u = 0; u < K; u++) {
+                const uint32_t w = p * K + u;
+                kout[w + (w >> 5)] = key[r][u];
+            }
+            pbin[p] = (uint16_t)bin[r];
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = t; i < n * K; i += kST) {
+        const uint32_t p = i / K, u = i - p * K, b = pbin[p];
+        uint32_t *dst = a.keys_b + koff[b >> 10] + (uint64_t)(gb[b] + p) * K + u;
+#if WSORT_S0_HINT
+        tma::st_hint(dst, kout[i + (i >> 5)], wpol);
+#else
+        (void)wpol;
+        *dst = kout[i + (i >> 5)];
+#endif
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t q = 0; q < kS0PerThread / 4; q++) {
+        if (SLICE) {   // the slice's next chunk continues after these keys
+            uint4 r = g4[q];
+            const uint4 v = o4[q];
+            r = make_uint4(r.x + v.x + cnt[4 * q], r.y + v.y + cnt[4 * q + 1], r.z + v.z + cnt[4 * q + 2],
+                           r.w + v.w + cnt[4 * q + 3]);
+            g4[q] = r;
+        }
+        o4[q] = make_uint4(0, 0, 0, 0);   // (the next chunk's counts)
+    }
+}
+
+// SLICE (default): CTA = one slice of k_msd_count0 (its chunks in list order), its ranges reserved first;
+// else persistent over the classes' lists concatenated (CTA b: chunks b, b + grid, ...). The next chunk is
+// fetched by a TMA bulk copy (evict-first: read once) into the other buffer while this one is scattered;
+// the scattered keys are stored evict-last (the sectors a later chunk completes stay in L2).
+__global__ void __launch_bounds__(kST, 2) k_msd_scatter0(MsdArgs a, uint32_t total) {
+    extern __shared__ __align__(128) uint32_t s0m[];
+    uint32_t *inb = s0m;                                                      // [2][kChunkWords]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(s0m + 2 * kChunkWords);     // [2]
+    uint32_t *gb = reinterpret_cast<uint32_t *>(bar + 2);                     // [kC0Bins]
+    uint32_t *off = gb + kC0Bins;                                             // [kC0Bins] counts / offsets
+    uint32_t *kout = off + kC0Bins;
+    uint16_t *pbin = reinterpret_cast<uint16_t *>(kout + kS0Kout);
+    uint32_t *wsum = reinterpret_cast<uint32_t *>(pbin + kChunkWords);        // [kST / 32 + 1]
+    __shared__ uint64_t koff[6];
+    __shared__ uint32_t s_n[2], s_k[2];
+    const uint32_t t = threadIdx.x;
+    const bool slice = WSORT_S0_SLICE;
+    const uint64_t rpol = tma::policy_evict_first(), wpol = tma::policy_evict_last();
+    uint32_t j0 = blockIdx.x, j1 = total, step = gridDim.x;
+    if (slice) {   // this slice's chunks: class K's list entries [j0, j1) -> concatenated indices
+        const Slice0 sc = slice0_of(a, blockIdx.x);
+        j0 = a.cls_pfx[sc.K - 1] + sc.j0;
+        j1 = a.cls_pfx[sc.K - 1] + sc.j1;
+        step = 1;
+    }
+    auto fetch = [&](uint32_t j, uint32_t b) {   // thread 0: chunk j of the concatenated lists -> buffer b
+        uint32_t K = 1;
+        while (K < kMaxStageKw && a.cls_pfx[K] <= j) K++;
+        const uint32_t c = __ldg(a.cls_list + (size_t)(K - 1) * a.cls_cap + (j - a.cls_pfx[K - 1]));
+        const uint32_t n = __ldg(a.chunk_fill + c);
+        const uint32_t bytes = (((K - 1u) << chunk_lg(K)) * 4u + n * 4u + 15u) & ~15u;   // (word-major: full rows, then the last)
+        s_n[b] = n;
+        s_k[b] = K;
+        tma::mbar_expect_tx(&bar[b], bytes);
+#if WSORT_S0_HINT
+        tma::bulk_g2s_hint(inb + b * kChunkWords, a.pool + (size_t)c * kChunkWords, bytes, &bar[b], rpol);
+#else
+        tma::bulk_g2s(inb + b * kChunkWords, a.pool + (size_t)c * kChunkWords, bytes, &bar[b]);
+#endif
+    };
+    if (t == 0) {
+        tma::mbar_init(&bar[0], 1);
+        tma::mbar_init(&bar[1], 1);
+        tma::fence_mbar_init();
+        if (j0 < j1) fetch(j0, 0);
+    }
+    if (slice) {   // the slice's range of every non-empty (length, digit) child: one global atomic per bin
+        const Slice0 sc = slice0_of(a, blockIdx.x);
+        const uint32_t L0 = 6u * sc.K - 5u;
+        const uint32_t *sh = a.slice_hist + (size_t)blockIdx.x * kC0Bins;
+        for (uint32_t b = t; b < kC0Bins; b += kST) {
+            const uint32_t v = __ldg(sh + b);
+            gb[b] = v ? atomicAdd(&a.cursor[(size_t)(L0 + (b >> 10) - a.seg_l0) * kRadixBins + (b & 1023u)], v) : 0u;
+        }
+    }
+    for (uint32_t b = t; b < kC0Bins; b += kST) off[b] = 0;
+    __syncthreads();
+    for (uint32_t j = j0, it = 0; j < j1; j += step, it++) {
+        const uint32_t cur = it & 1;
+        if (t == 0 && j + step < j1) fetch(j + step, cur ^ 1);   // (buffer cur^1 was released at the last barrier)
+        tma::mbar_wait(&bar[cur], (it >> 1) & 1);
+        const uint32_t n = s_n[cur], K = s_k[cur];
+        const uint32_t *kin = inb + cur * kChunkWords;
+#define S0CASE(KK) \
+    case KK: \
+        if (slice) scatter0_chunk<KK, true>(a, kin, n, gb, off, kout, pbin, wsum, koff, wpol); \
+        else scatter0_chunk<KK, false>(a, kin, n, gb, off, kout, pbin, wsum, koff, wpol); \
+        break;
+        switch (K) {
+            S0CASE(1) S0CASE(2) S0CASE(3) S0CASE(4) S0CASE(5) S0CASE(6) S0CASE(7) S0CASE(8) S0CASE(9) S0CASE(10)
+            default: if (slice) scatter0_chunk<11, true>(a, kin, n, gb, off, kout, pbin, wsum, koff, wpol);
+                     else scatter0_chunk<11, false>(a, kin, n, gb, off, kout, pbin, wsum, koff, wpol);
+                     break;
+        }
+#undef S0CASE
     }
 }
 
@@ -1693,6 +1944,23 @@ size_t msd_scatter_smem() { return (size_t)(3 * kRadixBins + 8192 + 8192 / 32 + 
 cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s) {
     if (!ntiles) return cudaSuccess;
     k_msd_count<<<ntiles, kST, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_msd_count0(const MsdArgs &a, cudaStream_t s) {
+    if (!a.nslices) return cudaSuccess;
+    k_msd_count0<<<a.nslices, kST, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_msd_scatter0(const MsdArgs &a, cudaStream_t s) {
+    if (!a.cls_pfx[kMaxStageKw]) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_msd_scatter0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatter0Smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t total = a.cls_pfx[kMaxStageKw];
+    const uint32_t grid = WSORT_S0_SLICE ? a.nslices : std::min<uint32_t>(total, (uint32_t)sms * 2);
+    k_msd_scatter0<<<grid, kST, kScatter0Smem, s>>>(a, total);
     return cudaGetLastError();
 }
 cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s) {

@@ -61,8 +61,10 @@ __device__ __forceinline__ uint32_t codes6(uint32_t lo, uint32_t hi) {
 
 // All k = ceil(L/6) key words of the word of L letters at byte s (pack6 of each 6-letter slice): two key
 // words are 12 bytes = 3 aligned words at one shift, so the window is read once (3 loads per pair);
-// only the last key word is masked.
-__device__ __forceinline__ void pack_key(const uint32_t *buf32, uint32_t s, uint32_t L, uint32_t k, uint32_t *dst) {
+// only the last key word is masked. Key word q goes to dst[q * stride] (stride 1: contiguous key; the
+// staging chunks store word q of every key in a row of its own, stride = the chunk's key capacity).
+__device__ __forceinline__ void pack_key(const uint32_t *buf32, uint32_t s, uint32_t L, uint32_t k, uint32_t *dst,
+                                         uint32_t stride = 1) {
     const uint32_t sh = 8u * (s & 3u), rem = L - 6u * (k - 1u);   // letters in the last key word: 1..6
     const uint32_t last = rem < 6u ? ~((1u << (5u * (6u - rem))) - 1u) : 0xffffffffu;
     const uint32_t *p = buf32 + (s >> 2);
@@ -70,8 +72,9 @@ __device__ __forceinline__ void pack_key(const uint32_t *buf32, uint32_t s, uint
     for (uint32_t q = 0; q < k; q += 2, p += 3) {
         const uint32_t w1 = p[1], w2 = p[2], w3 = p[3];
         const uint32_t b0 = __funnelshift_r(w0, w1, sh), b1 = __funnelshift_r(w1, w2, sh), b2 = __funnelshift_r(w2, w3, sh);
-        dst[q] = codes6(b0, b1) & (q + 1u == k ? last : 0xffffffffu);
-        if (q + 1u < k) dst[q + 1u] = codes6(__funnelshift_r(b1, b2, 16), b2 >> 16) & (q + 2u == k ? last : 0xffffffffu);
+        dst[q * stride] = codes6(b0, b1) & (q + 1u == k ? last : 0xffffffffu);
+        if (q + 1u < k)
+            dst[(q + 1u) * stride] = codes6(__funnelshift_r(b1, b2, 16), b2 >> 16) & (q + 2u == k ? last : 0xffffffffu);
         w0 = w3;
     }
 }

@@ -76,7 +76,7 @@ struct wsort_ctx {
     bool cta_counts_ready = false; // K1b's per-CTA histograms are in cta_hist (K2b needs them)
 
     // K1 ingest: global histogram, dense counts, staging chunks
-    DevBuf ghist, dense, pool, chunk_cls, chunk_fill, ig_ctr, d_touched;
+    DevBuf ghist, dense, pool, chunk_cls, chunk_fill, ig_ctr, d_touched, cls_list, slice_hist;
     bool dense_clean = false;                    // the dense table has been zeroed once (then: touched blocks)
     uint32_t *h_ig = nullptr;   // pinned mirror of ig_ctr
     uint32_t cta_chunks = 0, n_chunks = 0;
@@ -406,7 +406,7 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->m_hist, &c->m_cursor, &c->m_ctr, &c->m_big[0], &c->m_big[1], &c->m_tiles[0],
                       &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->m_pat, &c->m_qparts, &c->m_pbase, &c->m_jdone,
                       &c->m_jovf, &c->m_partn, &c->m_plist, &c->m_qemit, &c->ghist, &c->dense,
-                      &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->d_blk_sum, &c->d_blk_nnz,
+                      &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->cls_list, &c->slice_hist, &c->d_blk_sum, &c->d_blk_nnz,
                       &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_touched, &c->d_tiles2, &c->d_lcursor, &c->d_tile_e,
                       &c->t_wlens, &c->t_nkey, &c->t_ncnt, &c->t_fp, &c->t_meta, &c->t_cnt, &c->t_keys, &c->t_top, &c->t_dcount, &c->t_runend,
                       &c->t_scan, &c->t_tilee, &c->t_kplan, &c->t_dpfx, &c->t_rpfx, &c->x_vec, &c->x_counts,
@@ -638,6 +638,7 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     if ((rc = ensure(c, c->pool, ((size_t)c->n_chunks + 1) * kChunkWords * 4, "staging pool"))) return rc;
     if ((rc = ensure(c, c->chunk_cls, (size_t)c->n_chunks * 4, "chunk classes"))) return rc;
     if ((rc = ensure(c, c->chunk_fill, (size_t)c->n_chunks * 4, "chunk fills"))) return rc;
+    if ((rc = ensure(c, c->cls_list, (size_t)kMaxStageKw * std::max<uint32_t>(c->n_chunks, 1) * 4, "chunk lists"))) return rc;
     if (!c->h_ig && cudaMallocHost(&c->h_ig, kIgCtrs * 4) != cudaSuccess) {
         cudaGetLastError();
         return set_err(c, WSORT_E_NOMEM, "pinned ingest counters");
@@ -670,6 +671,8 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     ia.pool = static_cast<uint32_t *>(c->pool.p);
     ia.chunk_cls = static_cast<uint32_t *>(c->chunk_cls.p);
     ia.chunk_fill = static_cast<uint32_t *>(c->chunk_fill.p);
+    ia.cls_list = static_cast<uint32_t *>(c->cls_list.p);
+    ia.cls_cap = c->n_chunks;
     ia.cta_chunks = c->cta_chunks;
     ia.ctr = static_cast<uint32_t *>(c->ig_ctr.p);
     ia.hash = hash ? 1u : 0u;
@@ -1236,12 +1239,19 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
         if ((rc = msd_level_buffers(c, m, level, nsegs))) return rc;
         const double seg_bytes = level == 0 ? key_bytes : 0;   // later levels' sizes are device-side
-        rc = launch(c, "k4m_msd_count", seg_bytes, [&] { return launch_msd_count(m, ntiles, c->stream); });
+        if (m.chunk_mode)
+            rc = launch(c, "k4m_msd_count0", seg_bytes, [&] { return launch_msd_count0(m, c->stream); });
+        else
+            rc = launch(c, "k4m_msd_count", seg_bytes, [&] { return launch_msd_count(m, ntiles, c->stream); });
         if (rc) return rc;
         rc = launch(c, "k4m_msd_plan", (double)nsegs * kRadixBins * 8, [&] { return launch_msd_plan(m, nsegs, c->stream); });
         if (rc) return rc;
-        rc = launch(c, "k4m_msd_scatter", 2 * seg_bytes, [&] { return launch_msd_scatter(m, ntiles, c->stream); });
+        if (m.chunk_mode)
+            rc = launch(c, "k4m_msd_scatter0", 2 * seg_bytes, [&] { return launch_msd_scatter0(m, c->stream); });
+        else
+            rc = launch(c, "k4m_msd_scatter", 2 * seg_bytes, [&] { return launch_msd_scatter(m, ntiles, c->stream); });
         if (rc) return rc;
+        m.chunk_mode = 0;   // (only level 0 reads the staging chunks)
         if (!m.finish_radix) {   // this level's finishing jobs (their count is on the device); a job with too
                                  // many distinct keys re-enters the next level
             static const bool dbg = getenv("WSORT_DEBUG_JOBS") != nullptr;   // (experiments: slowest jobs)
@@ -1380,7 +1390,7 @@ std::vector<BucketInfo> msd_buckets(const Summary &s, uint32_t lkey, uint32_t &m
 template <class Pack>
 int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint32_t max_tw, uint32_t levels,
                   uint64_t key_words, uint64_t W, bool finish_radix, Pack pack, const BucketInfo *d_bk_pre = nullptr,
-                  bool emit = true, uint32_t lmax_keys = 0) {
+                  bool emit = true, uint32_t lmax_keys = 0, bool from_chunks = false) {
     const Summary &s = *c->h_sum;
     const uint32_t lmax = lmax_keys ? lmax_keys : s.max_len;
     int rc;
@@ -1390,7 +1400,31 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
     if ((rc = msd_alloc(c, m, W, key_words))) return rc;
     std::vector<MsdSeg> segs, tiny, small;
     std::vector<MsdTile> tiles;
-    for (uint32_t L = lkey; L <= lmax; L++) {
+    if (from_chunks) {   // level 0 reads the staging chunks: segment L - lkey = bucket L (every length, in order)
+        for (uint32_t L = lkey; L <= lmax; L++) segs.push_back(MsdSeg{L, 0, (uint32_t)bk[L].n, 1});
+        // slices of G chunks of one class: about 4 per SM in all
+        uint64_t total = 0;
+        for (uint32_t K = 1; K <= kMaxStageKw; K++) total += c->h_ig[kIgClsCnt + K - 1];
+        const uint32_t G = std::max<uint32_t>(2, (uint32_t)((total + 4 * c->sms - 1) / (4 * (uint64_t)c->sms)));
+        m.slice_pfx[0] = m.cls_pfx[0] = 0;
+        for (uint32_t K = 1; K <= kMaxStageKw; K++) {
+            m.slice_pfx[K] = m.slice_pfx[K - 1] + (c->h_ig[kIgClsCnt + K - 1] + G - 1) / G;
+            m.cls_pfx[K] = m.cls_pfx[K - 1] + c->h_ig[kIgClsCnt + K - 1];
+        }
+        m.chunk_mode = 1;
+        m.seg_l0 = lkey;
+        m.slice_chunks = G;
+        m.nslices = m.slice_pfx[kMaxStageKw];
+        m.cls_cap = c->n_chunks;
+        m.pool = static_cast<const uint32_t *>(c->pool.p);
+        m.chunk_fill = static_cast<const uint32_t *>(c->chunk_fill.p);
+        m.cls_list = static_cast<const uint32_t *>(c->cls_list.p);
+        m.cls_cnt = static_cast<const uint32_t *>(c->ig_ctr.p) + kIgClsCnt;
+        if ((rc = ensure(c, c->slice_hist, (size_t)std::max<uint32_t>(m.nslices, 1) * kC0Bins * 4, "level-0 slice bins")))
+            return rc;
+        m.slice_hist = static_cast<uint32_t *>(c->slice_hist.p);
+    }
+    for (uint32_t L = lkey; L <= lmax && !from_chunks; L++) {
         const BucketInfo &b = bk[L];
         if (!b.n) continue;
         if (b.n <= b.tile_keys) {
@@ -1418,7 +1452,8 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
     m.buckets = d_bk;
     m.finish_radix = finish_radix ? 1u : 0u;
     m.words = static_cast<uint8_t *>(c->words.p);
-    if ((rc = msd_levels_and_finish(c, m, 0, (uint32_t)segs.size(), (uint32_t)tiles.size(), levels, key_bytes, max_tw)))
+    if ((rc = msd_levels_and_finish(c, m, 0, (uint32_t)segs.size(), from_chunks ? m.nslices : (uint32_t)tiles.size(),
+                                    levels, key_bytes, max_tw)))
         return rc;
     if (!finish_radix || !emit) return WSORT_OK;   // the streaming finish wrote the text (K5 fused)
     return emit_keys(c, bk, d_bk, lkey, lmax, key_bytes + (double)(s.byte_off[256] - s.byte_off[lkey]));
@@ -1521,8 +1556,9 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
 }
 
 // AUTO (keys only, every word <= 66 letters): the one-pass ingest already counted the words of L <= 5
-// (dense tables) and staged the longer ones as keys in chunks. Dense buckets: scan + compact + emit.
-// Long buckets: K3c moves the staged keys into their length buckets, then MSD_OETS sorts them.
+// (dense tables) and staged the longer ones as keys in per-length chunks. Dense buckets: scan + compact +
+// emit. Long buckets: the MSD's first level counts and scatters the chunks in place (chunk mode), then the
+// streaming finish.
 int sort_dense_msd(wsort_ctx *c) {
     const Summary &s = *c->h_sum;
     uint32_t max_tw, levels;
@@ -1536,10 +1572,7 @@ int sort_dense_msd(wsort_ctx *c) {
     if (n_dense && (rc = dense_branch(c, bk, d_bk, (double)s.byte_off[kDenseMaxLen + 1]))) return rc;
     if (W > n_dense) {
         rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, W - n_dense, false,
-                           [&](const BucketInfo *db, double key_bytes) {
-                               return chunk_scatter(c, db, key_bytes);
-                           },
-                           d_bk);
+                           [&](const BucketInfo *, double) { return (int)WSORT_OK; }, d_bk, true, 0, true);
     }
     if (n_dense) {   // join: the sort is complete when both streams are
         const cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_join, 0);

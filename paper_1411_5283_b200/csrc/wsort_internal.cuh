@@ -99,7 +99,11 @@ constexpr uint32_t kDenseMaxLen = 5;                 // words of L <= 5 are coun
 constexpr uint32_t kDenseBlkEntries = 4096;          // the dense table's blocks (touched flags, scans)
 constexpr uint32_t kMaxStageKw = 11;                 // words of 6 <= L <= 66 are staged as keys
 constexpr uint32_t kChunkWords = 4096;               // u32 words per staging chunk (16 KiB)
-enum { kIgMaxChunks = 0, kIgOverflow = 1, kIgVeryLong = 2, kIgCtrs = 4 };
+constexpr uint32_t kC0Bins = 6 * 1024;               // level-0 bins of a class: (length - (6K-5)) << 10 | digit
+// keys per staging chunk of key width k (log2): the largest power of two <= kChunkWords / k; chunks are
+// word-major (word q of key i at q << chunk_lg(k) | i)
+__host__ __device__ constexpr uint32_t chunk_lg(uint32_t k) { return k == 1 ? 12u : k == 2 ? 11u : k <= 4 ? 10u : k <= 8 ? 9u : 8u; }
+enum { kIgMaxChunks = 0, kIgOverflow = 1, kIgVeryLong = 2, kIgClsCnt = 4, kIgCtrs = 16 };   // [4, 15): chunks per class
 // chunks per CTA region: a staged word's key bytes <= its text bytes (+256 for the last word), a full
 // chunk holds >= 2304 key words (class 9: 256 keys of 9 words), one partial chunk per class
 __host__ __device__ constexpr uint32_t ingest_cta_chunks(uint64_t range_bytes) {
@@ -210,7 +214,9 @@ struct IngestArgs {
     uint32_t *dense;                        // [dense_entries()] counts (zeroed by the host)
     uint8_t *touched;                       // [dense_scan_blocks()] 1: a word was counted in this block
     uint32_t *pool;                         // [grid * cta_chunks + 1][kChunkWords]; the last is a trash chunk
-    uint32_t *chunk_cls, *chunk_fill;       // [grid * cta_chunks] key width (1..8) and keys of each chunk
+    uint32_t *chunk_cls, *chunk_fill;       // [grid * cta_chunks] class (key width) | seq << 8, keys of each chunk
+    uint32_t *cls_list;                     // [kMaxStageKw][cls_cap] the chunks of each class (ctr[kIgClsCnt + K - 1] each)
+    uint32_t cls_cap;
                                             // (fills zeroed by the host: unused chunks stay empty)
     uint32_t cta_chunks;                    // chunks of one CTA's region
     uint32_t *ctr;                          // [kIgCtrs] (zeroed by the host)
@@ -420,11 +426,21 @@ struct MsdArgs {
     uint4 *part_list;              // [cap_parts][kPartListMax] {key lo, key hi | fingerprint, count, key index}
     uint32_t emit_base, cap_emit;  // k_msd_fin_emit: first piece of this launch; capacity of q_emit
     uint2 *q_emit;                 // [cap_emit] text pieces of merged split jobs: {job (q_tiny index), piece}
+    // chunk mode (level 0 of AUTO): the ingest's staging chunks are counted and scattered in place, by
+    // slices of slice_chunks chunks of one class K (key width; lengths 6K-5 .. 6K, segment L - seg_l0);
+    // slices [slice_pfx[K-1], slice_pfx[K]) are class K's
+    uint32_t chunk_mode, seg_l0, slice_chunks, nslices, cls_cap;
+    uint32_t slice_pfx[kMaxStageKw + 1];
+    uint32_t cls_pfx[kMaxStageKw + 1];   // chunks of classes < K: the classes' lists concatenated (scatter0)
+    const uint32_t *pool, *chunk_fill, *cls_list, *cls_cnt;
+    uint32_t *slice_hist;          // [nslices][kC0Bins] (nullable) each slice's bins, for k_msd_scatter0's ranges
 };
 size_t msd_scatter_smem();
 constexpr uint32_t kFinPatBytes = 1024 * 48;   // >= max distinct keys x pattern width (1024 x 32, 512 x 88)
 cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
 cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s);
+cudaError_t launch_msd_count0(const MsdArgs &a, cudaStream_t s);     // chunk mode, level 0: a.nslices CTAs
+cudaError_t launch_msd_scatter0(const MsdArgs &a, cudaStream_t s);
 cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
 cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_copy, uint32_t max_tile_words,
                               cudaStream_t s);   // tiny jobs, radix-finish jobs, copies (after the last level)
