@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--algo", default="auto")
     ap.add_argument("--impl", default="wsort", choices=["wsort", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=9)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-sample-mb", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -652,6 +652,7 @@ __global__ void __launch_bounds__(kST, 2) k_msd_scatter0(MsdArgs a, uint32_t tot
                      break;
         }
 #undef S0CASE
+        __syncthreads();   // every bin's count cleared (and its next index advanced) before the next chunk's atomics
     }
 }
 
@@ -1180,8 +1181,9 @@ __device__ __forceinline__ uint32_t run_of(const uint32_t *ends, uint32_t nd, ui
 // [ends[r-1], ends[r]). Its text `letters\n` is laid out repeated in R[r] (W bytes, W >= L+1+16), so
 // the 16 output bytes starting at phase f of the pattern are R[r][f .. f+16). Aligned 16-byte chunks
 // of the job's byte range are written straight to global memory (one warp takes a contiguous range of
-// chunks, so each lane's run index only moves forward); a chunk that crosses a run boundary, and the
-// unaligned head / tail bytes, are assembled byte by byte.
+// chunks, so each lane's run index only moves forward); a chunk that crosses run boundaries merges the
+// windows of each run's pattern (the next run's word starts at the boundary: its window begins at phase
+// -boundary mod L+1) with byte masks; the unaligned head / tail bytes are assembled byte by byte.
 __device__ __forceinline__ uint32_t div_by(uint32_t n, uint32_t d, uint32_t m) {   // n / d, m = 2^32/d + 1
     uint32_t q = __umulhi(n, m);
     if ((q + 1) * d <= n) q++;
@@ -1223,31 +1225,37 @@ __device__ __forceinline__ void emit_runs_text(const MsdArgs &a, const BucketInf
             while (ends[r] <= w) r++;
         }
         const uint32_t wl = div_by(rel + 15, L1, m);
+        // 16 bytes of run r's repeated pattern from phase f
         uint32_t v[4];
-        if (wl < ends[r]) {   // inside one run: a window of its repeated pattern
-            const uint8_t *p = R + r * W + f;
+        auto window = [&](uint32_t run, uint32_t ph, uint32_t (&o)[4]) {
+            const uint8_t *p = R + run * W + ph;
             const uint32_t al = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3u);
             const uint32_t *p4 = reinterpret_cast<const uint32_t *>(p - al);
             const uint32_t x0 = p4[0], x1 = p4[1], x2 = p4[2], x3 = p4[3], x4 = p4[4];
-            v[0] = __funnelshift_r(x0, x1, 8 * al);
-            v[1] = __funnelshift_r(x1, x2, 8 * al);
-            v[2] = __funnelshift_r(x2, x3, 8 * al);
-            v[3] = __funnelshift_r(x3, x4, 8 * al);
-        } else {   // crosses a run boundary: byte by byte
-            uint32_t rr = r, ww = w, ff = f;
+            o[0] = __funnelshift_r(x0, x1, 8 * al);
+            o[1] = __funnelshift_r(x1, x2, 8 * al);
+            o[2] = __funnelshift_r(x2, x3, 8 * al);
+            o[3] = __funnelshift_r(x3, x4, 8 * al);
+        };
+        window(r, f, v);
+        if (wl >= ends[r]) {   // crosses run boundaries: from byte nb on, the next run's window, whose
+            uint32_t rr = r;   // word starts at nb (phase -nb mod L1), merged in by byte masks
+            uint32_t nb = (ends[r] - w) * L1 - f;
+            while (nb < 16u) {
+                const uint32_t wb = ends[rr];
+                rr++;
+                uint32_t ph = nb;
+                while (ph >= L1) ph -= L1;
+                ph = ph ? L1 - ph : 0u;
+                uint32_t o[4];
+                window(rr, ph, o);
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                uint32_t acc = 0;
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    acc |= (uint32_t)R[rr * W + ff] << (8 * k);
-                    if (++ff == L1) {
-                        ff = 0;
-                        ww++;
-                        while (rr + 1 < nd && ends[rr] <= ww) rr++;
-                    }
+                for (int q = 0; q < 4; q++) {
+                    const uint32_t lo = 4u * q;
+                    const uint32_t keep = nb >= lo + 4u ? 0xffffffffu : nb <= lo ? 0u : (1u << (8u * (nb - lo))) - 1u;
+                    v[q] = (v[q] & keep) | (o[q] & ~keep);
                 }
-                v[q] = acc;
+                nb += (ends[rr] - wb) * L1;
             }
         }
         dst[c] = make_uint4(v[0], v[1], v[2], v[3]);
