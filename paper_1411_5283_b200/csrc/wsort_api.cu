@@ -57,6 +57,8 @@ struct wsort_ctx {
     cudaStream_t aux = nullptr;                  // second stream: the dense buckets run beside the MSD
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t split = nullptr;                // third stream: parts of split finishing jobs beside k_msd_fin
+    cudaStream_t hp = nullptr;                   // high-priority stream: the long words' MSD (the critical path)
+    cudaEvent_t ev_hp0 = nullptr, ev_hp1 = nullptr;   // beside the dense branch, which fills the idle SMs
     cudaEvent_t ev_lvl = nullptr, ev_split = nullptr;
     int sms = 148;
     State state = ST_CREATED;
@@ -429,6 +431,9 @@ void wsort_destroy(wsort_ctx *c) {
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->aux && c->aux != c->stream) cudaStreamDestroy(c->aux);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->hp) cudaStreamDestroy(c->hp);
+    if (c->ev_hp0) cudaEventDestroy(c->ev_hp0);
+    if (c->ev_hp1) cudaEventDestroy(c->ev_hp1);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->split) cudaStreamDestroy(c->split);
     if (c->ev_lvl) cudaEventDestroy(c->ev_lvl);
@@ -1264,7 +1269,9 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
             // the parts of split jobs (if any: their number is on the device) on the third stream, beside
             // the whole jobs; then the text of the split jobs, by pieces
             if (!c->split) {
-                CK(cudaStreamCreateWithFlags(&c->split, cudaStreamNonBlocking), "split stream");
+                int least = 0, greatest = 0;
+                CK(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+                CK(cudaStreamCreateWithPriority(&c->split, cudaStreamNonBlocking, greatest), "split stream");
                 CK(cudaEventCreateWithFlags(&c->ev_lvl, cudaEventDisableTiming), "level event");
                 CK(cudaEventCreateWithFlags(&c->ev_split, cudaEventDisableTiming), "split event");
             }
@@ -1571,8 +1578,31 @@ int sort_dense_msd(wsort_ctx *c) {
     const BucketInfo *d_bk = reinterpret_cast<const BucketInfo *>(c->plan.p);
     if (n_dense && (rc = dense_branch(c, bk, d_bk, (double)s.byte_off[kDenseMaxLen + 1]))) return rc;
     if (W > n_dense) {
+        // the MSD of the long words is the critical path: it runs on a high-priority stream, so the block
+        // scheduler gives the dense branch (default priority) only the SMs the MSD leaves idle
+        static const bool no_hp = getenv("WSORT_NO_HP") != nullptr;   // (experiments)
+        const bool use_hp = n_dense && !c->prof_serial && !no_hp;
+        cudaStream_t user = c->stream;
+        if (use_hp) {
+            if (!c->hp) {
+                int least = 0, greatest = 0;
+                CK(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+                CK(cudaStreamCreateWithPriority(&c->hp, cudaStreamNonBlocking, greatest), "high-priority stream");
+                CK(cudaEventCreateWithFlags(&c->ev_hp0, cudaEventDisableTiming), "hp event");
+                CK(cudaEventCreateWithFlags(&c->ev_hp1, cudaEventDisableTiming), "hp event");
+            }
+            CK(cudaEventRecord(c->ev_hp0, user), "hp fork");
+            CK(cudaStreamWaitEvent(c->hp, c->ev_hp0, 0), "hp fork wait");
+            c->stream = c->hp;
+        }
         rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, W - n_dense, false,
                            [&](const BucketInfo *, double) { return (int)WSORT_OK; }, d_bk, true, 0, true);
+        if (use_hp) {
+            c->stream = user;
+            const cudaError_t e0 = cudaEventRecord(c->ev_hp1, c->hp);
+            const cudaError_t e1 = e0 == cudaSuccess ? cudaStreamWaitEvent(user, c->ev_hp1, 0) : e0;
+            if (!rc && e1 != cudaSuccess) return cuda_err(c, e1, "hp join");
+        }
     }
     if (n_dense) {   // join: the sort is complete when both streams are
         const cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_join, 0);
