@@ -19,6 +19,7 @@ CLASS = {
     "k_msd_plan": "k4m_msd_plan", "k_msd_scatter": "k4m_msd_scatter", "k_msd_fin": "k4m_msd_finish",
     "k_msd_warp_sort": "k4m_msd_finish", "k_msd_copy": "k4m_msd_finish", "k_emit": "k5_emit",
     "k_msd_fin_split": "k4m_msd_fin_split", "k_msd_fin_emit": "k4m_msd_fin_emit",
+    "k_msd_count0": "k4m_msd_count0", "k_msd_scatter0": "k4m_msd_scatter0",
 }
 
 
