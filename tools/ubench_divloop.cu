@@ -1,0 +1,94 @@
+// Microbenchmark (experiments): a K1-like divergent per-lane loop over the set bits of a 32-bit mask, each
+// iteration two shared loads + index math, then either a shared atomic on a 702-entry table (mode 0),
+// a register accumulation (mode 1), or a shared atomic with the lanes' iterations made uniform (mode 2:
+// every lane runs the same trip count, extra iterations predicated off).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+template <int MODE>
+__global__ void __launch_bounds__(512) k_loop(uint32_t *out, int iters, uint32_t density) {
+    __shared__ uint32_t wb[512 * 9];
+    __shared__ uint32_t d12[702];
+    const int t = threadIdx.x, lane = t & 31;
+    for (int i = t; i < 512 * 9; i += 512) wb[i] = (i * 2654435761u) | 0x61616161u;
+    for (int i = t; i < 702; i += 512) d12[i] = 0;
+    __syncthreads();
+    uint32_t x = t * 2654435761u + blockIdx.x * 97u, acc = 0;
+    const uint32_t *w = wb + (t >> 5) * 288;
+    for (int it = 0; it < iters; it++) {
+        x = x * 1664525u + 1013904223u;
+        uint32_t y = x * 747796405u + 2891336453u;
+        uint32_t m = x & y & (density == 2 ? 0xffffffffu : (y >> 1)) & 0x55555555u;   // sparse set bits
+        const uint32_t seg0 = 32u * lane;
+        if (MODE == 3) {   // fixed slots: 8 groups of 4 bytes x <= 2 starts each, bytes from registers
+            uint32_t cur[9];
+#pragma unroll
+            for (int j = 0; j < 9; j++) cur[j] = (x + 0x9E3779B9u * j) | 0x61616161u;
+            const uint32_t mm = m;
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                uint32_t g = (mm >> (4 * j)) & 0xFu;
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    const uint32_t k = __ffs(g) - 1;
+                    const uint32_t lo = __funnelshift_r(cur[j], cur[j + 1], 8u * (k & 3u));
+                    const uint32_t c0 = (lo & 31u) - 1u, c1 = ((lo >> 8) & 31u) - 1u;
+                    if (g) atomicAdd(&d12[(26u + c0 * 26u + c1) % 702u], 1u);
+                    g &= g - 1;
+                }
+            }
+            continue;
+        }
+        if (MODE == 2) {
+            uint32_t mx = __popc(m);
+            for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            for (uint32_t k = 0; k < mx; k++) {
+                const bool v = m != 0;
+                const uint32_t bit = v ? __ffs(m) - 1 : 0u, s = seg0 + bit;
+                m &= m - 1;
+                const uint32_t lo = __funnelshift_r(w[(s >> 2) % 280], w[((s >> 2) + 1) % 280], 8u * (s & 3u));
+                const uint32_t c0 = (lo & 31u) - 1u, c1 = ((lo >> 8) & 31u) - 1u;
+                if (v) atomicAdd(&d12[(26u + c0 * 26u + c1) % 702u], 1u);
+            }
+            continue;
+        }
+        for (; m; m &= m - 1) {
+            const uint32_t bit = __ffs(m) - 1, s = seg0 + bit;
+            const uint32_t lo = __funnelshift_r(w[(s >> 2) % 280], w[((s >> 2) + 1) % 280], 8u * (s & 3u));
+            const uint32_t c0 = (lo & 31u) - 1u, c1 = ((lo >> 8) & 31u) - 1u;
+            if (MODE == 0) atomicAdd(&d12[(26u + c0 * 26u + c1) % 702u], 1u);
+            else acc += 26u + c0 * 26u + c1;
+        }
+    }
+    __syncthreads();
+    if (t == 0) out[blockIdx.x] = d12[5] + acc;
+    else if (acc == 12345u) out[0] = acc;
+}
+
+int main() {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    uint32_t *out;
+    cudaMalloc(&out, 4096 * 4);
+    const int iters = 2000, grid = sms * 2;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto run = [&](const char *name, auto kern) {
+        kern<<<grid, 512>>>(out, iters, 1);
+        cudaEventRecord(e0);
+        kern<<<grid, 512>>>(out, iters, 1);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("%-40s %8.3f ms  %7.1f SM-cycles per warp-iteration of the outer loop\n", name, ms,
+               ms * 1e-3 * 1.965e9 / ((double)grid * 16 * iters / sms));
+    };
+    run("divergent loop + shared atomic", k_loop<0>);
+    run("divergent loop + register add", k_loop<1>);
+    run("uniform trip count + predicated atomic", k_loop<2>);
+    run("fixed 8x2 slots from registers + atomic", k_loop<3>);
+    printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
+}
