@@ -81,6 +81,30 @@ __global__ void k_copy_small(uint8_t *dst, const uint8_t *src, size_t n) {
     }
 }
 
+// Several small host tables (pinned arena) -> device in one launch: block (x, y) copies part x of table y.
+__global__ void k_copy_batch(CopyBatch b) {
+    const uint32_t y = blockIdx.y;
+    const uint8_t *src = static_cast<const uint8_t *>(b.src[y]);
+    uint8_t *dst = static_cast<uint8_t *>(b.dst[y]);
+    const size_t n = b.bytes[y], t = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)dst | (uintptr_t)src) & 15u) == 0) {
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        for (size_t i = t; i < n / 16; i += stride) d4[i] = s4[i];
+        for (size_t i = (n & ~(size_t)15) + t; i < n; i += stride) dst[i] = src[i];
+    } else {
+        for (size_t i = t; i < n; i += stride) dst[i] = src[i];
+    }
+}
+cudaError_t launch_copy_batch(const CopyBatch &b, cudaStream_t s) {
+    if (!b.n) return cudaSuccess;
+    size_t mx = 0;
+    for (uint32_t i = 0; i < b.n; i++) mx = b.bytes[i] > mx ? b.bytes[i] : mx;
+    const uint32_t gx = (uint32_t)std::min<size_t>(64, (mx + 4095) / 4096);
+    k_copy_batch<<<dim3(gx ? gx : 1, b.n), 256, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_emit(const EmitArgs &a, cudaStream_t s) {
     if (a.ntiles == 0) return cudaSuccess;
     k_emit<<<a.ntiles, kEThreads, 0, s>>>(a);

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
     // from the registers that prefetched it. Each sub-step's letter mask is computed once, one iteration
     // ahead, so the tail needs neither its own loads nor its own mask.
     const uint64_t pol = evict_first_policy();
+    uint32_t nge[6] = {0, 0, 0, 0, 0, 0};   // this lane's words of >= 1, 2, ..., 6 letters
     uint4 va = make_uint4(0, 0, 0, 0), vb = va;
     uint32_t prev_last = 0, M = 0;
     if (w0 < w1) {
@@ -301,9 +302,18 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
         // categories from the masks: a word starting at bit i has L >= j iff bytes i..i+j-1 are letters
         // (X = this lane's letters followed by the next lane's / the tail's); one branch-free loop each
         const uint64_t X = (uint64_t)M | ((uint64_t)(lane < 31 ? nm : mt0) << 32);
-        const uint32_t ge3 = starts & (uint32_t)(X >> 1) & (uint32_t)(X >> 2);
-        const uint32_t ge6 = ge3 & (uint32_t)(X >> 3) & (uint32_t)(X >> 4) & (uint32_t)(X >> 5);
+        const uint32_t ge2 = starts & (uint32_t)(X >> 1);
+        const uint32_t ge3 = ge2 & (uint32_t)(X >> 2);
+        const uint32_t ge4 = ge3 & (uint32_t)(X >> 3), ge5 = ge4 & (uint32_t)(X >> 4);
+        const uint32_t ge6 = ge5 & (uint32_t)(X >> 5);
         const uint32_t s12 = starts & ~ge3, s345 = ge3 & ~ge6;
+        // words of >= 1..6 letters started by this lane (the length histogram of L <= 5 is their differences)
+        nge[0] += __popc(starts);
+        nge[1] += __popc(ge2);
+        nge[2] += __popc(ge3);
+        nge[3] += __popc(ge4);
+        nge[4] += __popc(ge5);
+        nge[5] += __popc(ge6);
         const uint32_t nlong = __popc(ge6), n345 = __popc(s345);
         const uint32_t cnt = n345 | (nlong << 16);
         const uint32_t ci = inclusive_scan_warp(cnt, lane);
@@ -392,6 +402,17 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
         __syncwarp();   // the slot and list are rewritten by the next sub-steps
         M = Mn;
     }
+#pragma unroll
+    for (int j = 0; j < 6; j++) {   // the warp's counts of L = 1..5 into the histogram (K2 needs no table scan)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) nge[j] += __shfl_xor_sync(kFull, nge[j], o);
+    }
+    if (lane < (int)kDenseMaxLen && !(a.debug & 64)) {
+        uint32_t v = nge[0] - nge[1];
+#pragma unroll
+        for (int j = 1; j < (int)kDenseMaxLen; j++) v = lane == j ? nge[j] - nge[j + 1] : v;
+        if (v) atomicAdd(&sm.hist[lane + 1], v);
+    }
     __syncthreads();
     if (t == 0) atomicMax(&a.ctr[kIgMaxChunks], sm.nchunk);
     if (!HASH) {   // keys in each chunk: full, except the last one of each class
@@ -414,7 +435,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
             a.touched[e / kDenseBlkEntries] = 1;
         }
     }
-    for (int i = t; i < kHistBins; i += kIgThreads) {   // lengths >= 6 (the dense ones come from the tables)
+    for (int i = t; i < kHistBins; i += kIgThreads) {   // every length (1..5 from the mask counts above)
         const uint32_t h = sm.hist[i];
         if (h) atomicAdd(&a.ghist[i], h);
     }

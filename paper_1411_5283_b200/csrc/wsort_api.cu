@@ -104,6 +104,12 @@ struct wsort_ctx {
     // next sort once `arena_done` has passed)
     uint8_t *arena = nullptr;
     size_t arena_cap = 0, arena_off = 0;
+    struct PendingCopy {
+        void *dst;
+        const void *src;
+        size_t bytes;
+    };
+    std::vector<PendingCopy> pcopy;   // arena uploads not yet issued (arena_flush)
     cudaEvent_t arena_done = nullptr;
     bool sorted_with_src = false;
     int last_algo = 0;
@@ -196,8 +202,30 @@ int upload_small(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const
 // Staged uploads: host tables are copied into the pinned arena and sent with one async copy each
 // (pageable cudaMemcpyAsync would stage through the driver); regions are not reused within a sort.
 int arena_begin(wsort_ctx *c) {
+    c->pcopy.clear();
     if (c->arena_done) CK(cudaEventSynchronize(c->arena_done), "arena reuse");
     c->arena_off = 0;
+    return WSORT_OK;
+}
+// The uploads of a sort are batched: one copy kernel launch per batch (arena_flush), issued on the
+// context's stream before the next kernel there and before every fork to a side stream.
+int arena_flush(wsort_ctx *c) {
+    size_t i = 0;
+    while (i < c->pcopy.size()) {
+        CopyBatch b{};
+        for (; i < c->pcopy.size() && b.n < kCopyBatch; i++, b.n++) {
+            b.dst[b.n] = c->pcopy[i].dst;
+            b.src[b.n] = c->pcopy[i].src;
+            b.bytes[b.n] = c->pcopy[i].bytes;
+        }
+        const cudaError_t e = launch_copy_batch(b, c->stream);
+        if (e != cudaSuccess) {
+            c->pcopy.clear();
+            return cuda_err(c, e, "upload batch");
+        }
+        c->launches++;
+    }
+    c->pcopy.clear();
     return WSORT_OK;
 }
 int arena_upload(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const char *what) {
@@ -205,6 +233,7 @@ int arena_upload(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const
     if (rc || !bytes) return rc;
     const size_t need = c->arena_off + ((bytes + 255) & ~(size_t)255);
     if (need > c->arena_cap) {   // grow (rare): earlier copies of this sort read the old buffer
+        if ((rc = arena_flush(c))) return rc;
         CK(cudaStreamSynchronize(c->stream), "arena grow");
         uint8_t *nb = nullptr;
         const size_t cap = std::max<size_t>(need * 2, 1 << 20);
@@ -220,10 +249,12 @@ int arena_upload(wsort_ctx *c, DevBuf &dst, const void *src, size_t bytes, const
     uint8_t *h = c->arena + c->arena_off;
     memcpy(h, src, bytes);
     c->arena_off += (bytes + 255) & ~(size_t)255;
-    CK(copy_small(dst.p, h, bytes, c->stream), what);   // (pinned arena: no copy-engine queue)
+    c->pcopy.push_back(wsort_ctx::PendingCopy{dst.p, h, bytes});   // (pinned arena, copied by a kernel: no copy-engine queue)
+    (void)what;
     return WSORT_OK;
 }
 int arena_end(wsort_ctx *c) {
+    if (int rc = arena_flush(c)) return rc;
     if (!c->arena_done) CK(cudaEventCreateWithFlags(&c->arena_done, cudaEventDisableTiming), "arena event");
     CK(cudaEventRecord(c->arena_done, c->stream), "arena event");
     return WSORT_OK;
@@ -247,8 +278,12 @@ cudaEvent_t get_event(wsort_ctx *c) {
     return e;
 }
 
+int arena_flush(wsort_ctx *c);
 template <class F>
 int launch_on(wsort_ctx *c, cudaStream_t s, const char *name, double bytes, F f) {
+    if (s == c->stream && !c->pcopy.empty()) {
+        if (int rc = arena_flush(c)) return rc;
+    }
     PendingEv pe{};
     if (c->prof) {
         pe.cls = class_id(c, name);
@@ -717,9 +752,7 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
         rc = launch(c, "k1_ingest", (double)c->n, [&] { return launch_ingest(ia, c->stream); });
         if (rc) return rc;
     }
-    rc = launch(c, "k2_dense_lensum", (double)dense_entries() * 4,
-                [&] { return launch_dense_lensum(ia.dense, ia.touched, ia.ghist, c->stream); });
-    if (rc) return rc;
+    // (the histogram of L <= 5 comes from K1's mask counts: no scan of the dense tables here)
     rc = launch(c, "k2_bucket_offsets", (double)kHistBins * 4,
                 [&] { return launch_bucket_offsets(ia.ghist, static_cast<Summary *>(c->d_sum.p), c->stream); });
     if (rc) return rc;
@@ -1275,6 +1308,7 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
                 CK(cudaEventCreateWithFlags(&c->ev_lvl, cudaEventDisableTiming), "level event");
                 CK(cudaEventCreateWithFlags(&c->ev_split, cudaEventDisableTiming), "split event");
             }
+            if ((rc = arena_flush(c))) return rc;
             CK(cudaEventRecord(c->ev_lvl, c->stream), "level event");
             cudaStream_t sp = c->prof_serial ? c->stream : c->split;   // (serial profiling: one stream)
             CK(cudaStreamWaitEvent(sp, c->ev_lvl, 0), "level wait");
@@ -1527,6 +1561,7 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
         CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
     }
+    if ((rc = arena_flush(c))) return rc;
     CK(cudaEventRecord(c->ev_fork, c->stream), "fork");
     cudaStream_t aux = c->prof_serial ? c->stream : c->aux;   // (serial profiling: one stream)
     CK(cudaStreamWaitEvent(aux, c->ev_fork, 0), "fork wait");
@@ -1591,6 +1626,7 @@ int sort_dense_msd(wsort_ctx *c) {
                 CK(cudaEventCreateWithFlags(&c->ev_hp0, cudaEventDisableTiming), "hp event");
                 CK(cudaEventCreateWithFlags(&c->ev_hp1, cudaEventDisableTiming), "hp event");
             }
+            if ((rc = arena_flush(c))) return rc;
             CK(cudaEventRecord(c->ev_hp0, user), "hp fork");
             CK(cudaStreamWaitEvent(c->hp, c->ev_hp0, 0), "hp fork wait");
             c->stream = c->hp;
@@ -1598,6 +1634,8 @@ int sort_dense_msd(wsort_ctx *c) {
         rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, W - n_dense, false,
                            [&](const BucketInfo *, double) { return (int)WSORT_OK; }, d_bk, true, 0, true);
         if (use_hp) {
+            const int rf = arena_flush(c);   // (on the high-priority stream)
+            if (!rc) rc = rf;
             c->stream = user;
             const cudaError_t e0 = cudaEventRecord(c->ev_hp1, c->hp);
             const cudaError_t e1 = e0 == cudaSuccess ? cudaStreamWaitEvent(user, c->ev_hp1, 0) : e0;

@@ -466,5 +466,14 @@ constexpr int kEmitStage = 16384;  // smem bytes of output staged per emit tile
 cudaError_t launch_emit(const EmitArgs &a, cudaStream_t s);
 // small (KB) host<->device copy by a kernel through UVA-mapped pinned host memory (no copy engine)
 cudaError_t copy_small(void *dst, const void *src, size_t bytes, cudaStream_t s);
+// up to kCopyBatch small host tables (pinned) -> device in one kernel launch
+constexpr uint32_t kCopyBatch = 16;
+struct CopyBatch {
+    void *dst[kCopyBatch];
+    const void *src[kCopyBatch];
+    size_t bytes[kCopyBatch];
+    uint32_t n;
+};
+cudaError_t launch_copy_batch(const CopyBatch &b, cudaStream_t s);
 
 }  // namespace wsort

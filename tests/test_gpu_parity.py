@@ -227,6 +227,23 @@ def test_deterministic_repeats(ws):
     assert all(np.array_equal(o[2], outs[0][2]) for o in outs)
 
 
+def test_auto_repeats_exact_c3_prefix_families(ws):
+    """Races in the multi-chunk level 0 (k_msd_count0 / k_msd_scatter0 slices of several chunks, the ring
+    of published chunk ids in K1) and the finishing jobs show up as run-to-run differences: AUTO is
+    repeated on config 3 (64 MiB, every slice several chunks long) and on a text of long prefix
+    families (config 5's shape: many chunks per class, wide keys, split jobs), each run byte-compared
+    with the oracle."""
+    text, _ = gen.generate(3)
+    ref = oracle.sort(text, oracle.MERGE)
+    fam = gen.generate(5, n=24 << 20)[0]
+    ref5 = oracle.sort(fam, oracle.MERGE)
+    for _ in range(3):
+        for t, r in ((text, ref), (fam, ref5)):
+            w, off, _ = gpu_sort(ws, t, "auto", src=False)
+            assert off == r.off
+            assert w == r.words
+
+
 def test_auto_equals_radix(ws):
     text, _ = gen.generate(1)
     assert gpu_sort(ws, text, "auto")[0] == gpu_sort(ws, text, "lsd_radix")[0]
