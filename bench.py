@@ -392,16 +392,23 @@ def two_in_flight(args, host, dev, n_words):
     e0.record(streams[0])
     streams[1].wait_event(e0)
 
+    errors = []
+
     def work(c):
-        for _ in range(K // 2):
-            c.tokenize()
-            c.sort(args.algo)
+        try:
+            for _ in range(K // 2):
+                c.tokenize()
+                c.sort(args.algo)
+        except Exception as e:   # re-raised below: a failed thread must not pass for a fast one
+            errors.append(e)
 
     ths = [threading.Thread(target=work, args=(c,)) for c in ctxs]
     for t in ths:
         t.start()
     for t in ths:
         t.join()
+    if errors:
+        raise errors[0]
     ev = torch.cuda.Event()
     ev.record(streams[1])
     streams[0].wait_event(ev)
