@@ -110,6 +110,10 @@ struct wsort_ctx {
         size_t bytes;
     };
     std::vector<PendingCopy> pcopy;   // arena uploads not yet issued (arena_flush)
+    cudaGraph_t tk_graph = nullptr;   // the tokenize launch sequence, captured (tokenize_impl)
+    cudaGraphExec_t tk_exec = nullptr;
+    std::vector<uintptr_t> tk_key;    // what it was captured for (size, mode, buffers)
+    uint64_t tk_nlaunch = 0;
     cudaEvent_t arena_done = nullptr;
     bool sorted_with_src = false;
     int last_algo = 0;
@@ -471,6 +475,8 @@ void wsort_destroy(wsort_ctx *c) {
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->aux && c->aux != c->stream) cudaStreamDestroy(c->aux);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->tk_exec) cudaGraphExecDestroy(c->tk_exec);
+    if (c->tk_graph) cudaGraphDestroy(c->tk_graph);
     if (c->hp) cudaStreamDestroy(c->hp);
     if (c->ev_hp0) cudaEventDestroy(c->ev_hp0);
     if (c->ev_hp1) cudaEventDestroy(c->ev_hp1);
@@ -690,20 +696,7 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     }
     a.cta_hist = static_cast<uint32_t *>(c->cta_hist.p);
     a.cta_base = static_cast<uint32_t *>(c->cta_base.p);
-    CK(cudaMemsetAsync(c->ghist.p, 0, kHistBins * 4, c->stream), "memset ghist");
     if ((rc = ensure(c, c->d_touched, dense_scan_blocks(dense_entries()), "dense touched flags", true))) return rc;
-    if (!c->dense_clean) {   // (first use of the table: zero it all; later only the touched blocks)
-        CK(cudaMemsetAsync(c->dense.p, 0, (size_t)dense_entries() * 4, c->stream), "memset dense");
-        CK(cudaMemsetAsync(c->d_touched.p, 0, dense_scan_blocks(dense_entries()), c->stream), "memset touched");
-        c->dense_clean = true;
-    } else {
-        rc = launch(c, "k0_dense_clear", 0, [&] {
-            return launch_dense_clear(static_cast<uint32_t *>(c->dense.p), static_cast<uint8_t *>(c->d_touched.p), c->stream);
-        });
-        if (rc) return rc;
-    }
-    CK(cudaMemsetAsync(c->ig_ctr.p, 0, kIgCtrs * 4, c->stream), "memset ingest counters");
-    CK(cudaMemsetAsync(c->chunk_fill.p, 0, (size_t)c->n_chunks * 4, c->stream), "memset chunk fills");
     IngestArgs ia{};
     ia.text = a.text;
     ia.n = a.n;
@@ -723,6 +716,23 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     ia.hash = hash ? 1u : 0u;
     ia.tab = c->tab;
     if (const char *dbg = getenv("WSORT_INGEST_DEBUG")) ia.debug = (uint32_t)atoi(dbg);
+    // Everything from here to the read-back is one launch sequence that depends only on the text size, the
+    // mode and the buffers: captured once as a CUDA graph and replayed by later tokenize calls (the
+    // launch-bound small texts; not while profiling, streaming the text in, or on the legacy stream)
+    auto enqueue = [&]() -> int {
+    CK(cudaMemsetAsync(c->ghist.p, 0, kHistBins * 4, c->stream), "memset ghist");
+    if (!c->dense_clean) {   // (first use of the table: zero it all; later only the touched blocks)
+        CK(cudaMemsetAsync(c->dense.p, 0, (size_t)dense_entries() * 4, c->stream), "memset dense");
+        CK(cudaMemsetAsync(c->d_touched.p, 0, dense_scan_blocks(dense_entries()), c->stream), "memset touched");
+        c->dense_clean = true;
+    } else {
+        rc = launch(c, "k0_dense_clear", 0, [&] {
+            return launch_dense_clear(static_cast<uint32_t *>(c->dense.p), static_cast<uint8_t *>(c->d_touched.p), c->stream);
+        });
+        if (rc) return rc;
+    }
+    CK(cudaMemsetAsync(c->ig_ctr.p, 0, kIgCtrs * 4, c->stream), "memset ingest counters");
+    CK(cudaMemsetAsync(c->chunk_fill.p, 0, (size_t)c->n_chunks * 4, c->stream), "memset chunk fills");
     if (c->stream_src) {
         // streamed ingest: S stages of K1 CTAs; stage s's bytes (+32 KiB: the warps' prefetch and words that
         // cross the range end) are copied on the copy stream, and its K1 launch waits for that copy only, so
@@ -766,6 +776,48 @@ int tokenize_impl(wsort_ctx *c, uint64_t *n_words, bool hash) {
     if (hash) {
         CK(copy_small(c->h_tab, c->t_top.p, 16, c->stream), "copy hash top");
         CK(copy_small(c->h_tab + 4, c->t_dcount.p, 256 * 4, c->stream), "copy hash distinct counts");
+    }
+    return (int)WSORT_OK;
+    };
+    static const bool no_graph = getenv("WSORT_NO_GRAPH") != nullptr;   // (experiments)
+    const char *dbg_env = getenv("WSORT_INGEST_DEBUG");
+    const bool graphable = !no_graph && !c->prof && !c->stream_src && c->dense_clean && c->stream != nullptr &&
+                           c->stream != cudaStreamLegacy && c->stream != cudaStreamPerThread;
+    const uintptr_t key[] = {(uintptr_t)c->n, (uintptr_t)hash, (uintptr_t)a.text, (uintptr_t)c->dense.p,
+                             (uintptr_t)c->d_touched.p, (uintptr_t)c->pool.p, (uintptr_t)c->chunk_cls.p,
+                             (uintptr_t)c->chunk_fill.p, (uintptr_t)c->cls_list.p, (uintptr_t)c->ig_ctr.p,
+                             (uintptr_t)c->ghist.p, (uintptr_t)c->d_sum.p, (uintptr_t)c->h_ig, (uintptr_t)c->h_sum,
+                             (uintptr_t)c->h_tab, (uintptr_t)c->tab.nkey, (uintptr_t)c->tab.fp, (uintptr_t)c->tab.keys,
+                             (uintptr_t)c->tab.nmask, (uintptr_t)c->tab.mask, (uintptr_t)(dbg_env ? atoi(dbg_env) : 0),
+                             (uintptr_t)c->cta_chunks, (uintptr_t)c->t_top.p, (uintptr_t)c->t_dcount.p,
+                             (uintptr_t)c->tab.ncnt, (uintptr_t)c->tab.cnt, (uintptr_t)c->tab.meta};
+    constexpr size_t nkey = sizeof(key) / sizeof(key[0]);
+    if (graphable && c->tk_exec && c->tk_key.size() == nkey && std::equal(key, key + nkey, c->tk_key.begin())) {
+        CK(cudaGraphLaunch(c->tk_exec, c->stream), "tokenize graph");
+        c->launches += c->tk_nlaunch;
+    } else if (graphable) {
+        if (c->tk_exec) cudaGraphExecDestroy(c->tk_exec);
+        if (c->tk_graph) cudaGraphDestroy(c->tk_graph);
+        c->tk_exec = nullptr;
+        c->tk_graph = nullptr;
+        c->tk_key.clear();
+        const uint64_t l0 = c->launches;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "tokenize capture");
+        rc = enqueue();
+        cudaGraph_t g = nullptr;
+        const cudaError_t ee = cudaStreamEndCapture(c->stream, &g);
+        if (rc || ee != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            return rc ? rc : cuda_err(c, ee, "tokenize capture");
+        }
+        CK(cudaGraphInstantiate(&c->tk_exec, g, 0), "tokenize graph");
+        c->tk_graph = g;
+        c->tk_nlaunch = c->launches - l0;
+        c->tk_key.assign(key, key + nkey);
+        CK(cudaGraphLaunch(c->tk_exec, c->stream), "tokenize graph");
+    } else if ((rc = enqueue())) {
+        return rc;
     }
     CK(cudaStreamSynchronize(c->stream), "tokenize");
     if (hash) {   // fill of the tables (distinct words per length counted by K1) against their capacity

@@ -244,6 +244,21 @@ def test_auto_repeats_exact_c3_prefix_families(ws):
             assert w == r.words
 
 
+def test_tokenize_graph_replays_with_new_text(ws):
+    """wsort_tokenize captures its launch sequence as a CUDA graph for a text size and replays it for the
+    next text of the same size: different contents (and the COUNT / STAGE modes alternating) must each
+    give the oracle's result."""
+    a = gen.generate(2)[0]
+    b = gen.generate(2, seed=77)[0]
+    c = np.frombuffer(bytes(reversed(a.tobytes())), dtype=np.uint8)
+    assert len(a) == len(b) == len(c)
+    refs = {id(t): oracle.sort(t, oracle.MERGE) for t in (a, b, c)}
+    for algo in ("dense_msd", "auto_count", "dense_msd"):
+        for t in (a, b, c, a):
+            w, off, _ = gpu_sort(ws, t, algo, src=False)
+            assert off == refs[id(t)].off and w == refs[id(t)].words, algo
+
+
 def test_auto_equals_radix(ws):
     text, _ = gen.generate(1)
     assert gpu_sort(ws, text, "auto")[0] == gpu_sort(ws, text, "lsd_radix")[0]

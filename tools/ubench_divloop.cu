@@ -21,6 +21,24 @@ __global__ void __launch_bounds__(512) k_loop(uint32_t *out, int iters, uint32_t
         uint32_t y = x * 747796405u + 2891336453u;
         uint32_t m = x & y & (density == 2 ? 0xffffffffu : (y >> 1)) & 0x55555555u;   // sparse set bits
         const uint32_t seg0 = 32u * lane;
+        if (MODE == 4) {   // divergent loop, bytes from registers by a select tree (no shared loads) + atomic
+            uint32_t cur[9];
+#pragma unroll
+            for (int j = 0; j < 9; j++) cur[j] = (x + 0x9E3779B9u * j) | 0x61616161u;
+            for (; m; m &= m - 1) {
+                const uint32_t bit = __ffs(m) - 1, w = bit >> 2;
+                const uint32_t a01 = (w & 1) ? cur[1] : cur[0], a23 = (w & 1) ? cur[3] : cur[2];
+                const uint32_t a45 = (w & 1) ? cur[5] : cur[4], a67 = (w & 1) ? cur[7] : cur[6];
+                const uint32_t b01 = (w & 1) ? cur[2] : cur[1], b23 = (w & 1) ? cur[4] : cur[3];
+                const uint32_t b45 = (w & 1) ? cur[6] : cur[5], b67 = (w & 1) ? cur[8] : cur[7];
+                const uint32_t a03 = (w & 2) ? a23 : a01, a47 = (w & 2) ? a67 : a45;
+                const uint32_t b03 = (w & 2) ? b23 : b01, b47 = (w & 2) ? b67 : b45;
+                const uint32_t lo = __funnelshift_r((w & 4) ? a47 : a03, (w & 4) ? b47 : b03, 8u * (bit & 3u));
+                const uint32_t c0 = (lo & 31u) - 1u, c1 = ((lo >> 8) & 31u) - 1u;
+                atomicAdd(&d12[(26u + c0 * 26u + c1) % 702u], 1u);
+            }
+            continue;
+        }
         if (MODE == 3) {   // fixed slots: 8 groups of 4 bytes x <= 2 starts each, bytes from registers
             uint32_t cur[9];
 #pragma unroll
@@ -90,5 +108,6 @@ int main() {
     run("divergent loop + register add", k_loop<1>);
     run("uniform trip count + predicated atomic", k_loop<2>);
     run("fixed 8x2 slots from registers + atomic", k_loop<3>);
+    run("divergent loop, select-tree bytes + atomic", k_loop<4>);
     printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
 }
