@@ -6,12 +6,12 @@ python -m pytest tests -q -m gpu > gpurun_out/f2_gputests.log 2>&1; echo "gputes
 python bench.py --steps 20 --warmup 5 > gpurun_out/f2_bench.json 2> gpurun_out/f2_bench.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/f2_ref.json 2> gpurun_out/f2_ref.err
 for c in 1 2 3; do python bench.py --config $c --steps 20 --warmup 5 --no-e2e > gpurun_out/f2_c$c.json 2> gpurun_out/f2_c$c.err; done
-CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-inflight"
 $CMD > /dev/null 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/f2_launches.csv $CMD > gpurun_out/f2_ncu1.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/f2_traffic.csv $CMD > gpurun_out/f2_ncu2.log 2>&1
-for KK in k_ingest:1 k_msd_scatter0:1 k_msd_fin:1 k_msd_count0:1; do
+for KK in k_ingest:1 k_msd_scatter0:1 "k_msd_fin$:0" k_msd_count0:1; do
   K=${KK%%:*}; S=${KK##*:}
   ncu --set full --clock-control none --import-source on -k regex:"$K" -s $S -c 1 -o "gpurun_out/f2_full_$K" -f $CMD > "gpurun_out/f2_ncu_$K.log" 2>&1
 done
