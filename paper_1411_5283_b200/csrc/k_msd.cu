@@ -221,10 +221,13 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
     }
     __syncthreads();
     const uint32_t nj = s_n[0], ntop = s_n[1];
-    // sort jobs, order-preserving split into tiny / small (each thread recounts its prefix)
-    for (uint32_t k = t; k < nj; k += kST) {
-        uint32_t before_tiny = 0;
-        for (uint32_t i = 0; i < k; i++) before_tiny += first_queue(a, jobs[i].n);
+    // sort jobs, order-preserving split into tiny / small: thread t takes a contiguous block of jobs, the
+    // tiny ones before it come from a block scan of the blocks' counts
+    const uint32_t per = (nj + kST - 1) / kST, k0 = min(nj, per * t), k1 = min(nj, k0 + per);
+    uint32_t my_tiny = 0;
+    for (uint32_t k = k0; k < k1; k++) my_tiny += first_queue(a, jobs[k].n);
+    uint32_t before_tiny = block_excl_scan_m(my_tiny, wsum, nullptr);
+    for (uint32_t k = k0; k < k1; k++) {
         const MsdSeg x = jobs[k];
         if (first_queue(a, x.n)) {
             const uint32_t q = s_q[0] + before_tiny;
@@ -239,6 +242,7 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
                     for (uint32_t p = 0; p < np && pb + p < a.cap_parts; p++) a.q_parts[pb + p] = q;
                 }
             }
+            before_tiny++;
         } else {
             const uint32_t q = s_q[1] + (k - before_tiny);
             if (q < a.cap_local) a.q_small[q] = x;
