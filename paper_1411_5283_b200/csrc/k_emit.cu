@@ -15,7 +15,7 @@ constexpr int kEThreads = 256;
 __global__ void __launch_bounds__(kEThreads) k_emit(EmitArgs a) {
     __shared__ __align__(16) uint8_t stage[kEmitStage + 32];
     const int t = threadIdx.x;
-    const TileDesc td = a.tile_pfx ? tile_from_prefix(a.tile_pfx, blockIdx.x) : a.tiles[blockIdx.x];
+    const TileDesc td = a.tile_pfx ? tile_from_prefix_cta(a.tile_pfx, blockIdx.x) : a.tiles[blockIdx.x];
     const uint32_t L = td.L;
     const BucketInfo b = a.buckets[L];
     const uint32_t te = kEmitStage / (L + 1);

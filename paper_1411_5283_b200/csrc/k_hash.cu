@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kHT) k_emit_runs(HashRunArgs a) {
     __shared__ __align__(16) uint8_t s_pat[kRunPatBytes + 16];
     __shared__ uint32_t s_end[2048];
     const uint32_t t = threadIdx.x;
-    const TileDesc td = tile_from_prefix(a.tile_pfx, blockIdx.x);
+    const TileDesc td = tile_from_prefix_cta(a.tile_pfx, blockIdx.x);
     const uint32_t L = td.L, P = L + 1u, PE = P + 4u, kw = (L + 5u) / 6u;
     const uint32_t rcap = min(2048u, kRunPatBytes / PE);
     const BucketInfo b = a.buckets[L];

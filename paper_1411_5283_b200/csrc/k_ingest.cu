@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(256) k_emit_dense(DenseEmitArgs a) {
     uint64_t *s_pat = reinterpret_cast<uint64_t *>(dsm);                 // entry j's word + '\n' (LE bytes)
     uint32_t *s_end = reinterpret_cast<uint32_t *>(dsm + 8 * kDenseTileEnt);   // inclusive end, tile-relative
     const uint32_t t = threadIdx.x;
-    const TileDesc td = tile_from_prefix(a.tile_pfx, blockIdx.x);
+    const TileDesc td = tile_from_prefix_cta(a.tile_pfx, blockIdx.x);
     const uint32_t L = td.L, P = L + 1u, magic = 65536u / P + 1u;   // (n * magic) >> 16 == n / P for n <= 21
     const BucketInfo b = a.buckets[L];
     const uint32_t te = dense_tile_words(L);

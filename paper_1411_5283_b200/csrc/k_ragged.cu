@@ -43,7 +43,7 @@ __device__ __forceinline__ bool ref_less(const uint8_t *text, uint32_t L, uint32
 // bitonic sort of one tile of a bucket's references in shared memory
 __global__ void __launch_bounds__(kRT) k_ragged_tiles(RaggedArgs a) {
     __shared__ uint32_t r[kRaggedTile];
-    const TileDesc td = tile_from_prefix(a.tile_pfx, blockIdx.x);
+    const TileDesc td = tile_from_prefix_cta(a.tile_pfx, blockIdx.x);
     const BucketInfo b = a.buckets[td.L];
     const uint32_t k0 = td.tile * kRaggedTile, n = min(kRaggedTile, b.n - k0);
     const uint32_t *src = a.in + b.word_off + k0;
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kRT) k_ragged_tiles(RaggedArgs a) {
 // one merge pass: sorted runs of `run` references -> runs of 2 run; block = 1024 outputs of one bucket,
 // each thread 4 consecutive outputs from its merge-path split (binary search on the diagonal)
 __global__ void __launch_bounds__(kRT) k_ragged_merge(RaggedArgs a) {
-    const TileDesc td = tile_from_prefix(a.tile_pfx, blockIdx.x);
+    const TileDesc td = tile_from_prefix_cta(a.tile_pfx, blockIdx.x);
     const BucketInfo b = a.buckets[td.L];
     const uint32_t L = td.L, run = a.run;
     const uint32_t *in = a.in + b.word_off;
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kRT) k_ragged_merge(RaggedArgs a) {
 
 // "word\n" of every reference (copied from the text, folded); src_off = global offsets
 __global__ void __launch_bounds__(kRT) k_ragged_emit(RaggedArgs a) {
-    const TileDesc td = tile_from_prefix(a.tile_pfx, blockIdx.x);
+    const TileDesc td = tile_from_prefix_cta(a.tile_pfx, blockIdx.x);
     const BucketInfo b = a.buckets[td.L];
     const uint32_t L = td.L;
     const uint32_t k = td.tile * kRaggedTile + threadIdx.x * 4u;

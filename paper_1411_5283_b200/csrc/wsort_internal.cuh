@@ -72,6 +72,20 @@ __device__ __forceinline__ TileDesc tile_from_prefix(const uint32_t *pfx, uint32
     return TileDesc{lo, b - __ldg(pfx + lo)};
 }
 
+// The same for a block-uniform b, called by every thread of the block (full warps): each warp finds it in
+// two dependent loads instead of eight (coarse: pfx[8 lane]; fine: pfx[8 k + lane], k the coarse interval)
+__device__ __forceinline__ TileDesc tile_from_prefix_cta(const uint32_t *pfx, uint32_t b) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t m = __ballot_sync(0xffffffffu, __ldg(pfx + 8u * lane) <= b);   // (pfx[0] = 0 <= b)
+    const uint32_t k = 31u - (uint32_t)__clz(m);
+    const uint32_t idx = min(8u * k + (lane & 15u), 256u);
+    const uint32_t v = __ldg(pfx + idx);
+    const uint32_t m2 = __ballot_sync(0xffffffffu, lane < 16u && v <= b);
+    const uint32_t f = 31u - (uint32_t)__clz(m2);
+    const uint32_t L = 8u * k + f;
+    return TileDesc{L, b - __shfl_sync(0xffffffffu, v, f)};
+}
+
 // ---------------- launchers (defined in the .cu files) ----------------
 struct TkArgs {
     const uint8_t *text;           // device copy, text[-kTextFrontPad..-1] = 0, zero tail padding
