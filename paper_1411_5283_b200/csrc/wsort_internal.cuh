@@ -234,8 +234,10 @@ struct IngestArgs {
                                             // (fills zeroed by the host: unused chunks stay empty)
     uint32_t cta_chunks;                    // chunks of one CTA's region
     uint32_t *ctr;                          // [kIgCtrs] (zeroed by the host)
-    uint32_t debug;                         // timing experiments only (WSORT_INGEST_DEBUG): 1 = skip dense
-                                            // counting, 2 = skip key packing, 4 = direct L3-5 counts
+    uint32_t debug;                         // timing experiments only (WSORT_INGEST_DEBUG; outputs wrong):
+                                            // 1 = skip the L <= 2 counting, 2 = skip key packing, 8 = skip
+                                            // the long words, 16 = skip the L = 3..5 cache, 32 = skip the
+                                            // end-of-CTA flush, 64 = skip the L <= 5 length counts
     uint32_t hash;                          // 1: count the long words into `tab` instead of staging them
     HashTab tab;
     uint32_t cta_first;                     // this launch's first CTA (streamed ingest launches K1 by CTA ranges)
