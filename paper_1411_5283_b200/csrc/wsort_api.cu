@@ -1319,16 +1319,25 @@ int msd_read_counters(wsort_ctx *c, const MsdArgs &m, uint32_t &nsegs, uint32_t 
 // MSD levels from `level` on (its segments / tiles are in m_big[level & 1] / m_tiles[level & 1]) until no
 // segment is left, then the finishing sorts: every key ends in buffer B at its final index.
 int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nsegs, uint32_t ntiles, uint32_t levels,
-                          double key_bytes, uint32_t max_tw) {
+                          double key_bytes, uint32_t max_tw, bool may_requeue = false) {
     int rc;
     m.stream_fin = m.finish_radix ? 0u : 1u;
     const uint32_t fin_grid = (uint32_t)c->sms * 4;   // k_msd_fin: 4 resident CTAs per SM
     uint32_t small_done = 0, parts_done = 0, emit_done = 0;
     if (!m.finish_radix && (c->h_ctr[kQSmall] || c->h_ctr[kQTiny])) {   // jobs planned before the first level
+        if (may_requeue) {   // (whole buckets larger than a tile: one with too many distinct keys goes back to
+                             // the MSD as a level-0 segment)
+            m.q_big = static_cast<MsdSeg *>(c->m_big[0].p);
+            m.q_tiles = static_cast<MsdTile *>(c->m_tiles[0].p);
+        }
         rc = launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_fin_jobs(m, 0, 0, fin_grid, c->stream); });
         if (rc) return rc;
         small_done = c->h_ctr[kQSmall];
         parts_done = c->h_ctr[kQParts];
+        if (may_requeue && nsegs == 0) {
+            if ((rc = msd_read_counters(c, m, nsegs, ntiles))) return rc;
+            small_done = std::min(c->h_ctr[kQSmall], m.cap_local);
+        }
     }
     for (; nsegs > 0; level++) {
         if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
@@ -1488,7 +1497,7 @@ std::vector<BucketInfo> msd_buckets(const Summary &s, uint32_t lkey, uint32_t &m
 template <class Pack>
 int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint32_t max_tw, uint32_t levels,
                   uint64_t key_words, uint64_t W, bool finish_radix, Pack pack, const BucketInfo *d_bk_pre = nullptr,
-                  bool emit = true, uint32_t lmax_keys = 0, bool from_chunks = false) {
+                  bool emit = true, uint32_t lmax_keys = 0, bool from_chunks = false, uint32_t direct_max = 0) {
     const Summary &s = *c->h_sum;
     const uint32_t lmax = lmax_keys ? lmax_keys : s.max_len;
     int rc;
@@ -1525,10 +1534,12 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
             return rc;
         m.slice_hist = static_cast<uint32_t *>(c->slice_hist.p);
     }
+    bool may_requeue = false;   // a whole-bucket job larger than a tile (streaming finish: may re-enter the MSD)
     for (uint32_t L = lkey; L <= lmax && !from_chunks; L++) {
         const BucketInfo &b = bk[L];
         if (!b.n) continue;
-        if (b.n <= b.tile_keys) {
+        if (b.n <= std::max(b.tile_keys, direct_max)) {
+            may_requeue |= b.n > b.tile_keys;
             (finish_radix ? b.n <= 32 : b.n > 16384) ? tiny.push_back(MsdSeg{L, 0, b.n, 1}) : small.push_back(MsdSeg{L, 0, b.n, 1});
         } else {
             const uint32_t q = (uint32_t)segs.size();
@@ -1554,7 +1565,7 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
     m.finish_radix = finish_radix ? 1u : 0u;
     m.words = static_cast<uint8_t *>(c->words.p);
     if ((rc = msd_levels_and_finish(c, m, 0, (uint32_t)segs.size(), from_chunks ? m.nslices : (uint32_t)tiles.size(),
-                                    levels, key_bytes, max_tw)))
+                                    levels, key_bytes, max_tw, may_requeue)))
         return rc;
     if (!finish_radix || !emit) return WSORT_OK;   // the streaming finish wrote the text (K5 fused)
     return emit_keys(c, bk, d_bk, lkey, lmax, key_bytes + (double)(s.byte_off[256] - s.byte_off[lkey]));
@@ -1657,6 +1668,7 @@ int dense_branch(wsort_ctx *c, const std::vector<BucketInfo> &bk, const BucketIn
     return WSORT_OK;
 }
 
+constexpr uint32_t kSmallJobKeys = 16384, kSmallPathKeys = 1u << 20;
 // AUTO (keys only, every word <= 66 letters): the one-pass ingest already counted the words of L <= 5
 // (dense tables) and staged the longer ones as keys in per-length chunks. Dense buckets: scan + compact +
 // emit. Long buckets: the MSD's first level counts and scatters the chunks in place (chunk mode), then the
@@ -1691,8 +1703,20 @@ int sort_dense_msd(wsort_ctx *c) {
             CK(cudaStreamWaitEvent(c->hp, c->ev_hp0, 0), "hp fork wait");
             c->stream = c->hp;
         }
-        rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, W - n_dense, false,
-                           [&](const BucketInfo *, double) { return (int)WSORT_OK; }, d_bk, true, 0, true);
+        // small texts (every long bucket one finishing job of <= 16 K keys, <= 1 M long words): the staged keys
+        // regrouped by length (K3c) and each bucket finished as one job — no level-0 count / plan / scatter
+        // launches (latency-bound sizes; with a bucket of more keys the level-0 chunk path is faster: c2
+        // 0.27 vs 0.36 ms through the per-bucket MSD)
+        uint32_t max_n = 0;
+        for (uint32_t L = kDenseMaxLen + 1; L <= s.max_len; L++) max_n = std::max<uint32_t>(max_n, bk[L].n);
+        const bool small = max_n <= kSmallJobKeys && W - n_dense <= kSmallPathKeys && !getenv("WSORT_NO_SMALL");
+        if (small)
+            rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, W - n_dense, false,
+                               [&](const BucketInfo *db, double kb) { return chunk_scatter(c, db, kb); }, d_bk, true, 0,
+                               false, kSmallJobKeys);
+        else
+            rc = sort_msd_core(c, bk, kDenseMaxLen + 1, max_tw, levels, key_words, W - n_dense, false,
+                               [&](const BucketInfo *, double) { return (int)WSORT_OK; }, d_bk, true, 0, true);
         if (use_hp) {
             const int rf = arena_flush(c);   // (on the high-priority stream)
             if (!rc) rc = rf;

@@ -137,6 +137,14 @@ def test_edge_cases(ws, name, algo):
     check(ws, EDGE[name], algo)
 
 
+@pytest.mark.parametrize("name", list(EDGE))
+def test_edge_cases_chunk_level0(ws, name, monkeypatch):
+    """Small texts take the small path (keys regrouped by length, one finishing job per bucket); the same
+    edge cases through the level-0 chunk path (count0 / scatter0) that large texts take."""
+    monkeypatch.setenv("WSORT_NO_SMALL", "1")
+    check(ws, EDGE[name], "dense_msd")
+
+
 def _split_cases():
     """MSD children of > 128K keys, which the streaming finish splits into parts of 32K keys (one CTA
     each) merged by the last part: one word (all-equal runs), few distinct words (merged), too many
