@@ -1325,8 +1325,8 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
     const uint32_t fin_grid = (uint32_t)c->sms * 4;   // k_msd_fin: 4 resident CTAs per SM
     uint32_t small_done = 0, parts_done = 0, emit_done = 0;
     if (!m.finish_radix && (c->h_ctr[kQSmall] || c->h_ctr[kQTiny])) {   // jobs planned before the first level
-        if (may_requeue) {   // (whole buckets larger than a tile: one with too many distinct keys goes back to
-                             // the MSD as a level-0 segment)
+        if (may_requeue && nsegs == 0) {   // (whole buckets larger than a tile: one with too many distinct keys
+                                           // goes back to the MSD as a level-0 segment)
             m.q_big = static_cast<MsdSeg *>(c->m_big[0].p);
             m.q_tiles = static_cast<MsdTile *>(c->m_tiles[0].p);
         }
@@ -1535,6 +1535,10 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
         m.slice_hist = static_cast<uint32_t *>(c->slice_hist.p);
     }
     bool may_requeue = false;   // a whole-bucket job larger than a tile (streaming finish: may re-enter the MSD)
+    // whole buckets of up to direct_max keys are jobs only if every bucket is (a re-entering job goes to the
+    // level-0 segment queue, which must be empty otherwise)
+    for (uint32_t L = lkey; L <= lmax && direct_max; L++)
+        if (bk[L].n > direct_max) direct_max = 0;
     for (uint32_t L = lkey; L <= lmax && !from_chunks; L++) {
         const BucketInfo &b = bk[L];
         if (!b.n) continue;
