@@ -118,6 +118,10 @@ def _edge_cases():
         "staged_classes_9_11": b" ".join(bytes([97 + (i * j + 3 * j) % 26 for j in range(49 + i % 18)])
                                          for i in range(6_000)) + b" " + b"z" * 66 + b" " + b"a" * 66,
         "unstaged_67": b"ab " * 1000 + b"m" * 67 + b" x",
+        # small-text path: one bucket of 12 000 distinct 7-letter words (more than one tile, more distinct
+        # keys than a finishing table holds: the whole-bucket job re-enters the MSD as a level-0 segment)
+        "small_bucket_overflows": b" ".join(bytes([97 + (i * 7919 // 26 ** j) % 26 for j in range(7)])
+                                            for i in range(12_000)),
     }
     # a word crossing every 8 KiB boundary of a multi-step text (CTA chunk boundaries too)
     t = bytearray(b"." * (S * 40))
