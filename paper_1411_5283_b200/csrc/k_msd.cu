@@ -1547,6 +1547,81 @@ __device__ __forceinline__ uint64_t fp64(const uint32_t (&k)[KW]) {
     h ^= h >> 29;
     return h == ~0ull ? 0x5555ull : h;   // never ~0 (= empty)
 }
+// A wide job with too many distinct keys and more keys than one CTA sorts (an MSD child of 13..66-letter
+// words, nearly all distinct): instead of going back to the MSD as a segment of the next level (a count /
+// plan / scatter pass and a host sync), the CTA that found it partitions it by its next 2-letter digit into
+// the other key buffer (same positions) and appends the sub-children, packed greedily into jobs of <= one
+// tile, to the sub-job queue; a second k_msd_fin launch (sub_mode, queued right behind, no host sync) runs
+// them on every CTA. Sub-jobs are marked (buf bit 4) and never partitioned again.
+constexpr uint32_t kSubPartMax = 65536;   // largest job partitioned in a CTA (more: next MSD level)
+template <int KW>
+__device__ __forceinline__ bool fin_partition(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw) {
+    const uint32_t t = threadIdx.x, n = sg.n, q = (sg.buf >> 8) + 1;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(smraw), *cur = hist + kRadixBins, *wsum = cur + kRadixBins;
+    MsdSeg *jobs = reinterpret_cast<MsdSeg *>(wsum + 16);   // [<= 729]
+    __shared__ uint32_t s_base, s_ns;
+    const uint32_t *src = ((sg.buf & 1u) ? a.keys_a : a.keys_b) + b.key_off + (uint64_t)sg.start * KW;
+    uint32_t *dst = ((sg.buf & 1u) ? a.keys_b : const_cast<uint32_t *>(a.keys_a)) + b.key_off + (uint64_t)sg.start * KW;
+    for (uint32_t i = t; i < kRadixBins; i += kST) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t i = t; i < n; i += kST) {
+        uint32_t k[KW];
+#pragma unroll
+        for (int u = 0; u < KW; u++) k[u] = __ldg(src + (size_t)i * KW + u);
+        atomicAdd(&hist[digit_reg<KW>(k, q)], 1u);
+    }
+    __syncthreads();
+    uint32_t c[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) c[e] = hist[4 * t + e];
+    uint32_t ex = block_excl_scan_m(c[0] + c[1] + c[2] + c[3], wsum, nullptr);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        hist[4 * t + e] = ex;   // base of digit 4t+e
+        cur[4 * t + e] = ex;
+        ex += c[e];
+    }
+    __syncthreads();
+    if (t == 0) {   // the sub-jobs (greedy packing, digit order), then their queue slots (none: next MSD level)
+        const uint32_t nbuf = ((sg.buf & 1u) ^ 1u) | 16u | (q << 8);
+        uint32_t ns = 0, js = 0, jn = 0;
+        for (uint32_t d = 0; d < kRadixBins; d++) {
+            const uint32_t st = hist[d], cnt = (d + 1 < kRadixBins ? hist[d + 1] : n) - st;
+            if (!cnt) continue;
+            if (jn && jn + cnt > b.tile_keys) {
+                jobs[ns++] = MsdSeg{sg.L, sg.start + js, jn, nbuf};
+                jn = 0;
+            }
+            if (!jn) js = st;
+            jn += cnt;
+        }
+        if (jn) jobs[ns++] = MsdSeg{sg.L, sg.start + js, jn, nbuf};
+        uint32_t base = 0xffffffffu;
+        if (*reinterpret_cast<volatile uint32_t *>(a.sub_n) + ns <= a.cap_sub) {
+            base = atomicAdd(a.sub_n, ns);
+            if (base + ns > a.cap_sub) {   // (lost the race for the last slots: fill ours with empty jobs)
+                for (uint32_t k = 0; base + k < a.cap_sub && k < ns; k++) a.sub_stack[base + k] = MsdSeg{sg.L, 0, 0, 0};
+                base = 0xffffffffu;
+            }
+        }
+        s_base = base;
+        s_ns = ns;
+    }
+    __syncthreads();
+    if (s_base == 0xffffffffu) return false;
+    for (uint32_t i = t; i < n; i += kST) {
+        uint32_t k[KW];
+#pragma unroll
+        for (int u = 0; u < KW; u++) k[u] = __ldg(src + (size_t)i * KW + u);
+        const uint32_t p = atomicAdd(&cur[digit_reg<KW>(k, q)], 1u);
+#pragma unroll
+        for (int u = 0; u < KW; u++) dst[(size_t)p * KW + u] = k[u];
+    }
+    for (uint32_t k = t; k < s_ns; k += kST) a.sub_stack[s_base + k] = jobs[k];
+    __syncthreads();
+    return true;
+}
+
 template <int KW, bool PART>
 __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw,
                                                 const FinPart pr) {
@@ -1694,12 +1769,19 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
 #pragma unroll
                 for (int u = 0; u < KW; u++) k[u] = kb[(size_t)i * KW + u];
             });
-        } else if (t == 0) {   // one child larger than a tile: back to the MSD as a segment of the next
-                               // level (a child without digits left holds one key only: this terminates)
-            const uint32_t nt = (n + b.aux - 1) / b.aux;
-            const uint32_t q = atomicAdd(a.ctr + kQBig, 1u), t0 = atomicAdd(a.ctr + kQTiles, nt);
-            if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, n, sg.buf & 1u};
-            for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++) a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, n - i * b.aux), 0};
+        } else {
+            bool done = false;   // partitioned here: the sub-jobs run in the sub_mode launch
+            if (!PART && a.sub_stack && !(sg.buf & 16u) && n <= kSubPartMax && (sg.buf >> 8) + 1 < b.ndig) {
+                __syncthreads();
+                done = fin_partition<KW>(a, sg, b, smraw);
+            }
+            if (!done && t == 0) {   // one child larger than a tile: back to the MSD as a segment of the next
+                                     // level (a child without digits left holds one key only: this terminates)
+                const uint32_t nt = (n + b.aux - 1) / b.aux;
+                const uint32_t q = atomicAdd(a.ctr + kQBig, 1u), t0 = atomicAdd(a.ctr + kQTiles, nt);
+                if (q < a.cap_big) a.q_big[q] = MsdSeg{sg.L, sg.start, n, sg.buf & 1u};
+                for (uint32_t i = 0; i < nt && t0 + i < a.cap_tiles; i++) a.q_tiles[t0 + i] = MsdTile{q, i * b.aux, min(b.aux, n - i * b.aux), 0};
+            }
         }
         return;
     }
@@ -1830,14 +1912,20 @@ __device__ __forceinline__ void fin_job(const MsdArgs &a, const MsdSeg &sg, cons
 __global__ void __launch_bounds__(kST, 4) k_msd_fin(MsdArgs a) {
     extern __shared__ __align__(16) uint8_t fsm[];
     __shared__ uint32_t s_job;
-    const uint32_t np = min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQParts), a.cap_parts) - a.parts_base;
-    const uint32_t end = np + min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQSmall), a.cap_local) - a.small_base;
+    // (sub_mode: the jobs are the sub-jobs fin_partition queued during the previous launch)
+    const uint32_t np = a.sub_mode ? 0u : min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQParts), a.cap_parts) - a.parts_base;
+    const uint32_t end = a.sub_mode ? min(*reinterpret_cast<volatile uint32_t *>(a.sub_n), a.cap_sub)
+                                    : np + min(*reinterpret_cast<volatile uint32_t *>(a.ctr + kQSmall), a.cap_local) - a.small_base;
     for (;;) {
     if (threadIdx.x == 0) s_job = atomicAdd(a.ctr + kQFinTicket, 1u);
     __syncthreads();
     const uint32_t j = s_job;
     if (j >= end) break;
-    const MsdSeg sg = j < np ? a.q_tiny[a.q_parts[a.parts_base + j]] : a.q_small[a.small_base + j - np];
+    const MsdSeg sg = a.sub_mode ? a.sub_stack[j] : j < np ? a.q_tiny[a.q_parts[a.parts_base + j]] : a.q_small[a.small_base + j - np];
+    if (sg.n == 0) {   // (a sub-job slot left empty)
+        __syncthreads();
+        continue;
+    }
     if (j < np && job_parts(sg.n) > 1) {   // a part of a split job: k_msd_fin_split's
         __syncthreads();
         continue;
@@ -2010,6 +2098,17 @@ cudaError_t launch_msd_fin_jobs(const MsdArgs &a, uint32_t first, uint32_t first
     if (e != cudaSuccess) return e;
     k_msd_fin<<<grid, kST, kFinSmem, s>>>(b);
     return cudaGetLastError();
+}
+
+cudaError_t launch_msd_fin_sub(const MsdArgs &a, uint32_t grid, cudaStream_t s) {
+    if (!a.sub_stack || !grid) return cudaSuccess;
+    MsdArgs b = a;
+    b.sub_mode = 1;
+    cudaError_t e = cudaMemsetAsync(a.ctr + kQFinTicket, 0, 4, s);
+    if (e != cudaSuccess) return e;
+    k_msd_fin<<<grid, kST, kFinSmem, s>>>(b);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaMemsetAsync(a.sub_n, 0, 4, s);   // (the queue is empty again for the next launch)
 }
 
 cudaError_t launch_msd_fin_split(const MsdArgs &a, uint32_t first_part, uint32_t grid, cudaStream_t s) {

@@ -78,7 +78,7 @@ struct wsort_ctx {
     bool cta_counts_ready = false; // K1b's per-CTA histograms are in cta_hist (K2b needs them)
 
     // K1 ingest: global histogram, dense counts, staging chunks
-    DevBuf ghist, dense, pool, chunk_cls, chunk_fill, ig_ctr, d_touched, cls_list, slice_hist;
+    DevBuf ghist, dense, pool, chunk_cls, chunk_fill, ig_ctr, d_touched, cls_list, slice_hist, m_sub, m_subn;
     bool dense_clean = false;                    // the dense table has been zeroed once (then: touched blocks)
     uint32_t *h_ig = nullptr;   // pinned mirror of ig_ctr
     uint32_t cta_chunks = 0, n_chunks = 0;
@@ -452,7 +452,7 @@ void wsort_destroy(wsort_ctx *c) {
                       &c->m_hist, &c->m_cursor, &c->m_ctr, &c->m_big[0], &c->m_big[1], &c->m_tiles[0],
                       &c->m_tiles[1], &c->m_tiny, &c->m_small, &c->m_copy, &c->m_skip, &c->m_pat, &c->m_qparts, &c->m_pbase, &c->m_jdone,
                       &c->m_jovf, &c->m_partn, &c->m_plist, &c->m_qemit, &c->ghist, &c->dense,
-                      &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->cls_list, &c->slice_hist, &c->d_blk_sum, &c->d_blk_nnz,
+                      &c->pool, &c->chunk_cls, &c->chunk_fill, &c->ig_ctr, &c->cls_list, &c->slice_hist, &c->m_sub, &c->m_subn, &c->d_blk_sum, &c->d_blk_nnz,
                       &c->d_ent_idx, &c->d_ent_end, &c->d_n_ent, &c->d_touched, &c->d_tiles2, &c->d_lcursor, &c->d_tile_e,
                       &c->t_wlens, &c->t_nkey, &c->t_ncnt, &c->t_fp, &c->t_meta, &c->t_cnt, &c->t_keys, &c->t_top, &c->t_dcount, &c->t_runend,
                       &c->t_scan, &c->t_tilee, &c->t_kplan, &c->t_dpfx, &c->t_rpfx, &c->x_vec, &c->x_counts,
@@ -1243,6 +1243,10 @@ int msd_alloc(wsort_ctx *c, MsdArgs &m, uint64_t W, uint64_t key_words) {
     if ((rc = ensure(c, c->m_ctr, kQCount * 4, "msd counters"))) return rc;
     if ((rc = ensure(c, c->m_skip, (size_t)cap_big * 4, "msd skip flags"))) return rc;
     if ((rc = ensure(c, c->m_pat, (size_t)c->sms * 4 * kFinPatBytes, "finish patterns"))) return rc;
+    // sub-jobs of the jobs a finishing CTA partitions itself (fin_partition), run by a second k_msd_fin launch
+    const uint32_t cap_sub = (uint32_t)(W / 64 + 65536);
+    if ((rc = ensure(c, c->m_sub, (size_t)cap_sub * sizeof(MsdSeg), "finish sub-jobs"))) return rc;
+    if ((rc = ensure(c, c->m_subn, 16, "finish sub-job count", true))) return rc;
     // finishing tickets of big jobs (> 16384 keys: one each, or one per part of <= kPartKeys keys when
     // split): <= W / 16384 + 2 W / kPartKeys
     const uint32_t cap_parts = (uint32_t)(W / 16384 + 2 * W / kPartKeys + 64);
@@ -1271,6 +1275,10 @@ int msd_alloc(wsort_ctx *c, MsdArgs &m, uint64_t W, uint64_t key_words) {
     m.keys_b = static_cast<uint32_t *>(c->keys_b.p);
     m.seg_skip = static_cast<uint32_t *>(c->m_skip.p);
     m.pat = static_cast<uint8_t *>(c->m_pat.p);
+    static const bool no_sub = getenv("WSORT_NO_SUBPART") != nullptr;   // (experiments)
+    m.sub_stack = no_sub ? nullptr : static_cast<MsdSeg *>(c->m_sub.p);
+    m.sub_n = static_cast<uint32_t *>(c->m_subn.p);
+    m.cap_sub = cap_sub;
     m.cap_parts = cap_parts;
     m.q_parts = static_cast<uint32_t *>(c->m_qparts.p);
     m.job_pbase = static_cast<uint32_t *>(c->m_pbase.p);
@@ -1387,6 +1395,8 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
             CK(cudaEventRecord(c->ev_split, sp), "split event");
             rc = launch(c, "k4m_msd_finish", level == 0 ? 2 * key_bytes : 0,
                         [&] { return launch_msd_fin_jobs(m, small_done, parts_done, fin_grid, c->stream); });
+            if (rc) return rc;
+            rc = launch(c, "k4m_msd_fin_sub", 0, [&] { return launch_msd_fin_sub(m, fin_grid, c->stream); });
             if (rc) return rc;
             CK(cudaStreamWaitEvent(c->stream, c->ev_split, 0), "split wait");
             if (dbg) {

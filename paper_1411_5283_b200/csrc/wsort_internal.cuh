@@ -450,12 +450,16 @@ struct MsdArgs {
     uint32_t cls_pfx[kMaxStageKw + 1];   // chunks of classes < K: the classes' lists concatenated (scatter0)
     const uint32_t *pool, *chunk_fill, *cls_list, *cls_cnt;
     uint32_t *slice_hist;          // [nslices][kC0Bins] (nullable) each slice's bins, for k_msd_scatter0's ranges
+    MsdSeg *sub_stack;             // (nullable) [cap_sub] sub-jobs of the jobs a finishing CTA partitioned
+    uint32_t *sub_n;               // [1] sub-jobs queued (reset after the sub_mode launch)
+    uint32_t cap_sub, sub_mode;    // sub_mode: this k_msd_fin launch runs the queued sub-jobs
 };
 size_t msd_scatter_smem();
 constexpr uint32_t kFinPatBytes = 1024 * 48;   // >= max distinct keys x pattern width (1024 x 32, 512 x 88)
 cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
 cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s);
-cudaError_t launch_msd_count0(const MsdArgs &a, cudaStream_t s);     // chunk mode, level 0: a.nslices CTAs
+cudaError_t launch_msd_count0(const MsdArgs &a, cudaStream_t s);
+cudaError_t launch_msd_fin_sub(const MsdArgs &a, uint32_t grid, cudaStream_t s);   // k_msd_fin over the sub-job queue     // chunk mode, level 0: a.nslices CTAs
 cudaError_t launch_msd_scatter0(const MsdArgs &a, cudaStream_t s);
 cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
 cudaError_t launch_msd_finish(const MsdArgs &a, uint32_t n_small, uint32_t n_copy, uint32_t max_tile_words,
