@@ -1554,9 +1554,12 @@ __device__ __forceinline__ uint64_t fp64(const uint32_t (&k)[KW]) {
 // tile, to the sub-job queue; a second k_msd_fin launch (sub_mode, queued right behind, no host sync) runs
 // them on every CTA. Sub-jobs are marked (buf bit 4) and never partitioned again.
 constexpr uint32_t kSubPartMax = 65536;   // largest job partitioned in a CTA (more: next MSD level)
+// the digit a job's keys are partitioned by next: 0 for a whole bucket (the small-text path's jobs), else
+// the one after the job's level
+__device__ __forceinline__ uint32_t fin_next_digit(const MsdSeg &sg) { return (sg.buf & kSegWhole) ? 0u : (sg.buf >> 8) + 1u; }
 template <int KW>
 __device__ __forceinline__ bool fin_partition(const MsdArgs &a, const MsdSeg &sg, const BucketInfo &b, uint8_t *smraw) {
-    const uint32_t t = threadIdx.x, n = sg.n, q = (sg.buf >> 8) + 1;
+    const uint32_t t = threadIdx.x, n = sg.n, q = fin_next_digit(sg);
     uint32_t *hist = reinterpret_cast<uint32_t *>(smraw), *cur = hist + kRadixBins, *wsum = cur + kRadixBins;
     MsdSeg *jobs = reinterpret_cast<MsdSeg *>(wsum + 16);   // [<= 729]
     __shared__ uint32_t s_base, s_ns;
@@ -1771,7 +1774,7 @@ __device__ __forceinline__ void fin_stream_wide(const MsdArgs &a, const MsdSeg &
             });
         } else {
             bool done = false;   // partitioned here: the sub-jobs run in the sub_mode launch
-            if (!PART && a.sub_stack && !(sg.buf & 16u) && n <= kSubPartMax && (sg.buf >> 8) + 1 < b.ndig) {
+            if (!PART && a.sub_stack && !(sg.buf & 16u) && n <= kSubPartMax && fin_next_digit(sg) < b.ndig) {
                 __syncthreads();
                 done = fin_partition<KW>(a, sg, b, smraw);
             }

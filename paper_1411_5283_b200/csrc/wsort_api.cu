@@ -1340,6 +1340,9 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         }
         rc = launch(c, "k4m_msd_finish", 0, [&] { return launch_msd_fin_jobs(m, 0, 0, fin_grid, c->stream); });
         if (rc) return rc;
+        // the sub-jobs of the whole-bucket jobs their finishing CTAs partitioned (fin_partition)
+        rc = launch(c, "k4m_msd_fin_sub", 0, [&] { return launch_msd_fin_sub(m, fin_grid, c->stream); });
+        if (rc) return rc;
         small_done = c->h_ctr[kQSmall];
         parts_done = c->h_ctr[kQParts];
         if (may_requeue && nsegs == 0) {
@@ -1554,7 +1557,7 @@ int sort_msd_core(wsort_ctx *c, std::vector<BucketInfo> &bk, uint32_t lkey, uint
         if (!b.n) continue;
         if (b.n <= std::max(b.tile_keys, direct_max)) {
             may_requeue |= b.n > b.tile_keys;
-            (finish_radix ? b.n <= 32 : b.n > 16384) ? tiny.push_back(MsdSeg{L, 0, b.n, 1}) : small.push_back(MsdSeg{L, 0, b.n, 1});
+            (finish_radix ? b.n <= 32 : b.n > 16384) ? tiny.push_back(MsdSeg{L, 0, b.n, 1 | kSegWhole}) : small.push_back(MsdSeg{L, 0, b.n, 1 | kSegWhole});
         } else {
             const uint32_t q = (uint32_t)segs.size();
             segs.push_back(MsdSeg{L, 0, b.n, 1});   // packed into buffer A

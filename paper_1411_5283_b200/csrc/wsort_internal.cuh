@@ -384,8 +384,11 @@ cudaError_t launch_regroup(const CopyRange *ranges, uint32_t nranges, const uint
 // ---------------- msd_radix: MSD partitioning + CTA-local odd-even transposition finish ----------------
 struct MsdSeg {
     uint32_t L, start, n, buf;     // key range [start, start+n) of bucket L; buf bit 0: 1 = in A, 0 = in B
-                                   // (segments and jobs alike); buf >> 8: the job's level (sort jobs)
+                                   // (segments and jobs alike); buf >> 8: the job's level (sort jobs) = the
+                                   // last digit its keys were partitioned by; bit 4: a sub-job of
+                                   // fin_partition; bit 5 (kSegWhole): a whole bucket, no digit partitioned
 };
+constexpr uint32_t kSegWhole = 32u;
 struct MsdTile {
     uint32_t seg, off, n, pad_;    // keys [off, off+n) of segment `seg` of this level
 };

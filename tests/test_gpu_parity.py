@@ -122,6 +122,12 @@ def _edge_cases():
         # keys than a finishing table holds: the whole-bucket job re-enters the MSD as a level-0 segment)
         "small_bucket_overflows": b" ".join(bytes([97 + (i * 7919 // 26 ** j) % 26 for j in range(7)])
                                             for i in range(12_000)),
+        # small-text path, wide keys: whole buckets of 3000 distinct 19- / 40-letter words (more than one
+        # tile, more distinct keys than a finishing table holds): the finishing CTA partitions the whole
+        # bucket itself, by digit 0 (first two letters, which vary here), into sub-jobs
+        "small_wide_bucket_partitioned": b" ".join(
+            bytes([97 + (i * 7919 + (i * i >> j % 11) * (j + 1)) % 26 for j in range(19 if i % 2 else 40)])
+            for i in range(6_000)),
     }
     # a word crossing every 8 KiB boundary of a multi-step text (CTA chunk boundaries too)
     t = bytearray(b"." * (S * 40))
