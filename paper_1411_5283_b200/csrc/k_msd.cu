@@ -42,6 +42,7 @@ __device__ __forceinline__ uint32_t digit_reg(const uint32_t (&k)[KW], uint32_t 
     return (w >> (20 - 10 * (q % 3))) & 1023u;
 }
 
+template <int NT = kST>
 __device__ __forceinline__ uint32_t block_excl_scan_m(uint32_t v, uint32_t *wsum, uint32_t *total) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     uint32_t incl = v;
@@ -53,18 +54,18 @@ __device__ __forceinline__ uint32_t block_excl_scan_m(uint32_t v, uint32_t *wsum
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        uint32_t w = lane < kST / 32 ? wsum[lane] : 0u, wi = w;
+        uint32_t w = lane < NT / 32 ? wsum[lane] : 0u, wi = w;
 #pragma unroll
-        for (int o = 1; o < kST / 32; o <<= 1) {
+        for (int o = 1; o < NT / 32; o <<= 1) {
             uint32_t y = __shfl_up_sync(kFullM, wi, o);
             if (lane >= o) wi += y;
         }
-        if (lane < kST / 32) wsum[lane] = wi - w;
-        if (lane == kST / 32 - 1) wsum[kST / 32] = wi;
+        if (lane < NT / 32) wsum[lane] = wi - w;
+        if (lane == NT / 32 - 1) wsum[NT / 32] = wi;
     }
     __syncthreads();
     const uint32_t r = wsum[warp] + incl - v;
-    if (total) *total = wsum[kST / 32];
+    if (total) *total = wsum[NT / 32];
     __syncthreads();
     return r;
 }
@@ -464,10 +465,15 @@ __global__ void __launch_bounds__(kST) k_msd_count0(MsdArgs a) {
     }
 }
 
-constexpr uint32_t kS0PerThread = kC0Bins / kST;   // 24 contiguous bins per thread in the scans
+#ifndef WSORT_S0_THREADS
+#define WSORT_S0_THREADS 512
+#endif
+constexpr int kS0T = WSORT_S0_THREADS;   // k_msd_scatter0's threads (2 CTAs / SM: 32 warps hide the chunk phases)
+constexpr uint32_t kS0PerThread = kC0Bins / kS0T;   // 12 contiguous bins per thread in the scans
+static_assert(kS0PerThread % 4 == 0 && kS0T / 32 + 1 <= 32, "scatter0 scan layout");
 constexpr uint32_t kS0Kout = kChunkWords + kChunkWords / 32 + 8;
 // [2][kChunkWords] TMA buffers | bar[2] | gb[kC0Bins] | off[kC0Bins] | kout | pbin (u16)[kChunkWords] | wsum
-constexpr size_t kScatter0Smem = 2 * kChunkWords * 4 + 16 + 2 * kC0Bins * 4 + kS0Kout * 4 + kChunkWords * 2 + 64;
+constexpr size_t kScatter0Smem = 2 * kChunkWords * 4 + 16 + 2 * kC0Bins * 4 + kS0Kout * 4 + kChunkWords * 2 + 4 * (kS0T / 32 + 1);
 
 #ifndef WSORT_S0_SLICE
 #define WSORT_S0_SLICE 1
@@ -484,19 +490,19 @@ template <int K, bool SLICE>
 __device__ __forceinline__ void scatter0_chunk(const MsdArgs &a, const uint32_t *kin, uint32_t n, uint32_t *gb,
                                                uint32_t *off, uint32_t *kout, uint16_t *pbin, uint32_t *wsum,
                                                uint64_t *koff, uint64_t wpol) {
-    constexpr uint32_t cap = 1u << chunk_lg(K), KPT = (cap + kST - 1) / kST, L0 = 6u * K - 5u;
+    constexpr uint32_t cap = 1u << chunk_lg(K), KPT = (cap + kS0T - 1) / kS0T, L0 = 6u * K - 5u;
     const uint32_t t = threadIdx.x;
     if (t < 6) koff[t] = L0 + t >= a.seg_l0 ? a.buckets[L0 + t].key_off : 0;
     uint32_t key[KPT][K], bin[KPT], slot[KPT];
 #pragma unroll
     for (uint32_t r = 0; r < KPT; r++) {
-        const uint32_t i = t + r * kST;
+        const uint32_t i = t + r * kS0T;
 #pragma unroll
         for (int u = 0; u < K; u++) key[r][u] = i < n ? kin[u * cap + i] : 0u;
     }
 #pragma unroll
     for (uint32_t r = 0; r < KPT; r++) {
-        const uint32_t i = t + r * kST;
+        const uint32_t i = t + r * kS0T;
         bin[r] = ((key_len0(i < n ? key[r][K - 1] : 1u, K) - L0) << 10) | (key[r][0] >> 20);
         slot[r] = i < n ? atomicAdd(&off[bin[r]], 1u) : 0u;
     }
@@ -513,7 +519,7 @@ __device__ __forceinline__ void scatter0_chunk(const MsdArgs &a, const uint32_t 
         cnt[4 * q + 3] = v.w;
         sum += v.x + v.y + v.z + v.w;
     }
-    uint32_t ex = block_excl_scan_m(sum, wsum, nullptr);   // (its barriers order the reads above before the writes)
+    uint32_t ex = block_excl_scan_m<kS0T>(sum, wsum, nullptr);   // (its barriers order the reads above before the writes)
     const uint32_t b0 = kS0PerThread * t;
     uint32_t g[SLICE ? 1 : kS0PerThread];
     if (!SLICE) {
@@ -545,7 +551,7 @@ __device__ __forceinline__ void scatter0_chunk(const MsdArgs &a, const uint32_t 
     // reorder by bin in shared memory (key-major, padded)
 #pragma unroll
     for (uint32_t r = 0; r < KPT; r++) {
-        const uint32_t i = t + r * kST;
+        const uint32_t i = t + r * kS0T;
         if (i < n) {
             const uint32_t p = off[bin[r]] + slot[r];
 #pragma unroll
@@ -557,7 +563,7 @@ __device__ __forceinline__ void scatter0_chunk(const MsdArgs &a, const uint32_t 
         }
     }
     __syncthreads();
-    for (uint32_t i = t; i < n * K; i += kST) {
+    for (uint32_t i = t; i < n * K; i += kS0T) {
         const uint32_t p = i / K, u = i - p * K, b = pbin[p];
         uint32_t *dst = a.keys_b + koff[b >> 10] + (uint64_t)(gb[b] + p) * K + u;
 #if WSORT_S0_HINT
@@ -585,7 +591,7 @@ __device__ __forceinline__ void scatter0_chunk(const MsdArgs &a, const uint32_t 
 // else persistent over the classes' lists concatenated (CTA b: chunks b, b + grid, ...). The next chunk is
 // fetched by a TMA bulk copy (evict-first: read once) into the other buffer while this one is scattered;
 // the scattered keys are stored evict-last (the sectors a later chunk completes stay in L2).
-__global__ void __launch_bounds__(kST, 2) k_msd_scatter0(MsdArgs a, uint32_t total) {
+__global__ void __launch_bounds__(kS0T, 2) k_msd_scatter0(MsdArgs a, uint32_t total) {
     extern __shared__ __align__(128) uint32_t s0m[];
     uint32_t *inb = s0m;                                                      // [2][kChunkWords]
     uint64_t *bar = reinterpret_cast<uint64_t *>(s0m + 2 * kChunkWords);     // [2]
@@ -593,7 +599,7 @@ __global__ void __launch_bounds__(kST, 2) k_msd_scatter0(MsdArgs a, uint32_t tot
     uint32_t *off = gb + kC0Bins;                                             // [kC0Bins] counts / offsets
     uint32_t *kout = off + kC0Bins;
     uint16_t *pbin = reinterpret_cast<uint16_t *>(kout + kS0Kout);
-    uint32_t *wsum = reinterpret_cast<uint32_t *>(pbin + kChunkWords);        // [kST / 32 + 1]
+    uint32_t *wsum = reinterpret_cast<uint32_t *>(pbin + kChunkWords);        // [kS0T / 32 + 1]
     __shared__ uint64_t koff[6];
     __shared__ uint32_t s_n[2], s_k[2];
     const uint32_t t = threadIdx.x;
@@ -631,12 +637,12 @@ __global__ void __launch_bounds__(kST, 2) k_msd_scatter0(MsdArgs a, uint32_t tot
         const Slice0 sc = slice0_of(a, blockIdx.x);
         const uint32_t L0 = 6u * sc.K - 5u;
         const uint32_t *sh = a.slice_hist + (size_t)blockIdx.x * kC0Bins;
-        for (uint32_t b = t; b < kC0Bins; b += kST) {
+        for (uint32_t b = t; b < kC0Bins; b += kS0T) {
             const uint32_t v = __ldg(sh + b);
             gb[b] = v ? atomicAdd(&a.cursor[(size_t)(L0 + (b >> 10) - a.seg_l0) * kRadixBins + (b & 1023u)], v) : 0u;
         }
     }
-    for (uint32_t b = t; b < kC0Bins; b += kST) off[b] = 0;
+    for (uint32_t b = t; b < kC0Bins; b += kS0T) off[b] = 0;
     __syncthreads();
     for (uint32_t j = j0, it = 0; j < j1; j += step, it++) {
         const uint32_t cur = it & 1;
@@ -2063,7 +2069,7 @@ cudaError_t launch_msd_scatter0(const MsdArgs &a, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t total = a.cls_pfx[kMaxStageKw];
     const uint32_t grid = WSORT_S0_SLICE ? a.nslices : std::min<uint32_t>(total, (uint32_t)sms * 2);
-    k_msd_scatter0<<<grid, kST, kScatter0Smem, s>>>(a, total);
+    k_msd_scatter0<<<grid, kS0T, kScatter0Smem, s>>>(a, total);
     return cudaGetLastError();
 }
 cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s) {
