@@ -136,10 +136,11 @@ __global__ void __launch_bounds__(kST) k_msd_plan(MsdArgs a) {
 #pragma unroll
     for (int e = 0; e < 4; e++) {
         const uint32_t d = 4 * t + e;
-        a.cursor[(size_t)s * kRadixBins + d] = sg.start + ex;
+        if (a.plan_mode != 2) a.cursor[(size_t)s * kRadixBins + d] = sg.start + ex;   // (mode 2: being consumed)
         if (c[e]) nz_d[nzx++] = sg.start + ex;
         ex += c[e];
     }
+    if (a.plan_mode == 1) return;   // the scatter's cursors only; the jobs are planned beside the scatter
     __syncthreads();
     const uint32_t src_a = sg.buf & 1u, dst_a = src_a ^ 1u;   // where the segment is / its children go
     // (chunk mode: the keys are in the staging chunks, every segment is scattered)
@@ -2072,9 +2073,11 @@ cudaError_t launch_msd_scatter0(const MsdArgs &a, cudaStream_t s) {
     k_msd_scatter0<<<grid, kS0T, kScatter0Smem, s>>>(a, total);
     return cudaGetLastError();
 }
-cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s) {
+cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s, uint32_t mode) {
     if (!nsegs) return cudaSuccess;
-    k_msd_plan<<<nsegs, kST, 0, s>>>(a);
+    MsdArgs b = a;
+    b.plan_mode = mode;
+    k_msd_plan<<<nsegs, kST, 0, s>>>(b);
     return cudaGetLastError();
 }
 cudaError_t launch_msd_scatter(const MsdArgs &a, uint32_t ntiles, cudaStream_t s) {

@@ -59,7 +59,7 @@ struct wsort_ctx {
     cudaStream_t split = nullptr;                // third stream: parts of split finishing jobs beside k_msd_fin
     cudaStream_t hp = nullptr;                   // high-priority stream: the long words' MSD (the critical path)
     cudaEvent_t ev_hp0 = nullptr, ev_hp1 = nullptr;   // beside the dense branch, which fills the idle SMs
-    cudaEvent_t ev_lvl = nullptr, ev_split = nullptr;
+    cudaEvent_t ev_lvl = nullptr, ev_split = nullptr, ev_plan = nullptr;
     int sms = 148;
     State state = ST_CREATED;
     char err[512] = {0};
@@ -484,6 +484,7 @@ void wsort_destroy(wsort_ctx *c) {
     if (c->split) cudaStreamDestroy(c->split);
     if (c->ev_lvl) cudaEventDestroy(c->ev_lvl);
     if (c->ev_split) cudaEventDestroy(c->ev_split);
+    if (c->ev_plan) cudaEventDestroy(c->ev_plan);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (auto e : c->copy_ev) cudaEventDestroy(e);
     if (c->ev_ingest) cudaEventDestroy(c->ev_ingest);
@@ -1324,6 +1325,18 @@ int msd_read_counters(wsort_ctx *c, const MsdArgs &m, uint32_t &nsegs, uint32_t 
     return WSORT_OK;
 }
 
+// The third stream (high priority): split finishing jobs, and level 0's job planning beside the scatter
+int ensure_split_stream(wsort_ctx *c) {
+    if (c->split) return WSORT_OK;
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+    CK(cudaStreamCreateWithPriority(&c->split, cudaStreamNonBlocking, greatest), "split stream");
+    CK(cudaEventCreateWithFlags(&c->ev_lvl, cudaEventDisableTiming), "level event");
+    CK(cudaEventCreateWithFlags(&c->ev_split, cudaEventDisableTiming), "split event");
+    CK(cudaEventCreateWithFlags(&c->ev_plan, cudaEventDisableTiming), "plan event");
+    return WSORT_OK;
+}
+
 // MSD levels from `level` on (its segments / tiles are in m_big[level & 1] / m_tiles[level & 1]) until no
 // segment is left, then the finishing sorts: every key ends in buffer B at its final index.
 int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nsegs, uint32_t ntiles, uint32_t levels,
@@ -1350,6 +1363,7 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
             small_done = std::min(c->h_ctr[kQSmall], m.cap_local);
         }
     }
+    static const bool no_plan_beside = getenv("WSORT_NO_PLAN_BESIDE") != nullptr;   // (experiments)
     for (; nsegs > 0; level++) {
         if (level >= levels) return set_err(c, WSORT_E_CUDA, "msd: segments left after the last digit");
         if ((rc = msd_level_buffers(c, m, level, nsegs))) return rc;
@@ -1359,13 +1373,30 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
         else
             rc = launch(c, "k4m_msd_count", seg_bytes, [&] { return launch_msd_count(m, ntiles, c->stream); });
         if (rc) return rc;
-        rc = launch(c, "k4m_msd_plan", (double)nsegs * kRadixBins * 8, [&] { return launch_msd_plan(m, nsegs, c->stream); });
-        if (rc) return rc;
+        // level 0 of the streaming path: the scatter needs only the children's cursors; the finishing jobs
+        // are planned on the split stream beside it (the serial per-segment job packing is off the critical path)
+        const bool plan_beside = m.chunk_mode && !m.finish_radix && !c->prof_serial && !no_plan_beside;
+        if (plan_beside) {
+            if ((rc = ensure_split_stream(c))) return rc;
+            rc = launch(c, "k4m_msd_plan", (double)nsegs * kRadixBins * 4, [&] { return launch_msd_plan(m, nsegs, c->stream, 1); });
+            if (rc) return rc;
+            if ((rc = arena_flush(c))) return rc;
+            CK(cudaEventRecord(c->ev_lvl, c->stream), "plan event");
+            CK(cudaStreamWaitEvent(c->split, c->ev_lvl, 0), "plan wait");
+            rc = launch_on(c, c->split, "k4m_msd_plan_jobs", (double)nsegs * kRadixBins * 4,
+                           [&] { return launch_msd_plan(m, nsegs, c->split, 2); });
+            if (rc) return rc;
+            CK(cudaEventRecord(c->ev_plan, c->split), "plan jobs event");
+        } else {
+            rc = launch(c, "k4m_msd_plan", (double)nsegs * kRadixBins * 8, [&] { return launch_msd_plan(m, nsegs, c->stream); });
+            if (rc) return rc;
+        }
         if (m.chunk_mode)
             rc = launch(c, "k4m_msd_scatter0", 2 * seg_bytes, [&] { return launch_msd_scatter0(m, c->stream); });
         else
             rc = launch(c, "k4m_msd_scatter", 2 * seg_bytes, [&] { return launch_msd_scatter(m, ntiles, c->stream); });
         if (rc) return rc;
+        if (plan_beside) CK(cudaStreamWaitEvent(c->stream, c->ev_plan, 0), "plan jobs wait");
         m.chunk_mode = 0;   // (only level 0 reads the staging chunks)
         if (!m.finish_radix) {   // this level's finishing jobs (their count is on the device); a job with too
                                  // many distinct keys re-enters the next level
@@ -1378,13 +1409,7 @@ int msd_levels_and_finish(wsort_ctx *c, MsdArgs &m, uint32_t level, uint32_t nse
             }
             // the parts of split jobs (if any: their number is on the device) on the third stream, beside
             // the whole jobs; then the text of the split jobs, by pieces
-            if (!c->split) {
-                int least = 0, greatest = 0;
-                CK(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
-                CK(cudaStreamCreateWithPriority(&c->split, cudaStreamNonBlocking, greatest), "split stream");
-                CK(cudaEventCreateWithFlags(&c->ev_lvl, cudaEventDisableTiming), "level event");
-                CK(cudaEventCreateWithFlags(&c->ev_split, cudaEventDisableTiming), "split event");
-            }
+            if ((rc = ensure_split_stream(c))) return rc;
             if ((rc = arena_flush(c))) return rc;
             CK(cudaEventRecord(c->ev_lvl, c->stream), "level event");
             cudaStream_t sp = c->prof_serial ? c->stream : c->split;   // (serial profiling: one stream)

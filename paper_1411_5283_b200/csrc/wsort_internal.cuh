@@ -456,11 +456,12 @@ struct MsdArgs {
     MsdSeg *sub_stack;             // (nullable) [cap_sub] sub-jobs of the jobs a finishing CTA partitioned
     uint32_t *sub_n;               // [1] sub-jobs queued (reset after the sub_mode launch)
     uint32_t cap_sub, sub_mode;    // sub_mode: this k_msd_fin launch runs the queued sub-jobs
+    uint32_t plan_mode;            // k_msd_plan: 0 = cursors + jobs, 1 = cursors only, 2 = jobs only
 };
 size_t msd_scatter_smem();
 constexpr uint32_t kFinPatBytes = 1024 * 48;   // >= max distinct keys x pattern width (1024 x 32, 512 x 88)
 cudaError_t launch_msd_count(const MsdArgs &a, uint32_t ntiles, cudaStream_t s);
-cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s);
+cudaError_t launch_msd_plan(const MsdArgs &a, uint32_t nsegs, cudaStream_t s, uint32_t mode = 0);
 cudaError_t launch_msd_count0(const MsdArgs &a, cudaStream_t s);
 cudaError_t launch_msd_fin_sub(const MsdArgs &a, uint32_t grid, cudaStream_t s);   // k_msd_fin over the sub-job queue     // chunk mode, level 0: a.nslices CTAs
 cudaError_t launch_msd_scatter0(const MsdArgs &a, cudaStream_t s);
