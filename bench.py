@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--algo", default="auto")
+    ap.add_argument("--ingest", default="auto", choices=["auto", "stage", "count"],
+                    help="how K1 treats the words of >= 6 letters (wsort_set_ingest; experiments)")
     ap.add_argument("--impl", default="wsort", choices=["wsort", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-sample-mb", type=int, default=96)
@@ -255,6 +257,8 @@ def run_wsort(args, rank, world, local_rank):
     host = torch.empty(cfg.n, dtype=torch.uint8, pin_memory=True)
     text, _ = gen.generate(args.config, out=host.numpy())
     ws = WSort(dev, stream=stream.cuda_stream)
+    if args.ingest != "auto":
+        ws.set_ingest(args.ingest)
     ws.load_text(host)
     n_words = ws.tokenize()
     ws.sort(args.algo)

@@ -638,10 +638,16 @@ __global__ void __launch_bounds__(kS0T, 2) k_msd_scatter0(MsdArgs a, uint32_t to
         const Slice0 sc = slice0_of(a, blockIdx.x);
         const uint32_t L0 = 6u * sc.K - 5u;
         const uint32_t *sh = a.slice_hist + (size_t)blockIdx.x * kC0Bins;
-        for (uint32_t b = t; b < kC0Bins; b += kS0T) {
-            const uint32_t v = __ldg(sh + b);
-            gb[b] = v ? atomicAdd(&a.cursor[(size_t)(L0 + (b >> 10) - a.seg_l0) * kRadixBins + (b & 1023u)], v) : 0u;
+        uint32_t v[kS0PerThread], g[kS0PerThread];   // (all loads, then all atomics in flight together)
+#pragma unroll
+        for (uint32_t r = 0; r < kS0PerThread; r++) v[r] = __ldg(sh + t + r * kS0T);
+#pragma unroll
+        for (uint32_t r = 0; r < kS0PerThread; r++) {
+            const uint32_t b = t + r * kS0T;
+            g[r] = v[r] ? atomicAdd(&a.cursor[(size_t)(L0 + (b >> 10) - a.seg_l0) * kRadixBins + (b & 1023u)], v[r]) : 0u;
         }
+#pragma unroll
+        for (uint32_t r = 0; r < kS0PerThread; r++) gb[t + r * kS0T] = g[r];
     }
     for (uint32_t b = t; b < kC0Bins; b += kS0T) off[b] = 0;
     __syncthreads();
@@ -1210,7 +1216,7 @@ __device__ __forceinline__ uint8_t run_byte(const uint8_t *R, uint32_t W, const 
 __device__ __forceinline__ void emit_runs_text(const MsdArgs &a, const BucketInfo &b, uint32_t L, uint32_t start, uint32_t n,
                                                const uint8_t *R, uint32_t W, const uint32_t *ends, uint32_t nd) {
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint32_t L1 = L + 1, m = (uint32_t)(0x100000000ull / L1) + 1u;
+    const uint32_t L1 = L + 1, m = 0xffffffffu / L1 + 1u;   // (2^32 / L1 or 2^32 / L1 + 1: div_by corrects by 1)
     const uint64_t B0 = b.byte_off + (uint64_t)start * L1, B1 = B0 + (uint64_t)n * L1;
     const uint64_t A0 = (B0 + 15) & ~15ull, A1 = B1 & ~15ull;
     if (A0 >= A1) {
