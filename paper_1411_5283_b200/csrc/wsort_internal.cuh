@@ -106,7 +106,10 @@ cudaError_t launch_cta_bases(const TkArgs &a, uint32_t max_len, cudaStream_t s);
 cudaError_t launch_pack_scatter(const TkArgs &a, cudaStream_t s);
 
 // ---------------- K1 ingest: one text pass (k_ingest.cu) ----------------
-constexpr int kIgThreads = 512;
+#ifndef WSORT_IG_THREADS
+#define WSORT_IG_THREADS 512
+#endif
+constexpr int kIgThreads = WSORT_IG_THREADS;
 constexpr int kIgStep = 16384;                       // bytes per ingest step = 32 per thread
 constexpr int kIgBuf = kTkPre + kIgStep + kTkHalo;   // 16656 bytes
 constexpr uint32_t kDenseMaxLen = 5;                 // words of L <= 5 are counted, not sorted
