@@ -36,21 +36,26 @@ namespace {
 using namespace text;
 
 constexpr int kIgWarps = kIgThreads / 32;
-constexpr int kCacheSlots = 2048;
+#ifndef WSORT_IG_CACHE_LG
+#define WSORT_IG_CACHE_LG 13
+#endif
+constexpr int kCacheLg = WSORT_IG_CACHE_LG, kCacheSlots = 1 << kCacheLg;   // (1024 .. 8192 slots measured: see DESIGN.md)
 
 // entries of the dense tables of lengths < L: (26^L - 26) / 25
 __host__ __device__ constexpr uint32_t dense_base(uint32_t L) {
     return L <= 1 ? 0u : L == 2 ? 26u : L == 3 ? 702u : L == 4 ? 18278u : L == 5 ? 475254u : 12356630u;
 }
 
+// One CTA of 1024 threads per SM (measured on c4: 1.31 ms against 1.45 ms with two CTAs of 512: one set of
+// shared tables, one hash cache of twice the slots and one open chunk per class per SM)
 #ifndef WSORT_IG_MINB
-#define WSORT_IG_MINB 2
+#define WSORT_IG_MINB 1
 #endif
 constexpr int kIgMinBlocks = WSORT_IG_MINB;
 #ifndef WSORT_IG_PIECE
 #define WSORT_IG_PIECE 0
 #endif
-// 0 (default): a CTA's range is split into 16 static contiguous warp ranges. > 0 (experiment, measured
+// 0 (default): a CTA's range is split into static contiguous warp ranges. > 0 (experiment, measured
 // slower: 1.70 vs 1.45 ms on c4 for pieces of 4 .. 32 sub-steps): the range is handed to the warps in pieces
 // of kIgPiece sub-steps taken from a shared counter as each warp finishes its piece
 constexpr uint32_t kIgPiece = WSORT_IG_PIECE;
@@ -120,7 +125,7 @@ __device__ __forceinline__ bool cache_try(IgSmem &sm, uint32_t h, uint32_t tag) 
 __device__ __forceinline__ void cache_add(IgSmem &sm, uint32_t *dense, uint8_t *touched, uint32_t L, uint32_t idx) {
     const uint32_t tag = (L << 24) | idx;
     const uint32_t hh = tag * 0x9E3779B1u;
-    if (cache_try(sm, hh >> 21, tag)) return;
+    if (cache_try(sm, hh >> (32 - kCacheLg), tag)) return;
     if (cache_try(sm, (hh >> 10) & (kCacheSlots - 1), tag)) return;
     const uint32_t e = dense_base(L) + idx;
     atomicAdd(&dense[e], 1u);
@@ -216,7 +221,7 @@ __device__ __forceinline__ void hash_long(const IngestArgs &a, IgSmem &sm, const
     }
 }
 
-// K1. The CTA's byte range is split into 16 contiguous warp ranges of 1 KiB sub-steps; each warp
+// K1. The CTA's byte range is split into contiguous warp ranges (32 warps) of 1 KiB sub-steps; each warp
 // streams its sub-steps with no block barrier: every lane classifies 32 bytes (SWAR letter mask, loaded
 // one sub-step ahead), word starts / ends come from mask shifts, the letter runs crossing lane
 // boundaries from a suffix scan of (l1,f1)+(l2,f2) = (l1 + f1*l2, f1 & f2) (l = letters leading a

@@ -107,7 +107,7 @@ cudaError_t launch_pack_scatter(const TkArgs &a, cudaStream_t s);
 
 // ---------------- K1 ingest: one text pass (k_ingest.cu) ----------------
 #ifndef WSORT_IG_THREADS
-#define WSORT_IG_THREADS 512
+#define WSORT_IG_THREADS 1024
 #endif
 constexpr int kIgThreads = WSORT_IG_THREADS;
 constexpr int kIgStep = 16384;                       // bytes per ingest step = 32 per thread
