@@ -85,7 +85,7 @@ struct IgSmem {
     uint4 wbuf[kIgWarps][2][kWBuf / 16 + 1];   // per warp, two slots: a sub-step + tail (+16 B: packing reads
                                                // whole words)
     uint16_t wlist[kIgWarps][kWList];      // per warp: s | (L-3) << 10; L = 3..5 from the front, 6..66 from the back
-    uint32_t d12[702];                     // dense counts of L = 1, 2
+    uint32_t d12[27 * 27];                 // counts of L = 1, 2: [code of letter 0 (1..26)][code of letter 1, 0 for L = 1]
     uint32_t ctag[kCacheSlots];            // hash cache for L = 3..5: tag = L << 24 | idx, 0 = empty
     uint32_t ccnt[kCacheSlots];
     uint32_t hist[kHistBins];
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
     const uint32_t cbase = c * a.cta_chunks;
     const uint32_t trash = a.grid * a.cta_chunks;
 
-    for (int i = t; i < 702; i += kIgThreads) sm.d12[i] = 0;
+    for (int i = t; i < 27 * 27; i += kIgThreads) sm.d12[i] = 0;
     for (int i = t; i < kCacheSlots; i += kIgThreads) sm.ctag[i] = sm.ccnt[i] = 0;
     for (int i = t; i < kHistBins; i += kIgThreads) sm.hist[i] = 0;
     for (uint32_t i = t; i < kMaxStageKw * kRing; i += kIgThreads) (&sm.ring[0][0])[i] = 0;
@@ -360,12 +360,12 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
         const uint32_t tot = __shfl_sync(kFull, ci, 31);
         uint32_t p3 = (ci - cnt) & 0xffffu, plg = (ci - cnt) >> 16;
         uint32_t *d12 = sm.d12;
-        for (uint32_t m = s12; m; m &= m - 1) {   // L = 1, 2: count now (shared-memory table)
-            const uint32_t bit = __ffs(m) - 1, s = seg0 + bit;
-            const uint32_t two = (uint32_t)(X >> (bit + 1)) & 1u;
-            const uint32_t lo = __funnelshift_r(wb32[s >> 2], wb32[(s >> 2) + 1], 8u * (s & 3u));
-            const uint32_t c0 = (lo & 31u) - 1u, c1 = ((lo >> 8) & 31u) - 1u;
-            if (!(a.debug & 1)) atomicAdd(&d12[two ? 26u + c0 * 26u + c1 : c0], 1u);
+        for (uint32_t m = s12; m;) {   // L = 1, 2: count now (shared-memory table [first code][second code or 0])
+            const uint32_t low = m & (0u - m), s = seg0 + 31u - (uint32_t)__clz(low);
+            m ^= low;
+            const uint32_t b0 = wb[s], b1 = wb[s + 1];   // (byte 1024 is the staged tail)
+            const uint32_t sel = (ge2 & low) ? (b1 & 31u) : 0u;
+            if (!(a.debug & 1)) atomicAdd(&d12[(b0 & 31u) * 27u + sel], 1u);
         }
         for (uint32_t m = s345; m; m &= m - 1) {   // L = 3..5: listed for the hash cache
             const uint32_t bit = __ffs(m) - 1;
@@ -463,9 +463,10 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
         }
     }
     if (a.debug & 32) return;   // (timing experiments: no flush of the shared-memory tables)
-    for (int i = t; i < 702; i += kIgThreads)
-        if (sm.d12[i]) {
-            atomicAdd(&a.dense[i], sm.d12[i]);
+    for (int i = t; i < 27 * 27; i += kIgThreads)
+        if (sm.d12[i]) {   // (rows / columns of code 0 stay empty) -> dense index: L = 1: c0; L = 2: 26 + 26 c0 + c1
+            const uint32_t c0 = (uint32_t)i / 27u - 1u, b1 = (uint32_t)i % 27u;
+            atomicAdd(&a.dense[b1 ? 26u + c0 * 26u + b1 - 1u : c0], sm.d12[i]);
             a.touched[0] = 1;   // (702 < one block)
         }
     for (int i = t; i < kCacheSlots; i += kIgThreads) {
