@@ -367,18 +367,22 @@ __global__ void __launch_bounds__(kIgThreads, kIgMinBlocks) k_ingest(IngestArgs 
             const uint32_t sel = (ge2 & low) ? (b1 & 31u) : 0u;
             if (!(a.debug & 1)) atomicAdd(&d12[(b0 & 31u) * 27u + sel], 1u);
         }
-        for (uint32_t m = s345; m; m &= m - 1) {   // L = 3..5: listed for the hash cache
-            const uint32_t bit = __ffs(m) - 1;
-            const uint32_t y = (uint32_t)(X >> (bit + 3));
-            wlst[p3++] = (uint16_t)((seg0 + bit) | (((y & 1u) + (y & (y >> 1) & 1u)) << 10));
+        for (uint32_t m = s345; m;) {   // L = 3..5: listed for the hash cache (L - 3 = the start is in ge4, in ge5)
+            const uint32_t low = m & (0u - m), bit = 31u - (uint32_t)__clz(low);
+            m ^= low;
+            wlst[p3++] = (uint16_t)(seg0 + bit + ((ge4 & low) ? 1024u : 0u) + ((ge5 & low) ? 1024u : 0u));
         }
-        for (uint32_t m = ge6; m; m &= m - 1) {   // L >= 6: listed for packing (above 66 kept as 67: not staged)
-            const uint32_t bit = __ffs(m) - 1;
-            const uint32_t em = ends & (0xffffffffu << bit);
-            const uint32_t L = em ? (uint32_t)(__ffs(em) - 1) - bit + 1u : (32u - bit) + carry;
+        const uint32_t past = 32u + carry;   // (a word with no end in this lane: its letters here + the carry)
+        uint32_t ntl = 0;
+        for (uint32_t m = ge6; m;) {   // L >= 6: listed for packing (above 66 kept as 67: not staged)
+            const uint32_t low = m & (0u - m), bit = 31u - (uint32_t)__clz(low);
+            m ^= low;
+            const uint32_t em = ends & (0u - low);   // ends at or after the start
+            const uint32_t L = (uint32_t)__ffs(em) - bit + (em ? 0u : past);   // (__ffs(0) = 0)
             wlst[kWList - 1 - plg++] = (uint16_t)((seg0 + bit) | ((min(L, 6u * kMaxStageKw + 1u) - 6u) << 10));
-            if (L > (uint32_t)kMaxLen) atomicAdd(&sm.hist[256], 1u);
+            ntl += L > (uint32_t)kMaxLen;
         }
+        if (ntl) atomicAdd(&sm.hist[256], ntl);
         __syncwarp();
         const uint32_t n3 = tot & 0xffffu, nlg = tot >> 16;
         for (uint32_t i = lane; i < ((a.debug & 17) ? 0u : n3); i += 32) {   // L = 3..5: hash cache
